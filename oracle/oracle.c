@@ -1,0 +1,376 @@
+/* oracle.c — plain CPU oracle. TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * Written from PAPER.md (arXiv 1804.06087). Each function cites the passage it follows.
+ * Loops are in the order the definitions are stated; no pruning, no fast paths.
+ */
+#include "oracle.h"
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---- A2: per-model top-1 ("top-1"; reading Q4: lowest index on ties) ---- */
+int or_top1_f32(const float* row, int C) {
+  int best = 0;
+  for (int c = 1; c < C; ++c)
+    if (row[c] > row[best]) best = c;
+  return best;
+}
+int or_top1_f64(const double* row, int C) {
+  int best = 0;
+  for (int c = 1; c < C; ++c)
+    if (row[c] > row[best]) best = c;
+  return best;
+}
+
+/* ---- A2: softmax probabilities, fp64, max-subtracted (reading Q5) ---------------------- */
+void or_softmax(const double* l, int C, double* p) {
+  double mx = l[0];
+  for (int c = 1; c < C; ++c) if (l[c] > mx) mx = l[c];
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) { p[c] = exp(l[c] - mx); s += p[c]; }
+  for (int c = 0; c < C; ++c) p[c] = p[c] / s;
+}
+double or_lse(const double* l, int C) {
+  double mx = l[0];
+  for (int c = 1; c < C; ++c) if (l[c] > mx) mx = l[c];
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) s += exp(l[c] - mx);
+  return mx + log(s);
+}
+
+/* ---- A3: majority vote of the members' top-1 predictions (§5.2:
+ * "Majority voting is applied to aggregate the predictions ... when there is a tie, the
+ * prediction from the model with the best accuracy is selected as the final prediction").
+ * cnt[c] = #members predicting c; M = max cnt.
+ *   BEST_MEMBER : top1[i*], i* = argmin rank[i] over members i with cnt[top1[i]] == M  (Q2)
+ *   LOWEST_CLASS: min { c : cnt[c] == M }                                             (north_star)
+ * cnt is a full class histogram (thread-local, re-zeroed after each call). */
+int or_vote(const int* top1, int K, int C, uint32_t v, const int* rank, int tie) {
+  static _Thread_local int* cnt = NULL; /* class histogram, all zero between calls */
+  static _Thread_local int cap = 0;
+  if (cap < C) { free(cnt); cnt = (int*)calloc((size_t)C, sizeof(int)); cap = C; }
+  int M = 0;
+  for (int i = 0; i < K; ++i)
+    if ((v >> i) & 1u) cnt[top1[i]]++;
+  for (int i = 0; i < K; ++i)
+    if (((v >> i) & 1u) && cnt[top1[i]] > M) M = cnt[top1[i]];
+  int winner = -1;
+  if (tie == OR_TIE_BEST_MEMBER) {
+    int best_i = -1;
+    for (int i = 0; i < K; ++i) {
+      if (!((v >> i) & 1u) || cnt[top1[i]] != M) continue;
+      if (best_i < 0 || (rank ? rank[i] < rank[best_i] : i < best_i)) best_i = i;
+    }
+    winner = top1[best_i];
+  } else {
+    for (int c = 0; c < C && winner < 0; ++c)
+      if (cnt[c] == M) winner = c;
+  }
+  for (int i = 0; i < K; ++i)
+    if ((v >> i) & 1u) cnt[top1[i]] = 0;
+  return winner;
+}
+
+/* ---- A4: averaged softmax probabilities ("ensemble multiple models and average
+ * the results"): avg[c] = (sum_{i in v, ascending i} p[i][c]) / |v|; prediction = smallest c
+ * attaining the max (reading Q6). a1 >= a2 are the two largest avg values over distinct
+ * classes; the pair is ambiguous if (a1 - a2)/a1 <= 1e-12 (includes exact ties). */
+int or_avg(const double* p, int K, int C, uint32_t v, int* amb, double* avg_out) {
+  int nv = 0;
+  for (int i = 0; i < K; ++i) nv += (int)((v >> i) & 1u);
+  int pred = 0;
+  double a1 = -1.0, a2 = -1.0;
+  for (int c = 0; c < C; ++c) {
+    double s = 0.0;
+    for (int i = 0; i < K; ++i)
+      if ((v >> i) & 1u) s += p[(int64_t)i * C + c];
+    double a = s / (double)nv;
+    if (avg_out) avg_out[c] = a;
+    if (a > a1) { a2 = a1; a1 = a; pred = c; }
+    else if (a > a2) a2 = a;
+  }
+  if (amb) *amb = (a1 - a2) / a1 <= 1e-12;
+  return pred;
+}
+
+/* ---- A1: synthetic dense heads (stand-in for the ConvNets' classifier layer, PAPER.md:152-154;
+ * "inference time which depends on the model complexity"). fp64 sums of exact
+ * bf16 products. ---------------------------------------------------------------------------- */
+static double bf16_val(uint16_t b) {
+  union { uint32_t u; float f; } v;
+  v.u = (uint32_t)b << 16;
+  return (double)v.f;
+}
+
+typedef struct {
+  const uint16_t *X, *W;
+  const float* bias;
+  int64_t n0, n1;
+  int K, C, D, s;
+  double* out;
+} gemm_job;
+
+static void* gemm_thr(void* a) {
+  gemm_job* j = (gemm_job*)a;
+  double* xr = (double*)malloc(sizeof(double) * j->D);
+  double scale = ldexp(1.0, j->s);
+  for (int64_t n = j->n0; n < j->n1; ++n) {
+    for (int d = 0; d < j->D; ++d) xr[d] = bf16_val(j->X[n * j->D + d]);
+    for (int m = 0; m < j->K; ++m)
+      for (int c = 0; c < j->C; ++c) {
+        const uint16_t* w = j->W + ((int64_t)m * j->C + c) * j->D;
+        double acc = 0.0;
+        for (int d = 0; d < j->D; ++d) acc += xr[d] * bf16_val(w[d]);
+        double b = j->bias ? (double)j->bias[(int64_t)m * j->C + c] : 0.0;
+        j->out[(n * j->K + m) * j->C + c] = acc * scale + b;
+      }
+  }
+  free(xr);
+  return NULL;
+}
+
+void or_logits_gemm(const uint16_t* X, const uint16_t* W, const float* bias, int64_t N, int K, int C, int D,
+                    int scale_log2, double* out, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  gemm_job jobs[256];
+  int64_t per = (N + threads - 1) / threads;
+  int nt = 0;
+  for (int t = 0; t < threads; ++t) {
+    int64_t a = t * per, b = a + per < N ? a + per : N;
+    if (a >= b) break;
+    gemm_job g = {X, W, bias, a, b, K, C, D, scale_log2, out};
+    jobs[t] = g;
+    pthread_create(&th[t], NULL, gemm_thr, &jobs[t]);
+    nt++;
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
+/* ---- arrivals (reading Q9) --------------------------------------------------------------- */
+int64_t or_arrival_ns(int64_t s, double rate) {
+  volatile double num = (double)s * 1e9; /* two IEEE roundings, in this order */
+  return (int64_t)floor(num / rate);
+}
+
+/* ---- A5-A7: table ------------------------------------------------------------------------- */
+typedef struct {
+  const float* lf;
+  int ldc;
+  const double* ld;
+  int64_t N, a, b;
+  int K, C;
+  const int32_t* labels;
+  const int* rank;
+  int tie;
+  const or_cfg* cfg;
+  int status;
+  /* thread-local accumulators */
+  uint64_t *cnt_vote, *cnt_avg, *n_amb, *corr, *O, *Q, *E;
+} table_job;
+
+static int64_t gcd64(int64_t a, int64_t b) { while (b) { int64_t t = a % b; a = b; b = t; } return a; }
+
+/* Row access: returns 0 on non-finite (NaN, +inf, or all -inf). */
+static int load_row(const table_job* j, int64_t n, int m, double* l, int* top1) {
+  double mx = -INFINITY;
+  for (int c = 0; c < j->C; ++c) {
+    double x = j->lf ? (double)j->lf[(n * j->K + m) * (int64_t)j->ldc + c] : j->ld[(n * j->K + m) * (int64_t)j->C + c];
+    if (isnan(x) || x == INFINITY) return 0;
+    l[c] = x;
+    if (x > mx) mx = x;
+  }
+  if (mx == -INFINITY) return 0;
+  *top1 = j->lf ? or_top1_f32(j->lf + (n * j->K + m) * (int64_t)j->ldc, j->C)
+                : or_top1_f64(j->ld + (n * j->K + m) * (int64_t)j->C, j->C);
+  return 1;
+}
+
+static int64_t arrival(const or_cfg* cfg, int r, int64_t s) {
+  return cfg->arrival_ns ? cfg->arrival_ns[s] : or_arrival_ns(s, cfg->rates[r]);
+}
+
+static void* table_thr(void* arg) {
+  table_job* j = (table_job*)arg;
+  const int K = j->K, C = j->C, S = (1 << K) - 1;
+  const or_cfg* cfg = j->cfg;
+  const int nB = cfg ? cfg->nB : 0, nR = cfg ? cfg->nR : 0;
+  double* l = (double*)malloc(sizeof(double) * C);
+  double* p = (double*)malloc(sizeof(double) * (size_t)K * C);
+  int top1[32];
+  uint8_t* vote_ok = (uint8_t*)malloc((size_t)S);
+  uint64_t* corr_cur = (uint64_t*)calloc((size_t)(nB > 0 ? nB : 1) * S, sizeof(uint64_t));
+  for (int64_t n = j->a; n < j->b; ++n) {
+    int y = j->labels[n];
+    if (y < 0 || y >= C) { j->status = OR_ELABEL; break; }
+    for (int m = 0; m < K; ++m) {
+      if (!load_row(j, n, m, l, &top1[m])) { j->status = OR_ENONFINITE; goto done; }
+      or_softmax(l, C, p + (int64_t)m * C);
+    }
+    for (uint32_t v = 1; v <= (uint32_t)S; ++v) {
+      int wv = or_vote(top1, K, C, v, j->rank, j->tie);
+      int amb = 0;
+      int wa = or_avg(p, K, C, v, &amb, NULL);
+      vote_ok[v - 1] = (uint8_t)(wv == y);
+      j->cnt_vote[v - 1] += (uint64_t)(wv == y);
+      j->cnt_avg[v - 1] += (uint64_t)(wa == y);
+      j->n_amb[v - 1] += (uint64_t)amb;
+    }
+    /* per-(v,b) batch moments over complete global batches j = [jb*b, (jb+1)*b) (reading Q8, Q13) */
+    for (int bi = 0; bi < nB; ++bi) {
+      const int64_t b = cfg->B[bi];
+      const int64_t nb = j->N / b;
+      const int64_t jb = n / b;
+      if (jb >= nb) continue; /* trailing partial batch excluded */
+      for (int v = 0; v < S; ++v) corr_cur[(int64_t)bi * S + v] += vote_ok[v];
+      if (n % b != b - 1) continue;
+      /* batch complete: latency of each request l(s) = wait + c(v,b),
+       * wait = t_last - t_s (dispatch when the batch is full), c(v,b) = max over members
+       * (straggler); overdue <=> l(s) > tau, strict (reading Q10) */
+      const int64_t s0 = jb * b, s1 = s0 + b;
+      for (int r = 0; r < nR; ++r) {
+        const int64_t tlast = arrival(cfg, r, s1 - 1);
+        for (uint32_t v = 1; v <= (uint32_t)S; ++v) {
+          int64_t c = 0;
+          for (int m = 0; m < K; ++m)
+            if (((v >> m) & 1u) && cfg->lat_ns[m * nB + bi] > c) c = cfg->lat_ns[m * nB + bi];
+          uint64_t o = 0, e = 0;
+          for (int64_t s = s0; s < s1; ++s) {
+            int64_t lat = (tlast - arrival(cfg, r, s)) + c;
+            if (lat > cfg->tau_ns) { o++; e += (uint64_t)(lat - cfg->tau_ns); }
+          }
+          const int64_t idx = ((int64_t)r * nB + bi) * S + (v - 1);
+          j->O[idx] += o;
+          j->Q[idx] += corr_cur[(int64_t)bi * S + (v - 1)] * o;
+          if (j->E) j->E[idx] += e;
+        }
+      }
+      for (int v = 0; v < S; ++v) {
+        j->corr[(int64_t)bi * S + v] += corr_cur[(int64_t)bi * S + v];
+        corr_cur[(int64_t)bi * S + v] = 0;
+      }
+    }
+  }
+done:
+  free(l); free(p); free(vote_ok); free(corr_cur);
+  return NULL;
+}
+
+int or_table_build(const float* logits_f32, int ldc, const double* logits_f64, int64_t N, int K, int C,
+                   const int32_t* labels, const int* rank, int tie, const or_cfg* cfg, or_table* out,
+                   int threads) {
+  if (K < 1 || K > 12 || C < 2 || N < 0 || (!logits_f32 == !logits_f64)) return OR_EINVAL;
+  if (cfg && cfg->nB > 0 && (!cfg->B || !cfg->lat_ns)) return OR_EINVAL;
+  if (cfg && cfg->nR > 0 && !cfg->rates && !cfg->arrival_ns) return OR_EINVAL;
+  if (cfg && cfg->arrival_ns && cfg->nR != 1) return OR_EINVAL;
+  const int S = (1 << K) - 1;
+  const int nB = cfg ? cfg->nB : 0, nR = cfg ? cfg->nR : 0;
+  const int64_t nT = (int64_t)nR * nB * S;
+  /* threads split at multiples of lcm(B) so no batch straddles two threads */
+  int64_t L = 1;
+  for (int bi = 0; bi < nB; ++bi) L = L / gcd64(L, cfg->B[bi]) * cfg->B[bi];
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  int64_t units = (N + L - 1) / L;
+  if (threads > units) threads = (int)(units > 0 ? units : 1);
+  int64_t per = (units + threads - 1) / threads;
+  pthread_t th[256];
+  table_job* jobs = (table_job*)calloc((size_t)threads, sizeof(table_job));
+  int nt = 0;
+  for (int t = 0; t < threads; ++t) {
+    int64_t a = t * per * L, b = (t + 1) * per * L;
+    if (b > N) b = N;
+    if (a >= b) break;
+    table_job* j = &jobs[t];
+    j->lf = logits_f32; j->ldc = ldc; j->ld = logits_f64; j->N = N; j->a = a; j->b = b;
+    j->K = K; j->C = C; j->labels = labels; j->rank = rank; j->tie = tie; j->cfg = cfg;
+    j->cnt_vote = (uint64_t*)calloc((size_t)S, 8);
+    j->cnt_avg = (uint64_t*)calloc((size_t)S, 8);
+    j->n_amb = (uint64_t*)calloc((size_t)S, 8);
+    j->corr = (uint64_t*)calloc((size_t)(nB ? nB : 1) * S, 8);
+    j->O = (uint64_t*)calloc((size_t)(nT ? nT : 1), 8);
+    j->Q = (uint64_t*)calloc((size_t)(nT ? nT : 1), 8);
+    j->E = (cfg && cfg->want_exceed) ? (uint64_t*)calloc((size_t)(nT ? nT : 1), 8) : NULL;
+    pthread_create(&th[t], NULL, table_thr, j);
+    nt++;
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  int status = OR_OK;
+  memset(out->cnt_vote, 0, (size_t)S * 8);
+  memset(out->cnt_avg, 0, (size_t)S * 8);
+  if (out->n_amb) memset(out->n_amb, 0, (size_t)S * 8);
+  if (nB && out->corr) memset(out->corr, 0, (size_t)nB * S * 8);
+  if (nT) {
+    if (out->O) memset(out->O, 0, (size_t)nT * 8);
+    if (out->Q) memset(out->Q, 0, (size_t)nT * 8);
+    if (out->E) memset(out->E, 0, (size_t)nT * 8);
+  }
+  for (int t = 0; t < nt; ++t) {
+    table_job* j = &jobs[t];
+    if (j->status != OR_OK && status == OR_OK) status = j->status;
+    for (int v = 0; v < S; ++v) {
+      out->cnt_vote[v] += j->cnt_vote[v];
+      out->cnt_avg[v] += j->cnt_avg[v];
+      if (out->n_amb) out->n_amb[v] += j->n_amb[v];
+    }
+    for (int64_t i = 0; i < (int64_t)nB * S; ++i) if (out->corr) out->corr[i] += j->corr[i];
+    for (int64_t i = 0; i < nT; ++i) {
+      if (out->O) out->O[i] += j->O[i];
+      if (out->Q) out->Q[i] += j->Q[i];
+      if (out->E && j->E) out->E[i] += j->E[i];
+    }
+    free(j->cnt_vote); free(j->cnt_avg); free(j->n_amb); free(j->corr); free(j->O); free(j->Q); free(j->E);
+  }
+  free(jobs);
+  if (status != OR_OK) return status;
+  /* A7: eq. `multi_acc_reward` a(M[v]) * (b - beta*|{s in batch : l(s) > tau}|),
+   * summed over the n_b complete batches. Surrogate a(v) = validation accuracy of the vote
+   * (reading Q7/Q11); labelled variant uses the batch's own correct fraction. */
+  for (int r = 0; r < nR; ++r)
+    for (int bi = 0; bi < nB; ++bi) {
+      const double b = (double)cfg->B[bi];
+      const double nb = (double)(N / cfg->B[bi]);
+      for (int v = 0; v < S; ++v) {
+        const int64_t idx = ((int64_t)r * nB + bi) * S + v;
+        const double a = N > 0 ? (double)out->cnt_vote[v] / (double)N : 0.0;
+        if (out->reward_sur) out->reward_sur[idx] = a * (nb * b - cfg->beta * (double)out->O[idx]);
+        if (out->reward_lab)
+          out->reward_lab[idx] = (double)out->corr[(int64_t)bi * S + v] - (cfg->beta / b) * (double)out->Q[idx];
+      }
+    }
+  return OR_OK;
+}
+
+/* ---- per-sample outputs for one action v --------------------------------------------------- */
+int or_predict(const float* logits_f32, int ldc, const double* logits_f64, int64_t N, int K, int C, uint32_t v,
+               const int* rank, int tie, int32_t* pred_vote, int32_t* pred_avg, double* avgprob, int32_t* top1_out,
+               double* lse_out, int threads) {
+  (void)threads;
+  if (K < 1 || K > 12 || C < 2 || v == 0 || v >= (1u << K) || (!logits_f32 == !logits_f64)) return OR_EINVAL;
+  table_job j;
+  memset(&j, 0, sizeof j);
+  j.lf = logits_f32; j.ldc = ldc; j.ld = logits_f64; j.K = K; j.C = C;
+  double* l = (double*)malloc(sizeof(double) * C);
+  double* p = (double*)malloc(sizeof(double) * (size_t)K * C);
+  int top1[32];
+  int status = OR_OK;
+  for (int64_t n = 0; n < N; ++n) {
+    for (int m = 0; m < K; ++m) {
+      if (!load_row(&j, n, m, l, &top1[m])) { status = OR_ENONFINITE; goto out; }
+      if (top1_out) top1_out[n * K + m] = top1[m];
+      if (lse_out) lse_out[n * K + m] = or_lse(l, C);
+      or_softmax(l, C, p + (int64_t)m * C);
+    }
+    if (pred_vote) pred_vote[n] = or_vote(top1, K, C, v, rank, tie);
+    if (pred_avg || avgprob) {
+      int amb;
+      int a = or_avg(p, K, C, v, &amb, avgprob ? avgprob + n * (int64_t)C : NULL);
+      if (pred_avg) pred_avg[n] = a;
+    }
+  }
+out:
+  free(l); free(p);
+  return status;
+}

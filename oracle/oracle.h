@@ -1,0 +1,92 @@
+/* oracle.h — plain, slow CPU oracle for the Rafiki ensemble-subset hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_1804_06087_b200/, librk.so) never links, imports or calls it, and shares no
+ * code with it (the seeded input generators in gen/ are the only shared module).
+ *
+ * Every function follows a definition in PAPER.md (arXiv 1804.06087) written out
+ * directly: loops over samples, then subsets v = 1..2^K-1, then members/classes.
+ * No pruning, no fast paths, fp64/int64 arithmetic. Readings of silent/ambiguous
+ * passages are the SURVEY.md §8(c) Q-readings, listed in DESIGN.md.
+ *
+ * Pins (tests/test_oracle_*.py, tests/golden/): hand-computed examples W1-W4,
+ * invariants I1-I8, reward examples R1-R5, brute force against an
+ * independently written pairwise formulation, library pins (numpy argmax/bincount,
+ * torch.softmax). Parity unpinned: the paper's Fig. `fig:ensemble` values (images only).
+ */
+#ifndef RK_ORACLE_H
+#define RK_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { OR_TIE_BEST_MEMBER = 0, OR_TIE_LOWEST_CLASS = 1 };
+enum { OR_OK = 0, OR_EINVAL = 1, OR_ELABEL = 6, OR_ENONFINITE = 7, OR_ENOMEM = 3 };
+
+/* Batch/latency configuration for the eq. `multi_acc_reward` moments. */
+typedef struct {
+  int nB;                 /* number of candidate batch sizes (0 = counts only)          */
+  const int* B;           /* [nB] batch sizes                         */
+  double beta;            /* balancing factor (PAPER.md:345 Table tb:notation)            */
+  int64_t tau_ns;         /* SLO tau in ns                                 */
+  const int64_t* lat_ns;  /* [K][nB] c(m,b) in ns                      */
+  int nR;                 /* number of arrival rates                                      */
+  const double* rates;    /* [nR] req/s; t_s = floor(s*1e9/r) (reading Q9)                */
+  const int64_t* arrival_ns; /* [N] or NULL: caller arrivals (then nR must be 1)          */
+  int want_exceed;        /* also compute E (eq. `eq:single`)           */
+} or_cfg;
+
+/* Output table (host, caller-allocated). S = 2^K-1, index v-1. */
+typedef struct {
+  uint64_t* cnt_vote;  /* [S]   majority-vote correct counts                     */
+  uint64_t* cnt_avg;   /* [S]   averaged-probability correct counts              */
+  uint64_t* n_amb;     /* [S]   (n,v) pairs whose fp64 avg top-2 gap <= 1e-12 rel */
+  uint64_t* corr;      /* [nB][S]                                                */
+  uint64_t* O;         /* [nR][nB][S]                                            */
+  uint64_t* Q;         /* [nR][nB][S]                                            */
+  uint64_t* E;         /* [nR][nB][S] or NULL                                    */
+  double* reward_sur;  /* [nR][nB][S]                                            */
+  double* reward_lab;  /* [nR][nB][S]                                            */
+} or_table;
+
+/* Per-model top-1: smallest class index attaining the max (reading Q4). */
+int or_top1_f32(const float* row, int C);
+int or_top1_f64(const double* row, int C);
+/* Softmax with max subtraction in fp64 (reading Q5, "average the results"). */
+void or_softmax(const double* l, int C, double* p);
+/* log-sum-exp in fp64. */
+double or_lse(const double* l, int C);
+/* Majority vote over members of v (§5.2). tie: OR_TIE_BEST_MEMBER (paper:
+ * prediction of the best-ranked member among the tied voters, reading Q2) or
+ * OR_TIE_LOWEST_CLASS (north_star). rank: [K] 0 = best, NULL = index order. */
+int or_vote(const int* top1, int K, int C, uint32_t v, const int* rank, int tie);
+/* Averaged-probability prediction: argmax_c (sum_{i in v asc} p[i][c])/|v|,
+ * smallest index on ties; *amb = 1 if (a1-a2)/a1 <= 1e-12 (reading Q6). p is [K][C]. */
+int or_avg(const double* p, int K, int C, uint32_t v, int* amb, double* avg_out /*[C] or NULL*/);
+
+/* Step A1: logits of K synthetic dense heads, fp64: out[n][m][c] = 2^s * sum_d x*w + bias.
+ * X [N][D] bf16 bits, W [K][C][D] bf16 bits, bias [K][C] or NULL. Exact for small-int inputs. */
+void or_logits_gemm(const uint16_t* X, const uint16_t* W, const float* bias, int64_t N, int K, int C,
+                    int D, int scale_log2, double* out, int threads);
+
+/* Steps A2-A7 over the whole dataset. Exactly one of logits_f32 ([N][K][ldc]) or
+ * logits_f64 ([N][K][C]) is non-NULL. top1 ties use the given precision. */
+int or_table_build(const float* logits_f32, int ldc, const double* logits_f64, int64_t N, int K, int C,
+                   const int32_t* labels, const int* rank, int tie, const or_cfg* cfg, or_table* out,
+                   int threads);
+
+/* Per-sample outputs for one action v (serving step, NEXT-1; parity hook for I4):
+ * pred_vote/pred_avg [N] and avgprob [N][C] (each may be NULL), top1 [N][K], lse [N][K] (NULL ok). */
+int or_predict(const float* logits_f32, int ldc, const double* logits_f64, int64_t N, int K, int C,
+               uint32_t v, const int* rank, int tie, int32_t* pred_vote, int32_t* pred_avg, double* avgprob,
+               int32_t* top1, double* lse, int threads);
+
+/* Arrival time of global request s at rate r (reading Q9): floor((double)s*1e9/r) ns. */
+int64_t or_arrival_ns(int64_t s, double rate);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
