@@ -1,0 +1,161 @@
+/* rk.h — C-ABI of librk.so: B200-native batched ensemble-subset scoring.
+ *
+ * The data-parallel hot path of Rafiki's online ensemble inference service (Wang et al.,
+ * arXiv 1804.06087, §5.2; PAPER.md line numbers cited below):
+ *   A1 rk_score            K synthetic dense classifier heads: logit = 2^s * X.W^T + bias
+ *                          (stand-in for the ConvNets' classifier layer).
+ *   A2                     per-model top-1 and softmax normaliser.
+ *   A3 rk_subset_*         majority vote of every model subset v, the action
+ *                          space (2^|M|-1)*|B| with v = 0 excluded.
+ *   A4                     averaged softmax probabilities of every subset.
+ *   A5                     per-subset / per-(subset, batch size) correct counts and batch
+ *                          overdue moments.
+ *   A6                     sum of the integer table across GPUs (one NCCL all-reduce).
+ *   A7                     the reward of eq. `multi_acc_reward`.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns rk_status; RK_OK = 0. On error, rk_last_error(ctx) holds a message.
+ *  - The caller owns every input and output buffer. The context owns its copy of the
+ *    weights and its device workspaces; rk_destroy frees them.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). Calls are
+ *    stream-ordered; rk_subset_finalize / rk_subset_stats synchronise `stream` and return
+ *    host results.
+ *  - Pointers documented "host or device" are classified with cudaPointerGetAttributes;
+ *    host buffers are staged through pinned bounce buffers inside the call.
+ *  - Subset mask v in [1, 2^K): bit m selects model m. Tables are indexed v-1 (v fastest),
+ *    then batch-size index, then rate index: T[r][b][v-1]. RL action index of (v, B[b]) is
+ *    (v-1)*nB + b (index 0 <-> (v = 0b001, B[0])).
+ *  - Not thread-safe per context; one context per process / GPU rank.
+ */
+#ifndef RK_H
+#define RK_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rk_ctx rk_ctx;
+
+typedef enum {
+  RK_OK = 0,
+  RK_EINVAL = 1,      /* bad argument (sizes, NULLs, v == 0, misaligned shard/chunk)      */
+  RK_ESTATE = 2,      /* call out of order (e.g. accumulate before score)                  */
+  RK_ENOMEM = 3,      /* device or pinned allocation failed                                */
+  RK_ECUDA = 4,       /* CUDA runtime/driver error (message in rk_last_error)              */
+  RK_ENCCL = 5,       /* NCCL error                                                        */
+  RK_ELABEL = 6,      /* a label outside [0, C)                                            */
+  RK_ENONFINITE = 7,  /* a NaN or +inf logit, or a row that is entirely -inf               */
+  RK_EUNSUPPORTED = 8 /* feature not available in this build (e.g. NCCL for world > 1)     */
+} rk_status;
+
+typedef enum {
+  RK_TIE_BEST_MEMBER = 0, /* paper: "when there is a tie, the prediction from the
+                             model with the best accuracy is selected" -- the best-ranked member
+                             among the tied voters (reading Q2)                          */
+  RK_TIE_LOWEST_CLASS = 1 /* north_star: lowest class index among the tied classes              */
+} rk_tie_mode;
+
+/* Create a context on `cuda_device`. world == 1: nccl_unique_id may be NULL. world > 1: every
+ * rank passes the same 128-byte ncclUniqueId (from rk_nccl_unique_id on rank 0, broadcast by
+ * the caller, e.g. through torch.distributed) and its rank; the table all-reduce (A6) then
+ * runs over NCCL (NVLink/NVSwitch). */
+rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, int rank, int world);
+/* Fill `out128` with a fresh ncclUniqueId (rank 0 only). */
+rk_status rk_nccl_unique_id(void* out128);
+
+/* Load the ensemble M (PAPER.md:337 Table tb:notation "M: model list").
+ *  K in [1,12] models (S = 2^K-1 <= 4095 subsets), C in [2,65535] classes.
+ *  W_bf16: [K][C][D] bfloat16 bit patterns, row-major (D contiguous), host or device; NULL
+ *          loads a logits-only ensemble (rk_score then returns RK_ESTATE). D % 64 == 0, D <= 16384.
+ *  bias:   [K][C] fp32 or NULL (= 0). logit = 2^logit_scale_log2 * sum_d x*w + bias.
+ *  member_rank: [K] permutation, 0 = most accurate model (used by RK_TIE_BEST_MEMBER);
+ *          NULL = index order (model 0 best). Never estimated inside the library (Q3).
+ *  The context copies everything it needs; the caller may free its buffers on return. */
+rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16, const float* bias,
+                           int logit_scale_log2, const int* member_rank, rk_tie_mode tie);
+
+/* A1+A2: run the K heads on N feature rows. X_bf16: [N][D] bfloat16 bits, host or device.
+ * global_offset = index of row 0 in the global request stream (fixes batch ids and arrival
+ * times). Produces the context's logits workspace [N][K][ldc] fp32 (ldc = C rounded up to 4),
+ * per-(row, model) top-1 and log-sum-exp, fused in the GEMM epilogue. */
+rk_status rk_score(rk_ctx* ctx, const void* X_bf16, int64_t N, int64_t global_offset, void* stream);
+
+/* Vote-stage entry on caller-provided logits: [N][K][ldc] fp32 DEVICE memory, ldc % 4 == 0,
+ * ldc >= C, 16-byte aligned. The pointer is borrowed until the next rk_score* call. */
+rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, int64_t global_offset,
+                          void* stream);
+
+/* Reward configuration for A5/A7 (eq. `multi_acc_reward`). */
+typedef struct {
+  int nB;                  /* 0..8 candidate batch sizes; 0 = counts only  */
+  const int* B;            /* [nB] host; lcm(B) <= 4096                                         */
+  double beta;             /* balancing factor beta                               */
+  int64_t tau_ns;          /* SLO tau in integer ns (strict l(s) > tau) */
+  const int64_t* lat_ns;   /* [K][nB] host: c(m, b) in ns                     */
+  int nR;                  /* 0..8 arrival rates                                                 */
+  const double* rates;     /* [nR] host, req/s: t_s = floor(s * 1e9 / r) ns, s global (Q9)      */
+  const int64_t* arrival_ns; /* [N] host or device, non-decreasing, for the last rk_score* call;
+                                if non-NULL, nR must be 1 and rates is ignored                   */
+  int want_exceed;         /* also accumulate E = sum max(0, l(s) - tau) (eq. `eq:single`)      */
+  int want_labelled;       /* also accumulate Q = sum_j corr_j * o_j (labelled reward variant)  */
+} rk_reward_cfg;
+
+/* Result table (host arrays, caller-allocated; any pointer may be NULL to skip it). */
+typedef struct {
+  int64_t N;               /* samples accumulated over all chunks and ranks                      */
+  uint64_t* cnt_vote;      /* [S] majority-vote correct counts; a(M[v]) = cnt_vote/N */
+  uint64_t* cnt_avg;       /* [S] averaged-probability correct counts                            */
+  uint64_t* n_recheck;     /* [S] (sample, v) pairs whose fp32 top-2 gap was within the band and
+                              were decided in fp64                                              */
+  uint64_t* corr;          /* [nB][S] vote-correct samples inside complete batches of size B[b]   */
+  uint64_t* O;             /* [nR][nB][S] overdue requests sum_j o_j(v,b,r)                      */
+  uint64_t* Q;             /* [nR][nB][S] sum_j corr_j(v) * o_j(v,b,r)   (want_labelled)         */
+  uint64_t* E;             /* [nR][nB][S] exceed time in ns            (want_exceed)             */
+  double* reward_sur;      /* [nR][nB][S] sum over batches of a(v) * (b - beta*o_j)              */
+  double* reward_lab;      /* [nR][nB][S] sum over batches of corr_j/b * (b - beta*o_j)          */
+} rk_table;
+
+/* Streaming form: reset (zero the table, set cfg; cfg NULL = counts only), then one
+ * rk_score* + rk_subset_accumulate per chunk, then finalize. Chunk (and shard) boundaries
+ * must be multiples of lcm(B); only the globally last chunk may be ragged. */
+rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg);
+/* A2-A5 on the last rk_score* batch. labels: [N] int32, host or device. */
+rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream);
+/* A6 (all-reduce when world > 1) + A7 (reward fold) + copy to `out`. Blocks on `stream`.
+ * Returns RK_ENONFINITE / RK_ELABEL if any accumulated chunk had bad input (table zeroed). */
+rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream);
+/* One-shot: reset + accumulate + finalize on the last rk_score* batch. */
+rk_status rk_subset_stats(rk_ctx* ctx, const int32_t* labels, const rk_reward_cfg* cfg, rk_table* out,
+                          void* stream);
+
+/* Serving of one action (NEXT-1) and parity hook: per-sample predictions of subset v on the
+ * last rk_score* batch. pred_vote, pred_avg: [N] int32; avgprob: [N][C] fp32 averaged
+ * probabilities. Device pointers; each may be NULL. v == 0 -> RK_EINVAL. */
+rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_avg, float* avgprob,
+                     void* stream);
+
+/* Device pointers of the last rk_score* outputs: logits [N][K][ldc] fp32, top1 [N][K] int32,
+ * lse [N][K] fp32 (top1/lse are NULL after rk_score_logits). Valid until the next rk_score*. */
+rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** lse,
+                     int64_t* N);
+
+/* Per-kernel device time, measured with CUDA events on the launch stream when profiling is on. */
+typedef struct {
+  const char* name;        /* static string                                                     */
+  int64_t launches;
+  double total_ms;
+  double bytes;            /* algorithmic bytes moved (HBM roofline), summed over launches      */
+  double flops;            /* algorithmic flops (tensor roofline), summed over launches         */
+} rk_kernel_stat;
+rk_status rk_set_profiling(rk_ctx* ctx, int on);   /* on=1 resets the counters                  */
+/* Writes up to max entries; *n = number of kernel kinds. Synchronises the context's events. */
+rk_status rk_kernel_stats(rk_ctx* ctx, rk_kernel_stat* out, int max, int* n);
+
+const char* rk_last_error(const rk_ctx* ctx);
+const char* rk_status_string(rk_status s);
+void rk_destroy(rk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,695 @@
+// rk_api.cpp — host orchestration behind the C-ABI in include/rk.h.
+//
+// Owns the per-rank context: the ensemble copy in HBM, workspaces sized to the largest chunk seen,
+// the integer result table, the NCCL communicator for the cross-GPU sum (A6), and the per-kernel
+// CUDA-event profiler used by bench.py. Every compute step runs in the CUDA kernels of
+// rk_gemm.cu / rk_vote.cu / rk_moments.cu; this file only validates, allocates and launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/rk.h"
+#include "rk_internal.h"
+
+using namespace rk;
+
+namespace {
+
+enum KernelKind { KK_GEMM = 0, KK_VOTE, KK_OVERDUE, KK_MERGE, KK_Q, KK_FOLD, KK_PREDICT, KK_ALLREDUCE, KK_COUNT };
+const char* kKernelNames[KK_COUNT] = {"gemm_heads_tcgen05", "vote_subsets", "overdue_moments", "merge_table",
+                                      "labelled_moments", "reward_fold", "predict", "nccl_allreduce"};
+
+struct Prof {
+  bool on = false;
+  struct Ev { cudaEvent_t a, b; int kind; double bytes, flops; };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> pool;
+  int64_t launches[KK_COUNT] = {};
+  double ms[KK_COUNT] = {}, bytes[KK_COUNT] = {}, flops[KK_COUNT] = {};
+};
+
+int64_t gcd64(int64_t a, int64_t b) { while (b) { int64_t t = a % b; a = b; b = t; } return a; }
+
+}  // namespace
+
+struct rk_ctx {
+  int dev = 0, rank = 0, world = 1, sm_count = 148;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  // ensemble
+  bool loaded = false, has_heads = false;
+  int K = 0, C = 0, D = 0, S = 0, Cp = 0, ldc = 0, scale_log2 = 0, tie = 0;
+  int member_rank[kMaxK] = {};
+  uint8_t* d_best_of = nullptr;
+  uint16_t* d_W = nullptr;
+  float* d_bias = nullptr;
+  // last rk_score* batch
+  bool have_batch = false, batch_stats = false;
+  const float* cur_logits = nullptr;
+  int64_t cur_ldc = 0, cur_N = 0, cur_off = 0;
+  // GEMM workspaces
+  float* ws_logits = nullptr;
+  int32_t* ws_top1 = nullptr;
+  float* ws_lse = nullptr;
+  int64_t ws_cap = 0, ws_top1_cap = 0, ws_lse_cap = 0;
+  uint16_t* ws_x = nullptr;
+  int64_t ws_x_cap = 0;
+  alignas(64) uint8_t tmaps[3 * 128];
+  // accumulation state
+  bool reset_done = false, final_seen = false;
+  bool has_cfg = false;
+  int nB = 0, nR = 0, want_exceed = 0, want_labelled = 0;
+  int B[kMaxB] = {};
+  int64_t lat[kMaxK * kMaxB] = {};
+  double rates[kMaxR] = {};
+  double beta = 0;
+  int64_t tau = 0;
+  const int64_t* arrival_user = nullptr;
+  int64_t L = 1;       // lcm(B)
+  int gs = 0;          // group size for labelled moments
+  unsigned long long* d_table = nullptr;
+  size_t table_words = 0;
+  int64_t off_N = 0, off_err = 1, off_vote = 0, off_avg = 0, off_rc = 0, off_corr = 0, off_O = 0, off_Q = 0, off_E = 0;
+  unsigned long long* d_chunk = nullptr;
+  size_t chunk_words = 0;
+  uint8_t* d_slow = nullptr;
+  uint8_t* d_grp = nullptr;
+  size_t grp_cap = 0;
+  int32_t* d_labels = nullptr;
+  int64_t labels_cap = 0;
+  int64_t* d_arr = nullptr;
+  int64_t arr_cap = 0;
+  float* d_scratch = nullptr;
+  int32_t* d_scratch_cls = nullptr;
+  size_t scratch_floats = 0, scratch_ints = 0;
+  double* d_rew = nullptr;
+  size_t rew_cap = 0;
+  int64_t chunks = 0;
+  Prof prof;
+};
+
+namespace {
+
+rk_status fail(rk_ctx* c, rk_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(ctx, RK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+rk_status ensure(rk_ctx* ctx, T** p, int64_t* cap, int64_t need) {
+  if (*cap >= need && *p) return RK_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  if (cudaMalloc((void**)p, sizeof(T) * std::max<int64_t>(need, 1)) != cudaSuccess)
+    return fail(ctx, RK_ENOMEM, "cudaMalloc failed (" + std::to_string(sizeof(T) * need) + " bytes)");
+  *cap = need;
+  return RK_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Begin / end a profiled launch on stream st.
+struct ProfScope {
+  rk_ctx* c; int kind; cudaStream_t st; double bytes, flops; cudaEvent_t a = nullptr;
+  ProfScope(rk_ctx* c_, int k, cudaStream_t s, double by, double fl) : c(c_), kind(k), st(s), bytes(by), flops(fl) {
+    c->prof.launches[kind]++;
+    if (!c->prof.on) return;
+    a = take();
+    cudaEventRecord(a, st);
+  }
+  cudaEvent_t take() {
+    if (!c->prof.pool.empty()) { cudaEvent_t e = c->prof.pool.back(); c->prof.pool.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+  }
+  ~ProfScope() {
+    if (!c->prof.on || !a) return;
+    cudaEvent_t b = take();
+    cudaEventRecord(b, st);
+    c->prof.pending.push_back({a, b, kind, bytes, flops});
+  }
+};
+
+void prof_collect(rk_ctx* c) {
+  for (auto& e : c->prof.pending) {
+    cudaEventSynchronize(e.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    c->prof.ms[e.kind] += ms;
+    c->prof.bytes[e.kind] += e.bytes;
+    c->prof.flops[e.kind] += e.flops;
+    c->prof.pool.push_back(e.a);
+    c->prof.pool.push_back(e.b);
+  }
+  c->prof.pending.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rk_status_string(rk_status s) {
+  switch (s) {
+    case RK_OK: return "RK_OK";
+    case RK_EINVAL: return "RK_EINVAL";
+    case RK_ESTATE: return "RK_ESTATE";
+    case RK_ENOMEM: return "RK_ENOMEM";
+    case RK_ECUDA: return "RK_ECUDA";
+    case RK_ENCCL: return "RK_ENCCL";
+    case RK_ELABEL: return "RK_ELABEL";
+    case RK_ENONFINITE: return "RK_ENONFINITE";
+    case RK_EUNSUPPORTED: return "RK_EUNSUPPORTED";
+  }
+  return "RK_?";
+}
+
+const char* rk_last_error(const rk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+rk_status rk_nccl_unique_id(void* out128) {
+  if (!out128) return RK_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return RK_ENCCL;
+  memcpy(out128, &id, sizeof(id));
+  return RK_OK;
+}
+
+rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, int rank, int world) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return RK_EINVAL;
+  if (world > 1 && !nccl_unique_id) return RK_EINVAL;
+  *out = nullptr;
+  rk_ctx* ctx = new rk_ctx();
+  ctx->dev = cuda_device;
+  ctx->rank = rank;
+  ctx->world = world;
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e != cudaSuccess) { delete ctx; return RK_ECUDA; }
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) { delete ctx; return RK_ENCCL; }
+  }
+  *out = ctx;
+  return RK_OK;
+}
+
+void rk_destroy(rk_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->dev);
+  cudaDeviceSynchronize();
+  void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_x,
+                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_labels, ctx->d_arr, ctx->d_scratch,
+                  ctx->d_scratch_cls, ctx->d_rew};
+  for (void* p : ptrs) if (p) cudaFree(p);
+  for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+  for (auto e : ctx->prof.pool) cudaEventDestroy(e);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  delete ctx;
+}
+
+rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16, const float* bias,
+                           int logit_scale_log2, const int* member_rank, rk_tie_mode tie) {
+  if (!ctx) return RK_EINVAL;
+  if (K < 1 || K > kMaxK) return fail(ctx, RK_EINVAL, "K must be in [1,12]");
+  if (C < 2 || C > 65535) return fail(ctx, RK_EINVAL, "C must be in [2,65535]");
+  if (tie != RK_TIE_BEST_MEMBER && tie != RK_TIE_LOWEST_CLASS) return fail(ctx, RK_EINVAL, "bad tie mode");
+  if (W_bf16 && (D <= 0 || D % 64 != 0 || D > 16384)) return fail(ctx, RK_EINVAL, "D must be a positive multiple of 64 (<= 16384)");
+  if (logit_scale_log2 < -60 || logit_scale_log2 > 60) return fail(ctx, RK_EINVAL, "scale out of range");
+  int rk_[kMaxK];
+  bool seen[kMaxK] = {};
+  for (int m = 0; m < K; ++m) {
+    rk_[m] = member_rank ? member_rank[m] : m;
+    if (rk_[m] < 0 || rk_[m] >= K || seen[rk_[m]]) return fail(ctx, RK_EINVAL, "member_rank must be a permutation of 0..K-1");
+    seen[rk_[m]] = true;
+  }
+  CK(cudaSetDevice(ctx->dev));
+  ctx->K = K; ctx->C = C; ctx->D = W_bf16 ? D : 0; ctx->S = (1 << K) - 1; ctx->tie = tie;
+  ctx->ldc = (C + 3) / 4 * 4;
+  ctx->Cp = (C + 15) / 16 * 16;
+  ctx->scale_log2 = logit_scale_log2;
+  memcpy(ctx->member_rank, rk_, sizeof(rk_));
+  // best_of[mask] = member of `mask` with the smallest rank ("the model with the best accuracy")
+  std::vector<uint8_t> best(size_t(1) << K, 0);
+  for (uint32_t msk = 1; msk < (1u << K); ++msk) {
+    int b = -1;
+    for (int m = 0; m < K; ++m)
+      if (((msk >> m) & 1u) && (b < 0 || rk_[m] < rk_[b])) b = m;
+    best[msk] = (uint8_t)b;
+  }
+  if (ctx->d_best_of) cudaFree(ctx->d_best_of);
+  CK(cudaMalloc(&ctx->d_best_of, best.size()));
+  CK(cudaMemcpy(ctx->d_best_of, best.data(), best.size(), cudaMemcpyHostToDevice));
+  if (ctx->d_W) { cudaFree(ctx->d_W); ctx->d_W = nullptr; }
+  if (ctx->d_bias) { cudaFree(ctx->d_bias); ctx->d_bias = nullptr; }
+  ctx->has_heads = W_bf16 != nullptr;
+  if (ctx->has_heads) {
+    // pad each model's C rows to Cp (zero rows) and its bias to -inf, so tiles never mix models
+    const size_t wrows = (size_t)K * ctx->Cp;
+    CK(cudaMalloc(&ctx->d_W, wrows * D * 2));
+    CK(cudaMemset(ctx->d_W, 0, wrows * D * 2));
+    const bool wdev = is_device_ptr(W_bf16);
+    CK(cudaMemcpy2D(ctx->d_W, (size_t)ctx->Cp * D * 2, W_bf16, (size_t)C * D * 2, (size_t)C * D * 2, K,
+                    wdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    std::vector<float> hb(wrows, -INFINITY);
+    std::vector<float> ub;
+    if (bias) {
+      ub.resize((size_t)K * C);
+      CK(cudaMemcpy(ub.data(), bias, ub.size() * 4, is_device_ptr(bias) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    }
+    for (int m = 0; m < K; ++m)
+      for (int c = 0; c < C; ++c) {
+        const float b = bias ? ub[(size_t)m * C + c] : 0.f;
+        if (!(b == b) || b == INFINITY || b == -INFINITY) return fail(ctx, RK_ENONFINITE, "bias must be finite");
+        hb[(size_t)m * ctx->Cp + c] = b;
+      }
+    CK(cudaMalloc(&ctx->d_bias, wrows * 4));
+    CK(cudaMemcpy(ctx->d_bias, hb.data(), wrows * 4, cudaMemcpyHostToDevice));
+  }
+  ctx->loaded = true;
+  ctx->have_batch = false;
+  ctx->reset_done = false;
+  return RK_OK;
+}
+
+rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
+  if (N < 0 || goff < 0 || (N > 0 && !X)) return fail(ctx, RK_EINVAL, "bad X / N / offset");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  rk_status s;
+  if ((s = ensure(ctx, &ctx->ws_logits, &ctx->ws_cap, std::max<int64_t>(N, 1) * ctx->K * ctx->ldc)) != RK_OK) return s;
+  if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
+  if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
+  const void* Xd = X;
+  if (N > 0 && !is_device_ptr(X)) {
+    if ((s = ensure(ctx, &ctx->ws_x, &ctx->ws_x_cap, N * ctx->D)) != RK_OK) return s;
+    CK(cudaMemcpyAsync(ctx->ws_x, X, (size_t)N * ctx->D * 2, cudaMemcpyHostToDevice, st));
+    Xd = ctx->ws_x;
+  }
+  ctx->cur_logits = ctx->ws_logits;
+  ctx->cur_ldc = ctx->ldc;
+  ctx->cur_N = N;
+  ctx->cur_off = goff;
+  ctx->batch_stats = true;
+  ctx->have_batch = true;
+  if (N == 0) return RK_OK;
+  GemmParams gp{};
+  gp.N = N; gp.K = ctx->K; gp.C = ctx->C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
+  gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias; gp.top1 = ctx->ws_top1; gp.lse = ctx->ws_lse;
+  gp.logits = ctx->ws_logits;
+  int rc = gemm_build_tmaps(gp, Xd, ctx->d_W, ctx->ws_logits, ctx->tmaps);
+  if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
+  const double flops = 2.0 * N * ctx->D * (double)ctx->K * ctx->C;
+  {
+    ProfScope ps(ctx, KK_GEMM, st, (double)N * ctx->D * 2 + (double)N * ctx->K * ctx->C * 4, flops);
+    CK(launch_gemm(gp, ctx->sm_count, st));
+  }
+  return RK_OK;
+}
+
+rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, int64_t goff, void* stream) {
+  (void)stream;
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
+  if (N < 0 || goff < 0 || ldc < ctx->C || ldc % 4 != 0) return fail(ctx, RK_EINVAL, "bad ldc / N / offset (ldc % 4 == 0, ldc >= C)");
+  if (N > 0 && (!logits || (reinterpret_cast<uintptr_t>(logits) & 15))) return fail(ctx, RK_EINVAL, "logits must be 16-byte aligned");
+  if (N > 0 && !is_device_ptr(logits)) return fail(ctx, RK_EINVAL, "logits must be device memory");
+  ctx->cur_logits = logits;
+  ctx->cur_ldc = ldc;
+  ctx->cur_N = N;
+  ctx->cur_off = goff;
+  ctx->batch_stats = false;
+  ctx->have_batch = true;
+  return RK_OK;
+}
+
+rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
+  CK(cudaSetDevice(ctx->dev));
+  const int K = ctx->K, S = ctx->S;
+  ctx->has_cfg = cfg != nullptr;
+  ctx->nB = ctx->nR = ctx->want_exceed = ctx->want_labelled = 0;
+  ctx->L = 1;
+  ctx->gs = 0;
+  ctx->arrival_user = nullptr;
+  ctx->beta = 0; ctx->tau = 0;
+  if (cfg) {
+    if (cfg->nB < 0 || cfg->nB > kMaxB || (cfg->nB > 0 && (!cfg->B || !cfg->lat_ns))) return fail(ctx, RK_EINVAL, "nB in [0,8] with B and lat_ns");
+    if (cfg->arrival_ns && cfg->nR != 1) return fail(ctx, RK_EINVAL, "arrival_ns requires nR == 1");
+    if (cfg->nR < 0 || cfg->nR > kMaxR || (cfg->nR > 0 && !cfg->rates && !cfg->arrival_ns)) return fail(ctx, RK_EINVAL, "nR in [0,8] with rates");
+    if (cfg->tau_ns < 0 || !(cfg->beta == cfg->beta)) return fail(ctx, RK_EINVAL, "tau >= 0, finite beta");
+    ctx->nB = cfg->nB;
+    ctx->nR = cfg->nB > 0 ? cfg->nR : 0;
+    ctx->beta = cfg->beta;
+    ctx->tau = cfg->tau_ns;
+    ctx->want_exceed = cfg->want_exceed ? 1 : 0;
+    ctx->want_labelled = cfg->want_labelled ? 1 : 0;
+    ctx->arrival_user = cfg->arrival_ns;
+    int64_t g = 0;
+    for (int i = 0; i < cfg->nB; ++i) {
+      if (cfg->B[i] < 1 || cfg->B[i] > 4096) return fail(ctx, RK_EINVAL, "batch sizes in [1,4096]");
+      ctx->B[i] = cfg->B[i];
+      ctx->L = ctx->L / gcd64(ctx->L, cfg->B[i]) * cfg->B[i];
+      g = gcd64(g, cfg->B[i]);
+      if (ctx->L > 4096) return fail(ctx, RK_EINVAL, "lcm(B) must be <= 4096");
+      for (int m = 0; m < K; ++m) {
+        if (cfg->lat_ns[m * cfg->nB + i] < 0) return fail(ctx, RK_EINVAL, "latencies must be >= 0");
+        ctx->lat[m * cfg->nB + i] = cfg->lat_ns[m * cfg->nB + i];
+      }
+    }
+    for (int r = 0; r < ctx->nR; ++r) {
+      const double rt = cfg->arrival_ns ? 1.0 : cfg->rates[r];
+      if (!(rt > 0) || rt > 1e12) return fail(ctx, RK_EINVAL, "rates must be > 0");
+      ctx->rates[r] = rt;
+    }
+    if (g > 0) {
+      int gs = 1;
+      while (gs < 16 && g % (gs * 2) == 0) gs *= 2;
+      ctx->gs = gs;
+    }
+  }
+  const int nB = ctx->nB, nR = ctx->nR;
+  // table layout (u64 words): N, err[3], vote[S], avg[S], rc[S], corr[nB][S], O, Q, E [nR][nB][S]
+  ctx->off_N = 0; ctx->off_err = 1;
+  ctx->off_vote = 4;
+  ctx->off_avg = ctx->off_vote + S;
+  ctx->off_rc = ctx->off_avg + S;
+  ctx->off_corr = ctx->off_rc + S;
+  ctx->off_O = ctx->off_corr + (int64_t)nB * S;
+  ctx->off_Q = ctx->off_O + (int64_t)nR * nB * S;
+  ctx->off_E = ctx->off_Q + (int64_t)nR * nB * S;
+  const size_t words = (size_t)(ctx->off_E + (int64_t)nR * nB * S);
+  if (ctx->table_words < words) {
+    if (ctx->d_table) cudaFree(ctx->d_table);
+    ctx->d_table = nullptr;
+    CK(cudaMalloc(&ctx->d_table, words * 8));
+    ctx->table_words = words;
+  }
+  CK(cudaMemset(ctx->d_table, 0, ctx->table_words * 8));
+  // chunk counters: vote, avg, rc [S], tail [nB][S], osum, esum [nR][nB][K], err (4 x u32 = 2 words)
+  const size_t cw = 3 * (size_t)S + (size_t)nB * S + 2 * (size_t)nR * nB * K + 2;
+  if (ctx->chunk_words < cw) {
+    if (ctx->d_chunk) cudaFree(ctx->d_chunk);
+    ctx->d_chunk = nullptr;
+    CK(cudaMalloc(&ctx->d_chunk, cw * 8));
+    ctx->chunk_words = cw;
+  }
+  // slowest member of each subset at each batch size (PAPER.md:410 stragglers)
+  if (nB > 0) {
+    std::vector<uint8_t> slow((size_t)nB * S);
+    for (int bi = 0; bi < nB; ++bi)
+      for (uint32_t v = 1; v <= (uint32_t)S; ++v) {
+        int sm = -1;
+        for (int m = 0; m < K; ++m)
+          if (((v >> m) & 1u) && (sm < 0 || ctx->lat[m * nB + bi] > ctx->lat[sm * nB + bi])) sm = m;
+        slow[(size_t)bi * S + v - 1] = (uint8_t)sm;
+      }
+    if (ctx->d_slow) cudaFree(ctx->d_slow);
+    CK(cudaMalloc(&ctx->d_slow, slow.size()));
+    CK(cudaMemcpy(ctx->d_slow, slow.data(), slow.size(), cudaMemcpyHostToDevice));
+  }
+  if (ctx->want_labelled && nB > 0 && nR > 0) {
+    int tot = 0;
+    for (int bi = 0; bi < nB; ++bi) tot += (int)(ctx->L / ctx->B[bi]);
+    if ((size_t)tot * nR * K * 2 > 48 * 1024)
+      return fail(ctx, RK_EUNSUPPORTED, "labelled moments: lcm(B)/b * nR * K too large");
+  }
+  ctx->reset_done = true;
+  ctx->final_seen = false;
+  ctx->chunks = 0;
+  return RK_OK;
+}
+
+rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->reset_done) return fail(ctx, RK_ESTATE, "rk_subset_reset first");
+  if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "rk_score / rk_score_logits first");
+  const int64_t N = ctx->cur_N;
+  if (N > 0 && !labels) return fail(ctx, RK_EINVAL, "labels required");
+  if (ctx->final_seen && N > 0) return fail(ctx, RK_EINVAL, "a ragged chunk must be the last one (chunks are multiples of lcm(B))");
+  if (ctx->cur_off % ctx->L != 0) return fail(ctx, RK_EINVAL, "chunk offset must be a multiple of lcm(B)");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int K = ctx->K, S = ctx->S, nB = ctx->nB, nR = ctx->nR, C = ctx->C;
+  rk_status s;
+  CK(cudaMemsetAsync(ctx->d_chunk, 0, ctx->chunk_words * 8, st));
+  if (N > 0) {
+    const int32_t* dl = labels;
+    if (!is_device_ptr(labels)) {
+      if ((s = ensure(ctx, &ctx->d_labels, &ctx->labels_cap, N)) != RK_OK) return s;
+      CK(cudaMemcpyAsync(ctx->d_labels, labels, N * 4, cudaMemcpyHostToDevice, st));
+      dl = ctx->d_labels;
+    }
+    unsigned long long* ch = ctx->d_chunk;
+    unsigned int* errp = reinterpret_cast<unsigned int*>(ch + 3 * (size_t)S + (size_t)nB * S + 2 * (size_t)nR * nB * K);
+    // ---- A2-A5: vote / average / counts ----
+    if (ctx->cur_ldc > kMaxCFast) return fail(ctx, RK_EUNSUPPORTED, "ldc > 1024 not supported by this build's vote kernel");
+    VoteParams vp{};
+    vp.logits = ctx->cur_logits; vp.ldc = ctx->cur_ldc;
+    vp.lse_in = ctx->batch_stats ? ctx->ws_lse : nullptr;
+    vp.top1_in = ctx->batch_stats ? ctx->ws_top1 : nullptr;
+    vp.labels = dl; vp.N = N; vp.K = K; vp.C = C; vp.S = S; vp.tie = ctx->tie;
+    const int gs = (ctx->want_labelled && nB > 0 && nR > 0) ? ctx->gs : 0;
+    VoteLayout L = choose_vote_layout(K, C, (int)ctx->cur_ldc, gs, ctx->sm_count);
+    vp.LPR = L.LPR; vp.VPL = L.VPL; vp.RS = L.RS; vp.G = L.G;
+    vp.gs = gs;
+    vp.U = std::max(L.G, gs);
+    vp.nW32 = (C + 31) / 32;
+    vp.K1 = K / 2;
+    vp.CAP = 128;
+    {
+      const int TT = (1 << vp.K1) + (1 << (K - vp.K1));
+      int tcap = (int)(32768 / (4 * (size_t)TT * L.G));
+      vp.TCAP = std::max(0, std::min(tcap, vp.CAP));
+    }
+    vp.band = 2e-5f;
+    vp.best_of = ctx->d_best_of;
+    vp.nB = nB;
+    for (int bi = 0; bi < nB; ++bi) vp.tail_start[bi] = (N / ctx->B[bi]) * ctx->B[bi];
+    vp.cnt_vote = ch; vp.cnt_avg = ch + S; vp.n_recheck = ch + 2 * S; vp.tail = ch + 3 * S;
+    vp.err = errp;
+    if (gs > 0) {
+      const size_t need = (size_t)((N + gs - 1) / gs) * S;
+      if (ctx->grp_cap < need) {
+        if (ctx->d_grp) cudaFree(ctx->d_grp);
+        ctx->d_grp = nullptr;
+        CK(cudaMalloc(&ctx->d_grp, need));
+        ctx->grp_cap = need;
+      }
+      vp.grp = ctx->d_grp;
+    }
+    L.smem = vote_smem_bytes(vp);
+    int occ = 0;
+    // grid: as many persistent CTAs as fit (>= 1 per SM), never more than units
+    {
+      const int64_t units = (N + vp.U - 1) / vp.U;
+      int per_sm = L.smem <= 100 * 1024 ? 2 : 1;
+      (void)occ;
+      L.grid = (int)std::min<int64_t>(units, (int64_t)ctx->sm_count * per_sm);
+    }
+    const size_t sf = (size_t)L.grid * L.G * C * K, si = (size_t)L.grid * L.G * C;
+    if (ctx->scratch_floats < sf) {
+      if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+      ctx->d_scratch = nullptr;
+      CK(cudaMalloc(&ctx->d_scratch, sf * 4));
+      ctx->scratch_floats = sf;
+    }
+    if (ctx->scratch_ints < si) {
+      if (ctx->d_scratch_cls) cudaFree(ctx->d_scratch_cls);
+      ctx->d_scratch_cls = nullptr;
+      CK(cudaMalloc(&ctx->d_scratch_cls, si * 4));
+      ctx->scratch_ints = si;
+    }
+    vp.scratch = ctx->d_scratch;
+    vp.scratch_cls = ctx->d_scratch_cls;
+    {
+      const double bytes = (double)N * ((double)K * C * 4 + 4);
+      ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
+      CK(launch_vote(vp, L, st));
+    }
+    // ---- A5: batch latency moments (label independent) ----
+    const int64_t* arr = nullptr;
+    if (nB > 0 && nR > 0) {
+      if (ctx->arrival_user) {
+        if (is_device_ptr(ctx->arrival_user)) arr = ctx->arrival_user;
+        else {
+          if ((s = ensure(ctx, &ctx->d_arr, &ctx->arr_cap, N)) != RK_OK) return s;
+          CK(cudaMemcpyAsync(ctx->d_arr, ctx->arrival_user, N * 8, cudaMemcpyHostToDevice, st));
+          arr = ctx->d_arr;
+        }
+      }
+      MomentParams mp{};
+      mp.K = K; mp.S = S; mp.nB = nB; mp.nR = nR;
+      for (int bi = 0; bi < nB; ++bi) mp.B[bi] = ctx->B[bi];
+      memcpy(mp.lat, ctx->lat, sizeof(mp.lat));
+      memcpy(mp.rates, ctx->rates, sizeof(mp.rates));
+      mp.arrival = arr; mp.tau = ctx->tau; mp.goff = ctx->cur_off; mp.N = N; mp.want_exceed = ctx->want_exceed;
+      mp.osum = ch + 3 * (size_t)S + (size_t)nB * S;
+      mp.esum = mp.osum + (size_t)nR * nB * K;
+      ProfScope ps(ctx, KK_OVERDUE, st, 0, 0);
+      CK(launch_overdue(mp, st));
+    }
+    // ---- merge chunk counters into the table ----
+    MergeParams gp{};
+    gp.S = S; gp.nB = nB; gp.nR = nR; gp.K = K; gp.chunk = ch; gp.slow = ctx->d_slow; gp.table = ctx->d_table;
+    gp.off_vote = ctx->off_vote; gp.off_avg = ctx->off_avg; gp.off_rc = ctx->off_rc; gp.off_corr = ctx->off_corr;
+    gp.off_O = ctx->off_O; gp.off_E = ctx->off_E; gp.want_exceed = ctx->want_exceed;
+    gp.err = errp; gp.off_err = ctx->off_err;
+    {
+      ProfScope ps(ctx, KK_MERGE, st, 0, 0);
+      CK(launch_merge(gp, N, ctx->off_N, st));
+    }
+    // ---- labelled moments ----
+    if (gs > 0) {
+      QParams qp{};
+      qp.K = K; qp.S = S; qp.nB = nB; qp.nR = nR; qp.gs = gs;
+      for (int bi = 0; bi < nB; ++bi) qp.B[bi] = ctx->B[bi];
+      memcpy(qp.lat, ctx->lat, sizeof(qp.lat));
+      memcpy(qp.rates, ctx->rates, sizeof(qp.rates));
+      qp.arrival = arr; qp.tau = ctx->tau; qp.goff = ctx->cur_off; qp.N = N; qp.L = ctx->L;
+      qp.grp = ctx->d_grp; qp.slow = ctx->d_slow; qp.Q = ctx->d_table + ctx->off_Q;
+      ProfScope ps(ctx, KK_Q, st, 0, 0);
+      CK(launch_q(qp, st));
+    }
+  }
+  if (N % ctx->L != 0) ctx->final_seen = true;
+  ctx->chunks++;
+  return RK_OK;
+}
+
+rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->reset_done) return fail(ctx, RK_ESTATE, "rk_subset_reset first");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = ctx->S, nB = ctx->nB, nR = ctx->nR;
+  // A6: one all-reduce of the whole integer table (order-free, bit-exact)
+  if (ctx->world > 1) {
+    ProfScope ps(ctx, KK_ALLREDUCE, st, (double)ctx->table_words * 8, 0);
+    if (ncclAllReduce(ctx->d_table, ctx->d_table, ctx->table_words, ncclUint64, ncclSum, ctx->comm, st) != ncclSuccess)
+      return fail(ctx, RK_ENCCL, "ncclAllReduce failed");
+  }
+  // A7: reward fold on the device
+  const size_t nrew = (size_t)nR * nB * S;
+  if (nrew > 0) {
+    if (ctx->rew_cap < 2 * nrew) {
+      if (ctx->d_rew) cudaFree(ctx->d_rew);
+      ctx->d_rew = nullptr;
+      CK(cudaMalloc(&ctx->d_rew, 2 * nrew * 8));
+      ctx->rew_cap = 2 * nrew;
+    }
+    FoldParams fp{};
+    fp.S = S; fp.nB = nB; fp.nR = nR;
+    for (int bi = 0; bi < nB; ++bi) fp.B[bi] = ctx->B[bi];
+    fp.beta = ctx->beta; fp.table = ctx->d_table;
+    fp.off_vote = ctx->off_vote; fp.off_corr = ctx->off_corr; fp.off_O = ctx->off_O; fp.off_Q = ctx->off_Q;
+    fp.off_N = ctx->off_N; fp.has_Q = ctx->want_labelled;
+    fp.reward_sur = ctx->d_rew; fp.reward_lab = ctx->d_rew + nrew;
+    ProfScope ps(ctx, KK_FOLD, st, 0, 0);
+    CK(launch_fold(fp, st));
+  }
+  std::vector<unsigned long long> h(ctx->table_words);
+  CK(cudaMemcpyAsync(h.data(), ctx->d_table, ctx->table_words * 8, cudaMemcpyDeviceToHost, st));
+  std::vector<double> rew(2 * nrew);
+  if (nrew) CK(cudaMemcpyAsync(rew.data(), ctx->d_rew, 2 * nrew * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  rk_status status = RK_OK;
+  if (h[ctx->off_err + 0]) status = fail(ctx, RK_ENONFINITE, "non-finite logits (NaN, +inf or an all -inf row)");
+  else if (h[ctx->off_err + 1]) status = fail(ctx, RK_ELABEL, "label outside [0, C)");
+  else if (h[ctx->off_err + 2]) status = fail(ctx, RK_EINVAL, "arrival_ns not non-decreasing inside a batch");
+  if (status != RK_OK) {
+    std::fill(h.begin(), h.end(), 0ull);
+    std::fill(rew.begin(), rew.end(), 0.0);
+  }
+  if (out) {
+    out->N = (int64_t)h[ctx->off_N];
+    auto cp = [&](uint64_t* dst, int64_t off, size_t n) { if (dst && n) memcpy(dst, h.data() + off, n * 8); };
+    cp(out->cnt_vote, ctx->off_vote, S);
+    cp(out->cnt_avg, ctx->off_avg, S);
+    cp(out->n_recheck, ctx->off_rc, S);
+    cp(out->corr, ctx->off_corr, (size_t)nB * S);
+    cp(out->O, ctx->off_O, nrew);
+    cp(out->Q, ctx->off_Q, ctx->want_labelled ? nrew : 0);
+    cp(out->E, ctx->off_E, ctx->want_exceed ? nrew : 0);
+    if (out->reward_sur && nrew) memcpy(out->reward_sur, rew.data(), nrew * 8);
+    if (out->reward_lab && nrew) memcpy(out->reward_lab, rew.data() + nrew, nrew * 8);
+  }
+  return status;
+}
+
+rk_status rk_subset_stats(rk_ctx* ctx, const int32_t* labels, const rk_reward_cfg* cfg, rk_table* out, void* stream) {
+  rk_status s = rk_subset_reset(ctx, cfg);
+  if (s != RK_OK) return s;
+  if ((s = rk_subset_accumulate(ctx, labels, stream)) != RK_OK) return s;
+  return rk_subset_finalize(ctx, out, stream);
+}
+
+rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_avg, float* avgprob, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "rk_score / rk_score_logits first");
+  if (v == 0 || v >= (1u << ctx->K)) return fail(ctx, RK_EINVAL, "v must be in [1, 2^K) (PAPER.md:429 excludes v = 0)");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  PredictParams pp{};
+  pp.logits = ctx->cur_logits; pp.ldc = ctx->cur_ldc; pp.lse_in = ctx->batch_stats ? ctx->ws_lse : nullptr;
+  pp.N = ctx->cur_N; pp.K = ctx->K; pp.C = ctx->C; pp.tie = ctx->tie; pp.v = v; pp.best_of = ctx->d_best_of;
+  pp.pred_vote = pred_vote; pp.pred_avg = pred_avg; pp.avgprob = avgprob;
+  ProfScope ps(ctx, KK_PREDICT, st, 0, 0);
+  CK(launch_predict(pp, st));
+  return RK_OK;
+}
+
+rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** lse, int64_t* N) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "no batch scored yet");
+  if (logits) *logits = ctx->cur_logits;
+  if (ldc) *ldc = (int)ctx->cur_ldc;
+  if (top1) *top1 = ctx->batch_stats ? ctx->ws_top1 : nullptr;
+  if (lse) *lse = ctx->batch_stats ? ctx->ws_lse : nullptr;
+  if (N) *N = ctx->cur_N;
+  return RK_OK;
+}
+
+rk_status rk_set_profiling(rk_ctx* ctx, int on) {
+  if (!ctx) return RK_EINVAL;
+  prof_collect(ctx);
+  ctx->prof.on = on != 0;
+  if (on) {
+    for (int k = 0; k < KK_COUNT; ++k) { ctx->prof.launches[k] = 0; ctx->prof.ms[k] = 0; ctx->prof.bytes[k] = 0; ctx->prof.flops[k] = 0; }
+  }
+  return RK_OK;
+}
+
+rk_status rk_kernel_stats(rk_ctx* ctx, rk_kernel_stat* out, int max, int* n) {
+  if (!ctx) return RK_EINVAL;
+  prof_collect(ctx);
+  if (n) *n = KK_COUNT;
+  for (int k = 0; k < KK_COUNT && k < max; ++k) {
+    out[k].name = kKernelNames[k];
+    out[k].launches = ctx->prof.launches[k];
+    out[k].total_ms = ctx->prof.ms[k];
+    out[k].bytes = ctx->prof.bytes[k];
+    out[k].flops = ctx->prof.flops[k];
+  }
+  return RK_OK;
+}
+
+}  // extern "C"

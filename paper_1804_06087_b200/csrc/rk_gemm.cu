@@ -1,0 +1,381 @@
+// rk_gemm.cu — step A1 (+A2 fused): K synthetic dense classifier heads on the 5th-generation
+// tensor cores, with the per-(row, model) softmax normaliser and top-1 fused in the epilogue.
+//
+//   logit[n][m][c] = 2^s * sum_d X[n][d] * W[m][c][d] + bias[m][c]
+//   top1[n][m]     = lowest c attaining max_c logit          (reading Q4)
+//   lse[n][m]      = log sum_c exp(logit[n][m][c])           (softmax normaliser)
+// The heads stand in for the classifier layer of the paper's ConvNets (the
+// inference time "depends on the model complexity, hardware efficiency ... and the batch size",
+// PAPER.md:361).
+//
+// sm_100a design:
+//   * persistent, one CTA per SM, 6 warps: warp 0 = TMA producer, warp 1 = tcgen05.mma issuer and
+//     TMEM owner, warps 2-5 = epilogue (TMEM lane quarter = warp % 4).
+//   * tile 128 rows x up to 256 columns of ONE model, K-block 64 (128-byte swizzle), 4-stage
+//     smem ring fed by TMA (cp.async.bulk.tensor + mbarrier complete_tx).
+//   * fp32 accumulators in TMEM, double-buffered (2 x 256 columns) so the epilogue of tile i
+//     overlaps the MMAs of tile i+1.
+//   * a work unit is (128-row block, model): the CTA walks the model's column tiles in ascending
+//     order, so the epilogue keeps an ONLINE max / lowest-index argmax / rescaled sum-exp per row
+//     in registers and writes top1/lse once per unit; logits leave through swizzled smem staging
+//     and TMA bulk tensor stores (rows >= N and columns >= C are clipped by the tensor map).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "rk_internal.h"
+
+namespace rk {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, NS = 4;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BYTES = BN * BK * 2;   // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EPI_WARPS = 4;
+constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging box
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + NS * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: kind::f16, A/B = BF16, D = F32, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t umma_idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+#pragma unroll
+  for (int i = 16; i < 32; ++i) v[i] = -INFINITY;
+}
+
+struct GemmArgs {
+  int64_t N;
+  int K, C, Cp, D, nt, scale_log2;
+  const float* bias;
+  int32_t* top1;
+  float* lse;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_heads_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                      const __grid_constant__ CUtensorMap tmo, const GemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  uint8_t* staging = smem + NS * STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + EPI_WARPS * 2 * STG_BYTES);
+  uint64_t* full = bars;            // [NS]
+  uint64_t* empty = bars + NS;      // [NS]
+  uint64_t* tfull = bars + 2 * NS;  // [2]
+  uint64_t* tempty = bars + 2 * NS + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t mtiles = (a.N + BM - 1) / BM;
+  const int64_t units = mtiles * a.K;
+  const int kblocks = a.D / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmx) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmw) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmo) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int mt = (int)(u / a.K), model = (int)(u % a.K);
+        for (int j = 0; j < a.nt; ++j) {
+          const int col0 = model * a.Cp + j * BN;
+          for (int kb = 0; kb < kblocks; ++kb, ++it) {
+            const int s = it % NS;
+            const uint32_t ph = (it / NS) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* sa = stages + s * STAGE_BYTES;
+            uint8_t* sb = sa + A_BYTES;
+            mbar_expect_tx(&full[s], STAGE_BYTES);
+            tma_load_2d(sa, &tmx, &full[s], kb * BK, mt * BM);
+            tma_load_2d(sb, &tmw, &full[s], kb * BK, col0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      uint32_t it = 0, tc = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int j = 0; j < a.nt; ++j, ++tc) {
+          const int width = min(BN, a.Cp - j * BN);
+          const uint32_t idesc = umma_idesc(width);
+          const uint32_t as = tc & 1;
+          mbar_wait(&tempty[as], ((tc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t dtm = tmem_base + as * BN;
+          for (int kb = 0; kb < kblocks; ++kb, ++it) {
+            const int s = it % NS;
+            mbar_wait(&full[s], (it / NS) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(stages + s * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              // advance 16 bf16 = 32 bytes inside the 128-byte swizzle atom
+              umma_bf16(dtm, umma_desc(sa + k * 32), umma_desc(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
+            }
+            umma_commit(&empty[s]);  // smem slot reusable once these MMAs complete
+          }
+          umma_commit(&tfull[as]);  // accumulator ready for the epilogue
+        }
+      }
+    }
+  } else {
+    // ===== epilogue: TMEM -> registers -> (stats, swizzled smem) -> TMA store =====
+    const int q = warp & 3;  // TMEM lane quarter accessible by this warp
+    const int row_in_tile = q * 32 + lane;
+    uint8_t* stg = staging + (warp - 2) * 2 * STG_BYTES;
+    const float scale = ldexpf(1.0f, a.scale_log2);
+    uint32_t tc = 0, nstore = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int mt = (int)(u / a.K), model = (int)(u % a.K);
+      const int64_t row = (int64_t)mt * BM + row_in_tile;
+      float mx = -INFINITY, sum = 0.f;
+      int arg = 0;
+      for (int j = 0; j < a.nt; ++j, ++tc) {
+        const int width = min(BN, a.Cp - j * BN);
+        const uint32_t as = tc & 1;
+        mbar_wait(&tfull[as], (tc >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+        for (int c0 = 0; c0 < width; c0 += 32) {
+          float v[32];
+          if (width - c0 >= 32) tmem_ld32(tbase + c0, v);
+          else tmem_ld16(tbase + c0, v);
+          const int colbase = j * BN + c0;  // column inside the model
+          const float* bptr = a.bias + (size_t)model * a.Cp + colbase;
+          float cmax = -INFINITY;
+          int carg = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float b = (colbase + i < a.Cp) ? __ldg(bptr + i) : -INFINITY;
+            v[i] = fmaf(v[i], scale, b);  // scale is a power of two: exact product, one rounding
+            if (v[i] > cmax) { cmax = v[i]; carg = colbase + i; }
+          }
+          if (cmax > mx) {
+            sum = sum * __expf(mx - cmax);
+            mx = cmax;
+            arg = carg;
+          }
+          if (mx != -INFINITY) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum += __expf(v[i] - mx);
+          }
+          // stage 32 rows x 32 cols (128B-swizzled) and store with TMA
+          uint8_t* buf = stg + (nstore & 1) * STG_BYTES;
+          if (lane == 0 && nstore >= 2) tma_store_wait_read1();
+          __syncwarp();
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const int phys = c4 ^ (lane & 7);
+            float4 w4 = make_float4(v[c4 * 4], v[c4 * 4 + 1], v[c4 * 4 + 2], v[c4 * 4 + 3]);
+            *reinterpret_cast<float4*>(buf + lane * 128 + phys * 16) = w4;
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmo, buf, colbase, model, (int)(mt * BM + q * 32));
+            tma_store_commit();
+          }
+          ++nstore;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[as]);
+      }
+      if (row < a.N) {
+        a.top1[row * a.K + model] = arg;
+        a.lse[row * a.K + model] = mx + logf(sum);
+      }
+    }
+    if (lane == 0) tma_store_wait_all();
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+// ---- host: tensor maps through the driver entry point (no libcuda link dependency) -------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits, void* storage) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return -1;
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(storage);
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)p.D, (cuuint64_t)p.N};
+    cuuint64_t strides[1] = {(cuuint64_t)p.D * 2};
+    cuuint32_t box[2] = {BK, BM};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&maps[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -2;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)p.D, (cuuint64_t)p.K * p.Cp};
+    cuuint64_t strides[1] = {(cuuint64_t)p.D * 2};
+    cuuint32_t box[2] = {BK, BN};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&maps[1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(W), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -3;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)p.C, (cuuint64_t)p.K, (cuuint64_t)p.N};
+    cuuint64_t strides[2] = {(cuuint64_t)p.ldc * 4, (cuuint64_t)p.K * p.ldc * 4};
+    cuuint32_t box[3] = {32, 1, 32};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&maps[2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, logits, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -4;
+  }
+  p.tmap_x = &maps[0];
+  p.tmap_w = &maps[1];
+  p.tmap_out = &maps[2];
+  return 0;
+}
+
+cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
+  if (p.N <= 0) return cudaSuccess;
+  GemmArgs a;
+  a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D; a.nt = (p.Cp + BN - 1) / BN;
+  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lse = p.lse;
+  cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int64_t units = ((p.N + BM - 1) / BM) * p.K;
+  const int grid = (int)(units < sm_count ? units : sm_count);
+  gemm_heads_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(*reinterpret_cast<const CUtensorMap*>(p.tmap_x),
+                                                      *reinterpret_cast<const CUtensorMap*>(p.tmap_w),
+                                                      *reinterpret_cast<const CUtensorMap*>(p.tmap_out), a);
+  return cudaGetLastError();
+}
+
+}  // namespace rk

@@ -1,0 +1,140 @@
+// rk_internal.h — structures shared between the host orchestration (rk_api.cpp) and the
+// CUDA kernels of librk.so. Not part of the public ABI (include/rk.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rk {
+
+constexpr int kMaxK = 12;
+constexpr int kMaxB = 8;
+constexpr int kMaxR = 8;
+constexpr int kVoteThreads = 256;   // vote kernel block size (8 warps)
+constexpr int kMaxCFast = 1024;     // register-resident rows up to ldc <= 1024 (8 float4 / lane)
+
+// ---- vote / average / subset-count kernel (steps A2-A5) --------------------------------------
+struct VoteParams {
+  const float* logits;       // [N][K][ldc]
+  int64_t ldc;
+  const float* lse_in;       // [N][K] or null (then computed here)
+  const int32_t* top1_in;    // [N][K] or null
+  const int32_t* labels;     // [N] device
+  int64_t N;                 // samples in this chunk
+  int K, C, S, tie;
+  // thread <-> data mapping (host heuristic, see choose_vote_layout)
+  int LPR;                   // lanes per row (power of 2, <= 32)
+  int VPL;                   // float4 per lane per row slot
+  int RS;                    // rows per pass = 256 / LPR
+  int G;                     // samples per tile (power of 2)
+  int gs;                    // samples per count group (power of 2 dividing gcd(B)); 0 = no groups
+  int U;                     // samples per unit = max(G, gs)
+  int nW32;                  // ceil(C / 32) candidate-bitmap words
+  int CAP;                   // candidate capacity (P matrix in smem)
+  int TCAP;                  // candidate capacity of the subset-sum tables in smem
+  int K1;                    // low half of the models for the subset-sum tables
+  float band;                // relative fp32 near-tie band -> fp64 recheck
+  const uint8_t* best_of;    // [2^K] best-ranked model in a mask (device)
+  int nB;
+  int64_t tail_start[kMaxB]; // local sample index from which a sample is in the tail of B[b]
+  // outputs (device)
+  unsigned long long* cnt_vote;   // [S]
+  unsigned long long* cnt_avg;    // [S]
+  unsigned long long* n_recheck;  // [S]
+  unsigned long long* tail;       // [nB][S]
+  uint8_t* grp;                   // [ceil(N/gs)][S] or null
+  float* scratch;                 // per-CTA overflow P [gridDim][G][C][K]
+  int32_t* scratch_cls;           // per-CTA overflow class list [gridDim][G][C]
+  unsigned int* err;              // [0] non-finite logits, [1] bad label
+};
+
+struct VoteLayout {
+  int LPR, VPL, RP, RS, G, NV;
+  size_t smem;
+  int grid;
+};
+
+VoteLayout choose_vote_layout(int K, int C, int ldc, int gs, int sm_count);
+size_t vote_smem_bytes(const VoteParams& p);
+cudaError_t launch_vote(const VoteParams& p, const VoteLayout& L, cudaStream_t st);
+
+// ---- per-sample predictions for one action v (rk_predict) ---------------------------------------
+struct PredictParams {
+  const float* logits; int64_t ldc;
+  const float* lse_in;
+  int64_t N; int K, C, tie; uint32_t v;
+  const uint8_t* best_of;
+  int32_t* pred_vote; int32_t* pred_avg; float* avgprob;
+  unsigned int* err;
+};
+cudaError_t launch_predict(const PredictParams& p, cudaStream_t st);
+
+// ---- batch moments, merge and reward fold (A5 tail, A7) ----------------------------------------
+struct MomentParams {
+  int K, S, nB, nR;
+  int B[kMaxB];
+  int64_t lat[kMaxK * kMaxB];     // [K][nB]
+  double rates[kMaxR];
+  const int64_t* arrival;         // [N] device or null
+  int64_t tau, goff, N;           // chunk
+  int want_exceed;
+  unsigned long long* osum;       // [nR][nB][K] overdue counts per slowest model
+  unsigned long long* esum;       // [nR][nB][K]
+};
+cudaError_t launch_overdue(const MomentParams& p, cudaStream_t st);  // err flags follow esum
+
+struct QParams {
+  int K, S, nB, nR, gs;
+  int B[kMaxB];
+  int64_t lat[kMaxK * kMaxB];
+  double rates[kMaxR];
+  const int64_t* arrival;
+  int64_t tau, goff, N, L;        // L = lcm(B)
+  const uint8_t* grp;             // [ceil(N/gs)][S]
+  const uint8_t* slow;            // [nB][S] slowest member of v at batch size b
+  unsigned long long* Q;          // [nR][nB][S] (table section)
+};
+cudaError_t launch_q(const QParams& p, cudaStream_t st);
+
+struct MergeParams {
+  int S, nB, nR;
+  const unsigned long long* chunk;  // chunk counters: vote[S], avg[S], rc[S], tail[nB][S], osum, esum
+  const uint8_t* slow;              // [nB][S]
+  int K;
+  unsigned long long* table;        // table sections
+  int64_t off_vote, off_avg, off_rc, off_corr, off_O, off_E;
+  int want_exceed;
+  const unsigned int* err;          // chunk error flags [3] -> table words off_err..off_err+2
+  int64_t off_err;
+};
+cudaError_t launch_merge(const MergeParams& p, int64_t N, int64_t off_N, cudaStream_t st);
+
+struct FoldParams {
+  int S, nB, nR;
+  int B[kMaxB];
+  double beta;
+  const unsigned long long* table;
+  int64_t off_vote, off_corr, off_O, off_Q, off_N;
+  int has_Q;
+  double* reward_sur;  // [nR][nB][S]
+  double* reward_lab;
+};
+cudaError_t launch_fold(const FoldParams& p, cudaStream_t st);
+
+// ---- GEMM (A1) -----------------------------------------------------------------------------------
+struct GemmParams {
+  const void* tmap_x;    // CUtensorMap* (host copy passed by value via __grid_constant__)
+  const void* tmap_w;
+  const void* tmap_out;
+  int64_t N;             // rows
+  int K, C, Cp, D, ldc;  // Cp = per-model padded columns (multiple of 16)
+  int scale_log2;
+  const float* bias;     // [K][Cp] (-inf on padding columns)
+  int32_t* top1;         // [N][K]
+  float* lse;            // [N][K]
+  float* logits;         // [N][K][ldc]
+  unsigned int* err;
+};
+cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st);
+int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits, void* storage /*3*128B*/);
+
+}  // namespace rk

@@ -1,0 +1,108 @@
+"""GPU parity of the tcgen05 head GEMM (rk_score, A1+A2) and of the end-to-end path.
+
+P3: integer-exact mode (X, W in {-1,0,1}, integer bias, scale 2^-k): logits bit-exact, hence votes
+and counts bit-exact end to end. P4: real-valued bf16 mode: |dlogit| <= c * D * 2^-24 * sum|x*w|.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from gpu_helpers import compare_tables, default_cfg
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def rk():
+    import paper_1804_06087_b200 as m
+    m.load_library()
+    return m
+
+
+def make(K, C, D, N, seed, real, bias=True):
+    psig, f0, df, sh = gen.head_params(D, C, K)
+    y = gen.labels(seed, 0, N, C)
+    X = gen.features(seed, 0, N, D, C, psig, real, y=y)
+    W = gen.weights(seed + 100, K, C, D, f0, df, real)
+    b = gen.bias(seed + 200, K, C, real) if bias else None
+    return y, X, W, b, sh
+
+
+def run_gemm(rk, K, C, D, N, X, W, b, sh, tie=0):
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C, D, torch.from_numpy(W).cuda(), None if b is None else torch.from_numpy(b).cuda(), sh,
+                      tie=tie)
+    ctx.score(torch.from_numpy(X).cuda(), N)
+    out = ctx.outputs()
+    ldc = out["ldc"]
+    torch.cuda.synchronize()
+    lg = torch.empty((N, K, ldc), dtype=torch.float32, device="cuda")
+    t1 = torch.empty((N, K), dtype=torch.int32, device="cuda")
+    ls = torch.empty((N, K), dtype=torch.float32, device="cuda")
+    import ctypes
+    nb = N * K * ldc * 4
+    ctypes.memmove  # noqa: B018 (device copies below go through torch)
+    torch.cuda.synchronize()
+    cudart = torch.cuda.cudart()
+    cudart.cudaMemcpy(lg.data_ptr(), out["logits"], nb, 3)
+    cudart.cudaMemcpy(t1.data_ptr(), out["top1"], N * K * 4, 3)
+    cudart.cudaMemcpy(ls.data_ptr(), out["lse"], N * K * 4, 3)
+    torch.cuda.synchronize()
+    return ctx, lg.cpu().numpy(), t1.cpu().numpy(), ls.cpu().numpy()
+
+
+@pytest.mark.parametrize("K,C,D,N", [(3, 10, 128, 200), (2, 100, 256, 300), (3, 1000, 512, 130),
+                                     (12, 100, 1024, 257), (1, 2, 64, 5), (4, 300, 192, 129)])
+def test_int_mode_bit_exact(rk, K, C, D, N):
+    y, X, W, b, sh = make(K, C, D, N, 3, real=False)
+    ctx, lg, t1, ls = run_gemm(rk, K, C, D, N, X, W, b, sh)
+    ref = oracle.logits_gemm(X, W, b, sh)  # fp64, exact for these integer inputs
+    np.testing.assert_array_equal(lg[:, :, :C], ref.astype(np.float32))
+    np.testing.assert_array_equal(t1, np.argmax(ref, axis=2))
+    ref_lse = np.array([[oracle.lse(ref[n, m]) for m in range(K)] for n in range(N)])
+    np.testing.assert_allclose(ls, ref_lse, rtol=2e-6, atol=2e-6)
+
+
+def test_real_mode_tolerance(rk):
+    K, C, D, N = 3, 1000, 1024, 300
+    y, X, W, b, sh = make(K, C, D, N, 5, real=True)
+    ctx, lg, t1, ls = run_gemm(rk, K, C, D, N, X, W, b, sh)
+    ref = oracle.logits_gemm(X, W, b, sh)
+    absum = np.einsum("nd,kcd->nkc", np.abs(gen.bf16_to_f64(X)), np.abs(gen.bf16_to_f64(W))) * 2.0**sh
+    bound = 4 * D * 2.0**-24 * absum + 2.0**-24 * np.abs(ref)
+    err = np.abs(lg[:, :, :C].astype(np.float64) - ref)
+    assert (err <= bound).all(), float((err / np.maximum(bound, 1e-30)).max())
+    # top-1 exact except where the oracle's top-2 logit gap is within the bound (flagged)
+    srt = np.sort(ref, axis=2)
+    gap = srt[:, :, -1] - srt[:, :, -2]
+    clear = gap > 2 * bound.max(axis=2)
+    np.testing.assert_array_equal(t1[clear], np.argmax(ref, axis=2)[clear])
+
+
+@pytest.mark.parametrize("K,C,D,N,tie", [(3, 1000, 512, 600, 0), (8, 1000, 256, 150, 1), (12, 100, 512, 64, 0)])
+def test_end_to_end_int_mode(rk, K, C, D, N, tie):
+    """X -> tcgen05 heads -> vote/average/moments -> reward table equals the oracle on its own fp64 logits."""
+    y, X, W, b, sh = make(K, C, D, N, 9, real=False)
+    ctx = rk.Context(0)
+    rank = np.random.default_rng(1).permutation(K).astype(np.int32)
+    ctx.load_ensemble(K, C, D, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), sh, member_rank=rank, tie=tie)
+    gcfg, ocfg = default_cfg(K)
+    ctx.score(torch.from_numpy(X).cuda(), N)
+    t = ctx.subset_stats(torch.from_numpy(y).cuda(), gcfg)
+    ref = oracle.logits_gemm(X, W, b, sh)
+    o = oracle.table(ref, y, K, C, tie=tie, rank=rank, cfg=ocfg)
+    compare_tables(t, o, K=K)
+
+
+def test_host_buffers_e2e(rk):
+    """Host (numpy) X and labels are staged by the library (the e2e path bench.py times)."""
+    K, C, D, N = 3, 100, 256, 500
+    y, X, W, b, sh = make(K, C, D, N, 13, real=False)
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C, D, W, b, sh)
+    ctx.score(X, N)
+    t = ctx.subset_stats(y, None)
+    o = oracle.table(oracle.logits_gemm(X, W, b, sh), y, K, C)
+    compare_tables(t, o, K=K, check_moments=False)

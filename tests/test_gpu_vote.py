@@ -1,0 +1,175 @@
+"""GPU parity of the vote stage (rk_score_logits -> rk_subset_*) against the CPU oracle.
+
+Parity classes: P1 votes / counts / batch moments bit-exact in both tie modes;
+P2 averaged-probability counts exact except oracle-flagged ambiguous pairs, avg vectors <= 1e-5
+relative; P5 shard/chunk additivity bit-exact; P6 rewards <= 1e-5 relative.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from gpu_helpers import compare_tables, default_cfg
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def rk():
+    import paper_1804_06087_b200 as m
+    m.load_library()
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_vote(rk, L, y, K, C, tie=0, rank=None, cfg=None, offset=0):
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C, member_rank=rank, tie=tie)
+    dl = dev(L)
+    ctx.score_logits(dl, L.shape[2], L.shape[0], offset)
+    t = ctx.subset_stats(dev(y), cfg)
+    torch.cuda.synchronize()
+    return t, ctx
+
+
+CASES = [  # (K, C, N, seed)
+    (3, 10, 1000, 1),     # config c1 shape
+    (3, 1000, 700, 2),    # c2 shape (K=3, C=1000), ragged N
+    (6, 1000, 300, 3),    # c3 shape
+    (8, 1000, 150, 4),    # c4 shape
+    (12, 100, 70, 5),     # c5 shape (4095 subsets)
+    (1, 2, 33, 6),        # degenerate: one model, two classes
+    (5, 37, 517, 7),      # odd sizes, ragged everything
+]
+
+
+@pytest.mark.parametrize("K,C,N,seed", CASES)
+@pytest.mark.parametrize("tie", [0, 1])
+def test_vote_stage_parity(rk, K, C, N, seed, tie):
+    y = gen.labels(seed, 0, N, C)
+    L = gen.logits(seed, 0, N, K, C, y=y)
+    rank = np.random.default_rng(seed).permutation(K).astype(np.int32)
+    gcfg, ocfg = default_cfg(K)
+    t, _ = run_vote(rk, L, y, K, C, tie=tie, rank=rank, cfg=gcfg)
+    o = oracle.table(L, y, K, C, tie=tie, rank=rank, cfg=ocfg)
+    assert t["N"] == N
+    compare_tables(t, o, K=K)
+
+
+def test_integer_logits_ties(rk):
+    """Integer-valued logits: many exact top-1 ties and exact average ties (ambiguous pairs)."""
+    K, C, N = 5, 6, 2000
+    rng = np.random.default_rng(11)
+    L = rng.integers(0, 3, size=(N, K, 8)).astype(np.float32)
+    L[:, :, C:] = np.nan
+    y = rng.integers(0, C, N).astype(np.int32)
+    for tie in (0, 1):
+        t, _ = run_vote(rk, L, y, K, C, tie=tie)
+        o = oracle.table(L, y, K, C, tie=tie)
+        compare_tables(t, o, K=K, check_moments=False)
+        assert o.n_amb.sum() > 0  # the case is exercised
+
+
+def test_overflow_candidates_all_equal_rows(rk):
+    """Rows with equal logits make every class a candidate (smem overflow path)."""
+    K, C, N = 4, 300, 64
+    rng = np.random.default_rng(3)
+    L = gen.logits(3, 0, N, K, C)
+    L[::2, 1:, :C] = 0.0  # half the samples: models 1.. flat
+    L[::4, :, :C] = rng.normal(0, 1e-3, size=(len(L[::4]), K, C)).astype(np.float32)
+    y = rng.integers(0, C, N).astype(np.int32)
+    t, _ = run_vote(rk, L, y, K, C)
+    o = oracle.table(L, y, K, C)
+    compare_tables(t, o, K=K, check_moments=False)
+
+
+def test_chunked_and_sharded_equal_one_shot(rk):
+    """Streaming chunks (multiples of lcm(B)) and disjoint shards sum to the one-shot table (I7, P5)."""
+    K, C, N = 4, 100, 1000
+    y = gen.labels(21, 0, N, C)
+    L = gen.logits(21, 0, N, K, C, y=y)
+    gcfg, ocfg = default_cfg(K, B=(16, 32, 64))
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C)
+    ctx.subset_reset(gcfg)
+    for off, n in [(0, 256), (256, 512), (768, 232)]:
+        ctx.score_logits(dev(L[off:off + n]), L.shape[2], n, off)
+        ctx.subset_accumulate(dev(y[off:off + n]))
+    t = ctx.subset_finalize()
+    compare_tables(t, o, K=K)
+    # two independent "ranks" (world=1 contexts) on disjoint shards: integer tables add exactly
+    parts = []
+    for off, n in [(0, 512), (512, 488)]:
+        c2 = rk.Context(0)
+        c2.load_ensemble(K, C)
+        c2.score_logits(dev(L[off:off + n]), L.shape[2], n, off)
+        parts.append(c2.subset_stats(dev(y[off:off + n]), gcfg))
+    for k in ("cnt_vote", "corr", "O", "Q", "E"):
+        np.testing.assert_array_equal(parts[0][k] + parts[1][k], getattr(o, k), err_msg=k)
+
+
+def test_arrival_ns_input(rk):
+    K, C, N = 3, 10, 640
+    y = gen.labels(5, 0, N, C)
+    L = gen.logits(5, 0, N, K, C, y=y)
+    arr = np.cumsum(np.random.default_rng(0).integers(0, 40_000_000, N)).astype(np.int64)
+    import paper_1804_06087_b200 as m
+    gcfg, ocfg = default_cfg(K)
+    gcfg = m.RewardCfg(B=gcfg.B, beta=0.5, tau_ns=300_000_000, lat_ns=gcfg.lat_ns, arrival_ns=arr)
+    ocfg = oracle.RewardCfg(B=ocfg.B, beta=0.5, tau_ns=300_000_000, lat_ns=ocfg.lat_ns, arrival_ns=arr)
+    t, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    compare_tables(t, o, K=K)
+
+
+def test_predict_parity(rk):
+    K, C, N = 4, 50, 300
+    y = gen.labels(8, 0, N, C)
+    L = gen.logits(8, 0, N, K, C, y=y)
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C, tie=0)
+    ctx.score_logits(dev(L), L.shape[2], N)
+    for v in (1, 5, 15):
+        pv = torch.empty(N, dtype=torch.int32, device="cuda")
+        pa = torch.empty(N, dtype=torch.int32, device="cuda")
+        ap = torch.empty((N, C), dtype=torch.float32, device="cuda")
+        ctx.predict(v, pv, pa, ap)
+        opv, opa, oap, _, _ = oracle.predict(L, K, C, v, want_avgprob=True)
+        np.testing.assert_array_equal(pv.cpu().numpy(), opv)
+        np.testing.assert_allclose(ap.cpu().numpy(), oap, rtol=1e-5, atol=1e-7)  # I4 at 1e-5
+        srt = np.sort(oap, axis=1)
+        clear = (srt[:, -1] - srt[:, -2]) > 1e-5 * srt[:, -1]
+        np.testing.assert_array_equal(pa.cpu().numpy()[clear], opa[clear])
+    with pytest.raises(rk.RkError):
+        ctx.predict(0)
+
+
+def test_errors(rk):
+    K, C, N = 3, 10, 64
+    y = gen.labels(1, 0, N, C)
+    L = gen.logits(1, 0, N, K, C, y=y)
+    bad = L.copy()
+    bad[5, 1, 3] = np.nan
+    with pytest.raises(rk.RkError) as e:
+        run_vote(rk, bad, y, K, C)
+    assert e.value.status == 7  # RK_ENONFINITE
+    yy = y.copy()
+    yy[3] = C
+    with pytest.raises(rk.RkError) as e:
+        run_vote(rk, L, yy, K, C)
+    assert e.value.status == 6  # RK_ELABEL
+    ok = L.copy()
+    ok[5, 1, 3] = -np.inf  # legal
+    run_vote(rk, ok, y, K, C)
+    # empty batch
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C)
+    ctx.score_logits(None, 12, 0)
+    t = ctx.subset_stats(None)
+    assert t["N"] == 0 and t["cnt_vote"].sum() == 0
