@@ -98,8 +98,10 @@ def test_chunked_and_sharded_equal_one_shot(rk):
     ctx = rk.Context(0)
     ctx.load_ensemble(K, C)
     ctx.subset_reset(gcfg)
+    keep = []  # the library borrows the logits pointer until the next rk_score*: keep buffers alive
     for off, n in [(0, 256), (256, 512), (768, 232)]:
-        ctx.score_logits(dev(L[off:off + n]), L.shape[2], n, off)
+        keep.append(dev(L[off:off + n]))
+        ctx.score_logits(keep[-1], L.shape[2], n, off)
         ctx.subset_accumulate(dev(y[off:off + n]))
     t = ctx.subset_finalize()
     compare_tables(t, o, K=K)
@@ -108,7 +110,8 @@ def test_chunked_and_sharded_equal_one_shot(rk):
     for off, n in [(0, 512), (512, 488)]:
         c2 = rk.Context(0)
         c2.load_ensemble(K, C)
-        c2.score_logits(dev(L[off:off + n]), L.shape[2], n, off)
+        keep.append(dev(L[off:off + n]))
+        c2.score_logits(keep[-1], L.shape[2], n, off)
         parts.append(c2.subset_stats(dev(y[off:off + n]), gcfg))
     for k in ("cnt_vote", "corr", "O", "Q", "E"):
         np.testing.assert_array_equal(parts[0][k] + parts[1][k], getattr(o, k), err_msg=k)
@@ -134,7 +137,8 @@ def test_predict_parity(rk):
     L = gen.logits(8, 0, N, K, C, y=y)
     ctx = rk.Context(0)
     ctx.load_ensemble(K, C, tie=0)
-    ctx.score_logits(dev(L), L.shape[2], N)
+    dl = dev(L)
+    ctx.score_logits(dl, L.shape[2], N)
     for v in (1, 5, 15):
         pv = torch.empty(N, dtype=torch.int32, device="cuda")
         pa = torch.empty(N, dtype=torch.int32, device="cuda")
