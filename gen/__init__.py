@@ -40,11 +40,13 @@ def logit_params(K: int, C: int):
 # GEMM heads: psig (fraction of prototype-matched feature dims) and flip rates, all /65536.
 def head_params(D: int, C: int, K: int):
     """(psig_q16, flip0_q16, dflip_q16, scale_log2) for the dense heads. Logit = 2^scale_log2 * x.w."""
+    # calibrated to Inception-like ensemble statistics (SURVEY.md §8(d)): per-model top-1 ~0.72-0.84,
+    # correlated errors (K=8: ~64% unanimous), mean max-softmax ~0.8, |S_c| mean ~4 (K=8, C=1000)
     if C <= 10:
-        return 4000, 3000, 400, -4
+        return 3800, 800, 150, -3
     if C <= 100:
-        return 6200, 3000, 250, -3
-    return 5800, 4000, 600 if K <= 3 else 400, -4
+        return 5800, 800, 80, -3
+    return 5200, 1000, 300 if K <= 3 else 150, -3
 
 
 def _src(*names):

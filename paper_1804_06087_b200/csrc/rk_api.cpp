@@ -58,7 +58,8 @@ struct rk_ctx {
   float* ws_logits = nullptr;
   int32_t* ws_top1 = nullptr;
   float* ws_lse = nullptr;
-  int64_t ws_cap = 0, ws_top1_cap = 0, ws_lse_cap = 0;
+  float* ws_max = nullptr;
+  int64_t ws_cap = 0, ws_top1_cap = 0, ws_lse_cap = 0, ws_max_cap = 0;
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[3 * 128];
@@ -213,7 +214,7 @@ void rk_destroy(rk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
-  void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_x,
+  void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_max, ctx->ws_x,
                   ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_labels, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -297,6 +298,7 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
   if ((s = ensure(ctx, &ctx->ws_logits, &ctx->ws_cap, std::max<int64_t>(N, 1) * ctx->K * ctx->ldc)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
+  if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   const void* Xd = X;
   if (N > 0 && !is_device_ptr(X)) {
     if ((s = ensure(ctx, &ctx->ws_x, &ctx->ws_x_cap, N * ctx->D)) != RK_OK) return s;
@@ -313,6 +315,7 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
   GemmParams gp{};
   gp.N = N; gp.K = ctx->K; gp.C = ctx->C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
   gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias; gp.top1 = ctx->ws_top1; gp.lse = ctx->ws_lse;
+  gp.rmax = ctx->ws_max;
   gp.logits = ctx->ws_logits;
   int rc = gemm_build_tmaps(gp, Xd, ctx->d_W, ctx->ws_logits, ctx->tmaps);
   if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
@@ -468,17 +471,23 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     vp.top1_in = ctx->batch_stats ? ctx->ws_top1 : nullptr;
     vp.labels = dl; vp.N = N; vp.K = K; vp.C = C; vp.S = S; vp.tie = ctx->tie;
     const int gs = (ctx->want_labelled && nB > 0 && nR > 0) ? ctx->gs : 0;
+    vp.rmax_in = ctx->batch_stats ? ctx->ws_max : nullptr;
+    // K <= 8: barrier-free warp-per-sample kernel; K > 8 (up to 4095 subsets): CTA-tile kernel
+    const bool warp_path = K <= 8 && ctx->cur_ldc <= 1024;
     VoteLayout L = choose_vote_layout(K, C, (int)ctx->cur_ldc, gs, ctx->sm_count);
+    if (warp_path) L.G = 1;
     vp.LPR = L.LPR; vp.VPL = L.VPL; vp.RS = L.RS; vp.G = L.G;
     vp.gs = gs;
     vp.U = std::max(L.G, gs);
     vp.nW32 = (C + 31) / 32;
     vp.K1 = K / 2;
-    vp.CAP = 128;
-    {
-      const int TT = (1 << vp.K1) + (1 << (K - vp.K1));
-      int tcap = (int)(32768 / (4 * (size_t)TT * L.G));
-      vp.TCAP = std::max(0, std::min(tcap, vp.CAP));
+    const int TT = (1 << vp.K1) + (1 << (K - vp.K1));
+    if (warp_path) {
+      vp.CAP = 96;
+      vp.TCAP = std::min(vp.CAP, (int)(6272 / (4 * TT)));
+    } else {
+      vp.CAP = 128;
+      vp.TCAP = std::max(0, std::min((int)(16384 / (4 * (size_t)TT * L.G)), vp.CAP));
     }
     vp.band = 2e-5f;
     vp.best_of = ctx->d_best_of;
@@ -496,16 +505,32 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       }
       vp.grp = ctx->d_grp;
     }
-    L.smem = vote_smem_bytes(vp);
-    int occ = 0;
-    // grid: as many persistent CTAs as fit (>= 1 per SM), never more than units
+    if (warp_path) {
+      const int wt = vote_warp_threads();
+      const size_t smem = vote_warp_smem_per_warp(vp) * (wt / 32);
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (227 * 1024) / (smem + 1024)));
+      const int64_t units = (N + (gs > 0 ? gs : 16) - 1) / (gs > 0 ? gs : 16);
+      L.grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + wt / 32 - 1) / (wt / 32), (int64_t)ctx->sm_count * per_sm));
+      L.smem = smem;
+    } else {
+    // ring depth: fill the per-CTA shared-memory budget (2 CTAs/SM when >= 2 slots fit)
     {
+      vp.NSTAGE = 0;
+      const size_t base = vote_smem_bytes(vp), slot = vote_slot_bytes(vp);
+      const size_t half = 112 * 1024, full = 224 * 1024;
+      int per_sm = 2;
+      int ns = (int)((half - std::min(half, base)) / slot);
+      if (ns < 2) { per_sm = 1; ns = (int)((full - std::min(full, base)) / slot); }
+      if (ns < 2) return fail(ctx, RK_EUNSUPPORTED, "vote kernel: tile does not fit in shared memory");
+      vp.NSTAGE = std::min(ns, 8);
+      L.smem = vote_smem_bytes(vp);
       const int64_t units = (N + vp.U - 1) / vp.U;
-      int per_sm = L.smem <= 100 * 1024 ? 2 : 1;
-      (void)occ;
       L.grid = (int)std::min<int64_t>(units, (int64_t)ctx->sm_count * per_sm);
     }
-    const size_t sf = (size_t)L.grid * L.G * C * K, si = (size_t)L.grid * L.G * C;
+    }
+    // overflow scratch: per CTA x G samples (tile kernel) or per warp (warp kernel)
+    const size_t owners = warp_path ? (size_t)L.grid * (vote_warp_threads() / 32) : (size_t)L.grid * L.G;
+    const size_t sf = owners * C * K, si = owners * C;
     if (ctx->scratch_floats < sf) {
       if (ctx->d_scratch) cudaFree(ctx->d_scratch);
       ctx->d_scratch = nullptr;
@@ -523,7 +548,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     {
       const double bytes = (double)N * ((double)K * C * 4 + 4);
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
-      CK(launch_vote(vp, L, st));
+      if (warp_path) CK(launch_vote_warp(vp, L.grid, st));
+      else CK(launch_vote(vp, L, st));
     }
     // ---- A5: batch latency moments (label independent) ----
     const int64_t* arr = nullptr;

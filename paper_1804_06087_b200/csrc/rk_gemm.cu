@@ -138,6 +138,7 @@ struct GemmArgs {
   const float* bias;
   int32_t* top1;
   float* lse;
+  float* rmax;
 };
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (row < a.N) {
         a.top1[row * a.K + model] = arg;
         a.lse[row * a.K + model] = mx + logf(sum);
+        a.rmax[row * a.K + model] = mx;
       }
     }
     if (lane == 0) tma_store_wait_all();
@@ -367,7 +369,7 @@ cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
   if (p.N <= 0) return cudaSuccess;
   GemmArgs a;
   a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D; a.nt = (p.Cp + BN - 1) / BN;
-  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lse = p.lse;
+  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lse = p.lse; a.rmax = p.rmax;
   cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int64_t units = ((p.N + BM - 1) / BM) * p.K;

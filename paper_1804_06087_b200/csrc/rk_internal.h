@@ -18,6 +18,7 @@ struct VoteParams {
   int64_t ldc;
   const float* lse_in;       // [N][K] or null (then computed here)
   const int32_t* top1_in;    // [N][K] or null
+  const float* rmax_in;      // [N][K] or null (row max, from the GEMM epilogue)
   const int32_t* labels;     // [N] device
   int64_t N;                 // samples in this chunk
   int K, C, S, tie;
@@ -33,6 +34,7 @@ struct VoteParams {
   int TCAP;                  // candidate capacity of the subset-sum tables in smem
   int K1;                    // low half of the models for the subset-sum tables
   float band;                // relative fp32 near-tie band -> fp64 recheck
+  int NSTAGE;                // logits ring depth (tiles in flight per CTA, TMA bulk copies)
   const uint8_t* best_of;    // [2^K] best-ranked model in a mask (device)
   int nB;
   int64_t tail_start[kMaxB]; // local sample index from which a sample is in the tail of B[b]
@@ -54,8 +56,14 @@ struct VoteLayout {
 };
 
 VoteLayout choose_vote_layout(int K, int C, int ldc, int gs, int sm_count);
-size_t vote_smem_bytes(const VoteParams& p);
+size_t vote_smem_bytes(const VoteParams& p);   // includes NSTAGE ring slots
+size_t vote_slot_bytes(const VoteParams& p);   // one ring slot (G*K*ldc*4, 128-aligned)
 cudaError_t launch_vote(const VoteParams& p, const VoteLayout& L, cudaStream_t st);
+
+// warp-per-sample variant for K <= 8, C <= 1024 (rk_vote_warp.cu); uses CAP, TCAP, K1, gs, scratch
+size_t vote_warp_smem_per_warp(const VoteParams& p);
+int vote_warp_threads();
+cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st);
 
 // ---- per-sample predictions for one action v (rk_predict) ---------------------------------------
 struct PredictParams {
@@ -131,6 +139,7 @@ struct GemmParams {
   const float* bias;     // [K][Cp] (-inf on padding columns)
   int32_t* top1;         // [N][K]
   float* lse;            // [N][K]
+  float* rmax;           // [N][K] row max (theta of the candidate pruning)
   float* logits;         // [N][K][ldc]
   unsigned int* err;
 };

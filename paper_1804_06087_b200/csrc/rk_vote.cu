@@ -12,16 +12,20 @@
 //                 accuracy of the subset on a labelled validation set.
 //
 // Design (B200, HBM-bound):
-//   * One CTA of 256 threads processes a tile of G samples. Each (sample, model) row of ldc fp32
-//     logits is held in REGISTERS by LPR lanes (VPL float4 each, 128-bit streaming loads that
-//     bypass L1), so the logits are read from HBM exactly once.
-//   * Row max / lowest-index argmax / sum-exp by lane-local loops + xor-shuffle reductions.
+//   * Persistent CTAs of 256 threads; a CTA processes a tile of G contiguous samples (G*K rows of
+//     ldc fp32 logits = one contiguous block). Tiles stream HBM -> shared memory through a ring of
+//     NSTAGE slots filled by 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx) issued
+//     NSTAGE-1 tiles ahead, so DRAM latency is off the critical path and logits are read once.
+//   * Each (sample, model) row is then held in registers by LPR lanes (VPL float4 each): row max /
+//     lowest-index argmax / sum-exp by lane loops + xor-shuffle reductions.
+//   * Per-sample setup is warp-parallel (lanes = models; __match_any_sync builds the distinct-class
+//     vote masks; warp reductions give theta).
 //   * Exact candidate pruning: class c can be the averaged argmax of SOME subset only if
 //     p[m][c] >= theta = min_j p[j][top_j] / K for some m (SURVEY.md §8(d) proof). Candidates are
-//     marked in a per-sample smem bitmap; their probabilities are gathered into a small matrix.
-//   * Per-subset sums come from two precomputed half-tables (low / high models) -> one add per
-//     (subset, candidate). fp32 decisions whose top-2 relative gap is inside `band` are redone
-//     in fp64 from the logits (rare), so results equal the fp64 definition.
+//     marked in a per-sample smem bitmap (warp scan -> slots); their probabilities are gathered.
+//   * Per-subset sums come from two half-tables (low / high models): one add per (subset,
+//     candidate). fp32 decisions whose top-2 relative gap is inside `band` are redone in fp64
+//     from the logits (rare), so results equal the fp64 definition.
 //   * Unanimous samples, "label not predicted by any member" and "label not a candidate" are
 //     exact shortcuts (invariant I6 and the pruning proof) -- no per-subset work.
 //   * Counts: per-unit shared-memory histograms (exclusive ownership or register slot counters),
@@ -38,17 +42,34 @@ namespace rk {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int NW = kVoteThreads / 32;
 
 // sample flags
 constexpr uint32_t F_VALID = 1u, F_UNAN = 2u, F_UNI_OK = 4u, F_VOTE_POSS = 8u, F_AVG_POSS = 16u,
                    F_OVF = 32u, F_TABLES = 64u, F_SKIP = 128u;
 
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-  float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p));
-  return r;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ float comp(const float4& v, int e) {
@@ -56,6 +77,8 @@ __device__ __forceinline__ float comp(const float4& v, int e) {
 }
 
 struct Smem {
+  float* ring;           // [NSTAGE][tile_floats]
+  uint64_t* full;        // [NSTAGE]
   uint8_t* best_of;      // [2^K]
   uint32_t* cta_vote;    // [S]
   uint32_t* cta_avg;     // [S]
@@ -76,14 +99,16 @@ struct Smem {
   double* lse64;         // [G][K]
   uint32_t* bitmap;      // [G][nW32]
   uint32_t* prefix;      // [G][nW32]
-  float* P;              // [G][CAP][K]
+  float* P;              // [G][K][CAP+1]
   int32_t* ccls;         // [G][CAP]
-  float* T;              // [G][TA+TB][TCAP]
+  float* T;              // [G][TA+TB][TCAP|1]
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
 
 __host__ __device__ inline int ngu_of(const VoteParams& p) { return p.gs > 0 ? p.U / p.gs : 1; }
+__host__ __device__ inline size_t tile_floats(const VoteParams& p) { return (size_t)p.G * p.K * p.ldc; }
 
 // Carve the dynamic shared memory. Host and device use the same function.
 __host__ __device__ inline size_t carve(const VoteParams& p, char* base, Smem* s) {
@@ -91,7 +116,8 @@ __host__ __device__ inline size_t carve(const VoteParams& p, char* base, Smem* s
   const int TA = 1 << p.K1, TB = 1 << (K - p.K1);
   size_t o = 0;
   auto take = [&](size_t bytes) -> char* { char* r = base ? base + o : nullptr; o = al16(o + bytes); return r; };
-  // 8-byte aligned items first
+  char* ring = take(al128(4 * tile_floats(p)) * p.NSTAGE);
+  char* full = take(8 * p.NSTAGE);
   char* lse64 = take(sizeof(double) * G * K);
   char* best = take(size_t(1) << K);
   char* cv = take(4ull * S);
@@ -112,10 +138,11 @@ __host__ __device__ inline size_t carve(const VoteParams& p, char* base, Smem* s
   char* smsk = take(4ull * G * K);
   char* bm = take(4ull * G * p.nW32);
   char* pf = take(4ull * G * p.nW32);
-  char* P = take(4ull * G * p.CAP * K);
+  char* P = take(4ull * G * (p.CAP + 1) * K);  // [G][K][CAP+1]: odd stride, conflict-free
   char* cc = take(4ull * G * p.CAP);
-  char* T = take(4ull * G * (TA + TB) * p.TCAP);
+  char* T = take(4ull * G * (TA + TB) * (p.TCAP | 1));  // odd row stride: conflict-free
   if (s) {
+    s->ring = (float*)ring; s->full = (uint64_t*)full;
     s->lse64 = (double*)lse64; s->best_of = (uint8_t*)best; s->cta_vote = (uint32_t*)cv; s->cta_avg = (uint32_t*)ca;
     s->grpcnt = (uint32_t*)gc; s->uni = (uint32_t*)un; s->rmax = (float*)rmax; s->rlse = (float*)rlse;
     s->rtop = (int32_t*)rtop; s->rthr = (float*)rthr; s->sy = (int32_t*)sy; s->sflag = (uint32_t*)sf;
@@ -135,12 +162,31 @@ __device__ double row_lse64(const float* row, int C) {
   return (double)mx + log(s);
 }
 
+// Start of the CTA's k-th tile (k counts valid tiles only), or -1.
+__device__ __forceinline__ int64_t tile_start(const VoteParams& p, int64_t k, int tpu, int64_t nunits) {
+  const int64_t unit = blockIdx.x + (k / tpu) * gridDim.x;
+  if (unit >= nunits) return -1;
+  const int64_t n0 = unit * p.U + (k % tpu) * p.G;
+  return n0 < p.N ? n0 : -1;
+}
+
+__device__ __forceinline__ void issue_tile(const VoteParams& p, Smem& sm, int64_t k, int tpu, int64_t nunits) {
+  const int64_t n0 = tile_start(p, k, tpu, nunits);
+  if (n0 < 0) return;
+  const int s = (int)(k % p.NSTAGE);
+  const int64_t ns = (p.N - n0) < p.G ? (p.N - n0) : p.G;
+  const uint32_t bytes = (uint32_t)(ns * p.K * p.ldc * 4);
+  float* dst = reinterpret_cast<float*>(reinterpret_cast<char*>(sm.ring) + (size_t)s * al128(4 * tile_floats(p)));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  bulk_load(dst, p.logits + n0 * p.K * p.ldc, bytes, &sm.full[s]);
+}
+
 template <int VPL, int RP, bool STATS>
 __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams p) {
-  extern __shared__ __align__(16) char smem_raw[];
+  extern __shared__ __align__(128) char smem_raw[];
   Smem sm;
   carve(p, smem_raw, &sm);
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int K = p.K, S = p.S, G = p.G, C = p.C;
   const int R = G * K;
   const int NGU = ngu_of(p);
@@ -151,6 +197,17 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
   const int F = (int)(p.ldc >> 2);
   const int lane_in_row = t % p.LPR;
   const int row0 = t / p.LPR;
+  const uint32_t kmask = (1u << K) - 1u;
+  const size_t slot_bytes = al128(4 * tile_floats(p));
+  const int tpu = p.U / G;
+  const int64_t nunits = (N + p.U - 1) / p.U;
+  const int CAPS = p.CAP + 1;   // P stride (odd)
+  const int TSTR = p.TCAP | 1;  // half-table row stride (odd)
+  // candidate probability matrix of sample g: element (slot, model m) at base[m * stride + slot]
+  auto Pbase = [&](int g, uint32_t fl) -> float* {
+    return (fl & F_OVF) ? p.scratch + ((size_t)blockIdx.x * G + g) * (size_t)C * K : sm.P + (size_t)g * K * CAPS;
+  };
+  auto Pstride = [&](uint32_t fl) -> int { return (fl & F_OVF) ? C : CAPS; };
 
   // ---- CTA init ----------------------------------------------------------------------------
   if (p.tie == 0)
@@ -158,36 +215,54 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
   for (int i = t; i < S; i += kVoteThreads) { sm.cta_vote[i] = 0; sm.cta_avg[i] = 0; }
   for (int i = t; i < NGU * S; i += kVoteThreads) sm.grpcnt[i] = 0;
   for (int i = t; i < NGU; i += kVoteThreads) sm.uni[i] = 0;
+  if (t == 0) {
+    for (int s = 0; s < p.NSTAGE; ++s) mbar_init(&sm.full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < p.NSTAGE - 1; ++k) issue_tile(p, sm, k, tpu, nunits);  // prologue
+  }
 
   constexpr int NIMAX = 4;  // register slot counters when G > 1 (host guarantees G*S <= NIMAX*256)
   uint32_t slot_vote[NIMAX], slot_avg[NIMAX];
 #pragma unroll
   for (int i = 0; i < NIMAX; ++i) { slot_vote[i] = 0; slot_avg[i] = 0; }
 
-  const int64_t nunits = (N + p.U - 1) / p.U;
-  const int tiles_per_unit = p.U / G;
-
+  int64_t k = 0;
   for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
-    for (int tile = 0; tile < tiles_per_unit; ++tile) {
+    for (int tile = 0; tile < tpu; ++tile, ++k) {
       const int64_t n0 = unit * p.U + (int64_t)tile * G;
-      __syncthreads();  // previous tile's smem fully consumed
+      if (n0 >= N) break;
+      __syncthreads();  // previous tile fully consumed: its ring slot and all per-tile smem are free
+      if (t == 0) issue_tile(p, sm, k + p.NSTAGE - 1, tpu, nunits);
+      const int slot = (int)(k % p.NSTAGE);
+      mbar_wait(&sm.full[slot], (uint32_t)((k / p.NSTAGE) & 1));
+      const float* tileb = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sm.ring) + slot * slot_bytes);
 
-      // ---- 1. row pass: registers <- logits; max / argmax / (sum exp) per row ------------------
+      // ---- 1. row pass: smem -> registers; max / argmax / (sum exp) per row -------------------
       float4 val[RP][VPL];
       int rrow[RP];
 #pragma unroll
       for (int j = 0; j < RP; ++j) {
         const int r = j * p.RS + row0;
         rrow[j] = r;
-        const int g = r / K, m = r - g * K;
-        const int64_t n = n0 + g;
-        const bool rv = (r < R) && (n < N);
-        const float4* base = reinterpret_cast<const float4*>(p.logits + (n * K + m) * p.ldc);
+        const int g = r / K;
+        const bool rv = (r < R) && (n0 + g < N);
+        const float4* base = reinterpret_cast<const float4*>(tileb + (size_t)r * p.ldc);
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
           const int c4 = lane_in_row + i * p.LPR;
-          if (rv && c4 < F) val[j][i] = ld_stream(base + c4);
-          else val[j][i] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+          float4 x = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+          if (rv && c4 < F) {
+            x = base[c4];
+            if ((C & 3) && c4 == (C >> 2)) {  // padding components of the last partial float4
+              const int valid = C & 3;
+              if (valid < 4) x.w = -INFINITY;
+              if (valid < 3) x.z = -INFINITY;
+              if (valid < 2) x.y = -INFINITY;
+            } else if (c4 * 4 >= C) {
+              x = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            }
+          }
+          val[j][i] = x;
         }
       }
 #pragma unroll
@@ -197,120 +272,95 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
         const bool rv = (r < R) && (n0 + g < N);
         float mx = -INFINITY;
         int arg = 0x7fffffff;
-        bool bad = false;
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
           const int cbase = (lane_in_row + i * p.LPR) * 4;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int c = cbase + e;
-            float x = comp(val[j][i], e);
-            if (c >= C) { x = -INFINITY; }
-            if (c < C) bad |= (isnan(x) || x == INFINITY);
-            if (x > mx) { mx = x; arg = c; }
+            const float x = comp(val[j][i], e);
+            if (x > mx) { mx = x; arg = cbase + e; }
           }
         }
-        // lowest index among equal maxima across lanes
         for (int off = p.LPR >> 1; off > 0; off >>= 1) {
           const float om = __shfl_xor_sync(FULL, mx, off);
           const int oa = __shfl_xor_sync(FULL, arg, off);
           if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
         }
         float lse;
+        bool bad;
         if (!STATS) {
+          // NaN anywhere makes the sum NaN; +inf makes max +inf -> inf - inf = NaN.
           float s = 0.f;
-          if (mx != -INFINITY) {
 #pragma unroll
-            for (int i = 0; i < VPL; ++i)
+          for (int i = 0; i < VPL; ++i)
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int c = (lane_in_row + i * p.LPR) * 4 + e;
-                if (c < C) s += __expf(comp(val[j][i], e) - mx);
-              }
-          }
+            for (int e = 0; e < 4; ++e) s += __expf(comp(val[j][i], e) - mx);
           for (int off = p.LPR >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
           lse = mx + logf(s);
+          bad = !(s == s) || !(mx > -INFINITY) || mx == INFINITY;
         } else {
           lse = rv ? p.lse_in[(n0 + g) * K + (r - g * K)] : 0.f;
+          bad = !(lse > -INFINITY && lse < INFINITY) || !(mx > -INFINITY);
         }
-        const bool anybad = __any_sync(FULL, bad && rv);
         if (rv && lane_in_row == 0) {
           sm.rmax[r] = mx;
           sm.rtop[r] = arg;
           sm.rlse[r] = lse;
-          if (anybad || mx == -INFINITY) atomicOr(p.err, 1u);
+          if (bad) atomicOr(p.err, 1u);
         }
       }
       __syncthreads();
 
-      // ---- 2. per-sample setup ---------------------------------------------------------------
-      for (int g = t; g < G; g += kVoteThreads) {
+      // ---- 2. per-sample setup, warp-parallel (lane = model) ---------------------------------
+      for (int g = warp; g < G; g += NW) {
         const int64_t n = n0 + g;
         uint32_t fl = 0;
         if (n < N) {
           const int y = p.labels[n];
           if (y < 0 || y >= C) {
-            atomicOr(p.err + 1, 1u);
-            sm.sy[g] = -1;
+            if (lane == 0) { atomicOr(p.err + 1, 1u); sm.sy[g] = -1; }
           } else {
             fl |= F_VALID;
-            sm.sy[g] = y;
-            // distinct predicted classes, ascending, with the mask of models voting for each
-            int nd = 0;
-            bool unan = true;
-            const int t0 = sm.rtop[g * K];
-            for (int m = 0; m < K; ++m) {
-              const int c = sm.rtop[g * K + m];
-              unan &= (c == t0);
-              int pos = 0;
-              while (pos < nd && sm.scls[g * K + pos] < c) ++pos;
-              if (pos < nd && sm.scls[g * K + pos] == c) {
-                sm.smsk[g * K + pos] |= 1u << m;
-              } else {
-                for (int q = nd; q > pos; --q) {
-                  sm.scls[g * K + q] = sm.scls[g * K + q - 1];
-                  sm.smsk[g * K + q] = sm.smsk[g * K + q - 1];
-                }
-                sm.scls[g * K + pos] = c;
-                sm.smsk[g * K + pos] = 1u << m;
-                ++nd;
-              }
-            }
-            sm.snd[g] = nd;
-            bool vp = false;
-            for (int q = 0; q < nd; ++q) vp |= (sm.scls[g * K + q] == y);
-            if (vp) fl |= F_VOTE_POSS;
-            // tail membership (samples after the last complete batch of size B[b] in this chunk)
+            const int c = lane < K ? sm.rtop[g * K + lane] : -1 - lane;
+            const uint32_t mm = __match_any_sync(FULL, c);  // models predicting the same class
+            const bool leader = lane < K && (__ffs(mm) - 1) == lane;
+            const uint32_t lb = __ballot_sync(FULL, leader);
+            const int pos = __popc(lb & ((1u << lane) - 1u));
+            if (leader) { sm.scls[g * K + pos] = c; sm.smsk[g * K + pos] = mm; }
+            const int nd = __popc(lb);
+            const bool unan = __shfl_sync(FULL, mm, 0) == kmask;
+            if (__any_sync(FULL, lane < K && c == y)) fl |= F_VOTE_POSS;
             uint32_t tm = 0;
             for (int bi = 0; bi < p.nB; ++bi)
               if (n >= p.tail_start[bi]) tm |= 1u << bi;
-            sm.stail[g] = tm;
             if (unan) {
               fl |= F_UNAN;
-              if (t0 == y) {
-                fl |= F_UNI_OK;
+              if (c == y) fl |= F_UNI_OK;  // lane 0's class (all equal)
+              fl = __shfl_sync(FULL, fl, 0);
+              if ((fl & F_UNI_OK) && lane == 0) {
                 const int grp = (p.gs > 0 && G > p.gs) ? g / p.gs : 0;
                 atomicAdd(&sm.uni[grp], 1u);
-                if (tm)  // rare: unanimous-correct sample in the ragged tail
-                  for (int bi = 0; bi < p.nB; ++bi)
-                    if ((tm >> bi) & 1u)
-                      for (int v = 0; v < S; ++v) atomicAdd(p.tail + (size_t)bi * S + v, 1ull);
               }
+              if ((fl & F_UNI_OK) && tm)  // rare: unanimous-correct sample in the ragged tail
+                for (int bi = 0; bi < p.nB; ++bi)
+                  if ((tm >> bi) & 1u)
+                    for (int v = lane; v < S; v += 32) atomicAdd(p.tail + (size_t)bi * S + v, 1ull);
             } else {
               // theta = min_j p[j][top_j] / K ; candidate <=> l[m][c] - lse_m >= log(theta)
-              float th = INFINITY;
-              for (int m = 0; m < K; ++m) th = fminf(th, __expf(sm.rmax[g * K + m] - sm.rlse[g * K + m]));
+              float th = lane < K ? __expf(sm.rmax[g * K + lane] - sm.rlse[g * K + lane]) : INFINITY;
+              for (int off = 16; off > 0; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
               const float lth = logf(th / (float)K);
-              for (int m = 0; m < K; ++m) {
-                const float l = sm.rlse[g * K + m];
-                sm.rthr[g * K + m] = (l + lth) - (1e-3f + 1e-6f * fabsf(l) + 1e-6f * fabsf(lth));
-                sm.lse64[g * K + m] = __longlong_as_double(0x7ff8000000000000ll);
+              if (lane < K) {
+                const float l = sm.rlse[g * K + lane];
+                sm.rthr[g * K + lane] = (l + lth) - (1e-3f + 1e-6f * fabsf(l) + 1e-6f * fabsf(lth));
+                sm.lse64[g * K + lane] = __longlong_as_double(0x7ff8000000000000ll);
               }
-              for (int w = 0; w < p.nW32; ++w) sm.bitmap[g * p.nW32 + w] = 0;
+              for (int w = lane; w < p.nW32; w += 32) sm.bitmap[g * p.nW32 + w] = 0;
             }
+            if (lane == 0) { sm.sy[g] = y; sm.snd[g] = nd; sm.stail[g] = tm; }
           }
         }
-        sm.sflag[g] = fl;
+        if (lane == 0) sm.sflag[g] = fl;
       }
       __syncthreads();
 
@@ -327,36 +377,46 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
             for (int i = 0; i < VPL; ++i)
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const int c = (lane_in_row + i * p.LPR) * 4 + e;
-                if (c < C && comp(val[j][i], e) >= thr) atomicOr(&sm.bitmap[g * p.nW32 + (c >> 5)], 1u << (c & 31));
+                if (comp(val[j][i], e) >= thr) {
+                  const int c = (lane_in_row + i * p.LPR) * 4 + e;
+                  atomicOr(&sm.bitmap[g * p.nW32 + (c >> 5)], 1u << (c & 31));
+                }
               }
           }
         }
       }
       __syncthreads();
 
-      // ---- 4. candidate prefix counts --------------------------------------------------------
-      for (int g = t; g < G; g += kVoteThreads) {
+      // ---- 4. candidate slots: warp scan over bitmap words --------------------------------------
+      for (int g = warp; g < G; g += NW) {
         uint32_t fl = sm.sflag[g];
         if ((fl & F_VALID) && !(fl & F_UNAN)) {
-          uint32_t run = 0;
-          for (int w = 0; w < p.nW32; ++w) {
-            sm.prefix[g * p.nW32 + w] = run;
-            run += __popc(sm.bitmap[g * p.nW32 + w]);
+          const uint32_t wv = lane < p.nW32 ? sm.bitmap[g * p.nW32 + lane] : 0u;
+          const int cnt = __popc(wv);
+          int incl = cnt;
+          for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += o;
           }
-          sm.sncand[g] = (int)run;
+          if (lane < p.nW32) sm.prefix[g * p.nW32 + lane] = (uint32_t)(incl - cnt);
+          const int run = __shfl_sync(FULL, incl, 31);
           const int y = sm.sy[g];
-          const uint32_t wy = sm.bitmap[g * p.nW32 + (y >> 5)];
-          if ((wy >> (y & 31)) & 1u) {
-            fl |= F_AVG_POSS;
-            sm.sys[g] = (int)(sm.prefix[g * p.nW32 + (y >> 5)] + __popc(wy & ((1u << (y & 31)) - 1u)));
-          } else {
-            sm.sys[g] = -1;
+          const int wy = y >> 5;
+          const uint32_t word_y = __shfl_sync(FULL, wv, wy);
+          const int pre_y = __shfl_sync(FULL, incl - cnt, wy);
+          if (lane == 0) {
+            sm.sncand[g] = run;
+            if ((word_y >> (y & 31)) & 1u) {
+              fl |= F_AVG_POSS;
+              sm.sys[g] = pre_y + __popc(word_y & ((1u << (y & 31)) - 1u));
+            } else {
+              sm.sys[g] = -1;
+            }
+            if (run > p.CAP) fl |= F_OVF;
+            else if (run <= p.TCAP) fl |= F_TABLES;
+            if (!(fl & (F_VOTE_POSS | F_AVG_POSS))) fl |= F_SKIP;
+            sm.sflag[g] = fl;
           }
-          if ((int)run > p.CAP) fl |= F_OVF;
-          else if ((int)run <= p.TCAP) fl |= F_TABLES;
-          if (!(fl & (F_VOTE_POSS | F_AVG_POSS))) fl |= F_SKIP;
-          sm.sflag[g] = fl;
         }
       }
       __syncthreads();
@@ -370,51 +430,51 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
           const uint32_t fl = sm.sflag[g];
           if ((fl & F_VALID) && (fl & F_AVG_POSS) && !(fl & (F_UNAN | F_SKIP))) {
             const float lse = sm.rlse[r];
-            float* Pg = (fl & F_OVF) ? p.scratch + ((size_t)blockIdx.x * G + g) * (size_t)C * K
-                                     : sm.P + (size_t)g * p.CAP * K;
+            float* Pg = Pbase(g, fl);
+            const int ps = Pstride(fl);
             int32_t* Cg = (fl & F_OVF) ? p.scratch_cls + ((size_t)blockIdx.x * G + g) * (size_t)C
                                        : sm.ccls + (size_t)g * p.CAP;
 #pragma unroll
-            for (int i = 0; i < VPL; ++i)
+            for (int i = 0; i < VPL; ++i) {
+              const int cb = (lane_in_row + i * p.LPR) * 4;
+              if (cb < C) {
+                const uint32_t w = sm.bitmap[g * p.nW32 + (cb >> 5)];
+                const uint32_t bits4 = (w >> (cb & 31)) & 0xFu;  // 4 consecutive classes share a word
+                if (bits4) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int c = (lane_in_row + i * p.LPR) * 4 + e;
-                if (c < C) {
-                  const uint32_t w = sm.bitmap[g * p.nW32 + (c >> 5)];
-                  if ((w >> (c & 31)) & 1u) {
-                    const int slot = (int)(sm.prefix[g * p.nW32 + (c >> 5)] + __popc(w & ((1u << (c & 31)) - 1u)));
-                    Pg[(size_t)slot * K + m] = expf(comp(val[j][i], e) - lse);
-                    if (m == 0) Cg[slot] = c;
-                  }
+                  for (int e = 0; e < 4; ++e)
+                    if ((bits4 >> e) & 1u) {
+                      const int c = cb + e;
+                      const int slot = (int)(sm.prefix[g * p.nW32 + (c >> 5)] + __popc(w & ((1u << (c & 31)) - 1u)));
+                      Pg[(size_t)m * ps + slot] = expf(comp(val[j][i], e) - lse);
+                      if (m == 0) Cg[slot] = c;
+                    }
                 }
               }
+            }
           }
         }
       }
       __syncthreads();
 
       // ---- 6. half tables: A[a][c] = sum_{i in a, asc} p[i][c] (low models), B likewise (high) -
-      {
-        const int per = TT * p.TCAP;
-        for (int idx = t; idx < G * per; idx += kVoteThreads) {
-          const int g = idx / per;
-          const int rem = idx - g * per;
-          const int h = rem / p.TCAP, slot = rem - h * p.TCAP;
-          const uint32_t fl = sm.sflag[g];
-          if (!(fl & F_TABLES) || (fl & (F_UNAN | F_SKIP)) || !(fl & F_VALID) || !(fl & F_AVG_POSS)) continue;
-          if (slot >= sm.sncand[g]) continue;
-          const float* Pr = sm.P + ((size_t)g * p.CAP + slot) * K;
-          float s = 0.f;
-          if (h < TA) {
-            for (uint32_t a = (uint32_t)h; a; a &= a - 1) s += Pr[__ffs(a) - 1];
-          } else {
-            for (uint32_t b = (uint32_t)(h - TA); b; b &= b - 1) s += Pr[p.K1 + __ffs(b) - 1];
+      for (int g = 0; g < G; ++g) {
+        const uint32_t fl = sm.sflag[g];
+        if (!(fl & F_TABLES) || (fl & (F_UNAN | F_SKIP)) || !(fl & F_VALID) || !(fl & F_AVG_POSS)) continue;
+        const int nc = sm.sncand[g];
+        for (int h = warp; h < TT; h += NW)
+          for (int slot = lane; slot < nc; slot += 32) {
+            const float* Pr = sm.P + (size_t)g * K * CAPS + slot;
+            float s = 0.f;
+            if (h < TA) {
+              for (uint32_t a = (uint32_t)h; a; a &= a - 1) s += Pr[(size_t)(__ffs(a) - 1) * CAPS];
+            } else {
+              for (uint32_t b = (uint32_t)(h - TA); b; b &= b - 1) s += Pr[(size_t)(p.K1 + __ffs(b) - 1) * CAPS];
+            }
+            sm.T[((size_t)g * TT + h) * TSTR + slot] = s;
           }
-          sm.T[((size_t)g * TT + h) * p.TCAP + slot] = s;
-        }
       }
       __syncthreads();
-
       // ---- 7. subsets -------------------------------------------------------------------------
       const int GS = G * S;
       for (int i = 0; i < (GS + kVoteThreads - 1) / kVoteThreads; ++i) {
@@ -429,15 +489,17 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
         // A3: majority vote
         if (fl & F_VOTE_POSS) {
           const int nd = sm.snd[g];
-          int bc = 0, bj = 0;
+          int bc = 0, bcls = 0x7fffffff;
           uint32_t tied = 0;
           for (int q = 0; q < nd; ++q) {
             const uint32_t mv = v & sm.smsk[g * K + q];
             const int cnt = __popc(mv);
-            if (cnt > bc) { bc = cnt; bj = q; tied = mv; }
-            else if (cnt == bc) tied |= mv;
+            const int cq = sm.scls[g * K + q];
+            if (cnt > bc) { bc = cnt; bcls = cq; tied = mv; }
+            else if (cnt == bc && cnt > 0) { tied |= mv; bcls = min(bcls, cq); }
           }
-          const int winner = (p.tie == 0) ? sm.rtop[g * K + sm.best_of[tied]] : sm.scls[g * K + bj];
+          // BEST_MEMBER: best-ranked member among the tied voters (reading Q2); LOWEST_CLASS: min class
+          const int winner = (p.tie == 0) ? sm.rtop[g * K + sm.best_of[tied]] : bcls;
           okv = (winner == y);
         }
         // A4: averaged probabilities
@@ -449,20 +511,20 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
             const int ys = sm.sys[g];
             float sy_ = 0.f, m2 = -1.f;
             if (fl & F_TABLES) {
-              const float* TAg = sm.T + (size_t)g * TT * p.TCAP;
-              const float* A = TAg + (size_t)(v & (TA - 1)) * p.TCAP;
-              const float* B = TAg + (size_t)(TA + (v >> p.K1)) * p.TCAP;
+              const float* TAg = sm.T + (size_t)g * TT * TSTR;
+              const float* A = TAg + (size_t)(v & (TA - 1)) * TSTR;
+              const float* B = TAg + (size_t)(TA + (v >> p.K1)) * TSTR;
               sy_ = A[ys] + B[ys];
               for (int c = 0; c < nc; ++c) {
                 const float s = A[c] + B[c];
                 if (c != ys) m2 = fmaxf(m2, s);
               }
             } else {
-              const float* Pg = (fl & F_OVF) ? p.scratch + ((size_t)blockIdx.x * G + g) * (size_t)C * K
-                                             : sm.P + (size_t)g * p.CAP * K;
+              const float* Pg = Pbase(g, fl);
+              const int ps = Pstride(fl);
               for (int c = 0; c < nc; ++c) {
                 float s = 0.f;
-                for (uint32_t a = v; a; a &= a - 1) s += Pg[(size_t)c * K + (__ffs(a) - 1)];
+                for (uint32_t a = v; a; a &= a - 1) s += Pg[(size_t)(__ffs(a) - 1) * ps + c];
                 if (c == ys) sy_ = s; else m2 = fmaxf(m2, s);
               }
             }
@@ -476,8 +538,8 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
               const int64_t n = n0 + g;
               const int32_t* Cg = (fl & F_OVF) ? p.scratch_cls + ((size_t)blockIdx.x * G + g) * (size_t)C
                                                : sm.ccls + (size_t)g * p.CAP;
-              const float* Pg = (fl & F_OVF) ? p.scratch + ((size_t)blockIdx.x * G + g) * (size_t)C * K
-                                             : sm.P + (size_t)g * p.CAP * K;
+              const float* Pg = Pbase(g, fl);
+              const int ps = Pstride(fl);
               const float lo = sy_ * (1.f - p.band);
               double best = -1.0;
               int bestc = 0x7fffffff;
@@ -485,10 +547,10 @@ __global__ void __launch_bounds__(kVoteThreads, 2) vote_kernel(const VoteParams 
               for (int c = 0; c < nc; ++c) {
                 float s32 = 0.f;
                 if (fl & F_TABLES) {
-                  const float* TAg = sm.T + (size_t)g * TT * p.TCAP;
-                  s32 = TAg[(size_t)(v & (TA - 1)) * p.TCAP + c] + TAg[(size_t)(TA + (v >> p.K1)) * p.TCAP + c];
+                  const float* TAg = sm.T + (size_t)g * TT * TSTR;
+                  s32 = TAg[(size_t)(v & (TA - 1)) * TSTR + c] + TAg[(size_t)(TA + (v >> p.K1)) * TSTR + c];
                 } else {
-                  for (uint32_t a = v; a; a &= a - 1) s32 += Pg[(size_t)c * K + (__ffs(a) - 1)];
+                  for (uint32_t a = v; a; a &= a - 1) s32 += Pg[(size_t)(__ffs(a) - 1) * ps + c];
                 }
                 if (c != ys && s32 < lo) continue;
                 const int cls = Cg[c];
@@ -603,6 +665,7 @@ cudaError_t launch_s(const VoteParams& p, const VoteLayout& L, cudaStream_t st) 
 }  // namespace
 
 size_t vote_smem_bytes(const VoteParams& p) { return carve(p, nullptr, nullptr); }
+size_t vote_slot_bytes(const VoteParams& p) { return al128(4 * tile_floats(p)); }
 
 static int pow2ceil(int x) { int r = 1; while (r < x) r <<= 1; return r; }
 
@@ -619,9 +682,8 @@ VoteLayout choose_vote_layout(int K, int C, int ldc, int gs, int sm_count) {
       int G = 1;
       while (G * 2 * K <= RS * RP && G * 2 <= 64) G *= 2;
       if (G * K > RS * RP) continue;  // one sample must fit
-      if (G > 1 && G * S > 4 * kVoteThreads) {  // register slot counters limit
-        while (G > 1 && G * S > 4 * kVoteThreads) G >>= 1;
-      }
+      while (G > 1 && G * S > 4 * kVoteThreads) G >>= 1;  // register slot counters limit
+      while (G > 1 && (size_t)G * K * ldc * 4 > 24 * 1024) G >>= 1;  // ring slot size
       const double util = double(G * K) / double(RS * RP);
       const double lane_util = double(F) / double(LPR * VPL);
       // prefer utilisation, then fewer registers, then wide rows (coalescing)
@@ -633,7 +695,7 @@ VoteLayout choose_vote_layout(int K, int C, int ldc, int gs, int sm_count) {
     }
   }
   (void)gs;
-  best.grid = sm_count;  // persistent, 1 CTA per SM (launch_bounds 1); refined by occupancy later
+  best.grid = sm_count;
   return best;
 }
 
