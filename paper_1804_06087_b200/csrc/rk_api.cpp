@@ -85,6 +85,8 @@ struct rk_ctx {
   size_t grp_cap = 0;
   int32_t* d_labels = nullptr;
   int64_t labels_cap = 0;
+  int32_t* d_work = nullptr;  // vote worklist [N] + count
+  int64_t work_cap = 0;
   int64_t* d_arr = nullptr;
   int64_t arr_cap = 0;
   float* d_scratch = nullptr;
@@ -215,7 +217,7 @@ void rk_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
   void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_max, ctx->ws_x,
-                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_labels, ctx->d_arr, ctx->d_scratch,
+                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -508,7 +510,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     if (warp_path) {
       const int wt = vote_warp_threads();
       const size_t smem = vote_warp_smem_per_warp(vp) * (wt / 32);
-      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (227 * 1024) / (smem + 1024)));
+      const int per_sm = (int)std::max<size_t>(
+          1, std::min<size_t>((size_t)vote_warp_min_blocks(), (227 * 1024) / (smem + 1024)));
       const int64_t units = (N + (gs > 0 ? gs : 16) - 1) / (gs > 0 ? gs : 16);
       L.grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + wt / 32 - 1) / (wt / 32), (int64_t)ctx->sm_count * per_sm));
       L.smem = smem;
@@ -548,8 +551,21 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     {
       const double bytes = (double)N * ((double)K * C * 4 + 4);
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
-      if (warp_path) CK(launch_vote_warp(vp, L.grid, st));
-      else CK(launch_vote(vp, L, st));
+      if (warp_path) {
+        if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, N + 1)) != RK_OK) return s;  // [N] list + count
+        int32_t* st_top = nullptr;
+        float *st_lse = nullptr, *st_max = nullptr;
+        if (!ctx->batch_stats) {  // kernel A writes row statistics for kernel B
+          if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, N * K)) != RK_OK) return s;
+          if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, N * K)) != RK_OK) return s;
+          if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, N * K)) != RK_OK) return s;
+          st_top = ctx->ws_top1; st_lse = ctx->ws_lse; st_max = ctx->ws_max;
+        }
+        CK(launch_vote_warp(vp, L.grid, st, ctx->d_work, reinterpret_cast<unsigned int*>(ctx->d_work + N), st_top,
+                            st_lse, st_max, ctx->sm_count));
+      } else {
+        CK(launch_vote(vp, L, st));
+      }
     }
     // ---- A5: batch latency moments (label independent) ----
     const int64_t* arr = nullptr;

@@ -63,7 +63,12 @@ cudaError_t launch_vote(const VoteParams& p, const VoteLayout& L, cudaStream_t s
 // warp-per-sample variant for K <= 8, C <= 1024 (rk_vote_warp.cu); uses CAP, TCAP, K1, gs, scratch
 size_t vote_warp_smem_per_warp(const VoteParams& p);
 int vote_warp_threads();
-cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st);
+int vote_warp_min_blocks();
+// Two kernels: classify+votes over all samples, then averages over the worklist of samples whose
+// label is an averaging candidate. work: [N] int32, work_count: 1 uint; st_*: [N][K] statistics
+// scratch (written by kernel A when the logits came without statistics).
+cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
+                             int32_t* st_top, float* st_lse, float* st_max, int sm_count);
 
 // ---- per-sample predictions for one action v (rk_predict) ---------------------------------------
 struct PredictParams {

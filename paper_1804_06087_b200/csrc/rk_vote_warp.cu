@@ -1,27 +1,28 @@
-// rk_vote_warp.cu — steps A2-A5 for K <= 8 models, C <= 1024 classes: one WARP per sample, no
-// block-level barriers. (rk_vote.cu holds the CTA-tile kernel used for K > 8.)
+// rk_vote_warp.cu — steps A2-A5 for K <= 8 models, C <= 1024 classes. One WARP per sample, no
+// block-level barriers, two kernels (rk_vote.cu holds the CTA-tile kernel used for K > 8).
 //
 // PAPER.md passages: :153 top-1 (reading Q4), :407 majority vote with best-accuracy tie-break
 // (RK_TIE_BEST_MEMBER; RK_TIE_LOWEST_CLASS = north_star), :72 averaged softmax (readings Q5, Q6),
 // :429 every non-empty subset v is an action; a(M[v]) = validation accuracy.
 //
-// Per sample (warp; lane m < K owns model m's row statistics):
-//   1. row statistics: from the GEMM epilogue (top1, lse, max) or, for caller logits, one pass
-//      over the K rows (lanes stride the row; xor-shuffle reductions).
-//   2. decided from statistics alone, before touching the logits again:
-//        * unanimous members -> (t == y) for every subset (invariant I6)           no logit reads
-//        * theta = min_j p[j][top_j] / K; label y is an averaging candidate iff some model has
-//          l[m][y] >= lse_m + log(theta) (K scattered loads). If not, the averaged argmax of every
-//          subset differs from y (pruning proof) and only votes are evaluated.
-//   3. otherwise: one coalesced streaming pass over the K*ldc logits marks the candidate set S_c in
-//      a warp-private bitmap; a warp scan assigns slots in class order; p[m][c] = exp(l - lse_m) is
-//      gathered for c in S_c; two half-tables (low / high models) give every subset's sums with
-//      one add per candidate.
-//   4. lanes own subsets v = lane + 32j + 1 (j < 8): vote via the distinct-class masks
-//      (__match_any_sync), average via the half-tables; fp32 decisions inside the relative band
-//      are redone in fp64 with warp-cooperative fp64 log-sum-exp (rare).
-//   5. counts live in registers (exclusive ownership), per-group counts for the labelled moments
-//      are written once per unit, totals are flushed with one 64-bit atomic per (warp, subset).
+// Kernel A, vote_classify (every sample; reads per-row statistics, not the logits):
+//   * row statistics (top1, lse, max) from the GEMM epilogue, or one pass over the rows for caller
+//     logits (then written out for kernel B);
+//   * unanimous members -> (t == y) for every subset, vote AND average (invariant I6);
+//   * majority vote of every subset (lanes own subsets v = lane + 32j + 1; distinct-class masks
+//     from __match_any_sync);
+//   * theta = min_j p[j][top_j] / K; the label y can be the averaged argmax of some subset only if
+//     some model has l[m][y] >= lse_m + log(theta) (K scattered loads; pruning proof, SURVEY.md
+//     §8(d)). If not, every subset's average is wrong; otherwise the sample joins a worklist.
+// Kernel B, vote_average (worklist samples only; all warps run the same phases):
+//   * one coalesced streaming pass over the K*ldc logits marks
+//       R = S_c ∩ {c : exists m, l[m][c] >= l[m][y]}
+//     (S_c: theta candidates; a class below y in EVERY model has avg_v[c] < avg_v[y] for all v);
+//   * warp scan assigns slots in class order; p[m][c] = exp(l - lse_m) is gathered for c in R;
+//   * per subset: sum_y from two half-tables (low / high models), an upper bound on every
+//     competitor (half-table sums of q_m = max_{c != y} p[m][c]) decides most subsets in O(1),
+//     the rest scan R; fp32 decisions inside the relative band are redone in fp64 (rare).
+// Counts are lane-owned (no atomics in the loops), flushed with one 64-bit atomic per (warp, v).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -32,43 +33,9 @@ namespace rk {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int WT = 256;  // threads per CTA
+constexpr int WT = 128;  // threads per CTA (4 warps)
 constexpr int WPC = WT / 32;
 constexpr int JMAX = 8;  // subsets per lane (S <= 255)
-
-struct WS {  // per-warp shared memory
-  int32_t* scls;    // [8] distinct predicted classes
-  uint32_t* smsk;   // [8] models voting for each
-  int32_t* stop;    // [8] top-1 per model
-  double* lse64;    // [8]
-  uint32_t* bitmap; // [32] S_c (theta test)
-  uint32_t* bitmapB;// [32] classes not below y in some model
-  int32_t* ccls;    // [CAP] candidate classes in ascending order
-  float* P;         // [K][CAP+1]
-  float* T;         // [TT][TCAP|1]
-};
-
-__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
-
-__host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS* w) {
-  const int TT = (1 << p.K1) + (1 << (p.K - p.K1));
-  size_t o = 0;
-  auto take = [&](size_t b) -> char* { char* r = base ? base + o : nullptr; o = a16(o + b); return r; };
-  char* l64 = take(8 * 8);
-  char* sc = take(4 * 8);
-  char* sm = take(4 * 8);
-  char* st = take(4 * 8);
-  char* bm = take(4 * 32);
-  char* bmB = take(4 * 32);
-  char* cc = take(4ull * p.CAP);
-  char* P = take(4ull * p.K * (p.CAP + 1));
-  char* T = take(4ull * TT * (p.TCAP | 1));
-  if (w) {
-    w->lse64 = (double*)l64; w->scls = (int32_t*)sc; w->smsk = (uint32_t*)sm; w->stop = (int32_t*)st;
-    w->bitmap = (uint32_t*)bm; w->bitmapB = (uint32_t*)bmB; w->ccls = (int32_t*)cc; w->P = (float*)P; w->T = (float*)T;
-  }
-  return o;
-}
 
 __device__ __forceinline__ float4 ldg_stream(const float* p) {
   float4 r;
@@ -79,41 +46,64 @@ __device__ __forceinline__ float4 ldg_stream(const float* p) {
 }
 __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 
+__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// theta threshold of model m (lane m): candidate <=> l >= lse_m + log(theta), minus a slack that can
+// only enlarge the set (fp32 rounding of lse and of the comparison).
+__device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int lane) {
+  float th = lane < K ? __expf(mx - ls) : INFINITY;
+  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
+  const float lth = logf(th / (float)K);
+  return (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
+}
+
+// rare: a vote-correct sample in the ragged tail of the chunk (outside complete batches of B[b])
+__device__ __noinline__ void tail_add(const VoteParams& p, uint32_t tm, uint32_t v) {
+  for (int bi = 0; bi < p.nB; ++bi)
+    if ((tm >> bi) & 1u) atomicAdd(p.tail + (size_t)bi * p.S + (v - 1), 1ull);
+}
+
+// =============================== kernel A: classify + votes ====================================
+struct AS {  // per-warp shared memory
+  int32_t scls[8];
+  uint32_t smsk[8];
+  int32_t stop[8];
+};
+
 template <bool STATS>
-__global__ void __launch_bounds__(WT, 2) vote_warp_kernel(const VoteParams p) {
-  extern __shared__ __align__(16) char smem_raw[];
+__global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p, int32_t* work,
+                                                              unsigned int* work_count, int32_t* st_top,
+                                                              float* st_lse, float* st_max) {
+  __shared__ AS as_all[WPC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t wbytes = warp_smem(p, nullptr, nullptr);
-  WS ws;
-  warp_smem(p, smem_raw + warp * wbytes, &ws);
+  AS& as = as_all[warp];
   const int K = p.K, S = p.S, C = p.C;
   const int F = (int)(p.ldc >> 2);
   const uint32_t kmask = (1u << K) - 1u;
-  const int TA = 1 << p.K1, TT = TA + (1 << (K - p.K1));
-  const int TSTR = p.TCAP | 1, CAPS = p.CAP + 1;
   const int U = p.gs > 0 ? p.gs : 16;
   const int64_t N = p.N;
   const int64_t nunits = (N + U - 1) / U;
   const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
   const int64_t nw = (int64_t)gridDim.x * WPC;
-  float* ovP = p.scratch + gw * (size_t)K * C;       // overflow candidate matrix [K][C]
-  int32_t* ovC = p.scratch_cls + gw * (size_t)C;
+  int64_t tail0 = N;
+  for (int bi = 0; bi < p.nB; ++bi) tail0 = p.tail_start[bi] < tail0 ? p.tail_start[bi] : tail0;
 
   uint32_t cv[JMAX], ca[JMAX], gv[JMAX];
 #pragma unroll
   for (int j = 0; j < JMAX; ++j) { cv[j] = 0; ca[j] = 0; gv[j] = 0; }
 
   for (int64_t unit = gw; unit < nunits; unit += nw) {
-    uint32_t uni = 0;
-    const int64_t s1 = (unit + 1) * U < N ? (unit + 1) * U : N;
-    for (int64_t n = unit * U; n < s1; ++n) {
+    uint32_t uni = 0, wmask = 0;
+    const int64_t u0 = unit * U;
+    const int64_t s1 = u0 + U < N ? u0 + U : N;
+#pragma unroll 1
+    for (int64_t n = u0; n < s1; ++n) {
       const int y = p.labels[n];
       if (y < 0 || y >= C) {
         if (lane == 0) atomicOr(p.err + 1, 1u);
         continue;
       }
       const float* rowbase = p.logits + n * K * p.ldc;
-      // ---- 1. row statistics (lane m < K holds model m) --------------------------------------
       int tp = 0;
       float mx = 0.f, ls = 0.f;
       bool bad = false;
@@ -125,7 +115,8 @@ __global__ void __launch_bounds__(WT, 2) vote_warp_kernel(const VoteParams p) {
           bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
         }
       } else {
-        for (int m = 0; m < K; ++m) {
+#pragma unroll 1
+        for (int m = 0; m < K; ++m) {  // one pass over the row: max, lowest argmax, sum exp
           const float* row = rowbase + (size_t)m * p.ldc;
           float4 v[8];
 #pragma unroll
@@ -167,20 +158,23 @@ __global__ void __launch_bounds__(WT, 2) vote_warp_kernel(const VoteParams p) {
             bad = !(sum == sum) || !(bm > -INFINITY) || bm == INFINITY;
           }
         }
+        if (lane < K) {  // statistics for kernel B
+          st_top[n * K + lane] = tp;
+          st_lse[n * K + lane] = ls;
+          st_max[n * K + lane] = mx;
+        }
       }
       if (__any_sync(FULL, bad)) {
         if (lane == 0) atomicOr(p.err, 1u);
         continue;
       }
-      // ---- 2. vote structure and exact shortcuts ---------------------------------------------
+      // vote structure
       const int c = lane < K ? tp : -1 - lane;
       const uint32_t mm = __match_any_sync(FULL, c);
-      const bool leader = lane < K && (__ffs(mm) - 1) == lane;
-      const uint32_t lb = __ballot_sync(FULL, leader);
-      const int nd = __popc(lb);
       uint32_t tm = 0;
-      for (int bi = 0; bi < p.nB; ++bi)
-        if (n >= p.tail_start[bi]) tm |= 1u << bi;
+      if (n >= tail0)
+        for (int bi = 0; bi < p.nB; ++bi)
+          if (n >= p.tail_start[bi]) tm |= 1u << bi;
       if (__shfl_sync(FULL, mm, 0) == kmask) {  // unanimous (invariant I6)
         if (__shfl_sync(FULL, c, 0) == y) {
           ++uni;
@@ -191,220 +185,51 @@ __global__ void __launch_bounds__(WT, 2) vote_warp_kernel(const VoteParams p) {
         }
         continue;
       }
-      const bool vote_poss = __any_sync(FULL, lane < K && c == y);
-      // theta = min_j p[j][top_j] / K ; candidate <=> l[m][c] >= lse_m + log(theta) (- slack)
-      float th = lane < K ? __expf(mx - ls) : INFINITY;
-      for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
-      const float lth = logf(th / (float)K);
-      const float thr = (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
-      const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;  // l[m][y]
-      const bool ycand = __any_sync(FULL, lane < K && ly >= thr);
-      if (!vote_poss && !ycand) continue;  // no subset can be correct
+      // averaging candidate test (theta pruning) for the label
+      const float thr = theta_threshold(mx, ls, K, lane);
+      const bool ycand = __any_sync(FULL, lane < K && rowbase[(size_t)lane * p.ldc + y] >= thr);
+      if (ycand) wmask |= 1u << (int)(n - u0);
+      if (!__any_sync(FULL, lane < K && c == y)) continue;  // no member votes y: every vote wrong
+      const bool leader = lane < K && (__ffs(mm) - 1) == lane;
+      const uint32_t lb = __ballot_sync(FULL, leader);
+      const int nd = __popc(lb);
       __syncwarp();
       if (leader) {
         const int pos = __popc(lb & ((1u << lane) - 1u));
-        ws.scls[pos] = c;
-        ws.smsk[pos] = mm;
+        as.scls[pos] = c;
+        as.smsk[pos] = mm;
       }
-      if (lane < K) ws.stop[lane] = tp;
-      int nc = 0, ys = -1;
-      bool ovf = false, tables = false;
-      if (ycand) {
-        // ---- 3. candidate set: one streaming pass, warp-private bitmaps --------------------
-        // R = S_c  ∩  {c : exists m, l[m][c] >= l[m][y]}: a class below y in EVERY model has
-        // avg_v[c] < avg_v[y] for every subset v, so it can never decide "y is the argmax".
-        ws.bitmap[lane] = 0u;
-        ws.bitmapB[lane] = 0u;
-        __syncwarp();
-        for (int m0 = 0; m0 < K; m0 += 2) {  // two rows per step: 16 x 16-byte loads in flight per lane
-          float4 v[2][8];
+      if (lane < K) as.stop[lane] = tp;
+      __syncwarp();
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const float* row = rowbase + (size_t)(m0 + r) * p.ldc;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int c4 = lane + 32 * i;
-              v[r][i] = (m0 + r < K && c4 < F && c4 * 4 < C)
-                            ? ldg_stream(row + c4 * 4)
-                            : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const float t_m = __shfl_sync(FULL, thr, (m0 + r) < K ? m0 + r : 0);
-            const float y_m = __shfl_sync(FULL, ly, (m0 + r) < K ? m0 + r : 0);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int cb = (lane + 32 * i) * 4;
-              uint32_t bits = 0, bitsB = 0;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float x = f4c(v[r][i], e);
-                bits |= (x >= t_m && cb + e < C) ? (1u << e) : 0u;
-                bitsB |= (x >= y_m && cb + e < C) ? (1u << e) : 0u;
-              }
-              if (bits) atomicOr(&ws.bitmap[cb >> 5], bits << (cb & 31));
-              if (bitsB) atomicOr(&ws.bitmapB[cb >> 5], bitsB << (cb & 31));
-            }
-          }
-        }
-        __syncwarp();
-        const uint32_t word = ws.bitmap[lane] & ws.bitmapB[lane];
-        const int cnt = __popc(word);
-        int incl = cnt;
-        for (int off = 1; off < 32; off <<= 1) {
-          const int o = __shfl_up_sync(FULL, incl, off);
-          if (lane >= off) incl += o;
-        }
-        const int pre = incl - cnt;
-        nc = __shfl_sync(FULL, incl, 31);
-        ovf = nc > p.CAP;
-        tables = !ovf && nc <= p.TCAP;
-        int32_t* cls = ovf ? ovC : ws.ccls;
-        {
-          uint32_t w = word;
-          int k = pre;
-          while (w) {
-            const int b = __ffs(w) - 1;
-            cls[k++] = lane * 32 + b;
-            w &= w - 1;
-          }
-        }
-        {
-          const uint32_t wy = __shfl_sync(FULL, word, y >> 5);
-          const int py = __shfl_sync(FULL, pre, y >> 5);
-          ys = py + __popc(wy & ((1u << (y & 31)) - 1u));
-        }
-        __syncwarp();
-        // gather p[m][c] = exp(l - lse_m) for c in S_c
-        float* P = ovf ? ovP : ws.P;
-        const int ps = ovf ? C : CAPS;
-        float lsm[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) lsm[m] = __shfl_sync(FULL, ls, m < K ? m : 0);
-        for (int sl = lane; sl < nc; sl += 32) {
-          const int cq = cls[sl];
-          float l[8];
-#pragma unroll
-          for (int m = 0; m < 8; ++m)  // K independent loads in flight (L2 hits: the rows were just streamed)
-            l[m] = m < K ? __ldg(rowbase + (size_t)m * p.ldc + cq) : 0.f;
-#pragma unroll
-          for (int m = 0; m < 8; ++m)
-            if (m < K) P[(size_t)m * ps + sl] = expf(l[m] - lsm[m]);
-        }
-        __syncwarp();
-        if (tables) {
-          for (int h = 0; h < TT; ++h)
-            for (int sl = lane; sl < nc; sl += 32) {
-              float s = 0.f;
-              if (h < TA) {
-                for (uint32_t a = (uint32_t)h; a; a &= a - 1) s += ws.P[(size_t)(__ffs(a) - 1) * CAPS + sl];
-              } else {
-                for (uint32_t b = (uint32_t)(h - TA); b; b &= b - 1) s += ws.P[(size_t)(p.K1 + __ffs(b) - 1) * CAPS + sl];
-              }
-              ws.T[(size_t)h * TSTR + sl] = s;
-            }
-          __syncwarp();
-        }
-      } else {
-        __syncwarp();
-      }
-      // ---- 4. subsets owned by this lane ---------------------------------------------------
-      uint32_t pending = 0;  // subsets whose averaged decision needs the fp64 recheck
-      const float* Pm = ovf ? ovP : ws.P;
-      const int ps = ovf ? C : CAPS;
-#pragma unroll
-      for (int j = 0; j < JMAX; ++j) {
+      for (int j = 0; j < JMAX; ++j) {  // A3: majority vote
         const uint32_t v = (uint32_t)(lane + 32 * j + 1);
         if (v > (uint32_t)S) break;
-        uint32_t okv = 0, oka = 0;
-        if (vote_poss) {  // A3
-          int bc = 0, bcls = 0x7fffffff;
-          uint32_t tied = 0;
-          for (int q = 0; q < nd; ++q) {
-            const uint32_t mv = v & ws.smsk[q];
-            const int cnt = __popc(mv);
-            const int cq = ws.scls[q];
-            if (cnt > bc) { bc = cnt; bcls = cq; tied = mv; }
-            else if (cnt == bc && cnt > 0) { tied |= mv; bcls = min(bcls, cq); }
-          }
-          const int winner = (p.tie == 0) ? ws.stop[p.best_of[tied]] : bcls;
-          okv = (winner == y);
+        int bc = 0, bcls = 0x7fffffff;
+        uint32_t tied = 0;
+#pragma unroll 1
+        for (int q = 0; q < nd; ++q) {
+          const uint32_t mv = v & as.smsk[q];
+          const int cnt = __popc(mv);
+          const int cq = as.scls[q];
+          if (cnt > bc) { bc = cnt; bcls = cq; tied = mv; }
+          else if (cnt == bc && cnt > 0) { tied |= mv; bcls = min(bcls, cq); }
         }
-        if (ycand) {  // A4
-          if (__popc(v) == 1) {
-            oka = (ws.stop[__ffs(v) - 1] == y);  // softmax is monotone (invariant I1)
-          } else {
-            float sy = 0.f, m2 = -1.f;
-            if (tables) {
-              const float* A = ws.T + (size_t)(v & (TA - 1)) * TSTR;
-              const float* B = ws.T + (size_t)(TA + (v >> p.K1)) * TSTR;
-              sy = A[ys] + B[ys];
-              for (int q = 0; q < nc; ++q) {
-                const float s = A[q] + B[q];
-                if (q != ys) m2 = fmaxf(m2, s);
-              }
-            } else {
-              for (int q = 0; q < nc; ++q) {
-                float s = 0.f;
-                for (uint32_t a = v; a; a &= a - 1) s += Pm[(size_t)(__ffs(a) - 1) * ps + q];
-                if (q == ys) sy = s; else m2 = fmaxf(m2, s);
-              }
-            }
-            if (m2 > sy * (1.f + p.band)) oka = 0;
-            else if (m2 < sy * (1.f - p.band)) oka = 1;
-            else pending |= 1u << j;
-          }
-        }
+        // BEST_MEMBER: best-ranked member among the tied voters (reading Q2); LOWEST_CLASS: min class
+        const int winner = (p.tie == 0) ? as.stop[p.best_of[tied]] : bcls;
+        const uint32_t okv = winner == y;
         gv[j] += okv;
-        ca[j] += oka;
-        if (okv && tm)
-          for (int bi = 0; bi < p.nB; ++bi)
-            if ((tm >> bi) & 1u) atomicAdd(p.tail + (size_t)bi * S + (v - 1), 1ull);
-      }
-      // ---- fp64 recheck of near-ties (rare): warp-cooperative log-sum-exp, then per lane ----
-      if (__any_sync(FULL, pending != 0)) {
-        for (int m = 0; m < K; ++m) {
-          const float* row = rowbase + (size_t)m * p.ldc;
-          const double m64 = (double)__shfl_sync(FULL, mx, m);
-          double s = 0.0;
-          for (int cc = lane; cc < C; cc += 32) s += exp((double)row[cc] - m64);
-          for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-          if (lane == 0) ws.lse64[m] = m64 + log(s);
-        }
-        __syncwarp();
-        const int32_t* cls = ovf ? ovC : ws.ccls;
-#pragma unroll
-        for (int j = 0; j < JMAX; ++j) {
-          if (!((pending >> j) & 1u)) continue;
-          const uint32_t v = (uint32_t)(lane + 32 * j + 1);
-          atomicAdd(p.n_recheck + (v - 1), 1ull);
-          // fp32 sums again to select the band, fp64 decides
-          float sy = 0.f;
-          for (uint32_t a = v; a; a &= a - 1) sy += Pm[(size_t)(__ffs(a) - 1) * ps + ys];
-          const float lo = sy * (1.f - p.band);
-          const int nv = __popc(v);
-          double best = -1.0;
-          int bestc = 0x7fffffff;
-          for (int q = 0; q < nc; ++q) {
-            float s32 = 0.f;
-            for (uint32_t a = v; a; a &= a - 1) s32 += Pm[(size_t)(__ffs(a) - 1) * ps + q];
-            if (q != ys && s32 < lo) continue;
-            const int cq = cls[q];
-            double s = 0.0;
-            for (uint32_t a = v; a; a &= a - 1) {
-              const int m = __ffs(a) - 1;
-              s += exp((double)rowbase[(size_t)m * p.ldc + cq] - ws.lse64[m]);
-            }
-            const double a64 = s / (double)nv;
-            if (a64 > best || (a64 == best && cq < bestc)) { best = a64; bestc = cq; }
-          }
-          ca[j] += (bestc == y);
-        }
+        if (okv && tm) tail_add(p, tm, v);
       }
       __syncwarp();
-    }  // samples of the unit
-    // ---- unit end: group counts (labelled moments) and totals ---------------------------------
+    }
+    // unit end: worklist append (one atomic per unit), group counts, totals
+    if (wmask) {
+      unsigned int base = 0;
+      if (lane == 0) base = atomicAdd(work_count, (unsigned int)__popc(wmask));
+      base = __shfl_sync(FULL, base, 0);
+      if ((wmask >> lane) & 1u) work[base + __popc(wmask & ((1u << lane) - 1u))] = (int32_t)(u0 + lane);
+    }
 #pragma unroll
     for (int j = 0; j < JMAX; ++j) {
       const int v1 = lane + 32 * j;
@@ -427,19 +252,314 @@ __global__ void __launch_bounds__(WT, 2) vote_warp_kernel(const VoteParams p) {
   }
 }
 
+// =============================== kernel B: averages on the worklist ===========================
+struct WS {  // per-warp shared memory
+  double* lse64;    // [8]
+  int32_t* stop;    // [8]
+  uint32_t* bitmap; // [32] S_c (theta test)
+  uint32_t* bitmapB;// [32] classes not below y in some model
+  int32_t* ccls;    // [CAP] candidate classes in ascending order
+  float* P;         // [K][CAP+1]
+  float* T;         // [TT][TCAP|1]
+  float* Q;         // [8]  q_m = max competitor probability of model m
+  float* QB;        // [32] half-mask sums of q (competitor bound)
+  uint32_t* cnt;    // [JMAX][32] lane-owned avg counters
+};
+
+__host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS* w) {
+  const int TT = (1 << p.K1) + (1 << (p.K - p.K1));
+  size_t o = 0;
+  auto take = [&](size_t b) -> char* { char* r = base ? base + o : nullptr; o = a16(o + b); return r; };
+  char* l64 = take(8 * 8);
+  char* st = take(4 * 8);
+  char* bm = take(4 * 32);
+  char* bmB = take(4 * 32);
+  char* cc = take(4ull * p.CAP);
+  char* P = take(4ull * p.K * (p.CAP + 1));
+  char* T = take(4ull * TT * (p.TCAP | 1));
+  char* Q = take(4 * 8);
+  char* QB = take(4 * 32);
+  char* CN = take(4 * JMAX * 32);
+  if (w) {
+    w->lse64 = (double*)l64; w->stop = (int32_t*)st; w->bitmap = (uint32_t*)bm; w->bitmapB = (uint32_t*)bmB;
+    w->ccls = (int32_t*)cc; w->P = (float*)P; w->T = (float*)T; w->Q = (float*)Q; w->QB = (float*)QB;
+    w->cnt = (uint32_t*)CN;
+  }
+  return o;
+}
+
+// fp64 recheck of near-ties (rare, out of line): warp-cooperative fp64 log-sum-exp of every row, then
+// each lane decides its pending subsets exactly like the oracle (avg = (sum_{m in v, asc}
+// exp(l - lse_m)) / |v|, lowest class on ties) over the candidates inside the band.
+__device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t pending, const float* rowbase,
+                                          float mx, const float* Pm, int ps, const int32_t* cls, int nc, int ys,
+                                          int y, int lane) {
+  const int K = p.K, C = p.C;
+  for (int m = 0; m < K; ++m) {
+    const float* row = rowbase + (size_t)m * p.ldc;
+    const double m64 = (double)__shfl_sync(FULL, mx, m);
+    double s = 0.0;
+    for (int cc = lane; cc < C; cc += 32) s += exp((double)row[cc] - m64);
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (lane == 0) ws.lse64[m] = m64 + log(s);
+  }
+  __syncwarp();
+  for (int j = 0; j < JMAX; ++j) {
+    if (!((pending >> j) & 1u)) continue;
+    const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+    atomicAdd(p.n_recheck + (v - 1), 1ull);
+    float sy = 0.f;  // fp32 sums again select the band; fp64 decides
+    for (uint32_t a = v; a; a &= a - 1) sy += Pm[(size_t)(__ffs(a) - 1) * ps + ys];
+    const float lo = sy * (1.f - p.band);
+    const int nv = __popc(v);
+    double best = -1.0;
+    int bestc = 0x7fffffff;
+    for (int q = 0; q < nc; ++q) {
+      float s32 = 0.f;
+      for (uint32_t a = v; a; a &= a - 1) s32 += Pm[(size_t)(__ffs(a) - 1) * ps + q];
+      if (q != ys && s32 < lo) continue;
+      const int cq = cls[q];
+      double s = 0.0;
+      for (uint32_t a = v; a; a &= a - 1) {
+        const int m = __ffs(a) - 1;
+        s += exp((double)rowbase[(size_t)m * p.ldc + cq] - ws.lse64[m]);
+      }
+      const double a64 = s / (double)nv;
+      if (a64 > best || (a64 == best && cq < bestc)) { best = a64; bestc = cq; }
+    }
+    ws.cnt[j * 32 + lane] += (bestc == y);
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(WT, 4) vote_average_kernel(const VoteParams p, const int32_t* work,
+                                                              const unsigned int* work_count) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WS ws;
+  warp_smem(p, smem_raw + warp * warp_smem(p, nullptr, nullptr), &ws);
+  const int K = p.K, S = p.S, C = p.C;
+  const int F = (int)(p.ldc >> 2);
+  const int TA = 1 << p.K1, TT = TA + (1 << (K - p.K1));
+  const int TSTR = p.TCAP | 1, CAPS = p.CAP + 1;
+  const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
+  const int64_t nw = (int64_t)gridDim.x * WPC;
+  float* ovP = p.scratch + gw * (size_t)K * C;  // overflow candidate matrix [K][C]
+  int32_t* ovC = p.scratch_cls + gw * (size_t)C;
+  for (int i = lane; i < JMAX * 32; i += 32) ws.cnt[i] = 0u;
+  const int64_t W = *work_count;
+
+  for (int64_t e = gw; e < W; e += nw) {
+    const int64_t n = work[e];
+    const int y = p.labels[n];
+    const float* rowbase = p.logits + n * K * p.ldc;
+    int tp = 0;
+    float mx = 0.f, ls = 0.f;
+    if (lane < K) {
+      tp = p.top1_in[n * K + lane];
+      ls = p.lse_in[n * K + lane];
+      mx = p.rmax_in[n * K + lane];
+    }
+    const float thr = theta_threshold(mx, ls, K, lane);
+    const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;  // l[m][y]
+    __syncwarp();
+    if (lane < K) ws.stop[lane] = tp;
+    ws.bitmap[lane] = 0u;
+    ws.bitmapB[lane] = 0u;
+    __syncwarp();
+    // ---- candidate set R: one streaming pass over the sample's K rows ------------------------
+#pragma unroll 1
+    for (int m = 0; m < K; ++m) {
+      const float* row = rowbase + (size_t)m * p.ldc;
+      float4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c4 = lane + 32 * i;
+        v[i] = (c4 < F && c4 * 4 < C) ? ldg_stream(row + c4 * 4)
+                                       : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+      const float t_m = __shfl_sync(FULL, thr, m);
+      const float y_m = __shfl_sync(FULL, ly, m);
+      const float lo = fminf(t_m, y_m);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 x4 = v[i];
+        // fast reject: almost every float4 is below both thresholds (fmaxf drops NaN padding)
+        if (fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)) >= lo) {
+          const int cb = (lane + 32 * i) * 4;
+          uint32_t bits = 0, bitsB = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float x = f4c(x4, q);
+            bits |= (x >= t_m && cb + q < C) ? (1u << q) : 0u;
+            bitsB |= (x >= y_m && cb + q < C) ? (1u << q) : 0u;
+          }
+          if (bits) atomicOr(&ws.bitmap[cb >> 5], bits << (cb & 31));
+          if (bitsB) atomicOr(&ws.bitmapB[cb >> 5], bitsB << (cb & 31));
+        }
+      }
+    }
+    __syncwarp();
+    const uint32_t word = ws.bitmap[lane] & ws.bitmapB[lane];
+    const int cnt = __popc(word);
+    int incl = cnt;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(FULL, incl, off);
+      if (lane >= off) incl += o;
+    }
+    const int pre = incl - cnt;
+    const int nc = __shfl_sync(FULL, incl, 31);
+    const bool ovf = nc > p.CAP;
+    const bool tables = !ovf && nc <= p.TCAP;
+    int32_t* cls = ovf ? ovC : ws.ccls;
+    {
+      uint32_t w = word;
+      int k = pre;
+      while (w) {
+        cls[k++] = lane * 32 + (__ffs(w) - 1);
+        w &= w - 1;
+      }
+    }
+    const int ys = __shfl_sync(FULL, pre, y >> 5) +
+                   __popc(__shfl_sync(FULL, word, y >> 5) & ((1u << (y & 31)) - 1u));
+    __syncwarp();
+    // ---- gather p[m][c] = exp(l - lse_m) for c in R ------------------------------------------
+    float* P = ovf ? ovP : ws.P;
+    const int ps = ovf ? C : CAPS;
+    float lsm[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) lsm[m] = __shfl_sync(FULL, ls, m < K ? m : 0);
+    for (int sl = lane; sl < nc; sl += 32) {
+      const int cq = cls[sl];
+      float l[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)  // K independent loads in flight (L2 hits: the rows were just streamed)
+        l[m] = m < K ? __ldg(rowbase + (size_t)m * p.ldc + cq) : 0.f;
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (m < K) P[(size_t)m * ps + sl] = expf(l[m] - lsm[m]);
+    }
+    __syncwarp();
+    // ---- competitor bound: q_m = max_{c in R, c != y} p[m][c]; QB = half-mask sums of q -------
+#pragma unroll 1
+    for (int m = 0; m < K; ++m) {
+      float q = 0.f;
+      for (int sl = lane; sl < nc; sl += 32)
+        if (sl != ys) q = fmaxf(q, P[(size_t)m * ps + sl]);
+      for (int off = 16; off; off >>= 1) q = fmaxf(q, __shfl_xor_sync(FULL, q, off));
+      if (lane == 0) ws.Q[m] = q;
+    }
+    __syncwarp();
+    if (lane < TT) {
+      float s = 0.f;
+      if (lane < TA) {
+        for (uint32_t a = (uint32_t)lane; a; a &= a - 1) s += ws.Q[__ffs(a) - 1];
+      } else {
+        for (uint32_t b = (uint32_t)(lane - TA); b; b &= b - 1) s += ws.Q[p.K1 + __ffs(b) - 1];
+      }
+      ws.QB[lane] = s * (1.f + 1e-6f);  // round the bound up past fp32 summation error
+    }
+    // ---- half tables: A[a][c] = sum_{m in a, asc} p[m][c] (low models), B likewise (high) ------
+    if (tables) {
+#pragma unroll 1
+      for (int h = 0; h < TT; ++h)
+        for (int sl = lane; sl < nc; sl += 32) {
+          float s = 0.f;
+          if (h < TA) {
+            for (uint32_t a = (uint32_t)h; a; a &= a - 1) s += ws.P[(size_t)(__ffs(a) - 1) * CAPS + sl];
+          } else {
+            for (uint32_t b = (uint32_t)(h - TA); b; b &= b - 1) s += ws.P[(size_t)(p.K1 + __ffs(b) - 1) * CAPS + sl];
+          }
+          ws.T[(size_t)h * TSTR + sl] = s;
+        }
+    }
+    __syncwarp();
+    // ---- A4: averaged-probability decision of every subset ------------------------
+    uint32_t pending = 0;  // subsets whose decision needs the fp64 recheck
+#pragma unroll 1
+    for (int j = 0; j < JMAX; ++j) {
+      const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+      if (v > (uint32_t)S) break;
+      uint32_t oka = 0;
+      if (__popc(v) == 1) {
+        oka = (ws.stop[__ffs(v) - 1] == y);  // softmax is monotone (invariant I1)
+      } else {
+        float sy = 0.f, m2 = -1.f;
+        const float* A = ws.T + (size_t)(v & (TA - 1)) * TSTR;
+        const float* B = ws.T + (size_t)(TA + (v >> p.K1)) * TSTR;
+        if (tables) {
+          sy = A[ys] + B[ys];
+        } else {
+          for (uint32_t a = v; a; a &= a - 1) sy += P[(size_t)(__ffs(a) - 1) * ps + ys];
+        }
+        const float bnd = ws.QB[v & (TA - 1)] + ws.QB[TA + (v >> p.K1)];
+        if (bnd < sy * (1.f - 2.f * p.band)) {
+          oka = 1;  // no competitor can reach y: decided without scanning R
+        } else {
+          if (tables) {
+            for (int q = 0; q < nc; ++q) {
+              const float s = A[q] + B[q];
+              if (q != ys) m2 = fmaxf(m2, s);
+            }
+          } else {
+            for (int q = 0; q < nc; ++q) {
+              if (q == ys) continue;
+              float s = 0.f;
+              for (uint32_t a = v; a; a &= a - 1) s += P[(size_t)(__ffs(a) - 1) * ps + q];
+              m2 = fmaxf(m2, s);
+            }
+          }
+          if (m2 > sy * (1.f + p.band)) oka = 0;
+          else if (m2 < sy * (1.f - p.band)) oka = 1;
+          else pending |= 1u << j;
+        }
+      }
+      ws.cnt[j * 32 + lane] += oka;
+    }
+    if (__any_sync(FULL, pending != 0)) recheck_fp64(p, ws, pending, rowbase, mx, P, ps, cls, nc, ys, y, lane);
+    __syncwarp();
+  }
+#pragma unroll 1
+  for (int j = 0; j < JMAX; ++j) {
+    const int v1 = lane + 32 * j;
+    const uint32_t c = ws.cnt[j * 32 + lane];
+    if (v1 < S && c) atomicAdd(p.cnt_avg + v1, (unsigned long long)c);
+  }
+}
+
 }  // namespace
 
 size_t vote_warp_smem_per_warp(const VoteParams& p) { return warp_smem(p, nullptr, nullptr); }
 int vote_warp_threads() { return WT; }
+int vote_warp_min_blocks() { return 4; }
 
-cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st) {
+cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
+                             int32_t* st_top, float* st_lse, float* st_max, int sm_count) {
   if (p.N <= 0) return cudaSuccess;
-  const size_t smem = warp_smem(p, nullptr, nullptr) * WPC;
-  auto k = p.lse_in ? vote_warp_kernel<true> : vote_warp_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaMemsetAsync(work_count, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
-  k<<<grid, WT, smem, st>>>(p);
-  return cudaGetLastError();
+  // kernel A: classify + votes
+  {
+    const int U = p.gs > 0 ? p.gs : 16;
+    const int64_t units = (p.N + U - 1) / U;
+    int64_t ga = (units + WPC - 1) / WPC;
+    if (ga > (int64_t)sm_count * 8) ga = (int64_t)sm_count * 8;
+    if (p.lse_in) vote_classify_kernel<true><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+    else vote_classify_kernel<false><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // kernel B: averages on the worklist (always from statistics: the GEMM's or kernel A's)
+  {
+    VoteParams q = p;
+    if (!p.lse_in) { q.top1_in = st_top; q.lse_in = st_lse; q.rmax_in = st_max; }
+    const size_t smem = warp_smem(q, nullptr, nullptr) * WPC;
+    if ((e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    vote_average_kernel<<<grid, WT, smem, st>>>(q, work, work_count);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace rk
