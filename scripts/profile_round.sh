@@ -1,0 +1,11 @@
+# Round profiling: (1) launch list of the bench command, (2) --set full of the GEMM, (3) of the vote kernels.
+R=${ROUND:-r01}
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv \
+  python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${R}_launches_bench.json 2> gpurun_out/${R}_launches.err
+echo "launches rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_heads -c 1 -o gpurun_out/${R}_gemm \
+  python scripts/prof_vote.py --K 8 --C 1000 --N 65536 --gemm 2048 --reps 1 > gpurun_out/${R}_gemm.log 2>&1
+echo "gemm rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:vote -c 2 -o gpurun_out/${R}_vote \
+  python scripts/prof_vote.py --K 8 --C 1000 --N 200000 --gemm 2048 --reps 1 > gpurun_out/${R}_vote.log 2>&1
+echo "vote rc=$?"

@@ -1,0 +1,80 @@
+"""Summarise the round's ncu artefacts (gpurun_out/<R>_*) into profiles/<R>_*.md / .json (committed)."""
+import collections
+import csv
+import json
+import re
+import subprocess
+import sys
+
+R = sys.argv[1] if len(sys.argv) > 1 else "r01"
+OUT = "profiles"
+
+
+def short(name):
+    name = re.sub(r"\(.*", "", name)
+    name = re.sub(r"^void ", "", name)
+    return name.split("::")[-1]
+
+
+# ---- launch list of the bench command ------------------------------------------------------
+rows = [r for r in csv.reader(open(f"gpurun_out/{R}_launches.csv")) if len(r) == 15 and r[0] != "ID"]
+per = collections.OrderedDict()
+for r in rows:
+    k = short(r[4])
+    d = per.setdefault(k, [0, 0.0])
+    d[0] += 1
+    d[1] += float(r[14]) / 1e6
+ours = {"gemm_heads_kernel", "vote_classify_kernel", "vote_average_kernel", "vote_kernel", "overdue_kernel",
+        "merge_kernel", "q_kernel", "fold_kernel"}
+tot_ours = sum(v[1] for k, v in per.items() if any(k.startswith(o) for o in ours))
+lines = [f"# {R} launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of",
+         "`python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1`",
+         "", "Cold-cache, serialised per-launch times (compare SHARES, not absolutes). Raw CSV: "
+         f"`{R}_launches.csv`.", "", "| kernel | launches | total ms | ms/launch | share of our kernels |",
+         "|---|---|---|---|---|"]
+for k, (n, ms) in per.items():
+    ours_k = any(k.startswith(o) for o in ours)
+    share = f"{100 * ms / tot_ours:.1f} %" if ours_k else "(harness)"
+    lines.append(f"| {k} | {n} | {ms:.3f} | {ms / n:.3f} | {share} |")
+open(f"{OUT}/{R}_launches.md", "w").write("\n".join(lines) + "\n")
+subprocess.run(["cp", f"gpurun_out/{R}_launches.csv", f"{OUT}/{R}_launches.csv"])
+
+
+# ---- --set full captures ----------------------------------------------------------------------
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(out.splitlines()))
+    hdr, units = rr[0], rr[1]
+    res = []
+    for r in rr[2:]:
+        res.append({h: (f"{v} {u}".strip() if u else v) for h, v, u in zip(hdr, r, units)})
+    return res
+
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "smsp__inst_executed.sum", "launch__grid_size", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
+summary = {}
+for tag in ("gemm", "vote"):
+    try:
+        recs = raw(f"gpurun_out/{R}_{tag}.ncu-rep")
+    except Exception as e:  # noqa: BLE001
+        print("skip", tag, e)
+        continue
+    for rec in recs:
+        name = short(rec.get("Kernel Name", "?"))
+        d = {}
+        for w in WANT:
+            for k, v in rec.items():
+                if k.startswith(w):
+                    d[k] = v
+        summary[f"{tag}:{name}"] = d
+json.dump(summary, open(f"{OUT}/{R}_ncu_full.json", "w"), indent=1)
+print(open(f"{OUT}/{R}_launches.md").read())
+for k, d in summary.items():
+    print(k)
+    for kk, vv in d.items():
+        print("   ", kk, vv)
