@@ -63,6 +63,9 @@ struct rk_ctx {
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[3 * 128];
+  cudaStream_t copy_stream = nullptr;  // H2D of host X, overlapped with the GEMM
+  cudaEvent_t ev_start = nullptr;
+  std::vector<cudaEvent_t> ev_chunks;
   // accumulation state
   bool reset_done = false, final_seen = false;
   bool has_cfg = false;
@@ -222,6 +225,9 @@ void rk_destroy(rk_ctx* ctx) {
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   for (auto e : ctx->prof.pool) cudaEventDestroy(e);
+  for (auto e : ctx->ev_chunks) cudaEventDestroy(e);
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   delete ctx;
 }
@@ -301,12 +307,6 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
   if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
-  const void* Xd = X;
-  if (N > 0 && !is_device_ptr(X)) {
-    if ((s = ensure(ctx, &ctx->ws_x, &ctx->ws_x_cap, N * ctx->D)) != RK_OK) return s;
-    CK(cudaMemcpyAsync(ctx->ws_x, X, (size_t)N * ctx->D * 2, cudaMemcpyHostToDevice, st));
-    Xd = ctx->ws_x;
-  }
   ctx->cur_logits = ctx->ws_logits;
   ctx->cur_ldc = ctx->ldc;
   ctx->cur_N = N;
@@ -314,16 +314,44 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
   ctx->batch_stats = true;
   ctx->have_batch = true;
   if (N == 0) return RK_OK;
-  GemmParams gp{};
-  gp.N = N; gp.K = ctx->K; gp.C = ctx->C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
-  gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias; gp.top1 = ctx->ws_top1; gp.lse = ctx->ws_lse;
-  gp.rmax = ctx->ws_max;
-  gp.logits = ctx->ws_logits;
-  int rc = gemm_build_tmaps(gp, Xd, ctx->d_W, ctx->ws_logits, ctx->tmaps);
-  if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
-  const double flops = 2.0 * N * ctx->D * (double)ctx->K * ctx->C;
-  {
-    ProfScope ps(ctx, KK_GEMM, st, (double)N * ctx->D * 2 + (double)N * ctx->K * ctx->C * 4, flops);
+  // Host X: the H2D copy of chunk i+1 (copy stream) overlaps the GEMM of chunk i (caller stream).
+  // Device X: one launch over all rows.
+  const bool host = !is_device_ptr(X);
+  const int64_t chunk = host ? std::max<int64_t>(65536, ((N + 7) / 8 + 127) / 128 * 128) : N;
+  if (host) {
+    if ((s = ensure(ctx, &ctx->ws_x, &ctx->ws_x_cap, N * ctx->D)) != RK_OK) return s;
+    if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    if (!ctx->ev_start) CK(cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->ev_start, st));  // copies must not overwrite ws_x still read by earlier work
+    CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_start, 0));
+  }
+  for (int64_t r0 = 0, ci = 0; r0 < N; r0 += chunk, ++ci) {
+    const int64_t n = std::min(chunk, N - r0);
+    const void* Xd = X;
+    if (host) {
+      uint16_t* dst = ctx->ws_x + r0 * ctx->D;
+      CK(cudaMemcpyAsync(dst, static_cast<const uint16_t*>(X) + r0 * ctx->D, (size_t)n * ctx->D * 2,
+                         cudaMemcpyHostToDevice, ctx->copy_stream));
+      if ((int64_t)ctx->ev_chunks.size() <= ci) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->ev_chunks.push_back(e);
+      }
+      CK(cudaEventRecord(ctx->ev_chunks[ci], ctx->copy_stream));
+      CK(cudaStreamWaitEvent(st, ctx->ev_chunks[ci], 0));
+      Xd = dst;
+    } else {
+      Xd = static_cast<const uint16_t*>(X) + r0 * ctx->D;
+    }
+    GemmParams gp{};
+    gp.N = n; gp.K = ctx->K; gp.C = ctx->C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
+    gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias;
+    gp.top1 = ctx->ws_top1 + r0 * ctx->K; gp.lse = ctx->ws_lse + r0 * ctx->K; gp.rmax = ctx->ws_max + r0 * ctx->K;
+    gp.logits = ctx->ws_logits + r0 * ctx->K * ctx->ldc;
+    int rc = gemm_build_tmaps(gp, Xd, ctx->d_W, gp.logits, ctx->tmaps);  // maps are passed by value
+    if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
+    const double flops = 2.0 * n * ctx->D * (double)ctx->K * ctx->C;
+    ProfScope ps(ctx, KK_GEMM, st, (double)n * ctx->D * 2 + (double)n * ctx->K * ctx->C * 4, flops);
     CK(launch_gemm(gp, ctx->sm_count, st));
   }
   return RK_OK;
