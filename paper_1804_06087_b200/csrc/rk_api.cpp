@@ -502,23 +502,16 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     vp.labels = dl; vp.N = N; vp.K = K; vp.C = C; vp.S = S; vp.tie = ctx->tie;
     const int gs = (ctx->want_labelled && nB > 0 && nR > 0) ? ctx->gs : 0;
     vp.rmax_in = ctx->batch_stats ? ctx->ws_max : nullptr;
-    // K <= 8: barrier-free warp-per-sample kernel; K > 8 (up to 4095 subsets): CTA-tile kernel
-    const bool warp_path = K <= 8 && ctx->cur_ldc <= 1024;
-    VoteLayout L = choose_vote_layout(K, C, (int)ctx->cur_ldc, gs, ctx->sm_count);
-    if (warp_path) L.G = 1;
-    vp.LPR = L.LPR; vp.VPL = L.VPL; vp.RS = L.RS; vp.G = L.G;
+    // K <= 8: warp-per-sample kernels (rk_vote_warp.cu); K = 9..12: batch-transposed (rk_vote_batch.cu)
+    const bool warp_path = K <= 8;
+    vp.G = 1;
     vp.gs = gs;
-    vp.U = std::max(L.G, gs);
+    vp.U = std::max(1, gs);
     vp.nW32 = (C + 31) / 32;
     vp.K1 = K / 2;
     const int TT = (1 << vp.K1) + (1 << (K - vp.K1));
-    if (warp_path) {
-      vp.CAP = 96;
-      vp.TCAP = std::min(vp.CAP, (int)(6272 / (4 * TT)));
-    } else {
-      vp.CAP = 128;
-      vp.TCAP = std::max(0, std::min((int)(16384 / (4 * (size_t)TT * L.G)), vp.CAP));
-    }
+    vp.CAP = warp_path ? 96 : 64;
+    vp.TCAP = warp_path ? std::min(vp.CAP, (int)(6272 / (4 * TT))) : std::min(vp.CAP, (int)(16384 / (4 * TT)) - 1);
     vp.band = 2e-5f;
     vp.best_of = ctx->d_best_of;
     vp.nB = nB;
@@ -535,32 +528,20 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       }
       vp.grp = ctx->d_grp;
     }
+    int grid = 0;
     if (warp_path) {
       const int wt = vote_warp_threads();
       const size_t smem = vote_warp_smem_per_warp(vp) * (wt / 32);
       const int per_sm = (int)std::max<size_t>(
           1, std::min<size_t>((size_t)vote_warp_min_blocks(), (227 * 1024) / (smem + 1024)));
       const int64_t units = (N + (gs > 0 ? gs : 16) - 1) / (gs > 0 ? gs : 16);
-      L.grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + wt / 32 - 1) / (wt / 32), (int64_t)ctx->sm_count * per_sm));
-      L.smem = smem;
-    } else {
-    // ring depth: fill the per-CTA shared-memory budget (2 CTAs/SM when >= 2 slots fit)
-    {
-      vp.NSTAGE = 0;
-      const size_t base = vote_smem_bytes(vp), slot = vote_slot_bytes(vp);
-      const size_t half = 112 * 1024, full = 224 * 1024;
-      int per_sm = 2;
-      int ns = (int)((half - std::min(half, base)) / slot);
-      if (ns < 2) { per_sm = 1; ns = (int)((full - std::min(full, base)) / slot); }
-      if (ns < 2) return fail(ctx, RK_EUNSUPPORTED, "vote kernel: tile does not fit in shared memory");
-      vp.NSTAGE = std::min(ns, 8);
-      L.smem = vote_smem_bytes(vp);
-      const int64_t units = (N + vp.U - 1) / vp.U;
-      L.grid = (int)std::min<int64_t>(units, (int64_t)ctx->sm_count * per_sm);
+      grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + wt / 32 - 1) / (wt / 32), (int64_t)ctx->sm_count * per_sm));
+    } else if (vote_batch_smem_per_sample(vp) * vote_batch_avg_ctas_samples() > 220 * 1024) {
+      return fail(ctx, RK_EUNSUPPORTED, "vote kernel: per-sample tables do not fit in shared memory");
     }
-    }
-    // overflow scratch: per CTA x G samples (tile kernel) or per warp (warp kernel)
-    const size_t owners = warp_path ? (size_t)L.grid * (vote_warp_threads() / 32) : (size_t)L.grid * L.G;
+    // overflow scratch (candidate sets larger than CAP): one region per warp
+    const size_t owners = warp_path ? (size_t)grid * (vote_warp_threads() / 32)
+                                    : (size_t)ctx->sm_count * vote_batch_avg_ctas_samples();
     const size_t sf = owners * C * K, si = owners * C;
     if (ctx->scratch_floats < sf) {
       if (ctx->d_scratch) cudaFree(ctx->d_scratch);
@@ -577,23 +558,20 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     vp.scratch = ctx->d_scratch;
     vp.scratch_cls = ctx->d_scratch_cls;
     {
+      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, N + 1)) != RK_OK) return s;  // worklist [N] + count
+      int32_t* st_top = nullptr;
+      float *st_lse = nullptr, *st_max = nullptr;
+      if (!ctx->batch_stats) {  // the classify kernel writes row statistics for the averaging kernel
+        if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, N * K)) != RK_OK) return s;
+        if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, N * K)) != RK_OK) return s;
+        if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, N * K)) != RK_OK) return s;
+        st_top = ctx->ws_top1; st_lse = ctx->ws_lse; st_max = ctx->ws_max;
+      }
+      unsigned int* wc = reinterpret_cast<unsigned int*>(ctx->d_work + N);
       const double bytes = (double)N * ((double)K * C * 4 + 4);
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
-      if (warp_path) {
-        if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, N + 1)) != RK_OK) return s;  // [N] list + count
-        int32_t* st_top = nullptr;
-        float *st_lse = nullptr, *st_max = nullptr;
-        if (!ctx->batch_stats) {  // kernel A writes row statistics for kernel B
-          if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, N * K)) != RK_OK) return s;
-          if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, N * K)) != RK_OK) return s;
-          if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, N * K)) != RK_OK) return s;
-          st_top = ctx->ws_top1; st_lse = ctx->ws_lse; st_max = ctx->ws_max;
-        }
-        CK(launch_vote_warp(vp, L.grid, st, ctx->d_work, reinterpret_cast<unsigned int*>(ctx->d_work + N), st_top,
-                            st_lse, st_max, ctx->sm_count));
-      } else {
-        CK(launch_vote(vp, L, st));
-      }
+      if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lse, st_max, ctx->sm_count));
+      else CK(launch_vote_batch(vp, ctx->sm_count, st, ctx->d_work, wc, st_top, st_lse, st_max));
     }
     // ---- A5: batch latency moments (label independent) ----
     const int64_t* arr = nullptr;

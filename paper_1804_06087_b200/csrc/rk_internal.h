@@ -22,19 +22,14 @@ struct VoteParams {
   const int32_t* labels;     // [N] device
   int64_t N;                 // samples in this chunk
   int K, C, S, tie;
-  // thread <-> data mapping (host heuristic, see choose_vote_layout)
-  int LPR;                   // lanes per row (power of 2, <= 32)
-  int VPL;                   // float4 per lane per row slot
-  int RS;                    // rows per pass = 256 / LPR
-  int G;                     // samples per tile (power of 2)
+  int G;                     // samples per tile (1)
   int gs;                    // samples per count group (power of 2 dividing gcd(B)); 0 = no groups
-  int U;                     // samples per unit = max(G, gs)
+  int U;                     // samples per unit
   int nW32;                  // ceil(C / 32) candidate-bitmap words
   int CAP;                   // candidate capacity (P matrix in smem)
   int TCAP;                  // candidate capacity of the subset-sum tables in smem
   int K1;                    // low half of the models for the subset-sum tables
   float band;                // relative fp32 near-tie band -> fp64 recheck
-  int NSTAGE;                // logits ring depth (tiles in flight per CTA, TMA bulk copies)
   const uint8_t* best_of;    // [2^K] best-ranked model in a mask (device)
   int nB;
   int64_t tail_start[kMaxB]; // local sample index from which a sample is in the tail of B[b]
@@ -49,21 +44,22 @@ struct VoteParams {
   unsigned int* err;              // [0] non-finite logits, [1] bad label
 };
 
-struct VoteLayout {
-  int LPR, VPL, RP, RS, G, NV;
-  size_t smem;
-  int grid;
-};
-
-VoteLayout choose_vote_layout(int K, int C, int ldc, int gs, int sm_count);
-size_t vote_smem_bytes(const VoteParams& p);   // includes NSTAGE ring slots
-size_t vote_slot_bytes(const VoteParams& p);   // one ring slot (G*K*ldc*4, 128-aligned)
-cudaError_t launch_vote(const VoteParams& p, const VoteLayout& L, cudaStream_t st);
-
 // warp-per-sample variant for K <= 8, C <= 1024 (rk_vote_warp.cu); uses CAP, TCAP, K1, gs, scratch
 size_t vote_warp_smem_per_warp(const VoteParams& p);
 int vote_warp_threads();
 int vote_warp_min_blocks();
+// averaging kernel of the warp path (rk_vote_avg.cu)
+size_t vote_avg_smem_per_warp(const VoteParams& p);
+cudaError_t launch_vote_avg(const VoteParams& q, int grid, cudaStream_t st, const int32_t* work,
+                            const unsigned int* work_count);
+
+// K = 9..12 (rk_vote_batch.cu): the same two-kernel split with a batch-transposed layout (threads
+// own subsets, sweep a batch of per-sample records in shared memory).
+size_t vote_batch_smem_per_sample(const VoteParams& p);
+int vote_batch_avg_ctas_samples();
+cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work,
+                              unsigned int* work_count, int32_t* st_top, float* st_lse, float* st_max);
+
 // Two kernels: classify+votes over all samples, then averages over the worklist of samples whose
 // label is an averaging candidate. work: [N] int32, work_count: 1 uint; st_*: [N][K] statistics
 // scratch (written by kernel A when the logits came without statistics).

@@ -1,0 +1,349 @@
+// rk_vote_avg.cu — step A4 for K <= 8: averaged-probability decision of every subset for the
+// worklist samples (label y is an averaging candidate), one WARP per sample.
+//
+// PAPER.md:72 "ensemble multiple models and average the results" (softmax average, reading Q5;
+// lowest class on ties, Q6); :429 every non-empty subset is an action.
+//
+// Per sample:
+//   1. one coalesced streaming pass over the K*ldc logits marks
+//        R = S_c ∩ {c : exists m, l[m][c] >= l[m][y]}
+//      S_c = {c : exists m, p[m][c] >= theta}, theta = min_j p[j][top_j] / K (the averaged argmax of
+//      every subset lies in S_c); a class below y in EVERY model has
+//      avg_v[c] < avg_v[y] for all v and can never decide whether y wins;
+//   2. p[m][c] = exp(l - lse_m) is gathered for c in R (slots in class order, warp scan);
+//   3. the members' distinct top-1 classes other than y (D, at most K) are the natural competitors:
+//      their subset sums, and y's, come from half-mask tables (one add per subset and column);
+//      every other candidate is bounded by Q[v] = sum_{m in v} max_{c in R \ ({y} ∪ D)} p[m][c];
+//   4. per subset: a D-class clearly above y -> wrong; D and the bound clearly below -> right;
+//      bound not conclusive -> scan R; decisions inside the relative band `band` are redone in fp64
+//      (warp-cooperative fp64 log-sum-exp, then the oracle's formula) -- rare.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "rk_internal.h"
+
+namespace rk {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int WT = 128;  // threads per CTA (4 warps)
+constexpr int WPC = WT / 32;
+constexpr int JMAX = 8;  // subsets per lane (S <= 255)
+constexpr int DSTR = 9;  // exact columns: y + up to 8 distinct top-1 classes (odd stride)
+
+__device__ __forceinline__ float4 ldg_stream(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int lane) {
+  float th = lane < K ? __expf(mx - ls) : INFINITY;
+  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
+  const float lth = logf(th / (float)K);
+  return (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
+}
+
+struct WS {  // per-warp shared memory
+  double* lse64;    // [8]
+  int32_t* stop;    // [8] top-1 per model
+  uint32_t* bitmap; // [32] S_c (theta test)
+  uint32_t* bitmapB;// [32] classes not below y in some model
+  int32_t* ccls;    // [CAP] candidate classes in ascending order
+  float* P;         // [K][CAP+1]
+  float* T;         // [32][DSTR] half-mask sums of the exact columns (col 0 = y, 1.. = D)
+  float* QB;        // [32] half-mask sums of the competitor bound
+  float* Q;         // [8]
+  uint32_t* cnt;    // [JMAX][32] lane-owned avg counters
+};
+
+__host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS* w) {
+  size_t o = 0;
+  auto take = [&](size_t b) -> char* { char* r = base ? base + o : nullptr; o = a16(o + b); return r; };
+  char* l64 = take(8 * 8);
+  char* st = take(4 * 8);
+  char* bm = take(4 * 32);
+  char* bmB = take(4 * 32);
+  char* cc = take(4ull * p.CAP);
+  char* P = take(4ull * p.K * (p.CAP + 1));
+  char* T = take(4ull * 32 * DSTR);
+  char* QB = take(4 * 32);
+  char* Q = take(4 * 8);
+  char* CN = take(4 * JMAX * 32);
+  if (w) {
+    w->lse64 = (double*)l64; w->stop = (int32_t*)st; w->bitmap = (uint32_t*)bm; w->bitmapB = (uint32_t*)bmB;
+    w->ccls = (int32_t*)cc; w->P = (float*)P; w->T = (float*)T; w->QB = (float*)QB; w->Q = (float*)Q;
+    w->cnt = (uint32_t*)CN;
+  }
+  return o;
+}
+
+// fp64 recheck of near-ties (rare, out of line): warp-cooperative fp64 log-sum-exp of every row, then
+// each lane decides its pending subsets exactly like the oracle (avg = (sum_{m in v, asc}
+// exp(l - lse_m)) / |v|, lowest class on ties) over the candidates inside the band.
+__device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t pending, const float* rowbase,
+                                          float mx, const float* Pm, int ps, const int32_t* cls, int nc, int ys,
+                                          int y, int lane) {
+  const int K = p.K, C = p.C;
+  for (int m = 0; m < K; ++m) {
+    const float* row = rowbase + (size_t)m * p.ldc;
+    const double m64 = (double)__shfl_sync(FULL, mx, m);
+    double s = 0.0;
+    for (int cc = lane; cc < C; cc += 32) s += exp((double)row[cc] - m64);
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (lane == 0) ws.lse64[m] = m64 + log(s);
+  }
+  __syncwarp();
+  for (int j = 0; j < JMAX; ++j) {
+    if (!((pending >> j) & 1u)) continue;
+    const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+    atomicAdd(p.n_recheck + (v - 1), 1ull);
+    float sy = 0.f;  // fp32 sums select the band; fp64 decides
+    for (uint32_t a = v; a; a &= a - 1) sy += Pm[(size_t)(__ffs(a) - 1) * ps + ys];
+    const float lo = sy * (1.f - p.band);
+    const int nv = __popc(v);
+    double best = -1.0;
+    int bestc = 0x7fffffff;
+    for (int q = 0; q < nc; ++q) {
+      float s32 = 0.f;
+      for (uint32_t a = v; a; a &= a - 1) s32 += Pm[(size_t)(__ffs(a) - 1) * ps + q];
+      if (q != ys && s32 < lo) continue;
+      const int cq = cls[q];
+      double s = 0.0;
+      for (uint32_t a = v; a; a &= a - 1) {
+        const int m = __ffs(a) - 1;
+        s += exp((double)rowbase[(size_t)m * p.ldc + cq] - ws.lse64[m]);
+      }
+      const double a64 = s / (double)nv;
+      if (a64 > best || (a64 == best && cq < bestc)) { best = a64; bestc = cq; }
+    }
+    ws.cnt[j * 32 + lane] += (bestc == y);
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(WT, 4) vote_average_kernel(const VoteParams p, const int32_t* work,
+                                                              const unsigned int* work_count) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WS ws;
+  warp_smem(p, smem_raw + warp * warp_smem(p, nullptr, nullptr), &ws);
+  const int K = p.K, S = p.S, C = p.C;
+  const int F = (int)(p.ldc >> 2);
+  const int TA = 1 << p.K1, TT = TA + (1 << (K - p.K1));
+  const int CAPS = p.CAP + 1;
+  const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
+  const int64_t nw = (int64_t)gridDim.x * WPC;
+  float* ovP = p.scratch + gw * (size_t)K * C;  // overflow candidate matrix [K][C]
+  int32_t* ovC = p.scratch_cls + gw * (size_t)C;
+  for (int i = lane; i < JMAX * 32; i += 32) ws.cnt[i] = 0u;
+  const int64_t W = *work_count;
+
+  for (int64_t e = gw; e < W; e += nw) {
+    const int64_t n = work[e];
+    const int y = p.labels[n];
+    const float* rowbase = p.logits + n * K * p.ldc;
+    int tp = 0;
+    float mx = 0.f, ls = 0.f;
+    if (lane < K) {
+      tp = p.top1_in[n * K + lane];
+      ls = p.lse_in[n * K + lane];
+      mx = p.rmax_in[n * K + lane];
+    }
+    const float thr = theta_threshold(mx, ls, K, lane);
+    const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;  // l[m][y]
+    __syncwarp();
+    if (lane < K) ws.stop[lane] = tp;
+    ws.bitmap[lane] = 0u;
+    ws.bitmapB[lane] = 0u;
+    __syncwarp();
+    // ---- 1. candidate set R: one streaming pass over the sample's K rows ----------------------
+#pragma unroll 1
+    for (int m = 0; m < K; ++m) {
+      const float* row = rowbase + (size_t)m * p.ldc;
+      float4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c4 = lane + 32 * i;
+        v[i] = (c4 < F && c4 * 4 < C) ? ldg_stream(row + c4 * 4)
+                                       : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+      const float t_m = __shfl_sync(FULL, thr, m);
+      const float y_m = __shfl_sync(FULL, ly, m);
+      const float lo = fminf(t_m, y_m);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 x4 = v[i];
+        if (fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)) >= lo) {  // fast reject (fmaxf drops NaN padding)
+          const int cb = (lane + 32 * i) * 4;
+          uint32_t bits = 0, bitsB = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float x = f4c(x4, q);
+            bits |= (x >= t_m && cb + q < C) ? (1u << q) : 0u;
+            bitsB |= (x >= y_m && cb + q < C) ? (1u << q) : 0u;
+          }
+          if (bits) atomicOr(&ws.bitmap[cb >> 5], bits << (cb & 31));
+          if (bitsB) atomicOr(&ws.bitmapB[cb >> 5], bitsB << (cb & 31));
+        }
+      }
+    }
+    __syncwarp();
+    const uint32_t word = ws.bitmap[lane] & ws.bitmapB[lane];
+    const int cnt = __popc(word);
+    int incl = cnt;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(FULL, incl, off);
+      if (lane >= off) incl += o;
+    }
+    const int pre = incl - cnt;
+    const int nc = __shfl_sync(FULL, incl, 31);
+    const bool ovf = nc > p.CAP;
+    int32_t* cls = ovf ? ovC : ws.ccls;
+    {
+      uint32_t w = word;
+      int k = pre;
+      while (w) {
+        cls[k++] = lane * 32 + (__ffs(w) - 1);
+        w &= w - 1;
+      }
+    }
+    auto slot_of = [&](int c) -> int {  // warp-uniform c in R
+      return __shfl_sync(FULL, pre, c >> 5) + __popc(__shfl_sync(FULL, word, c >> 5) & ((1u << (c & 31)) - 1u));
+    };
+    const int ys = slot_of(y);
+    // exact columns: y, then the members' distinct top-1 classes other than y (all lie in R)
+    int dslot[8];
+    int nd = 0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      dslot[m] = ys;
+      if (m < K) {
+        const int cm = __shfl_sync(FULL, tp, m);
+        bool dup = cm == y;
+        for (int q = 0; q < m; ++q) dup |= (__shfl_sync(FULL, tp, q) == cm);
+        if (!dup) dslot[nd++] = slot_of(cm);
+      }
+    }
+    __syncwarp();
+    // ---- 2. gather p[m][c] = exp(l - lse_m) for c in R ------------------------------------------
+    float* P = ovf ? ovP : ws.P;
+    const int ps = ovf ? C : CAPS;
+    float lsm[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) lsm[m] = __shfl_sync(FULL, ls, m < K ? m : 0);
+    for (int sl = lane; sl < nc; sl += 32) {
+      const int cq = cls[sl];
+      float l[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)  // K independent loads in flight (L2 hits: the rows were just streamed)
+        l[m] = m < K ? __ldg(rowbase + (size_t)m * p.ldc + cq) : 0.f;
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (m < K) P[(size_t)m * ps + sl] = expf(l[m] - lsm[m]);
+    }
+    __syncwarp();
+    // ---- 3. bound for candidates outside {y} ∪ D, and the exact-column half tables ------------
+#pragma unroll 1
+    for (int m = 0; m < K; ++m) {
+      float q = 0.f;
+      for (int sl = lane; sl < nc; sl += 32) {
+        bool ex = sl == ys;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) ex |= (d < nd && sl == dslot[d]);
+        if (!ex) q = fmaxf(q, P[(size_t)m * ps + sl]);
+      }
+      for (int off = 16; off; off >>= 1) q = fmaxf(q, __shfl_xor_sync(FULL, q, off));
+      if (lane == 0) ws.Q[m] = q;
+    }
+    __syncwarp();
+    if (lane < TT) {  // lane h builds half-mask row h
+      const uint32_t hm = lane < TA ? (uint32_t)lane : (uint32_t)(lane - TA);
+      const int mo = lane < TA ? 0 : p.K1;
+      float s = 0.f;
+      for (uint32_t a = hm; a; a &= a - 1) s += ws.Q[mo + __ffs(a) - 1];
+      ws.QB[lane] = s * (1.f + 1e-6f);  // round the bound up past fp32 summation error
+      float sy0 = 0.f;
+      for (uint32_t a = hm; a; a &= a - 1) sy0 += P[(size_t)(mo + __ffs(a) - 1) * ps + ys];
+      ws.T[lane * DSTR] = sy0;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        if (d < nd) {
+          float sd = 0.f;
+          for (uint32_t a = hm; a; a &= a - 1) sd += P[(size_t)(mo + __ffs(a) - 1) * ps + dslot[d]];
+          ws.T[lane * DSTR + 1 + d] = sd;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- 4. A4 decision of every subset ------------------------------------------
+    uint32_t pending = 0;
+#pragma unroll 1
+    for (int j = 0; j < JMAX; ++j) {
+      const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+      if (v > (uint32_t)S) break;
+      uint32_t oka = 0;
+      if (__popc(v) == 1) {
+        oka = (ws.stop[__ffs(v) - 1] == y);  // softmax is monotone (invariant I1)
+      } else {
+        const float* A = ws.T + (v & (TA - 1)) * DSTR;
+        const float* B = ws.T + (TA + (v >> p.K1)) * DSTR;
+        const float sy = A[0] + B[0];
+        const float hiT = sy * (1.f + p.band), loT = sy * (1.f - p.band);
+        bool beat = false, near = false;
+#pragma unroll 1
+        for (int d = 1; d <= nd; ++d) {
+          const float sd = A[d] + B[d];
+          beat |= sd > hiT;
+          near |= sd >= loT;
+        }
+        if (beat) {
+          oka = 0;
+        } else if (ws.QB[v & (TA - 1)] + ws.QB[TA + (v >> p.K1)] < loT) {
+          if (near) pending |= 1u << j;
+          else oka = 1;  // every competitor provably below y: decided in O(1)
+        } else {  // bound not conclusive: scan R
+          float m2 = -1.f;
+          for (int q = 0; q < nc; ++q) {
+            if (q == ys) continue;
+            float s = 0.f;
+            for (uint32_t a = v; a; a &= a - 1) s += P[(size_t)(__ffs(a) - 1) * ps + q];
+            m2 = fmaxf(m2, s);
+          }
+          if (m2 > hiT) oka = 0;
+          else if (m2 < loT) oka = 1;
+          else pending |= 1u << j;
+        }
+      }
+      ws.cnt[j * 32 + lane] += oka;
+    }
+    if (__any_sync(FULL, pending != 0)) recheck_fp64(p, ws, pending, rowbase, mx, P, ps, cls, nc, ys, y, lane);
+    __syncwarp();
+  }
+#pragma unroll 1
+  for (int j = 0; j < JMAX; ++j) {
+    const int v1 = lane + 32 * j;
+    const uint32_t c = ws.cnt[j * 32 + lane];
+    if (v1 < S && c) atomicAdd(p.cnt_avg + v1, (unsigned long long)c);
+  }
+}
+
+}  // namespace
+
+size_t vote_avg_smem_per_warp(const VoteParams& p) { return warp_smem(p, nullptr, nullptr); }
+
+cudaError_t launch_vote_avg(const VoteParams& q, int grid, cudaStream_t st, const int32_t* work,
+                            const unsigned int* work_count) {
+  const size_t smem = warp_smem(q, nullptr, nullptr) * WPC;
+  cudaError_t e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  vote_average_kernel<<<grid, WT, smem, st>>>(q, work, work_count);
+  return cudaGetLastError();
+}
+
+}  // namespace rk

@@ -252,284 +252,9 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
   }
 }
 
-// =============================== kernel B: averages on the worklist ===========================
-struct WS {  // per-warp shared memory
-  double* lse64;    // [8]
-  int32_t* stop;    // [8]
-  uint32_t* bitmap; // [32] S_c (theta test)
-  uint32_t* bitmapB;// [32] classes not below y in some model
-  int32_t* ccls;    // [CAP] candidate classes in ascending order
-  float* P;         // [K][CAP+1]
-  float* T;         // [TT][TCAP|1]
-  float* Q;         // [8]  q_m = max competitor probability of model m
-  float* QB;        // [32] half-mask sums of q (competitor bound)
-  uint32_t* cnt;    // [JMAX][32] lane-owned avg counters
-};
-
-__host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS* w) {
-  const int TT = (1 << p.K1) + (1 << (p.K - p.K1));
-  size_t o = 0;
-  auto take = [&](size_t b) -> char* { char* r = base ? base + o : nullptr; o = a16(o + b); return r; };
-  char* l64 = take(8 * 8);
-  char* st = take(4 * 8);
-  char* bm = take(4 * 32);
-  char* bmB = take(4 * 32);
-  char* cc = take(4ull * p.CAP);
-  char* P = take(4ull * p.K * (p.CAP + 1));
-  char* T = take(4ull * TT * (p.TCAP | 1));
-  char* Q = take(4 * 8);
-  char* QB = take(4 * 32);
-  char* CN = take(4 * JMAX * 32);
-  if (w) {
-    w->lse64 = (double*)l64; w->stop = (int32_t*)st; w->bitmap = (uint32_t*)bm; w->bitmapB = (uint32_t*)bmB;
-    w->ccls = (int32_t*)cc; w->P = (float*)P; w->T = (float*)T; w->Q = (float*)Q; w->QB = (float*)QB;
-    w->cnt = (uint32_t*)CN;
-  }
-  return o;
-}
-
-// fp64 recheck of near-ties (rare, out of line): warp-cooperative fp64 log-sum-exp of every row, then
-// each lane decides its pending subsets exactly like the oracle (avg = (sum_{m in v, asc}
-// exp(l - lse_m)) / |v|, lowest class on ties) over the candidates inside the band.
-__device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t pending, const float* rowbase,
-                                          float mx, const float* Pm, int ps, const int32_t* cls, int nc, int ys,
-                                          int y, int lane) {
-  const int K = p.K, C = p.C;
-  for (int m = 0; m < K; ++m) {
-    const float* row = rowbase + (size_t)m * p.ldc;
-    const double m64 = (double)__shfl_sync(FULL, mx, m);
-    double s = 0.0;
-    for (int cc = lane; cc < C; cc += 32) s += exp((double)row[cc] - m64);
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-    if (lane == 0) ws.lse64[m] = m64 + log(s);
-  }
-  __syncwarp();
-  for (int j = 0; j < JMAX; ++j) {
-    if (!((pending >> j) & 1u)) continue;
-    const uint32_t v = (uint32_t)(lane + 32 * j + 1);
-    atomicAdd(p.n_recheck + (v - 1), 1ull);
-    float sy = 0.f;  // fp32 sums again select the band; fp64 decides
-    for (uint32_t a = v; a; a &= a - 1) sy += Pm[(size_t)(__ffs(a) - 1) * ps + ys];
-    const float lo = sy * (1.f - p.band);
-    const int nv = __popc(v);
-    double best = -1.0;
-    int bestc = 0x7fffffff;
-    for (int q = 0; q < nc; ++q) {
-      float s32 = 0.f;
-      for (uint32_t a = v; a; a &= a - 1) s32 += Pm[(size_t)(__ffs(a) - 1) * ps + q];
-      if (q != ys && s32 < lo) continue;
-      const int cq = cls[q];
-      double s = 0.0;
-      for (uint32_t a = v; a; a &= a - 1) {
-        const int m = __ffs(a) - 1;
-        s += exp((double)rowbase[(size_t)m * p.ldc + cq] - ws.lse64[m]);
-      }
-      const double a64 = s / (double)nv;
-      if (a64 > best || (a64 == best && cq < bestc)) { best = a64; bestc = cq; }
-    }
-    ws.cnt[j * 32 + lane] += (bestc == y);
-  }
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(WT, 4) vote_average_kernel(const VoteParams p, const int32_t* work,
-                                                              const unsigned int* work_count) {
-  extern __shared__ __align__(16) char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WS ws;
-  warp_smem(p, smem_raw + warp * warp_smem(p, nullptr, nullptr), &ws);
-  const int K = p.K, S = p.S, C = p.C;
-  const int F = (int)(p.ldc >> 2);
-  const int TA = 1 << p.K1, TT = TA + (1 << (K - p.K1));
-  const int TSTR = p.TCAP | 1, CAPS = p.CAP + 1;
-  const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
-  const int64_t nw = (int64_t)gridDim.x * WPC;
-  float* ovP = p.scratch + gw * (size_t)K * C;  // overflow candidate matrix [K][C]
-  int32_t* ovC = p.scratch_cls + gw * (size_t)C;
-  for (int i = lane; i < JMAX * 32; i += 32) ws.cnt[i] = 0u;
-  const int64_t W = *work_count;
-
-  for (int64_t e = gw; e < W; e += nw) {
-    const int64_t n = work[e];
-    const int y = p.labels[n];
-    const float* rowbase = p.logits + n * K * p.ldc;
-    int tp = 0;
-    float mx = 0.f, ls = 0.f;
-    if (lane < K) {
-      tp = p.top1_in[n * K + lane];
-      ls = p.lse_in[n * K + lane];
-      mx = p.rmax_in[n * K + lane];
-    }
-    const float thr = theta_threshold(mx, ls, K, lane);
-    const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;  // l[m][y]
-    __syncwarp();
-    if (lane < K) ws.stop[lane] = tp;
-    ws.bitmap[lane] = 0u;
-    ws.bitmapB[lane] = 0u;
-    __syncwarp();
-    // ---- candidate set R: one streaming pass over the sample's K rows ------------------------
-#pragma unroll 1
-    for (int m = 0; m < K; ++m) {
-      const float* row = rowbase + (size_t)m * p.ldc;
-      float4 v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c4 = lane + 32 * i;
-        v[i] = (c4 < F && c4 * 4 < C) ? ldg_stream(row + c4 * 4)
-                                       : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      }
-      const float t_m = __shfl_sync(FULL, thr, m);
-      const float y_m = __shfl_sync(FULL, ly, m);
-      const float lo = fminf(t_m, y_m);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 x4 = v[i];
-        // fast reject: almost every float4 is below both thresholds (fmaxf drops NaN padding)
-        if (fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)) >= lo) {
-          const int cb = (lane + 32 * i) * 4;
-          uint32_t bits = 0, bitsB = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float x = f4c(x4, q);
-            bits |= (x >= t_m && cb + q < C) ? (1u << q) : 0u;
-            bitsB |= (x >= y_m && cb + q < C) ? (1u << q) : 0u;
-          }
-          if (bits) atomicOr(&ws.bitmap[cb >> 5], bits << (cb & 31));
-          if (bitsB) atomicOr(&ws.bitmapB[cb >> 5], bitsB << (cb & 31));
-        }
-      }
-    }
-    __syncwarp();
-    const uint32_t word = ws.bitmap[lane] & ws.bitmapB[lane];
-    const int cnt = __popc(word);
-    int incl = cnt;
-    for (int off = 1; off < 32; off <<= 1) {
-      const int o = __shfl_up_sync(FULL, incl, off);
-      if (lane >= off) incl += o;
-    }
-    const int pre = incl - cnt;
-    const int nc = __shfl_sync(FULL, incl, 31);
-    const bool ovf = nc > p.CAP;
-    const bool tables = !ovf && nc <= p.TCAP;
-    int32_t* cls = ovf ? ovC : ws.ccls;
-    {
-      uint32_t w = word;
-      int k = pre;
-      while (w) {
-        cls[k++] = lane * 32 + (__ffs(w) - 1);
-        w &= w - 1;
-      }
-    }
-    const int ys = __shfl_sync(FULL, pre, y >> 5) +
-                   __popc(__shfl_sync(FULL, word, y >> 5) & ((1u << (y & 31)) - 1u));
-    __syncwarp();
-    // ---- gather p[m][c] = exp(l - lse_m) for c in R ------------------------------------------
-    float* P = ovf ? ovP : ws.P;
-    const int ps = ovf ? C : CAPS;
-    float lsm[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) lsm[m] = __shfl_sync(FULL, ls, m < K ? m : 0);
-    for (int sl = lane; sl < nc; sl += 32) {
-      const int cq = cls[sl];
-      float l[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m)  // K independent loads in flight (L2 hits: the rows were just streamed)
-        l[m] = m < K ? __ldg(rowbase + (size_t)m * p.ldc + cq) : 0.f;
-#pragma unroll
-      for (int m = 0; m < 8; ++m)
-        if (m < K) P[(size_t)m * ps + sl] = expf(l[m] - lsm[m]);
-    }
-    __syncwarp();
-    // ---- competitor bound: q_m = max_{c in R, c != y} p[m][c]; QB = half-mask sums of q -------
-#pragma unroll 1
-    for (int m = 0; m < K; ++m) {
-      float q = 0.f;
-      for (int sl = lane; sl < nc; sl += 32)
-        if (sl != ys) q = fmaxf(q, P[(size_t)m * ps + sl]);
-      for (int off = 16; off; off >>= 1) q = fmaxf(q, __shfl_xor_sync(FULL, q, off));
-      if (lane == 0) ws.Q[m] = q;
-    }
-    __syncwarp();
-    if (lane < TT) {
-      float s = 0.f;
-      if (lane < TA) {
-        for (uint32_t a = (uint32_t)lane; a; a &= a - 1) s += ws.Q[__ffs(a) - 1];
-      } else {
-        for (uint32_t b = (uint32_t)(lane - TA); b; b &= b - 1) s += ws.Q[p.K1 + __ffs(b) - 1];
-      }
-      ws.QB[lane] = s * (1.f + 1e-6f);  // round the bound up past fp32 summation error
-    }
-    // ---- half tables: A[a][c] = sum_{m in a, asc} p[m][c] (low models), B likewise (high) ------
-    if (tables) {
-#pragma unroll 1
-      for (int h = 0; h < TT; ++h)
-        for (int sl = lane; sl < nc; sl += 32) {
-          float s = 0.f;
-          if (h < TA) {
-            for (uint32_t a = (uint32_t)h; a; a &= a - 1) s += ws.P[(size_t)(__ffs(a) - 1) * CAPS + sl];
-          } else {
-            for (uint32_t b = (uint32_t)(h - TA); b; b &= b - 1) s += ws.P[(size_t)(p.K1 + __ffs(b) - 1) * CAPS + sl];
-          }
-          ws.T[(size_t)h * TSTR + sl] = s;
-        }
-    }
-    __syncwarp();
-    // ---- A4: averaged-probability decision of every subset ------------------------
-    uint32_t pending = 0;  // subsets whose decision needs the fp64 recheck
-#pragma unroll 1
-    for (int j = 0; j < JMAX; ++j) {
-      const uint32_t v = (uint32_t)(lane + 32 * j + 1);
-      if (v > (uint32_t)S) break;
-      uint32_t oka = 0;
-      if (__popc(v) == 1) {
-        oka = (ws.stop[__ffs(v) - 1] == y);  // softmax is monotone (invariant I1)
-      } else {
-        float sy = 0.f, m2 = -1.f;
-        const float* A = ws.T + (size_t)(v & (TA - 1)) * TSTR;
-        const float* B = ws.T + (size_t)(TA + (v >> p.K1)) * TSTR;
-        if (tables) {
-          sy = A[ys] + B[ys];
-        } else {
-          for (uint32_t a = v; a; a &= a - 1) sy += P[(size_t)(__ffs(a) - 1) * ps + ys];
-        }
-        const float bnd = ws.QB[v & (TA - 1)] + ws.QB[TA + (v >> p.K1)];
-        if (bnd < sy * (1.f - 2.f * p.band)) {
-          oka = 1;  // no competitor can reach y: decided without scanning R
-        } else {
-          if (tables) {
-            for (int q = 0; q < nc; ++q) {
-              const float s = A[q] + B[q];
-              if (q != ys) m2 = fmaxf(m2, s);
-            }
-          } else {
-            for (int q = 0; q < nc; ++q) {
-              if (q == ys) continue;
-              float s = 0.f;
-              for (uint32_t a = v; a; a &= a - 1) s += P[(size_t)(__ffs(a) - 1) * ps + q];
-              m2 = fmaxf(m2, s);
-            }
-          }
-          if (m2 > sy * (1.f + p.band)) oka = 0;
-          else if (m2 < sy * (1.f - p.band)) oka = 1;
-          else pending |= 1u << j;
-        }
-      }
-      ws.cnt[j * 32 + lane] += oka;
-    }
-    if (__any_sync(FULL, pending != 0)) recheck_fp64(p, ws, pending, rowbase, mx, P, ps, cls, nc, ys, y, lane);
-    __syncwarp();
-  }
-#pragma unroll 1
-  for (int j = 0; j < JMAX; ++j) {
-    const int v1 = lane + 32 * j;
-    const uint32_t c = ws.cnt[j * 32 + lane];
-    if (v1 < S && c) atomicAdd(p.cnt_avg + v1, (unsigned long long)c);
-  }
-}
-
 }  // namespace
 
-size_t vote_warp_smem_per_warp(const VoteParams& p) { return warp_smem(p, nullptr, nullptr); }
+size_t vote_warp_smem_per_warp(const VoteParams& p) { return vote_avg_smem_per_warp(p); }
 int vote_warp_threads() { return WT; }
 int vote_warp_min_blocks() { return 4; }
 
@@ -552,12 +277,7 @@ cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int
   {
     VoteParams q = p;
     if (!p.lse_in) { q.top1_in = st_top; q.lse_in = st_lse; q.rmax_in = st_max; }
-    const size_t smem = warp_smem(q, nullptr, nullptr) * WPC;
-    if ((e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
-    vote_average_kernel<<<grid, WT, smem, st>>>(q, work, work_count);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_vote_avg(q, grid, st, work, work_count)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
