@@ -59,6 +59,8 @@ size_t vote_batch_smem_per_sample(const VoteParams& p);
 int vote_batch_avg_ctas_samples();
 cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work,
                               unsigned int* work_count, int32_t* st_top, float* st_lse, float* st_max);
+cudaError_t launch_vote_batch_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
+                                  const unsigned int* work_count);  // rk_vote_batch_avg.cu
 
 // Two kernels: classify+votes over all samples, then averages over the worklist of samples whose
 // label is an averaging candidate. work: [N] int32, work_count: 1 uint; st_*: [N][K] statistics

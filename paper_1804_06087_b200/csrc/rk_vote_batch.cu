@@ -32,14 +32,13 @@ constexpr int KM = 12;
 
 constexpr uint32_t R_EVAL = 1u, R_UNAN = 2u;
 
-struct Rec {  // per-sample vote record (kernel A)
-  int32_t y;
+struct Rec {  // per-sample vote record (kernel A), relative to the label y
   uint32_t flags;
-  int32_t nd;
-  uint32_t tm;
-  int32_t cls[KM];
-  uint32_t msk[KM];
-  int32_t top[KM];
+  uint32_t tm;      // ragged-tail membership per batch size
+  uint32_t my;      // members voting y
+  int32_t no;       // number of other predicted classes
+  uint32_t lt;      // bit j: other class j < y (LOWEST_CLASS tie rule)
+  uint32_t mo[KM];  // members voting each other class
 };
 
 __device__ __forceinline__ float4 ldg_stream(const float* p) {
@@ -169,15 +168,20 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
               if (__any_sync(FULL, lane < K && rowbase[(size_t)lane * p.ldc + y] >= thr)) wl |= 1u << i;
               if (__any_sync(FULL, lane < K && c == y)) {
                 fl = R_EVAL;
-                const bool leader = lane < K && (__ffs(mm) - 1) == lane;
-                const uint32_t lb = __ballot_sync(FULL, leader);
-                if (leader) {
-                  const int pos = __popc(lb & ((1u << lane) - 1u));
-                  rec[b].cls[pos] = c;
-                  rec[b].msk[pos] = mm;
+                const bool other = lane < K && (__ffs(mm) - 1) == lane && c != y;  // one lane per other class
+                const uint32_t ob = __ballot_sync(FULL, other);
+                const uint32_t ltb = __ballot_sync(FULL, other && c < y);
+                if (other) rec[b].mo[__popc(ob & ((1u << lane) - 1u))] = mm;
+                if (lane < K && c == y && (__ffs(mm) - 1) == lane) rec[b].my = mm;
+                if (lane == 0) {
+                  rec[b].no = __popc(ob);
+                  rec[b].tm = tm;
+                  // lt bit j refers to the j-th other class in lane order
+                  uint32_t lt = 0;
+                  for (uint32_t w = ob, j = 0; w; w &= w - 1, ++j)
+                    if ((ltb >> (__ffs(w) - 1)) & 1u) lt |= 1u << j;
+                  rec[b].lt = lt;
                 }
-                if (lane < K) rec[b].top[lane] = tp;
-                if (lane == 0) { rec[b].nd = __popc(lb); rec[b].y = y; rec[b].tm = tm; }
               }
             }
           }
@@ -200,24 +204,39 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
 #pragma unroll 1
       for (int b = g * gsz; b < (g + 1) * gsz; ++b) {
         if (!(rec[b].flags & R_EVAL)) continue;  // uniform across the CTA
-        const int nd = rec[b].nd, y = rec[b].y;
-        const uint32_t tm = rec[b].tm;
+        // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|,
+        // y wins iff c_y > 0, no class has more votes, and the tie (if any) goes to y:
+        // LOWEST_CLASS -> no tied class below y; BEST_MEMBER -> the best-ranked member among all
+        // tied voters votes y (reading Q2).
+        const uint32_t my = rec[b].my, lt = rec[b].lt, tm = rec[b].tm;
+        const int no = rec[b].no;
+        uint32_t cy[NK], tied[NK], lose = 0;
 #pragma unroll
-        for (int k = 0; k < NK; ++k) {  // A3: majority vote
+        for (int k = 0; k < NK; ++k) {
+          const uint32_t v = (uint32_t)(t + 1 + BT * k);
+          tied[k] = v & my;
+          cy[k] = __popc(tied[k]);
+          lose |= (cy[k] == 0u) ? (1u << k) : 0u;
+        }
+#pragma unroll 1
+        for (int j = 0; j < no; ++j) {
+          const uint32_t mj = rec[b].mo[j];
+          const bool ltj = (lt >> j) & 1u;
+#pragma unroll
+          for (int k = 0; k < NK; ++k) {
+            const uint32_t v = (uint32_t)(t + 1 + BT * k);
+            const uint32_t vm = v & mj;
+            const uint32_t cj = __popc(vm);
+            lose |= (cj > cy[k] || (p.tie != 0 && cj == cy[k] && ltj)) ? (1u << k) : 0u;
+            tied[k] |= (cj == cy[k]) ? vm : 0u;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
           const uint32_t v = (uint32_t)(t + 1 + BT * k);
           if (v > (uint32_t)S) break;
-          int bc = 0, bcls = 0x7fffffff;
-          uint32_t tied = 0;
-#pragma unroll 1
-          for (int q = 0; q < nd; ++q) {
-            const uint32_t mv = v & rec[b].msk[q];
-            const int cnt = __popc(mv);
-            const int cq = rec[b].cls[q];
-            if (cnt > bc) { bc = cnt; bcls = cq; tied = mv; }
-            else if (cnt == bc && cnt > 0) { tied |= mv; bcls = min(bcls, cq); }
-          }
-          const int winner = (p.tie == 0) ? rec[b].top[best_of[tied]] : bcls;
-          const uint32_t ok = winner == y;
+          uint32_t ok = !((lose >> k) & 1u);
+          if (p.tie == 0 && ok) ok = (my >> best_of[tied[k]]) & 1u;
           gv[k] += ok;
           if (ok && tm) tail_add_b(p, tm, v);
         }
@@ -248,270 +267,6 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
   }
 }
 
-// =============================== kernel B: averages on the worklist (batched) ====================
-struct SmpB {  // per-sample record (kernel B), pointers into the CTA's dynamic smem
-  float* P;      // [K][CAP+1]
-  float* T;      // [TT][TCAP|1]
-  float* QB;     // [TT]
-  int32_t* cls;  // [CAP]
-  uint32_t* bm;  // [32]
-  uint32_t* bmB; // [32]
-};
-
-__host__ __device__ inline size_t smp_bytes(const VoteParams& p, char* base, SmpB* s) {
-  const int TT = (1 << p.K1) + (1 << (p.K - p.K1));
-  size_t o = 0;
-  auto take = [&](size_t b) -> char* { char* r = base ? base + o : nullptr; o = a16(o + b); return r; };
-  char* P = take(4ull * p.K * (p.CAP + 1));
-  char* T = take(4ull * TT * (p.TCAP | 1));
-  char* QB = take(4ull * TT);
-  char* cl = take(4ull * p.CAP);
-  char* bm = take(4 * 32);
-  char* bmB = take(4 * 32);
-  if (s) { s->P = (float*)P; s->T = (float*)T; s->QB = (float*)QB; s->cls = (int32_t*)cl; s->bm = (uint32_t*)bm; s->bmB = (uint32_t*)bmB; }
-  return o;
-}
-
-struct HdrB {  // per-sample scalars
-  int64_t n;
-  int32_t y, nc, ys, valid, ovf, tables, need64;
-  int32_t top[KM];
-  float mx[KM];
-  float q[KM];
-  double lse64[KM];
-};
-
-template <int NK>
-__global__ void __launch_bounds__(BT, 1) vote_batch_average_kernel(const VoteParams p, const int32_t* work,
-                                                                   const unsigned int* work_count) {
-  extern __shared__ __align__(16) char smem_raw[];
-  __shared__ HdrB hd[SBW];
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int K = p.K, S = p.S, C = p.C;
-  const int F = (int)(p.ldc >> 2);
-  const int TA = 1 << p.K1, TT = TA + (1 << (K - p.K1));
-  const int TSTR = p.TCAP | 1, CAPS = p.CAP + 1;
-  const size_t sbytes = smp_bytes(p, nullptr, nullptr);
-  const int64_t W = *work_count;
-  const int64_t nbatch = (W + SBW - 1) / SBW;
-  uint32_t ca[NK];
-#pragma unroll
-  for (int k = 0; k < NK; ++k) ca[k] = 0;
-
-  for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
-    __syncthreads();
-    // ---- phase 1: warp `warp` prepares worklist sample e ----------------------------------------
-    {
-      const int64_t e = batch * SBW + warp;
-      SmpB sm;
-      smp_bytes(p, smem_raw + warp * sbytes, &sm);
-      if (e < W) {
-        const int64_t n = work[e];
-        const int y = p.labels[n];
-        const float* rowbase = p.logits + n * K * p.ldc;
-        int tp = 0;
-        float mx = 0.f, ls = 0.f;
-        if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lse_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
-        const float thr = theta_threshold(mx, ls, K, lane);
-        const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;
-        sm.bm[lane] = 0u;
-        sm.bmB[lane] = 0u;
-        __syncwarp();
-        // candidate set R = S_c ∩ {c : exists m, l[m][c] >= l[m][y]}, one streaming pass
-#pragma unroll 1
-        for (int m = 0; m < K; ++m) {
-          const float* row = rowbase + (size_t)m * p.ldc;
-          const float t_m = __shfl_sync(FULL, thr, m), y_m = __shfl_sync(FULL, ly, m);
-          const float lo = fminf(t_m, y_m);
-#pragma unroll 1
-          for (int c4 = lane; c4 < F; c4 += 32) {
-            if (c4 * 4 >= C) continue;
-            const float4 x4 = ldg_stream(row + c4 * 4);
-            if (fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)) >= lo) {
-              const int cb = c4 * 4;
-              uint32_t bits = 0, bitsB = 0;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float x = f4c(x4, q);
-                bits |= (x >= t_m && cb + q < C) ? (1u << q) : 0u;
-                bitsB |= (x >= y_m && cb + q < C) ? (1u << q) : 0u;
-              }
-              if (bits) atomicOr(&sm.bm[cb >> 5], bits << (cb & 31));
-              if (bitsB) atomicOr(&sm.bmB[cb >> 5], bitsB << (cb & 31));
-            }
-          }
-        }
-        __syncwarp();
-        const uint32_t word = sm.bm[lane] & sm.bmB[lane];
-        const int cnt = __popc(word);
-        int incl = cnt;
-        for (int off = 1; off < 32; off <<= 1) {
-          const int o = __shfl_up_sync(FULL, incl, off);
-          if (lane >= off) incl += o;
-        }
-        const int pre = incl - cnt;
-        const int nc = __shfl_sync(FULL, incl, 31);
-        const int ys = __shfl_sync(FULL, pre, y >> 5) +
-                       __popc(__shfl_sync(FULL, word, y >> 5) & ((1u << (y & 31)) - 1u));
-        const bool ovf = nc > p.CAP;
-        float* P = ovf ? p.scratch + ((size_t)blockIdx.x * SBW + warp) * (size_t)K * C : sm.P;
-        int32_t* cls = ovf ? p.scratch_cls + ((size_t)blockIdx.x * SBW + warp) * (size_t)C : sm.cls;
-        const int ps = ovf ? C : CAPS;
-        {
-          uint32_t w = word;
-          int k = pre;
-          while (w) { cls[k++] = lane * 32 + (__ffs(w) - 1); w &= w - 1; }
-        }
-        __syncwarp();
-        for (int m = 0; m < K; ++m) {
-          const float ls_m = __shfl_sync(FULL, ls, m);
-          for (int sl = lane; sl < nc; sl += 32) P[(size_t)m * ps + sl] = expf(__ldg(rowbase + (size_t)m * p.ldc + cls[sl]) - ls_m);
-        }
-        __syncwarp();
-        // competitor bound q_m and its half-mask sums
-        for (int m = 0; m < K; ++m) {
-          float q = 0.f;
-          for (int sl = lane; sl < nc; sl += 32)
-            if (sl != ys) q = fmaxf(q, P[(size_t)m * ps + sl]);
-          for (int off = 16; off; off >>= 1) q = fmaxf(q, __shfl_xor_sync(FULL, q, off));
-          if (lane == 0) hd[warp].q[m] = q;
-        }
-        __syncwarp();
-        for (int h = lane; h < TT; h += 32) {
-          float s = 0.f;
-          if (h < TA) { for (uint32_t a = (uint32_t)h; a; a &= a - 1) s += hd[warp].q[__ffs(a) - 1]; }
-          else { for (uint32_t b = (uint32_t)(h - TA); b; b &= b - 1) s += hd[warp].q[p.K1 + __ffs(b) - 1]; }
-          sm.QB[h] = s * (1.f + 1e-6f);
-        }
-        const bool tables = !ovf && nc <= p.TCAP;
-        if (tables) {
-          for (int h = 0; h < TT; ++h)
-            for (int sl = lane; sl < nc; sl += 32) {
-              float s = 0.f;
-              if (h < TA) { for (uint32_t a = (uint32_t)h; a; a &= a - 1) s += sm.P[(size_t)(__ffs(a) - 1) * CAPS + sl]; }
-              else { for (uint32_t b = (uint32_t)(h - TA); b; b &= b - 1) s += sm.P[(size_t)(p.K1 + __ffs(b) - 1) * CAPS + sl]; }
-              sm.T[(size_t)h * TSTR + sl] = s;
-            }
-        }
-        if (lane < K) { hd[warp].top[lane] = tp; hd[warp].mx[lane] = mx; }
-        if (lane == 0) {
-          hd[warp].n = n; hd[warp].y = y; hd[warp].nc = nc; hd[warp].ys = ys; hd[warp].valid = 1;
-          hd[warp].ovf = ovf; hd[warp].tables = tables; hd[warp].need64 = 0;
-        }
-      } else if (lane == 0) {
-        hd[warp].valid = 0;
-      }
-    }
-    __syncthreads();
-    // ---- phase 2: thread t owns subsets v = t + 1 + 256k ----------------------------------------
-    uint32_t pending[NK];
-#pragma unroll
-    for (int k = 0; k < NK; ++k) pending[k] = 0;
-#pragma unroll 1
-    for (int s = 0; s < SBW; ++s) {
-      if (!hd[s].valid) continue;
-      SmpB sm;
-      smp_bytes(p, smem_raw + s * sbytes, &sm);
-      const int y = hd[s].y, nc = hd[s].nc, ys = hd[s].ys;
-      const bool tables = hd[s].tables, ovf = hd[s].ovf;
-      const float* P = ovf ? p.scratch + ((size_t)blockIdx.x * SBW + s) * (size_t)K * C : sm.P;
-      const int ps = ovf ? C : CAPS;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {  // A4: averaged probabilities
-        const uint32_t v = (uint32_t)(t + 1 + BT * k);
-        if (v > (uint32_t)S) break;
-        uint32_t oka = 0;
-        if (__popc(v) == 1) {
-          oka = hd[s].top[__ffs(v) - 1] == y;  // softmax is monotone (invariant I1)
-        } else {
-          const uint32_t a = v & (TA - 1), bb = v >> p.K1;
-          float sy = 0.f;
-          if (tables) sy = sm.T[(size_t)a * TSTR + ys] + sm.T[(size_t)(TA + bb) * TSTR + ys];
-          else for (uint32_t m = v; m; m &= m - 1) sy += P[(size_t)(__ffs(m) - 1) * ps + ys];
-          const float bnd = sm.QB[a] + sm.QB[TA + bb];
-          if (bnd < sy * (1.f - 2.f * p.band)) {
-            oka = 1;
-          } else {
-            float m2 = -1.f;
-            if (tables) {
-              const float* A = sm.T + (size_t)a * TSTR;
-              const float* B = sm.T + (size_t)(TA + bb) * TSTR;
-              for (int q = 0; q < nc; ++q) if (q != ys) m2 = fmaxf(m2, A[q] + B[q]);
-            } else {
-              for (int q = 0; q < nc; ++q) {
-                if (q == ys) continue;
-                float x = 0.f;
-                for (uint32_t m = v; m; m &= m - 1) x += P[(size_t)(__ffs(m) - 1) * ps + q];
-                m2 = fmaxf(m2, x);
-              }
-            }
-            if (m2 > sy * (1.f + p.band)) oka = 0;
-            else if (m2 < sy * (1.f - p.band)) oka = 1;
-            else { pending[k] |= 1u << s; hd[s].need64 = 1; }
-          }
-        }
-        ca[k] += oka;
-      }
-    }
-    __syncthreads();
-    // ---- phase 3 (rare): fp64 log-sum-exp of flagged samples (warp each), then pending pairs ----
-    if (hd[warp].valid && hd[warp].need64) {
-      const int64_t n = hd[warp].n;
-      const float* rowbase = p.logits + n * K * p.ldc;
-      for (int m = 0; m < K; ++m) {
-        const double m64 = (double)hd[warp].mx[m];
-        double s = 0.0;
-        for (int c = lane; c < C; c += 32) s += exp((double)rowbase[(size_t)m * p.ldc + c] - m64);
-        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-        if (lane == 0) hd[warp].lse64[m] = m64 + log(s);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-      uint32_t pm = pending[k];
-      while (pm) {
-        const int s = __ffs(pm) - 1;
-        pm &= pm - 1;
-        const uint32_t v = (uint32_t)(t + 1 + BT * k);
-        atomicAdd(p.n_recheck + (v - 1), 1ull);
-        SmpB sm;
-        smp_bytes(p, smem_raw + s * sbytes, &sm);
-        const int y = hd[s].y, nc = hd[s].nc, ys = hd[s].ys;
-        const bool ovf = hd[s].ovf;
-        const float* P = ovf ? p.scratch + ((size_t)blockIdx.x * SBW + s) * (size_t)K * C : sm.P;
-        const int32_t* cls = ovf ? p.scratch_cls + ((size_t)blockIdx.x * SBW + s) * (size_t)C : sm.cls;
-        const int ps = ovf ? C : CAPS;
-        const float* rowbase = p.logits + hd[s].n * K * p.ldc;
-        float sy = 0.f;
-        for (uint32_t m = v; m; m &= m - 1) sy += P[(size_t)(__ffs(m) - 1) * ps + ys];
-        const float lo = sy * (1.f - p.band);
-        double best = -1.0;
-        int bestc = 0x7fffffff;
-        for (int q = 0; q < nc; ++q) {
-          float s32 = 0.f;
-          for (uint32_t m = v; m; m &= m - 1) s32 += P[(size_t)(__ffs(m) - 1) * ps + q];
-          if (q != ys && s32 < lo) continue;
-          const int cq = cls[q];
-          double acc = 0.0;
-          for (uint32_t m = v; m; m &= m - 1) {
-            const int mi = __ffs(m) - 1;
-            acc += exp((double)rowbase[(size_t)mi * p.ldc + cq] - hd[s].lse64[mi]);
-          }
-          const double a64 = acc / (double)__popc(v);
-          if (a64 > best || (a64 == best && cq < bestc)) { best = a64; bestc = cq; }
-        }
-        ca[k] += (bestc == y);
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NK; ++k) {
-    const int v1 = t + BT * k;
-    if (v1 < S && ca[k]) atomicAdd(p.cnt_avg + v1, (unsigned long long)ca[k]);
-  }
-}
-
 template <int NK>
 cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work, unsigned int* work_count,
                       int32_t* st_top, float* st_lse, float* st_max) {
@@ -523,23 +278,16 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
     else vote_batch_classify_kernel<NK, false><<<grid, BT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  {
+  {  // averages on the worklist, from statistics (the GEMM's or the classify kernel's)
     VoteParams q = p;
     if (!p.lse_in) { q.top1_in = st_top; q.lse_in = st_lse; q.rmax_in = st_max; }
-    const size_t smem = smp_bytes(q, nullptr, nullptr) * SBW;
-    if ((e = cudaFuncSetAttribute(vote_batch_average_kernel<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)) != cudaSuccess)
-      return e;
-    vote_batch_average_kernel<NK><<<sm_count, BT, smem, st>>>(q, work, work_count);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_vote_batch_avg(q, sm_count, st, work, work_count)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
 }  // namespace
 
-size_t vote_batch_smem_per_sample(const VoteParams& p) { return smp_bytes(p, nullptr, nullptr); }
-int vote_batch_avg_ctas_samples() { return SBW; }
 
 cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work,
                               unsigned int* work_count, int32_t* st_top, float* st_lse, float* st_max) {

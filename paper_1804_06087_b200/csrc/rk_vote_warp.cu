@@ -64,19 +64,11 @@ __device__ __noinline__ void tail_add(const VoteParams& p, uint32_t tm, uint32_t
 }
 
 // =============================== kernel A: classify + votes ====================================
-struct AS {  // per-warp shared memory
-  int32_t scls[8];
-  uint32_t smsk[8];
-  int32_t stop[8];
-};
-
 template <bool STATS>
 __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p, int32_t* work,
                                                               unsigned int* work_count, int32_t* st_top,
                                                               float* st_lse, float* st_max) {
-  __shared__ AS as_all[WPC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  AS& as = as_all[warp];
   const int K = p.K, S = p.S, C = p.C;
   const int F = (int)(p.ldc >> 2);
   const uint32_t kmask = (1u << K) - 1u;
@@ -189,39 +181,41 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
       const float thr = theta_threshold(mx, ls, K, lane);
       const bool ycand = __any_sync(FULL, lane < K && rowbase[(size_t)lane * p.ldc + y] >= thr);
       if (ycand) wmask |= 1u << (int)(n - u0);
-      if (!__any_sync(FULL, lane < K && c == y)) continue;  // no member votes y: every vote wrong
-      const bool leader = lane < K && (__ffs(mm) - 1) == lane;
-      const uint32_t lb = __ballot_sync(FULL, leader);
-      const int nd = __popc(lb);
-      __syncwarp();
-      if (leader) {
-        const int pos = __popc(lb & ((1u << lane) - 1u));
-        as.scls[pos] = c;
-        as.smsk[pos] = mm;
-      }
-      if (lane < K) as.stop[lane] = tp;
-      __syncwarp();
+      // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|, y wins iff
+      // c_y > 0, no class has more votes, and the tie (if any) goes to y: LOWEST_CLASS -> no tied
+      // class below y; BEST_MEMBER -> the best-ranked member among all tied voters votes y (Q2).
+      const uint32_t my = __ballot_sync(FULL, lane < K && c == y);  // members voting y
+      if (!my) continue;                                              // every vote wrong
+      const uint32_t ob = __ballot_sync(FULL, lane < K && (__ffs(mm) - 1) == lane && c != y);
+      uint32_t cy[JMAX], tied[JMAX], lose = 0;
 #pragma unroll
-      for (int j = 0; j < JMAX; ++j) {  // A3: majority vote
+      for (int j = 0; j < JMAX; ++j) {
+        const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+        tied[j] = v & my;
+        cy[j] = __popc(tied[j]);
+        lose |= (cy[j] == 0u) ? (1u << j) : 0u;
+      }
+      for (uint32_t w = ob; w; w &= w - 1) {  // other predicted classes (warp-uniform loop)
+        const int l = __ffs(w) - 1;
+        const uint32_t mj = __shfl_sync(FULL, mm, l);
+        const bool ltj = __shfl_sync(FULL, c, l) < y;
+#pragma unroll
+        for (int j = 0; j < JMAX; ++j) {
+          const uint32_t vm = (uint32_t)(lane + 32 * j + 1) & mj;
+          const uint32_t cj = __popc(vm);
+          lose |= (cj > cy[j] || (p.tie != 0 && cj == cy[j] && ltj)) ? (1u << j) : 0u;
+          tied[j] |= (cj == cy[j]) ? vm : 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < JMAX; ++j) {
         const uint32_t v = (uint32_t)(lane + 32 * j + 1);
         if (v > (uint32_t)S) break;
-        int bc = 0, bcls = 0x7fffffff;
-        uint32_t tied = 0;
-#pragma unroll 1
-        for (int q = 0; q < nd; ++q) {
-          const uint32_t mv = v & as.smsk[q];
-          const int cnt = __popc(mv);
-          const int cq = as.scls[q];
-          if (cnt > bc) { bc = cnt; bcls = cq; tied = mv; }
-          else if (cnt == bc && cnt > 0) { tied |= mv; bcls = min(bcls, cq); }
-        }
-        // BEST_MEMBER: best-ranked member among the tied voters (reading Q2); LOWEST_CLASS: min class
-        const int winner = (p.tie == 0) ? as.stop[p.best_of[tied]] : bcls;
-        const uint32_t okv = winner == y;
+        uint32_t okv = !((lose >> j) & 1u);
+        if (p.tie == 0 && okv) okv = (my >> p.best_of[tied[j]]) & 1u;
         gv[j] += okv;
         if (okv && tm) tail_add(p, tm, v);
       }
-      __syncwarp();
     }
     // unit end: worklist append (one atomic per unit), group counts, totals
     if (wmask) {
