@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -63,6 +64,7 @@ struct rk_ctx {
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[3 * 128];
+  int gemm_cluster = 1;                // CTAs per cluster in the head GEMM (env RK_GEMM_CLUSTER=1|2; 2 = W multicast, measured no faster)
   cudaStream_t copy_stream = nullptr;  // H2D of host X, overlapped with the GEMM
   cudaEvent_t ev_start = nullptr;
   std::vector<cudaEvent_t> ev_chunks;
@@ -206,6 +208,7 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e != cudaSuccess) { delete ctx; return RK_ECUDA; }
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (const char* gc = getenv("RK_GEMM_CLUSTER")) ctx->gemm_cluster = atoi(gc) == 2 ? 2 : 1;
   if (world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
@@ -346,6 +349,7 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
     GemmParams gp{};
     gp.N = n; gp.K = ctx->K; gp.C = ctx->C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
     gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias;
+    gp.cluster = ctx->gemm_cluster;
     gp.top1 = ctx->ws_top1 + r0 * ctx->K; gp.lse = ctx->ws_lse + r0 * ctx->K; gp.rmax = ctx->ws_max + r0 * ctx->K;
     gp.logits = ctx->ws_logits + r0 * ctx->K * ctx->ldc;
     int rc = gemm_build_tmaps(gp, Xd, ctx->d_W, gp.logits, ctx->tmaps);  // maps are passed by value

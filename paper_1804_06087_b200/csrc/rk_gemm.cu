@@ -66,10 +66,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+// Logits leave with an L2 evict-first policy: the 32 GB output stream must not evict the X / W
+// operand tiles that other CTAs are about to re-read from L2.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                             uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
+                   map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
                : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
@@ -141,6 +150,35 @@ struct GemmArgs {
   float* rmax;
 };
 
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// CL = CTAs per cluster. CL = 2: the two CTAs of a cluster take adjacent 128-row tiles of the same
+// (model, column tile); each loads one half of the W tile and multicasts it into both CTAs' shared
+// memory, halving the W traffic from L2 (the kernel is L2-feed-bound at CL = 1). The smem stage is
+// released only when BOTH CTAs' MMAs have consumed it (MMA commits multicast to both empty barriers).
+template <int CL>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_heads_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                       const __grid_constant__ CUtensorMap tmo, const GemmArgs a) {
@@ -157,11 +195,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mtiles = (a.N + BM - 1) / BM;
-  const int64_t units = mtiles * a.K;
+  // work unit = (group of CL adjacent row tiles, model); CTA `crank` of the cluster takes row tile
+  // CL * (u / K) + crank. All CTAs of a cluster walk the same unit sequence.
+  const int64_t units = ((mtiles + CL - 1) / CL) * a.K;
+  const int64_t ucl0 = blockIdx.x / CL, ucls = gridDim.x / CL;
+  const int crank = CL > 1 ? (int)cluster_rank() : 0;
   const int kblocks = a.D / BK;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], CL); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmx) : "memory");
@@ -173,7 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast arrives
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -181,19 +224,24 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ===== TMA producer =====
     if (lane == 0) {
       uint32_t it = 0;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int mt = (int)(u / a.K), model = (int)(u % a.K);
+      for (int64_t u = ucl0; u < units; u += ucls) {
+        const int mt = (int)(u / a.K) * CL + crank, model = (int)(u % a.K);
         for (int j = 0; j < a.nt; ++j) {
           const int col0 = model * a.Cp + j * BN;
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
             const int s = it % NS;
             const uint32_t ph = (it / NS) & 1;
-            mbar_wait(&empty[s], ph ^ 1);
+            mbar_wait(&empty[s], ph ^ 1);  // both CTAs' MMAs are done with stage s (CL arrivals)
             uint8_t* sa = stages + s * STAGE_BYTES;
             uint8_t* sb = sa + A_BYTES;
             mbar_expect_tx(&full[s], STAGE_BYTES);
             tma_load_2d(sa, &tmx, &full[s], kb * BK, mt * BM);
-            tma_load_2d(sb, &tmw, &full[s], kb * BK, col0);
+            if (CL == 1) {
+              tma_load_2d(sb, &tmw, &full[s], kb * BK, col0);
+            } else {  // this CTA's half of the W tile, into every CTA of the cluster
+              tma_load_2d_mc(sb + crank * (B_BYTES / CL), &tmw, &full[s], kb * BK, col0 + crank * (BN / CL),
+                             (uint16_t)((1u << CL) - 1u));
+            }
           }
         }
       }
@@ -202,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ===== MMA issuer =====
     if (lane == 0) {
       uint32_t it = 0, tc = 0;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int64_t u = ucl0; u < units; u += ucls) {
         for (int j = 0; j < a.nt; ++j, ++tc) {
           const int width = min(BN, a.Cp - j * BN);
           const uint32_t idesc = umma_idesc(width);
@@ -221,7 +269,9 @@ __global__ void __launch_bounds__(THREADS, 1)
               // advance 16 bf16 = 32 bytes inside the 128-byte swizzle atom
               umma_bf16(dtm, umma_desc(sa + k * 32), umma_desc(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
             }
-            umma_commit(&empty[s]);  // smem slot reusable once these MMAs complete
+            // smem slot reusable once these MMAs complete (in every CTA that received the multicast)
+            if (CL == 1) umma_commit(&empty[s]);
+            else umma_commit_mc(&empty[s], (uint16_t)((1u << CL) - 1u));
           }
           umma_commit(&tfull[as]);  // accumulator ready for the epilogue
         }
@@ -233,9 +283,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int row_in_tile = q * 32 + lane;
     uint8_t* stg = staging + (warp - 2) * 2 * STG_BYTES;
     const float scale = ldexpf(1.0f, a.scale_log2);
+    const uint64_t store_policy = policy_evict_first();
     uint32_t tc = 0, nstore = 0;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const int mt = (int)(u / a.K), model = (int)(u % a.K);
+    for (int64_t u = ucl0; u < units; u += ucls) {
+      const int mt = (int)(u / a.K) * CL + crank, model = (int)(u % a.K);
       const int64_t row = (int64_t)mt * BM + row_in_tile;
       float mx = -INFINITY, sum = 0.f;
       int arg = 0;
@@ -268,7 +319,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) sum += __expf(v[i] - mx);
           }
-          // stage 32 rows x 32 cols (128B-swizzled) and store with TMA
+          // stage 32 rows x 32 cols (128B-swizzled) and store with TMA. (Coalesced st.global.cs
+          // from the same staging box measured 18% slower for the whole kernel: DESIGN.md §6.)
           uint8_t* buf = stg + (nstore & 1) * STG_BYTES;
           if (lane == 0 && nstore >= 2) tma_store_wait_read1();
           __syncwarp();
@@ -281,7 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_3d(&tmo, buf, colbase, model, (int)(mt * BM + q * 32));
+            tma_store_3d(&tmo, buf, colbase, model, (int)(mt * BM + q * 32), store_policy);
             tma_store_commit();
           }
           ++nstore;
@@ -300,7 +352,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncwarp();
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no CTA leaves while a peer may still signal its barriers
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
@@ -342,7 +395,7 @@ int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits,
   {
     cuuint64_t dims[2] = {(cuuint64_t)p.D, (cuuint64_t)p.K * p.Cp};
     cuuint64_t strides[1] = {(cuuint64_t)p.D * 2};
-    cuuint32_t box[2] = {BK, BN};
+    cuuint32_t box[2] = {BK, (cuuint32_t)(BN / (p.cluster > 1 ? p.cluster : 1))};  // W tile (or its half)
     cuuint32_t es[2] = {1, 1};
     if (enc(&maps[1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(W), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -370,13 +423,36 @@ cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
   GemmArgs a;
   a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D; a.nt = (p.Cp + BN - 1) / BN;
   a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lse = p.lse; a.rmax = p.rmax;
-  cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(p.tmap_x);
+  const CUtensorMap& mw = *reinterpret_cast<const CUtensorMap*>(p.tmap_w);
+  const CUtensorMap& mo = *reinterpret_cast<const CUtensorMap*>(p.tmap_out);
+  if (p.cluster <= 1) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    const int64_t units = ((p.N + BM - 1) / BM) * p.K;
+    const int grid = (int)(units < sm_count ? units : sm_count);
+    gemm_heads_kernel<1><<<grid, THREADS, SMEM_BYTES, st>>>(mx, mw, mo, a);
+    return cudaGetLastError();
+  }
+  // 2-CTA clusters: the grid is a multiple of 2 (one CTA per SM, SM pairs share the W tile)
+  cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  const int64_t units = ((p.N + BM - 1) / BM) * p.K;
-  const int grid = (int)(units < sm_count ? units : sm_count);
-  gemm_heads_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(*reinterpret_cast<const CUtensorMap*>(p.tmap_x),
-                                                      *reinterpret_cast<const CUtensorMap*>(p.tmap_w),
-                                                      *reinterpret_cast<const CUtensorMap*>(p.tmap_out), a);
+  const int64_t units = ((p.N + 2 * BM - 1) / (2 * BM)) * p.K;
+  int64_t clusters = units < sm_count / 2 ? units : sm_count / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * clusters));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, gemm_heads_kernel<2>, mx, mw, mo, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -49,6 +49,8 @@ else:
 torch.cuda.synchronize()
 ctx.set_profiling(True)
 for _ in range(a.reps):
+    if a.gemm:
+        ctx.score(X, N)
     t = ctx.subset_stats(lab, cfg)
 ks = ctx.kernel_stats()
 v = ks["vote_subsets"]
@@ -58,4 +60,4 @@ print(f"K={K} C={C} N={N}: vote {ms:.3f} ms/launch, {v['bytes'] / v['launches'] 
       f"a(full)={t['cnt_vote'][-1] / N:.4f}")
 for k, s in ks.items():
     if s["launches"]:
-        print(f"  {k:22s} {s['ms'] / s['launches']:.3f} ms x {s['launches']}")
+        print(f"  {k:22s} {s["ms"] / s["launches"]:.3f} ms x {s["launches"]}", (f"{s['flops'] / s['ms'] / 1e9:.0f} TFLOP/s" if s["flops"] else ""))

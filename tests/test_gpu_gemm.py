@@ -56,7 +56,9 @@ def dev_view(ptr, shape, typestr):
 
 @pytest.mark.parametrize("K,C,D,N", [(3, 10, 128, 200), (2, 100, 256, 300), (3, 1000, 512, 130),
                                      (12, 100, 1024, 257), (1, 2, 64, 5), (4, 300, 192, 129)])
-def test_int_mode_bit_exact(rk, K, C, D, N):
+@pytest.mark.parametrize("cluster", ["1", "2"])
+def test_int_mode_bit_exact(rk, K, C, D, N, cluster, monkeypatch):
+    monkeypatch.setenv("RK_GEMM_CLUSTER", cluster)  # read by rk_create: 1 CTA or 2-CTA W multicast
     y, X, W, b, sh = make(K, C, D, N, 3, real=False)
     ctx, lg, t1, ls = run_gemm(rk, K, C, D, N, X, W, b, sh)
     ref = oracle.logits_gemm(X, W, b, sh)  # fp64, exact for these integer inputs
