@@ -16,7 +16,7 @@
 //      every other candidate is bounded by Q[v] = sum_{m in v} max_{c in R \ ({y} ∪ D)} p[m][c];
 //   4. per subset: a D-class clearly above y -> wrong; D and the bound clearly below -> right;
 //      bound not conclusive -> scan R; decisions inside the relative band `band` are redone in fp64
-//      (warp-cooperative fp64 log-sum-exp, then the oracle's formula) -- rare.
+//      (warp-cooperative fp64 log-sum-exp, then eq. (2) of PAPER.md:72 in fp64) -- rare.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -84,7 +84,7 @@ __host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS*
 }
 
 // fp64 recheck of near-ties (rare, out of line): warp-cooperative fp64 log-sum-exp of every row, then
-// each lane decides its pending subsets exactly like the oracle (avg = (sum_{m in v, asc}
+// each lane decides its pending subsets in fp64 per readings Q5-Q6 (avg = (sum_{m in v, asc}
 // exp(l - lse_m)) / |v|, lowest class on ties) over the candidates inside the band.
 __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t pending, const float* rowbase,
                                           float mx, const float* Pm, int ps, const int32_t* cls, int nc, int ys,
