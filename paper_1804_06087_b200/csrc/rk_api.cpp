@@ -64,7 +64,7 @@ struct rk_ctx {
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[3 * 128];
-  int gemm_cluster = 1;                // CTAs per cluster in the head GEMM (env RK_GEMM_CLUSTER=1|2; 2 = W multicast, measured no faster)
+  int gemm_cluster = 2;                // head GEMM: 2 = CTA pair (tcgen05 cta_group::2, M = 256), 1 = single CTA (env RK_GEMM_CLUSTER)
   cudaStream_t copy_stream = nullptr;  // H2D of host X, overlapped with the GEMM
   cudaEvent_t ev_start = nullptr;
   std::vector<cudaEvent_t> ev_chunks;
@@ -208,7 +208,7 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e != cudaSuccess) { delete ctx; return RK_ECUDA; }
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
-  if (const char* gc = getenv("RK_GEMM_CLUSTER")) ctx->gemm_cluster = atoi(gc) == 2 ? 2 : 1;
+  if (const char* gc = getenv("RK_GEMM_CLUSTER")) ctx->gemm_cluster = atoi(gc) == 1 ? 1 : 2;
   if (world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));

@@ -11,8 +11,10 @@
 // sm_100a design:
 //   * persistent, one CTA per SM, 6 warps: warp 0 = TMA producer, warp 1 = tcgen05.mma issuer and
 //     TMEM owner, warps 2-5 = epilogue (TMEM lane quarter = warp % 4).
-//   * tile 128 rows x up to 256 columns of ONE model, K-block 64 (128-byte swizzle), 4-stage
-//     smem ring fed by TMA (cp.async.bulk.tensor + mbarrier complete_tx).
+//   * default: CTA pairs (cluster of 2) computing 256 rows x up to 256 columns of ONE model with
+//     tcgen05.mma.cta_group::2 (each CTA stages its 128 X rows and half of the W tile; 6-stage
+//     32 KB smem ring fed by TMA); single-CTA variant: 128 x 256 tiles, 4-stage 48 KB ring.
+//     K-block 64, 128-byte swizzle, cp.async.bulk.tensor + mbarrier complete_tx.
 //   * fp32 accumulators in TMEM, double-buffered (2 x 256 columns) so the epilogue of tile i
 //     overlaps the MMAs of tile i+1.
 //   * a work unit is (128-row block, model): the CTA walks the model's column tiles in ascending
@@ -29,14 +31,23 @@
 namespace rk {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, NS = 4;
-constexpr int A_BYTES = BM * BK * 2;   // 16 KB
-constexpr int B_BYTES = BN * BK * 2;   // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB: this CTA's 128 rows of X
 constexpr int EPI_WARPS = 4;
 constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging box
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr int SMEM_BYTES = 1024 /*align slack*/ + NS * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 256;
+// CL = 1: one CTA computes a 128 x 256 tile (W tile 256 rows in its smem, 4 stages of 48 KB).
+// CL = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256): each CTA
+// holds its 128 X rows and HALF of the W tile (128 rows), 6 stages of 32 KB.
+template <int CL>
+struct Tile {
+  static constexpr int B_ROWS = BN / CL;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int NS = CL == 1 ? 4 : 6;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + NS * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 256;
+};
+static_assert(Tile<1>::SMEM_BYTES <= 232448 && Tile<2>::SMEM_BYTES <= 232448, "smem");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -95,9 +106,9 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor: kind::f16, A/B = BF16, D = F32, both K-major, M = 128, N = n.
-__device__ __forceinline__ uint32_t umma_idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// Instruction descriptor: kind::f16, A/B = BF16, D = F32, both K-major, M = m (128, or 256 for a pair), N = n.
+__device__ __forceinline__ uint32_t umma_idesc(int n, int m) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -150,20 +161,39 @@ struct GemmArgs {
   float* rmax;
 };
 
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                               uint16_t mask) {
+// CTA-pair (cta_group::2) forms. The TMA load lands in this CTA's shared memory but signals the
+// LEADER CTA's mbarrier (shared::cluster address from mapa), so the leader's full barrier counts
+// the bytes of both halves; the MMA commit arrives on the same barrier offset in both CTAs.
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                               uint32_t acc) {
   asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrives on `bar` in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"(mask)
+      "h"((uint16_t)3)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -174,86 +204,98 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-// CL = CTAs per cluster. CL = 2: the two CTAs of a cluster take adjacent 128-row tiles of the same
-// (model, column tile); each loads one half of the W tile and multicasts it into both CTAs' shared
-// memory, halving the W traffic from L2 (the kernel is L2-feed-bound at CL = 1). The smem stage is
-// released only when BOTH CTAs' MMAs have consumed it (MMA commits multicast to both empty barriers).
+// CL = 1: one CTA per work unit (128 rows, model). CL = 2: a CTA pair (cluster of 2 on one TPC)
+// per work unit (256 rows, model) with tcgen05.mma.cta_group::2: the leader (rank 0) issues M = 256
+// MMAs reading A (128 rows) and half of B (N/2 rows of W) from EACH CTA's shared memory, so every
+// operand byte crosses L2 -> smem once per pair instead of once per CTA (B traffic halved, smem
+// stage 32 KB instead of 48 KB -> 6 stages). Each CTA's TMEM receives its own 128 rows x N
+// accumulator and its epilogue is unchanged.
 template <int CL>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_heads_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                       const __grid_constant__ CUtensorMap tmo, const GemmArgs a) {
+  using T = Tile<CL>;
+  constexpr int NS = T::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
-  uint8_t* staging = smem + NS * STAGE_BYTES;
+  uint8_t* staging = smem + NS * T::STAGE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + EPI_WARPS * 2 * STG_BYTES);
-  uint64_t* full = bars;            // [NS]
+  uint64_t* full = bars;            // [NS]  (CL = 2: only the leader's are waited on)
   uint64_t* empty = bars + NS;      // [NS]
   uint64_t* tfull = bars + 2 * NS;  // [2]
-  uint64_t* tempty = bars + 2 * NS + 2;
+  uint64_t* tempty = bars + 2 * NS + 2;  // [2]  (CL = 2: the leader's counts both epilogues)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mtiles = (a.N + BM - 1) / BM;
-  // work unit = (group of CL adjacent row tiles, model); CTA `crank` of the cluster takes row tile
-  // CL * (u / K) + crank. All CTAs of a cluster walk the same unit sequence.
+  // work unit = (group of CL adjacent row tiles, model); CTA `crank` of the pair takes row tile
+  // CL * (u / K) + crank. Both CTAs of a pair walk the same unit sequence.
   const int64_t units = ((mtiles + CL - 1) / CL) * a.K;
   const int64_t ucl0 = blockIdx.x / CL, ucls = gridDim.x / CL;
   const int crank = CL > 1 ? (int)cluster_rank() : 0;
   const int kblocks = a.D / BK;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], CL); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI_WARPS); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI_WARPS * CL); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmx) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmw) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmo) : "memory");
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  if (warp == 1) {  // CL = 2: both CTAs allocate collectively (same warp id, same smem slot)
+    if (CL == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
-  if (CL > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast arrives
+  if (CL > 1) cluster_sync_all();  // both CTAs' barriers and TMEM exist before any cross-CTA signal
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer (both CTAs of a pair: each loads its own A rows and its half of B) =====
     if (lane == 0) {
       uint32_t it = 0;
       for (int64_t u = ucl0; u < units; u += ucls) {
         const int mt = (int)(u / a.K) * CL + crank, model = (int)(u % a.K);
         for (int j = 0; j < a.nt; ++j) {
-          const int col0 = model * a.Cp + j * BN;
+          const int width = min(BN, a.Cp - j * BN);
+          const int col0 = model * a.Cp + j * BN + crank * (width / CL);
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
             const int s = it % NS;
             const uint32_t ph = (it / NS) & 1;
-            mbar_wait(&empty[s], ph ^ 1);  // both CTAs' MMAs are done with stage s (CL arrivals)
-            uint8_t* sa = stages + s * STAGE_BYTES;
+            mbar_wait(&empty[s], ph ^ 1);  // the MMAs that read stage s are complete
+            uint8_t* sa = stages + s * T::STAGE_BYTES;
             uint8_t* sb = sa + A_BYTES;
-            mbar_expect_tx(&full[s], STAGE_BYTES);
-            tma_load_2d(sa, &tmx, &full[s], kb * BK, mt * BM);
             if (CL == 1) {
+              mbar_expect_tx(&full[s], T::STAGE_BYTES);
+              tma_load_2d(sa, &tmx, &full[s], kb * BK, mt * BM);
               tma_load_2d(sb, &tmw, &full[s], kb * BK, col0);
-            } else {  // this CTA's half of the W tile, into every CTA of the cluster
-              tma_load_2d_mc(sb + crank * (B_BYTES / CL), &tmw, &full[s], kb * BK, col0 + crank * (BN / CL),
-                             (uint16_t)((1u << CL) - 1u));
+            } else {
+              const uint32_t lbar = map_to_rank(smem_u32(&full[s]), 0);
+              if (crank == 0) mbar_expect_tx(&full[s], CL * T::STAGE_BYTES);  // both halves' bytes
+              tma_load_2d_pair(sa, &tmx, lbar, kb * BK, mt * BM);
+              tma_load_2d_pair(sb, &tmw, lbar, kb * BK, col0);
             }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+    // ===== MMA issuer (CL = 2: leader only) =====
+    if (lane == 0 && crank == 0) {
       uint32_t it = 0, tc = 0;
       for (int64_t u = ucl0; u < units; u += ucls) {
         for (int j = 0; j < a.nt; ++j, ++tc) {
           const int width = min(BN, a.Cp - j * BN);
-          const uint32_t idesc = umma_idesc(width);
+          const uint32_t idesc = umma_idesc(width, BM * CL);
           const uint32_t as = tc & 1;
           mbar_wait(&tempty[as], ((tc >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -262,18 +304,20 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int s = it % NS;
             mbar_wait(&full[s], (it / NS) & 1);
             tc_fence_after();
-            const uint32_t sa = smem_u32(stages + s * STAGE_BYTES);
+            const uint32_t sa = smem_u32(stages + s * T::STAGE_BYTES);
             const uint32_t sb = sa + A_BYTES;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               // advance 16 bf16 = 32 bytes inside the 128-byte swizzle atom
-              umma_bf16(dtm, umma_desc(sa + k * 32), umma_desc(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
+              if (CL == 1) umma_bf16(dtm, umma_desc(sa + k * 32), umma_desc(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
+              else umma_bf16_pair(dtm, umma_desc(sa + k * 32), umma_desc(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
             }
-            // smem slot reusable once these MMAs complete (in every CTA that received the multicast)
+            // smem slot reusable once these MMAs complete (CL = 2: in both CTAs)
             if (CL == 1) umma_commit(&empty[s]);
-            else umma_commit_mc(&empty[s], (uint16_t)((1u << CL) - 1u));
+            else umma_commit_pair(&empty[s]);
           }
-          umma_commit(&tfull[as]);  // accumulator ready for the epilogue
+          if (CL == 1) umma_commit(&tfull[as]);  // accumulator ready for the epilogue(s)
+          else umma_commit_pair(&tfull[as]);
         }
       }
     }
@@ -340,7 +384,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[as]);
+        if (lane == 0) {  // accumulator stage drained (CL = 2: signal the leader, whose MMAs refill it)
+          if (CL == 1) mbar_arrive(&tempty[as]);
+          else mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[as]), 0));
+        }
       }
       if (row < a.N) {
         a.top1[row * a.K + model] = arg;
@@ -356,7 +403,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    if (CL == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }
 }
 
@@ -427,22 +475,24 @@ cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
   const CUtensorMap& mw = *reinterpret_cast<const CUtensorMap*>(p.tmap_w);
   const CUtensorMap& mo = *reinterpret_cast<const CUtensorMap*>(p.tmap_out);
   if (p.cluster <= 1) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_heads_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tile<1>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     const int64_t units = ((p.N + BM - 1) / BM) * p.K;
     const int grid = (int)(units < sm_count ? units : sm_count);
-    gemm_heads_kernel<1><<<grid, THREADS, SMEM_BYTES, st>>>(mx, mw, mo, a);
+    gemm_heads_kernel<1><<<grid, THREADS, Tile<1>::SMEM_BYTES, st>>>(mx, mw, mo, a);
     return cudaGetLastError();
   }
   // 2-CTA clusters: the grid is a multiple of 2 (one CTA per SM, SM pairs share the W tile)
-  cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e =
+      cudaFuncSetAttribute(gemm_heads_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tile<2>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int64_t units = ((p.N + 2 * BM - 1) / (2 * BM)) * p.K;
   int64_t clusters = units < sm_count / 2 ? units : sm_count / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * clusters));
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = Tile<2>::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

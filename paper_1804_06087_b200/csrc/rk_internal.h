@@ -145,7 +145,7 @@ struct GemmParams {
   float* rmax;           // [N][K] row max (theta of the candidate pruning)
   float* logits;         // [N][K][ldc]
   unsigned int* err;
-  int cluster;           // 1 or 2 CTAs per cluster (2: W-tile halves multicast to both CTAs)
+  int cluster;           // 1 = one CTA per 128-row tile; 2 = CTA pair, tcgen05.mma.cta_group::2 on 256-row tiles
 };
 cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st);
 int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits, void* storage /*3*128B*/);

@@ -24,7 +24,7 @@ for r in rows:
     d = per.setdefault(k, [0, 0.0])
     d[0] += 1
     d[1] += float(r[14]) / 1e6
-ours = {"gemm_heads_kernel", "vote_classify_kernel", "vote_average_kernel", "vote_kernel", "overdue_kernel",
+ours = {"gemm_heads_kernel", "vote_classify_kernel", "vote_average_kernel", "vote_batch", "overdue_kernel",
         "merge_kernel", "q_kernel", "fold_kernel"}
 tot_ours = sum(v[1] for k, v in per.items() if any(k.startswith(o) for o in ours))
 lines = [f"# {R} launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of",
