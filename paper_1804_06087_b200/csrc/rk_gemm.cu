@@ -17,7 +17,7 @@
 //     K-block 64, 128-byte swizzle, cp.async.bulk.tensor + mbarrier complete_tx.
 //   * fp32 accumulators in TMEM, double-buffered (2 x 256 columns) so the epilogue of tile i
 //     overlaps the MMAs of tile i+1.
-//   * a work unit is (128-row block, model): the CTA walks the model's column tiles in ascending
+//   * a work unit is (128-row block (CL rows blocks for a pair), model): the CTA walks the model's column tiles in ascending
 //     order, so the epilogue keeps an ONLINE max / lowest-index argmax / rescaled sum-exp per row
 //     in registers and writes top1/lse once per unit; logits leave through swizzled smem staging
 //     and TMA bulk tensor stores (rows >= N and columns >= C are clipped by the tensor map).
@@ -170,12 +170,22 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
   return r;
 }
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
-                                                 int c1) {
+                                                 int c1, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(leader_bar), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                                uint32_t acc) {
@@ -262,6 +272,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ===== TMA producer (both CTAs of a pair: each loads its own A rows and its half of B) =====
     if (lane == 0) {
+      // W (re-read by every row block) is kept in L2 against the 32 KB/sample logits stream:
+      // measured -18% GEMM DRAM reads (ncu, N = 65,536), time unchanged
+      const uint64_t pol_w = policy_evict_last();
+      const uint64_t pol_x = policy_evict_normal();
       uint32_t it = 0;
       for (int64_t u = ucl0; u < units; u += ucls) {
         const int mt = (int)(u / a.K) * CL + crank, model = (int)(u % a.K);
@@ -281,8 +295,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             } else {
               const uint32_t lbar = map_to_rank(smem_u32(&full[s]), 0);
               if (crank == 0) mbar_expect_tx(&full[s], CL * T::STAGE_BYTES);  // both halves' bytes
-              tma_load_2d_pair(sa, &tmx, lbar, kb * BK, mt * BM);
-              tma_load_2d_pair(sb, &tmw, lbar, kb * BK, col0);
+              tma_load_2d_pair(sa, &tmx, lbar, kb * BK, mt * BM, pol_x);
+              tma_load_2d_pair(sb, &tmw, lbar, kb * BK, col0, pol_w);
             }
           }
         }

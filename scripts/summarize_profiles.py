@@ -78,3 +78,25 @@ for k, d in summary.items():
     print(k)
     for kk, vv in d.items():
         print("   ", kk, vv)
+
+# ---- DRAM traffic per launch for bench.py's roofline.traffic (scaled linearly in N to c4) ----------
+CAPN = {"gemm": 65536, "vote": 200000}  # N of the captures in scripts/profile_round.sh
+per_sample = {}
+for key, d in summary.items():
+    tag, name = key.split(":", 1)
+    rd = float(d.get("dram__bytes_read.sum", "0 byte").split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[
+        d.get("dram__bytes_read.sum", "0 byte").split()[1]]
+    wr = float(d.get("dram__bytes_write.sum", "0 byte").split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[
+        d.get("dram__bytes_write.sum", "0 byte").split()[1]]
+    per_sample[name] = (rd + wr) / CAPN[tag]
+gemm_ps = sum(v for k, v in per_sample.items() if k.startswith("gemm_heads"))
+vote_ps = sum(v for k, v in per_sample.items() if k.startswith("vote_"))
+tj = {"_note": f"DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch from the `ncu --set full` "
+               f"captures of {R} (profiles/{R}_ncu_full.json; GEMM at N={CAPN['gemm']}, vote kernels at N={CAPN['vote']}, "
+               f"K=8, C=1000, D=2048), scaled linearly in N to the c4 workload (N=1,000,000). vote_subsets = "
+               f"classify + average kernels. Algorithmic: GEMM 36,096 B/sample (X 4,096 + fp32 logits 32,000), "
+               f"vote 32,004 B/sample.",
+      "c4": {"gemm_heads_tcgen05": round(gemm_ps * 1e6), "vote_subsets": round(vote_ps * 1e6)},
+      "per_sample": {k: round(v, 1) for k, v in per_sample.items()}}
+json.dump(tj, open(f"{OUT}/traffic.json", "w"), indent=1)
+print(json.dumps(tj, indent=1))
