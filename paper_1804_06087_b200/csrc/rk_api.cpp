@@ -88,6 +88,8 @@ struct rk_ctx {
   uint8_t* d_slow = nullptr;
   uint8_t* d_grp = nullptr;
   size_t grp_cap = 0;
+  uint16_t* d_ovd = nullptr;  // per-batch overdue counts (labelled moments)
+  size_t ovd_cap = 0;
   int32_t* d_labels = nullptr;
   int64_t labels_cap = 0;
   int32_t* d_work = nullptr;  // vote worklist [N] + count
@@ -223,7 +225,7 @@ void rk_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
   void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_max, ctx->ws_x,
-                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
+                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -463,12 +465,6 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
     CK(cudaMalloc(&ctx->d_slow, slow.size()));
     CK(cudaMemcpy(ctx->d_slow, slow.data(), slow.size(), cudaMemcpyHostToDevice));
   }
-  if (ctx->want_labelled && nB > 0 && nR > 0) {
-    int tot = 0;
-    for (int bi = 0; bi < nB; ++bi) tot += (int)(ctx->L / ctx->B[bi]);
-    if ((size_t)tot * nR * K * 2 > 48 * 1024)
-      return fail(ctx, RK_EUNSUPPORTED, "labelled moments: lcm(B)/b * nR * K too large");
-  }
   ctx->reset_done = true;
   ctx->final_seen = false;
   ctx->chunks = 0;
@@ -596,6 +592,17 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       mp.arrival = arr; mp.tau = ctx->tau; mp.goff = ctx->cur_off; mp.N = N; mp.want_exceed = ctx->want_exceed;
       mp.osum = ch + 3 * (size_t)S + (size_t)nB * S;
       mp.esum = mp.osum + (size_t)nR * nB * K;
+      if (gs > 0) {  // per-batch counts for the labelled moments
+        const size_t need = (size_t)ovd_elems(nB, ctx->B, nR, K, N, mp.ovd_off) * sizeof(uint16_t);
+        if (ctx->ovd_cap < need) {
+          if (ctx->d_ovd) cudaFree(ctx->d_ovd);
+          ctx->d_ovd = nullptr;
+          CK(cudaMalloc(&ctx->d_ovd, need));
+          ctx->ovd_cap = need;
+        }
+        mp.ovd = ctx->d_ovd;
+        mp.ovd_nrp = ovd_nrp(nR);
+      }
       ProfScope ps(ctx, KK_OVERDUE, st, 0, 0);
       CK(launch_overdue(mp, st));
     }
@@ -614,12 +621,12 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       QParams qp{};
       qp.K = K; qp.S = S; qp.nB = nB; qp.nR = nR; qp.gs = gs;
       for (int bi = 0; bi < nB; ++bi) qp.B[bi] = ctx->B[bi];
-      memcpy(qp.lat, ctx->lat, sizeof(qp.lat));
-      memcpy(qp.rates, ctx->rates, sizeof(qp.rates));
-      qp.arrival = arr; qp.tau = ctx->tau; qp.goff = ctx->cur_off; qp.N = N; qp.L = ctx->L;
+      qp.N = N; qp.L = ctx->L;
       qp.grp = ctx->d_grp; qp.slow = ctx->d_slow; qp.Q = ctx->d_table + ctx->off_Q;
+      qp.ovd = ctx->d_ovd;
+      ovd_elems(nB, ctx->B, nR, K, N, qp.ovd_off);
       ProfScope ps(ctx, KK_Q, st, 0, 0);
-      CK(launch_q(qp, st));
+      CK(launch_q(qp, ctx->sm_count, st));
     }
   }
   if (N % ctx->L != 0) ctx->final_seen = true;

@@ -90,21 +90,26 @@ struct MomentParams {
   int want_exceed;
   unsigned long long* osum;       // [nR][nB][K] overdue counts per slowest model
   unsigned long long* esum;       // [nR][nB][K]
+  uint16_t* ovd;                  // per-batch overdue counts: ovd[ovd_off[bi] + (j*K + m)*ovd_nrp + r], or null
+  int64_t ovd_off[kMaxB];
+  int ovd_nrp;                    // rates padded to 4 or 8 (ovd_nrp(nR))
 };
+// elements of the per-batch overdue table for N samples
+int ovd_nrp(int nR);
+int64_t ovd_elems(int nB, const int* B, int nR, int K, int64_t N, int64_t* off /*[kMaxB] or null*/);
 cudaError_t launch_overdue(const MomentParams& p, cudaStream_t st);  // err flags follow esum
 
 struct QParams {
   int K, S, nB, nR, gs;
   int B[kMaxB];
-  int64_t lat[kMaxK * kMaxB];
-  double rates[kMaxR];
-  const int64_t* arrival;
-  int64_t tau, goff, N, L;        // L = lcm(B)
-  const uint8_t* grp;             // [ceil(N/gs)][S]
+  int64_t N, L;                   // L = lcm(B)
+  const uint8_t* grp;             // [ceil(N/gs)][S] correct votes per group of gs samples
   const uint8_t* slow;            // [nB][S] slowest member of v at batch size b
+  const uint16_t* ovd;            // per-batch overdue counts (MomentParams::ovd)
+  int64_t ovd_off[kMaxB];
   unsigned long long* Q;          // [nR][nB][S] (table section)
 };
-cudaError_t launch_q(const QParams& p, cudaStream_t st);
+cudaError_t launch_q(const QParams& p, int sm_count, cudaStream_t st);
 
 struct MergeParams {
   int S, nB, nR;

@@ -66,6 +66,7 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
       }
       cnt[m] = lo;
       atomicAdd(&so[(r * p.nB + bi) * p.K + m], (unsigned long long)lo);
+      if (p.ovd) p.ovd[p.ovd_off[bi] + (jl * p.K + m) * p.ovd_nrp + r] = (uint16_t)lo;
     }
     if (p.want_exceed) {
       // E = sum_{i < cnt} (tl - t_i + c - tau): one sweep with prefix sums of t_i
@@ -120,67 +121,125 @@ __global__ void merge_kernel(const MergeParams p, int64_t N, int64_t off_N) {
 }
 
 // ---- labelled moments Q[r][b][v] = sum_j corr_j(v) * o_j(v,b,r) --------------------------------
-// One CTA per L-chunk (L = lcm(B) samples, L/gs groups). o_j per (b, r, batch, slowest model) is
-// computed into shared memory, then each thread owns subsets v and sums group counts per batch.
-__global__ void q_kernel(const QParams p) {
-  extern __shared__ unsigned short so_q[];  // [sum_b L/b][nR][K]
+// o_j(v,b,r) = overdue count of batch j of size b at rate r when v's slowest member is m (written
+// per batch by overdue_kernel into `ovd`, layout [j][m][r] with r padded to NRP so one vector load
+// fetches every rate). Grid = (slice of QT subsets) x (range of L-chunks); a thread owns one subset,
+// reads each group count of its subset once (coalesced across the warp: grp is [group][S]), keeps
+// a running correct-count per batch size and, at each batch end, multiply-adds it into u32 register
+// accumulators [NRP][b], spilled to u64 shared accumulators every `flush` chunks (no u32 overflow:
+// a chunk adds at most L * max(B)); one atomic per (v, r, b) per block.
+constexpr int QT = 128;
+constexpr int kQStageBytes = 32 * 1024;
+constexpr int kQBlocksPerSM = 6;  // STAGED: the chunk's o values staged in shared memory
+template <int NRP>
+struct OVec;
+template <>
+struct OVec<4> { using T = uint2; };
+template <>
+struct OVec<8> { using T = uint4; };
+
+// Host-computed per-batch-size constants (kernel parameter space: constant-bank operands, no registers).
+struct QConst {
+  int bg[kMaxB];      // groups per batch
+  int nbc[kMaxB];     // batches per chunk (L / B)
+  int soff[kMaxB];    // first staged batch of each size
+  int64_t nbat[kMaxB];  // complete batches in this accumulate call (reading Q13)
+};
+
+// NB = nB exactly (1..8; 0 = generic loop bound p.nB for the unstaged fallback).
+template <int NRP, int NB, bool STAGED>
+__global__ void __launch_bounds__(QT, kQBlocksPerSM)
+    q_kernel(const QParams p, const QConst qc, int64_t chunks_per_block, int tot, int flush) {
+  constexpr int NBX = NB > 0 ? NB : kMaxB;
+  extern __shared__ unsigned long long qacc[];  // [nR * nB][QT], then (STAGED) u16 [tot][K][NRP]
+  uint16_t* so = reinterpret_cast<uint16_t*>(qacc + (size_t)p.nR * p.nB * QT);
+  using V = typename OVec<NRP>::T;
+  const int nB = NB > 0 ? NB : p.nB;
+  const int v1 = blockIdx.x * QT + threadIdx.x;
+  const bool own = v1 < p.S;
+  const int KR = p.K * NRP;  // u16 per batch
+  for (int i = 0; i < p.nR * nB; ++i) qacc[i * QT + threadIdx.x] = 0;
+  const int64_t gpc = p.L / p.gs;  // groups per chunk
+  const int64_t ngroups = (p.N + p.gs - 1) / p.gs;
   const int64_t nch = (p.N + p.L - 1) / p.L;
-  int off[kMaxB];
-  int tot = 0;
-  for (int bi = 0; bi < p.nB; ++bi) { off[bi] = tot; tot += (int)(p.L / p.B[bi]); }
-  for (int64_t q = blockIdx.x; q < nch; q += gridDim.x) {
-    __syncthreads();
-    // phase 1: overdue counts of every complete batch in this chunk
-    for (int w = threadIdx.x; w < tot * p.nR * p.K; w += blockDim.x) {
-      const int m = w % p.K;
-      const int r = (w / p.K) % p.nR;
-      const int jj = w / (p.K * p.nR);
-      int bi = 0;
-      while (bi + 1 < p.nB && jj >= off[bi + 1]) ++bi;
-      const int b = p.B[bi];
-      const int64_t s0 = q * p.L + (int64_t)(jj - off[bi]) * b;
-      unsigned short o = 0;
-      if (s0 + b <= (p.N / b) * b) {
-        const double rate = p.rates[r];
-        const int64_t tl = arrival_at(p.arrival, s0 + b - 1, p.goff + s0 + b - 1, rate);
-        const int64_t thr = tl + p.lat[m * p.nB + bi] - p.tau;
-        int lo = 0, hi = b;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (arrival_at(p.arrival, s0 + mid, p.goff + s0 + mid, rate) < thr) lo = mid + 1; else hi = mid;
+  const int64_t q0 = blockIdx.y * chunks_per_block;
+  const int64_t q1 = min(nch, q0 + chunks_per_block);
+  // slowest member of v per batch size, 4 bits each
+  uint32_t mpack = 0;
+  for (int bi = 0; bi < nB; ++bi) mpack |= (uint32_t)(own ? p.slow[(size_t)bi * p.S + v1] : 0) << (4 * bi);
+  unsigned int acc[NRP][NBX];
+#pragma unroll
+  for (int bi = 0; bi < NBX; ++bi)
+#pragma unroll
+    for (int r = 0; r < NRP; ++r) acc[r][bi] = 0;
+  const uint8_t* gp = p.grp + (own ? v1 : 0);
+  int since = 0;
+  for (int64_t q = q0; q < q1; ++q) {
+    if (STAGED) {
+      __syncthreads();
+#pragma unroll
+      for (int bi = 0; bi < NBX; ++bi) {
+        if (bi >= nB) break;
+        const int64_t jbase = q * qc.nbc[bi];
+        const int nvalid = (int)max((int64_t)0, min((int64_t)qc.nbc[bi], qc.nbat[bi] - jbase)) * p.K;
+        const V* src = reinterpret_cast<const V*>(p.ovd + p.ovd_off[bi] + jbase * KR);
+        V* dst = reinterpret_cast<V*>(so + qc.soff[bi] * KR);
+        for (int w = threadIdx.x; w < qc.nbc[bi] * p.K; w += QT) {
+          V z{};
+          dst[w] = w < nvalid ? src[w] : z;  // incomplete batches contribute 0
         }
-        o = (unsigned short)lo;
       }
-      so_q[w] = o;
+      __syncthreads();
     }
-    __syncthreads();
-    // phase 2: per subset
-    const int64_t g0 = q * p.L / p.gs;
-    const int64_t ngroups = (p.N + p.gs - 1) / p.gs;
-    for (int v1 = threadIdx.x; v1 < p.S; v1 += blockDim.x) {
-      unsigned long long acc[kMaxR * kMaxB];
-      for (int i = 0; i < p.nR * p.nB; ++i) acc[i] = 0;
-      for (int bi = 0; bi < p.nB; ++bi) {
-        const int b = p.B[bi];
-        const int m = p.slow[(size_t)bi * p.S + v1];
-        const int nbat = (int)(p.L / b);
-        for (int jj = 0; jj < nbat; ++jj) {
-          const int64_t s0 = q * p.L + (int64_t)jj * b;
-          if (s0 + b > (p.N / b) * b) break;
-          unsigned int corr = 0;
-          const int64_t gg = g0 + (int64_t)jj * (b / p.gs);
-          for (int k = 0; k < b / p.gs; ++k)
-            if (gg + k < ngroups) corr += p.grp[(gg + k) * p.S + v1];
-          if (!corr) continue;
-          for (int r = 0; r < p.nR; ++r)
-            acc[r * p.nB + bi] += (unsigned long long)corr * so_q[((off[bi] + jj) * p.nR + r) * p.K + m];
+    if (!own) continue;
+    // per size: (batch index in chunk) << 16 | groups left in the current batch
+    int lj[NBX];
+    unsigned int part[NBX];
+#pragma unroll
+    for (int bi = 0; bi < NBX; ++bi) { lj[bi] = qc.bg[bi]; part[bi] = 0; }
+    const int64_t ga = q * gpc, gb = min(ngroups, ga + gpc);
+#pragma unroll 4
+    for (int64_t g = ga; g < gb; ++g) {
+      const unsigned int c = gp[g * p.S];
+#pragma unroll
+      for (int bi = 0; bi < NBX; ++bi) {
+        if (NB == 0 && bi >= nB) break;
+        part[bi] += c;
+        if (((--lj[bi]) & 0xFFFF) == 0) {  // end of batch (lj >> 16) of size B[bi] in this chunk
+          const int jj = lj[bi] >> 16;
+          const int m = (mpack >> (4 * bi)) & 15;
+          if (part[bi] && (STAGED || q * qc.nbc[bi] + jj < qc.nbat[bi])) {
+            const uint16_t* ob = STAGED ? so + (qc.soff[bi] + jj) * KR
+                                        : p.ovd + p.ovd_off[bi] + (q * qc.nbc[bi] + jj) * KR;
+            union { V v; uint16_t h[NRP]; } o;
+            o.v = *reinterpret_cast<const V*>(ob + m * NRP);
+#pragma unroll
+            for (int r = 0; r < NRP; ++r) acc[r][bi] += part[bi] * o.h[r];
+          }
+          part[bi] = 0;
+          lj[bi] += (1 << 16) + qc.bg[bi];
         }
       }
-      for (int r = 0; r < p.nR; ++r)
-        for (int bi = 0; bi < p.nB; ++bi)
-          if (acc[r * p.nB + bi]) atomicAdd(p.Q + ((size_t)r * p.nB + bi) * p.S + v1, acc[r * p.nB + bi]);
+    }
+    if (++since == flush || q + 1 == q1) {  // spill the u32 accumulators
+      since = 0;
+#pragma unroll
+      for (int bi = 0; bi < NBX; ++bi) {
+        if (bi >= nB) break;
+#pragma unroll
+        for (int r = 0; r < NRP; ++r) {
+          if (r < p.nR) qacc[(r * nB + bi) * QT + threadIdx.x] += acc[r][bi];
+          acc[r][bi] = 0;
+        }
+      }
     }
   }
+  if (!own) return;
+  for (int r = 0; r < p.nR; ++r)
+    for (int bi = 0; bi < nB; ++bi) {
+      const unsigned long long x = qacc[(r * nB + bi) * QT + threadIdx.x];
+      if (x) atomicAdd(p.Q + ((size_t)r * nB + bi) * p.S + v1, x);
+    }
 }
 
 // ---- A7: reward fold -----------------------------------------------------------------------
@@ -221,16 +280,76 @@ cudaError_t launch_merge(const MergeParams& p, int64_t N, int64_t off_N, cudaStr
   return cudaGetLastError();
 }
 
-cudaError_t launch_q(const QParams& p, cudaStream_t st) {
-  if (p.nB == 0 || p.nR == 0 || p.N <= 0) return cudaSuccess;
-  int tot = 0;
-  for (int bi = 0; bi < p.nB; ++bi) tot += (int)(p.L / p.B[bi]);
-  const size_t smem = sizeof(unsigned short) * (size_t)tot * p.nR * p.K;
-  if (smem > 48 * 1024) return cudaErrorInvalidValue;
-  int64_t nch = (p.N + p.L - 1) / p.L;
-  int blocks = (int)(nch < 148 * 8 ? nch : 148 * 8);
-  q_kernel<<<blocks, 256, smem, st>>>(p);
+int ovd_nrp(int nR) { return nR <= 4 ? 4 : 8; }
+
+int64_t ovd_elems(int nB, const int* B, int nR, int K, int64_t N, int64_t* off) {
+  int64_t tot = 0;
+  for (int bi = 0; bi < nB; ++bi) {
+    if (off) off[bi] = tot;
+    tot += (N / B[bi]) * K * ovd_nrp(nR);
+  }
+  return tot;
+}
+
+template <int NRP, int NB, bool STAGED>
+static cudaError_t launch_q_t(const QParams& p, const QConst& qc, dim3 grid, size_t smem, int64_t cpb, int tot,
+                              int flush, cudaStream_t st) {
+  cudaError_t e =
+      cudaFuncSetAttribute(q_kernel<NRP, NB, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  q_kernel<NRP, NB, STAGED><<<grid, QT, smem, st>>>(p, qc, cpb, tot, flush);
   return cudaGetLastError();
+}
+template <int NRP>
+static cudaError_t launch_q_nb(const QParams& p, const QConst& qc, bool staged, dim3 grid, size_t smem, int64_t cpb,
+                               int tot, int flush, cudaStream_t st) {
+  if (!staged) return launch_q_t<NRP, 0, false>(p, qc, grid, smem, cpb, tot, flush, st);
+  switch (p.nB) {
+    case 1: return launch_q_t<NRP, 1, true>(p, qc, grid, smem, cpb, tot, flush, st);
+    case 2: return launch_q_t<NRP, 2, true>(p, qc, grid, smem, cpb, tot, flush, st);
+    case 3: return launch_q_t<NRP, 3, true>(p, qc, grid, smem, cpb, tot, flush, st);
+    case 4: return launch_q_t<NRP, 4, true>(p, qc, grid, smem, cpb, tot, flush, st);
+    case 5: return launch_q_t<NRP, 5, true>(p, qc, grid, smem, cpb, tot, flush, st);
+    case 6: return launch_q_t<NRP, 6, true>(p, qc, grid, smem, cpb, tot, flush, st);
+    case 7: return launch_q_t<NRP, 7, true>(p, qc, grid, smem, cpb, tot, flush, st);
+    default: return launch_q_t<NRP, 8, true>(p, qc, grid, smem, cpb, tot, flush, st);
+  }
+}
+
+cudaError_t launch_q(const QParams& p, int sm_count, cudaStream_t st) {
+  if (p.nB == 0 || p.nR == 0 || p.N <= 0) return cudaSuccess;
+  const int64_t nch = (p.N + p.L - 1) / p.L;
+  const int slices = (p.S + QT - 1) / QT;
+  QConst qc{};
+  int tot = 0, bmax = 1;
+  for (int bi = 0; bi < p.nB; ++bi) {
+    qc.bg[bi] = p.B[bi] / p.gs;
+    qc.nbc[bi] = (int)(p.L / p.B[bi]);
+    qc.soff[bi] = tot;
+    qc.nbat[bi] = p.N / p.B[bi];
+    tot += qc.nbc[bi];
+    bmax = p.B[bi] > bmax ? p.B[bi] : bmax;
+  }
+  const int nrp = ovd_nrp(p.nR);
+  const size_t acc = sizeof(unsigned long long) * (size_t)p.nR * p.nB * QT;
+  const size_t stage = sizeof(uint16_t) * (size_t)tot * p.K * nrp;
+  const bool staged = stage <= (size_t)kQStageBytes;
+  // one wave: resident blocks per SM limited by the launch bound and shared memory
+  const size_t smem = acc + (staged ? stage : 0);
+  int per_sm = (int)((200 * 1024) / (smem + 1024));
+  per_sm = per_sm < 1 ? 1 : (per_sm > kQBlocksPerSM ? kQBlocksPerSM : per_sm);
+  int64_t ranges = ((int64_t)sm_count * per_sm) / slices;
+  if (ranges < 1) ranges = 1;
+  if (ranges > nch) ranges = nch;
+  if (ranges > 65535) ranges = 65535;
+  const int64_t cpb = (nch + ranges - 1) / ranges;
+  ranges = (nch + cpb - 1) / cpb;
+  // u32 register accumulators: one chunk adds at most L * max(B) <= 2^24 per (r, b)
+  const unsigned long long fl = 0xFFFFFFFFull / ((unsigned long long)p.L * bmax);
+  const int flush = (int)(fl < 1024 ? fl : 1024);
+  const dim3 grid((unsigned)slices, (unsigned)ranges);
+  return nrp == 4 ? launch_q_nb<4>(p, qc, staged, grid, smem, cpb, tot, flush, st)
+                  : launch_q_nb<8>(p, qc, staged, grid, smem, cpb, tot, flush, st);
 }
 
 cudaError_t launch_fold(const FoldParams& p, cudaStream_t st) {

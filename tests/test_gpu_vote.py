@@ -117,6 +117,20 @@ def test_chunked_and_sharded_equal_one_shot(rk):
         np.testing.assert_array_equal(parts[0][k] + parts[1][k], getattr(o, k), err_msg=k)
 
 
+@pytest.mark.parametrize("B,N", [((16, 48, 80), 1000),   # non-nested sizes, L = 240, staged overdue table
+                                 ((1, 4096), 9000),       # gs = 1, L = 4096: per-chunk table > 32 KB, global path
+                                 ((3, 6, 12), 61)])       # ragged tail, gs = 1
+def test_labelled_moments_batch_sets(rk, B, N):
+    K, C = 4, 50
+    y = gen.labels(31, 0, N, C)
+    L = gen.logits(31, 0, N, K, C, y=y)
+    gcfg, ocfg = default_cfg(K, B=B, tau_ns=100_000_000)
+    t, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    compare_tables(t, o, K=K)
+    assert o.Q.sum() > 0  # the labelled moments are exercised
+
+
 def test_arrival_ns_input(rk):
     K, C, N = 3, 10, 640
     y = gen.labels(5, 0, N, C)
