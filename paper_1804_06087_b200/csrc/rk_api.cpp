@@ -558,7 +558,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     vp.scratch = ctx->d_scratch;
     vp.scratch_cls = ctx->d_scratch_cls;
     {
-      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, N + 1)) != RK_OK) return s;  // worklist [N] + count
+      // worklist [N] + count, then (K >= 9) the overflow worklist [N] + count
+      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, 2 * N + 2)) != RK_OK) return s;
       int32_t* st_top = nullptr;
       float *st_lse = nullptr, *st_max = nullptr;
       if (!ctx->batch_stats) {  // the classify kernel writes row statistics for the averaging kernel
@@ -568,6 +569,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
         st_top = ctx->ws_top1; st_lse = ctx->ws_lse; st_max = ctx->ws_max;
       }
       unsigned int* wc = reinterpret_cast<unsigned int*>(ctx->d_work + N);
+      vp.ovf_work = ctx->d_work + N + 1;
+      vp.ovf_count = reinterpret_cast<unsigned int*>(ctx->d_work + 2 * N + 1);
       const double bytes = (double)N * ((double)K * C * 4 + 4);
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
       if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lse, st_max, ctx->sm_count));

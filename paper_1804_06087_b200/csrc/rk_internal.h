@@ -42,6 +42,8 @@ struct VoteParams {
   float* scratch;                 // per-CTA overflow P [gridDim][G][C][K]
   int32_t* scratch_cls;           // per-CTA overflow class list [gridDim][G][C]
   unsigned int* err;              // [0] non-finite logits, [1] bad label
+  int32_t* ovf_work;              // K >= 9: worklist samples with |R| > 32 (rk_vote_cta_avg.cu) [N]
+  unsigned int* ovf_count;
 };
 
 // warp-per-sample variant for K <= 8, C <= 1024 (rk_vote_warp.cu); uses CAP, TCAP, K1, gs, scratch
@@ -61,6 +63,11 @@ cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st
                               unsigned int* work_count, int32_t* st_top, float* st_lse, float* st_max);
 cudaError_t launch_vote_batch_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
                                   const unsigned int* work_count);  // rk_vote_batch_avg.cu
+// CTA-per-sample averaging with exact tables over every competitor (rk_vote_cta_avg.cu); samples with
+// more than 32 competitors are appended to ovf_work for launch_vote_batch_avg.
+size_t vote_cta_avg_smem(const VoteParams& q);
+cudaError_t launch_vote_cta_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
+                                const unsigned int* work_count, int32_t* ovf_work, unsigned int* ovf_count);
 
 // Two kernels: classify+votes over all samples, then averages over the worklist of samples whose
 // label is an averaging candidate. work: [N] int32, work_count: 1 uint; st_*: [N][K] statistics

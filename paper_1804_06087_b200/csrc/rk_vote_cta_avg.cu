@@ -1,0 +1,348 @@
+// rk_vote_cta_avg.cu — step A4 (argmax of the averaged softmax, readings Q5/Q6) of every
+// subset for the worklist samples, one sample per CTA at a time, exact half-mask tables over every
+// competitor.
+//
+// For a worklist sample (label y is a candidate, models not unanimous), a class c can be the argmax
+// of some subset's average only if c ∈ S_c (θ pruning) and l[m][c] >= l[m][y] for some
+// model m (otherwise p[m][c] < p[m][y] in every member). R = that set minus y. With the models split
+// into a low half (K1) and a high half, every subset v = a | b<<K1 has
+//     sum_{m in v} p[m][c] = TA[a][c] + TB[b][c]
+// so y is the subset's averaged argmax iff TA[a][y] + TB[b][y] beats every c ∈ R (ties: lowest class).
+// The decision per (v, c) is one add and two compares in fp32 with a relative band: clear wins and
+// losses are exact (positive sums, relative error << band); the band (and tiny sums) goes to an fp64
+// recheck computed from the sample's rows, which are in shared memory.
+//
+// sm_100a layout: the K logit rows of a sample are contiguous ([N][K][ldc]); the CTA fetches them with
+// one cp.async.bulk (TMA, mbarrier complete_tx), prefetching the next sample while it decides the
+// current one (double buffer when two copies fit). 256 threads: thread t decides subsets t + 256k.
+// Samples whose columns do not fit 36 slots are appended to an overflow worklist for rk_vote_batch_avg.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "rk_internal.h"
+
+namespace rk {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int CT = 256;            // threads per CTA
+constexpr int CW = CT / 32;
+constexpr int JS = 36;             // table columns: y + up to 35 competitors, padded to float4; 144 B rows:
+                                   // 128-bit loads from 8 distinct rows hit distinct bank groups
+constexpr int KM = 12;
+
+__host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct Lay {  // dynamic shared memory layout
+  size_t rows, tab, pm, pend, total;
+  int nbuf;
+};
+__host__ __device__ inline Lay layout(const VoteParams& p) {
+  Lay L;
+  const size_t rowbytes = a128((size_t)p.K * p.ldc * 4);
+  L.nbuf = 2 * rowbytes <= 64 * 1024 ? 2 : 1;
+  const int TT = (1 << p.K1) + (1 << (p.K - p.K1));
+  L.rows = 0;
+  L.tab = L.rows + L.nbuf * rowbytes;
+  L.pm = L.tab + a128((size_t)TT * JS * 4);
+  L.pend = L.pm + a128((size_t)p.K * JS * 4);
+  L.total = L.pend + a128((size_t)(p.S + 1) * 2);
+  return L;
+}
+
+struct Stat {  // per-sample statistics, loaded one sample ahead (double-buffered)
+  int64_t n;
+  int32_t y;
+  int32_t top[KM];
+  float ls[KM], thr[KM], mx[KM];
+};
+struct Shared {  // static shared state
+  uint64_t bar[2];
+  uint32_t bm[32], bmB[32];
+  int32_t cols[JS];  // 0 = y, 1..nr = R ascending, -1 = unused
+  Stat st[2];
+  double lse64[KM];
+  int32_t nq, npend, skip;
+};
+
+// warp 0: labels, top-1, log-sum-exp, row max of worklist entry e; θ threshold per model
+__device__ __forceinline__ void load_stat(const VoteParams& p, const int32_t* work, int64_t e, Stat& st, int lane) {
+  const int K = p.K;
+  const int64_t n = work[e];
+  float mx = 0.f, ls = 0.f;
+  int tp = 0;
+  if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lse_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
+  float th = lane < K ? __expf(mx - ls) : INFINITY;
+  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
+  const float lth = logf(th / (float)K);
+  if (lane < K) {
+    st.top[lane] = tp; st.ls[lane] = ls; st.mx[lane] = mx;
+    st.thr[lane] = (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
+  }
+  if (lane == 0) { st.n = n; st.y = p.labels[n]; }
+}
+
+template <int NSUB>
+__global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParams p, const int32_t* work,
+                                                                 const unsigned int* work_count, int32_t* ovf_work,
+                                                                 unsigned int* ovf_count) {
+  extern __shared__ __align__(128) char dyn[];
+  __shared__ Shared sh;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int K = p.K, C = p.C, S = p.S, K1 = p.K1;
+  const int TAn = 1 << K1;
+  const Lay L = layout(p);
+  const size_t rowbytes = a128((size_t)K * p.ldc * 4);
+  const uint32_t ldbytes = (uint32_t)((size_t)K * p.ldc * 4);
+  float* TA = reinterpret_cast<float*>(dyn + L.tab);
+  float* TB = TA + (size_t)TAn * JS;
+  float* Pm = reinterpret_cast<float*>(dyn + L.pm);
+  uint16_t* pend = reinterpret_cast<uint16_t*>(dyn + L.pend);
+  const int64_t W = *work_count;
+
+  if (t == 0) {
+    mbar_init(&sh.bar[0], 1);
+    mbar_init(&sh.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (t < 32) { sh.bm[t] = 0u; sh.bmB[t] = 0u; }
+  if (t == 0) sh.npend = 0;
+  __syncthreads();
+  auto issue = [&](int64_t e, int buf) {
+    const int64_t n = work[e];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the buffer first
+    mbar_expect_tx(&sh.bar[buf], ldbytes);
+    bulk_load(dyn + L.rows + buf * rowbytes, p.logits + n * K * p.ldc, ldbytes, &sh.bar[buf]);
+  };
+  if (t == 0 && (int64_t)blockIdx.x < W) issue(blockIdx.x, 0);
+  if (warp == 0 && (int64_t)blockIdx.x < W) load_stat(p, work, blockIdx.x, sh.st[0], lane);
+
+  uint32_t ca[NSUB];
+#pragma unroll
+  for (int k = 0; k < NSUB; ++k) ca[k] = 0;
+
+  int64_t it = 0;
+  for (int64_t e = blockIdx.x; e < W; e += gridDim.x, ++it) {
+    const int buf = L.nbuf == 2 ? (int)(it & 1) : 0;
+    const uint32_t par = L.nbuf == 2 ? (uint32_t)((it >> 1) & 1) : (uint32_t)(it & 1);
+    if (t == 0 && L.nbuf == 2 && e + gridDim.x < W) issue(e + gridDim.x, buf ^ 1);  // prefetch
+    const float* rows = reinterpret_cast<const float*>(dyn + L.rows + buf * rowbytes);
+    const int sb = (int)(it & 1);
+    const Stat& st = sh.st[sb];
+    mbar_wait(&sh.bar[buf], par);  // the sample's rows have landed
+    __syncthreads();                // (and warp 0's statistics of this sample, loaded last iteration)
+    const int y = st.y;
+    // ---- S2: candidate bitmaps: bm = S_c, bmB = {c : exists m, l[m][c] >= l[m][y]} ---------------
+    {
+      const int nw = (C + 31) >> 5;
+      for (int m = warp; m < K; m += CW) {
+        const float* row = rows + (size_t)m * p.ldc;
+        const float tm = st.thr[m], ym = row[y];
+        for (int w = 0; w < nw; ++w) {
+          const int c = w * 32 + lane;
+          const float x = c < C ? row[c] : -INFINITY;
+          const uint32_t b1 = __ballot_sync(FULL, x >= tm);
+          const uint32_t b2 = __ballot_sync(FULL, x >= ym);
+          if (lane == 0) {
+            if (b1) atomicOr(&sh.bm[w], b1);
+            if (b2) atomicOr(&sh.bmB[w], b2);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- S3: columns (warp 0): 0 = y, 1..nr = R ascending; unused slots up to a float4 boundary hold
+    //      -1 (zero probability). Samples whose columns do not fit go to the overflow worklist.
+    if (warp == 0) {
+      uint32_t word = sh.bm[lane] & sh.bmB[lane];
+      if (lane == (y >> 5)) word &= ~(1u << (y & 31));
+      const int cnt = __popc(word);
+      int incl = cnt;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off) incl += o;
+      }
+      const int nr = __shfl_sync(FULL, incl, 31);
+      const int nq = (nr + 1 + 3) >> 2;
+      const bool fits = 4 * nq <= JS;
+      if (fits) {
+        if (lane < 4) sh.cols[4 * nq - 4 + lane] = -1;
+        __syncwarp();
+        int k = 1 + incl - cnt;
+        for (uint32_t w = word; w; w &= w - 1) sh.cols[k++] = lane * 32 + (__ffs(w) - 1);
+      }
+      if (lane == 0) {
+        sh.cols[0] = y;
+        sh.nq = nq;
+        sh.skip = !fits;
+        if (!fits) ovf_work[atomicAdd(ovf_count, 1u)] = (int32_t)st.n;  // rk_vote_batch_avg.cu
+      }
+    }
+    __syncthreads();
+    if (t < 32) { sh.bm[t] = 0u; sh.bmB[t] = 0u; }  // ready for the next sample (read only above)
+    if (warp == CW - 1 && e + gridDim.x < W) load_stat(p, work, e + gridDim.x, sh.st[sb ^ 1], lane);
+    if (!sh.skip) {
+      const int nq = sh.nq, nj4 = 4 * nq;
+      // ---- S4: p[m][c] = exp(l - lse) for every column ------------------------------------------
+      for (int i = t; i < K * nj4; i += CT) {
+        const int m = i / nj4, j = i - m * nj4;
+        const int c = sh.cols[j];
+        Pm[m * JS + j] = c >= 0 ? expf(rows[(size_t)m * p.ldc + c] - st.ls[m]) : 0.f;
+      }
+      __syncthreads();
+      // ---- S5: half-mask tables TA[h][j] = sum_{m in h} p[m][j] (ascending m), TB rows after TA ----
+      {
+        const int KB = K - K1, TT = TAn + (1 << KB);
+        for (int i = t; i < TT * nj4; i += CT) {
+          const int h = i / nj4, j = i - h * nj4;
+          const bool lo = h < TAn;
+          const uint32_t hm = lo ? (uint32_t)h : (uint32_t)(h - TAn);
+          const float* pc = Pm + (lo ? 0 : K1) * JS + j;
+          float s = 0.f;
+#pragma unroll
+          for (int b = 0; b < 6; ++b)
+            if ((hm >> b) & 1u) s += pc[b * JS];
+          TA[(size_t)h * JS + j] = s;
+        }
+      }
+      __syncthreads();
+      // ---- S6: every subset: sum of y's column and the largest competitor, branch-free ----------
+#pragma unroll
+      for (int k = 0; k < NSUB; ++k) {
+        const uint32_t v = (uint32_t)(t + CT * k);
+        if (v == 0 || v > (uint32_t)S) continue;
+        uint32_t ok = 0;
+        if (__popc(v) == 1) {
+          ok = st.top[__ffs(v) - 1] == y;  // softmax is monotone (invariant I1)
+        } else {
+          const float4* A = reinterpret_cast<const float4*>(TA + (size_t)(v & (TAn - 1)) * JS);
+          const float4* B = reinterpret_cast<const float4*>(TB + (size_t)(v >> K1) * JS);
+          float4 a4 = A[0], b4 = B[0];
+          const float sy = a4.x + b4.x;
+          float mc = fmaxf(a4.y + b4.y, fmaxf(a4.z + b4.z, a4.w + b4.w));
+          for (int q = 1; q < nq; ++q) {
+            a4 = A[q];
+            b4 = B[q];
+            mc = fmaxf(mc, fmaxf(fmaxf(a4.x + b4.x, a4.y + b4.y), fmaxf(a4.z + b4.z, a4.w + b4.w)));
+          }
+          bool beat, near;
+          if (sy >= 1e-30f) {  // positive sums: relative error << band
+            beat = mc > sy * (1.f + p.band);
+            near = mc >= sy * (1.f - p.band);
+          } else {  // y's sum is (nearly) subnormal: only a clearly larger competitor is decisive
+            beat = mc > 2e-30f;
+            near = !beat;
+          }
+          if (!beat) {
+            if (near) pend[atomicAdd(&sh.npend, 1)] = (uint16_t)v;
+            else ok = 1;
+          }
+        }
+        ca[k] += ok;
+      }
+      __syncthreads();
+      // ---- S7 (rare): fp64 recheck of the pending subsets from the rows in shared memory --------
+      const int np = sh.npend;
+      if (np) {
+        for (int m = warp; m < K; m += CW) {
+          const double m64 = (double)st.mx[m];
+          double s = 0.0;
+          for (int c = lane; c < C; c += 32) s += exp((double)rows[(size_t)m * p.ldc + c] - m64);
+          for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+          if (lane == 0) sh.lse64[m] = m64 + log(s);
+        }
+        __syncthreads();
+        for (int i = warp; i < np; i += CW) {
+          const uint32_t v = pend[i];
+          double best = -1.0;
+          int bestc = 0x7fffffff;
+          for (int j = lane; j < nj4; j += 32) {
+            const int c = sh.cols[j];
+            if (c < 0) continue;
+            double acc = 0.0;
+            for (uint32_t mm = v; mm; mm &= mm - 1) {
+              const int m = __ffs(mm) - 1;
+              acc += exp((double)rows[(size_t)m * p.ldc + c] - sh.lse64[m]);
+            }
+            const double a64 = acc / (double)__popc(v);
+            if (a64 > best || (a64 == best && c < bestc)) { best = a64; bestc = c; }
+          }
+          for (int off = 16; off; off >>= 1) {
+            const double ob = __shfl_xor_sync(FULL, best, off);
+            const int oc = __shfl_xor_sync(FULL, bestc, off);
+            if (ob > best || (ob == best && oc < bestc)) { best = ob; bestc = oc; }
+          }
+          if (lane == 0) {
+            atomicAdd(p.n_recheck + (v - 1), 1ull);
+            if (bestc == y) atomicAdd(p.cnt_avg + (v - 1), 1ull);
+          }
+        }
+      }
+    }
+    __syncthreads();  // rows, tables and the pending list are free again
+    if (t == 0) {
+      sh.npend = 0;
+      if (L.nbuf == 1 && e + gridDim.x < W) issue(e + gridDim.x, 0);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NSUB; ++k) {
+    const int v1 = t + CT * k - 1;
+    if (v1 >= 0 && v1 < S && ca[k]) atomicAdd(p.cnt_avg + v1, (unsigned long long)ca[k]);
+  }
+}
+
+template <int NSUB>
+cudaError_t launch_nsub(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
+                        const unsigned int* work_count, int32_t* ovf_work, unsigned int* ovf_count) {
+  const Lay L = layout(q);
+  cudaError_t e = cudaFuncSetAttribute(vote_cta_average_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)L.total);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vote_cta_average_kernel<NSUB>, CT, L.total);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  vote_cta_average_kernel<NSUB><<<sm_count * per_sm, CT, L.total, st>>>(q, work, work_count, ovf_work, ovf_count);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t vote_cta_avg_smem(const VoteParams& q) { return layout(q).total; }
+
+cudaError_t launch_vote_cta_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
+                                const unsigned int* work_count, int32_t* ovf_work, unsigned int* ovf_count) {
+  const int nsub = (q.S + 1 + CT - 1) / CT;  // subsets 1..S over thread slots t + 256k
+  if (nsub <= 1) return launch_nsub<1>(q, sm_count, st, work, work_count, ovf_work, ovf_count);
+  if (nsub <= 2) return launch_nsub<2>(q, sm_count, st, work, work_count, ovf_work, ovf_count);
+  if (nsub <= 4) return launch_nsub<4>(q, sm_count, st, work, work_count, ovf_work, ovf_count);
+  if (nsub <= 8) return launch_nsub<8>(q, sm_count, st, work, work_count, ovf_work, ovf_count);
+  return launch_nsub<16>(q, sm_count, st, work, work_count, ovf_work, ovf_count);
+}
+
+}  // namespace rk

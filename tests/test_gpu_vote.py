@@ -75,9 +75,11 @@ def test_integer_logits_ties(rk):
         assert o.n_amb.sum() > 0  # the case is exercised
 
 
-def test_overflow_candidates_all_equal_rows(rk):
-    """Rows with equal logits make every class a candidate (smem overflow path)."""
-    K, C, N = 4, 300, 64
+@pytest.mark.parametrize("K", [4, 10])
+def test_overflow_candidates_all_equal_rows(rk, K):
+    """Rows with equal logits make every class a candidate (smem overflow paths; K = 10: more than 32
+    competitors, the CTA kernel hands the sample to the batch kernel)."""
+    C, N = 300, 64
     rng = np.random.default_rng(3)
     L = gen.logits(3, 0, N, K, C)
     L[::2, 1:, :C] = 0.0  # half the samples: models 1.. flat
