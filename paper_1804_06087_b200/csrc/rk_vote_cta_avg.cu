@@ -106,6 +106,63 @@ __device__ __forceinline__ void load_stat(const VoteParams& p, const int32_t* wo
   if (lane == 0) { st.n = n; st.y = p.labels[n]; }
 }
 
+// S6 for the subsets v = t + 256k of this thread. Because 2^K1 divides 256, the low half a = v mod 2^K1
+// is the same for all k: its table row stays in registers (NQ float4 column groups; NQ = 0: runtime
+// count, row re-read). The high half b = v >> K1 is uniform across a warp (K1 <= 5) or shared by
+// groups of lanes, so its row is a broadcast read.
+template <int NSUB, int NQ>
+__device__ __forceinline__ void decide_subsets(const VoteParams& p, const float* TA, const float* TB, const Stat& st,
+                                               int y, uint32_t (&ca)[NSUB], int& npend, uint16_t* pend,
+                                               int nq_rt = 0) {
+  const int t = threadIdx.x;
+  const int K1 = p.K1, TAn = 1 << K1, S = p.S;
+  const uint32_t a = (uint32_t)t & (uint32_t)(TAn - 1);
+  const float4* A = reinterpret_cast<const float4*>(TA + a * JS);
+  float4 ar[NQ > 0 ? NQ : 1];
+#pragma unroll
+  for (int q = 0; q < (NQ > 0 ? NQ : 1); ++q) ar[q] = A[q];
+#pragma unroll
+  for (int k = 0; k < NSUB; ++k) {
+    const uint32_t v = (uint32_t)(t + CT * k);
+    if (v == 0 || v > (uint32_t)S) continue;
+    uint32_t ok = 0;
+    if (__popc(v) == 1) {
+      ok = st.top[__ffs(v) - 1] == y;  // softmax is monotone (invariant I1)
+    } else {
+      const float4* B = reinterpret_cast<const float4*>(TB + (v >> K1) * JS);
+      float4 b4 = B[0];
+      const float sy = ar[0].x + b4.x;
+      float mc = fmaxf(ar[0].y + b4.y, fmaxf(ar[0].z + b4.z, ar[0].w + b4.w));
+      if (NQ > 0) {
+#pragma unroll
+        for (int q = 1; q < NQ; ++q) {
+          b4 = B[q];
+          mc = fmaxf(mc, fmaxf(fmaxf(ar[q].x + b4.x, ar[q].y + b4.y), fmaxf(ar[q].z + b4.z, ar[q].w + b4.w)));
+        }
+      } else {
+        for (int q = 1; q < nq_rt; ++q) {
+          const float4 a4 = A[q];
+          b4 = B[q];
+          mc = fmaxf(mc, fmaxf(fmaxf(a4.x + b4.x, a4.y + b4.y), fmaxf(a4.z + b4.z, a4.w + b4.w)));
+        }
+      }
+      bool beat, near;
+      if (sy >= 1e-30f) {  // positive sums: relative error << band
+        beat = mc > sy * (1.f + p.band);
+        near = mc >= sy * (1.f - p.band);
+      } else {  // y's sum is (nearly) subnormal: only a clearly larger competitor is decisive
+        beat = mc > 2e-30f;
+        near = !beat;
+      }
+      if (!beat) {
+        if (near) pend[atomicAdd(&npend, 1)] = (uint16_t)v;
+        else ok = 1;
+      }
+    }
+    ca[k] += ok;
+  }
+}
+
 template <int NSUB>
 __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParams p, const int32_t* work,
                                                                  const unsigned int* work_count, int32_t* ovf_work,
@@ -231,38 +288,16 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       }
       __syncthreads();
       // ---- S6: every subset: sum of y's column and the largest competitor, branch-free ----------
-#pragma unroll
-      for (int k = 0; k < NSUB; ++k) {
-        const uint32_t v = (uint32_t)(t + CT * k);
-        if (v == 0 || v > (uint32_t)S) continue;
-        uint32_t ok = 0;
-        if (__popc(v) == 1) {
-          ok = st.top[__ffs(v) - 1] == y;  // softmax is monotone (invariant I1)
-        } else {
-          const float4* A = reinterpret_cast<const float4*>(TA + (size_t)(v & (TAn - 1)) * JS);
-          const float4* B = reinterpret_cast<const float4*>(TB + (size_t)(v >> K1) * JS);
-          float4 a4 = A[0], b4 = B[0];
-          const float sy = a4.x + b4.x;
-          float mc = fmaxf(a4.y + b4.y, fmaxf(a4.z + b4.z, a4.w + b4.w));
-          for (int q = 1; q < nq; ++q) {
-            a4 = A[q];
-            b4 = B[q];
-            mc = fmaxf(mc, fmaxf(fmaxf(a4.x + b4.x, a4.y + b4.y), fmaxf(a4.z + b4.z, a4.w + b4.w)));
-          }
-          bool beat, near;
-          if (sy >= 1e-30f) {  // positive sums: relative error << band
-            beat = mc > sy * (1.f + p.band);
-            near = mc >= sy * (1.f - p.band);
-          } else {  // y's sum is (nearly) subnormal: only a clearly larger competitor is decisive
-            beat = mc > 2e-30f;
-            near = !beat;
-          }
-          if (!beat) {
-            if (near) pend[atomicAdd(&sh.npend, 1)] = (uint16_t)v;
-            else ok = 1;
-          }
+      if (nq <= 5) {
+        switch (nq) {
+          case 1: decide_subsets<NSUB, 1>(p, TA, TB, st, y, ca, sh.npend, pend); break;
+          case 2: decide_subsets<NSUB, 2>(p, TA, TB, st, y, ca, sh.npend, pend); break;
+          case 3: decide_subsets<NSUB, 3>(p, TA, TB, st, y, ca, sh.npend, pend); break;
+          case 4: decide_subsets<NSUB, 4>(p, TA, TB, st, y, ca, sh.npend, pend); break;
+          default: decide_subsets<NSUB, 5>(p, TA, TB, st, y, ca, sh.npend, pend); break;
         }
-        ca[k] += ok;
+      } else {
+        decide_subsets<NSUB, 0>(p, TA, TB, st, y, ca, sh.npend, pend, nq);
       }
       __syncthreads();
       // ---- S7 (rare): fp64 recheck of the pending subsets from the rows in shared memory --------
