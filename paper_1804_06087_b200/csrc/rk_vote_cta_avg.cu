@@ -82,7 +82,7 @@ struct Stat {  // per-sample statistics, loaded one sample ahead (double-buffere
 };
 struct Shared {  // static shared state
   uint64_t bar[2];
-  uint32_t bm[32], bmB[32];
+  uint32_t bm[32];
   int32_t cols[JS];  // 0 = y, 1..nr = R ascending, -1 = unused
   Stat st[2];
   double lse64[KM];
@@ -186,7 +186,6 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
     mbar_init(&sh.bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (t < 32) { sh.bm[t] = 0u; sh.bmB[t] = 0u; }
   if (t == 0) sh.npend = 0;
   __syncthreads();
   auto issue = [&](int64_t e, int buf) {
@@ -213,29 +212,27 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
     mbar_wait(&sh.bar[buf], par);  // the sample's rows have landed
     __syncthreads();                // (and warp 0's statistics of this sample, loaded last iteration)
     const int y = st.y;
-    // ---- S2: candidate bitmaps: bm = S_c, bmB = {c : exists m, l[m][c] >= l[m][y]} ---------------
+    // ---- S2: R ∪ {y} as a bitmap: warp w owns 32-class words, ORs ballots over the K rows of
+    //      S_c (l >= θ-threshold) and of {c : l[m][c] >= l[m][y]}, then stores their AND -------------
     {
       const int nw = (C + 31) >> 5;
-      for (int m = warp; m < K; m += CW) {
-        const float* row = rows + (size_t)m * p.ldc;
-        const float tm = st.thr[m], ym = row[y];
-        for (int w = 0; w < nw; ++w) {
-          const int c = w * 32 + lane;
+      for (int w = warp; w < nw; w += CW) {
+        const int c = w * 32 + lane;
+        uint32_t b1 = 0, b2 = 0;
+        for (int m = 0; m < K; ++m) {
+          const float* row = rows + m * (int)p.ldc;
           const float x = c < C ? row[c] : -INFINITY;
-          const uint32_t b1 = __ballot_sync(FULL, x >= tm);
-          const uint32_t b2 = __ballot_sync(FULL, x >= ym);
-          if (lane == 0) {
-            if (b1) atomicOr(&sh.bm[w], b1);
-            if (b2) atomicOr(&sh.bmB[w], b2);
-          }
+          b1 |= __ballot_sync(FULL, x >= st.thr[m]);
+          b2 |= __ballot_sync(FULL, x >= row[y]);
         }
+        if (lane == 0) sh.bm[w] = b1 & b2;
       }
     }
     __syncthreads();
     // ---- S3: columns (warp 0): 0 = y, 1..nr = R ascending; unused slots up to a float4 boundary hold
     //      -1 (zero probability). Samples whose columns do not fit go to the overflow worklist.
     if (warp == 0) {
-      uint32_t word = sh.bm[lane] & sh.bmB[lane];
+      uint32_t word = lane < ((C + 31) >> 5) ? sh.bm[lane] : 0u;
       if (lane == (y >> 5)) word &= ~(1u << (y & 31));
       const int cnt = __popc(word);
       int incl = cnt;
@@ -260,7 +257,6 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       }
     }
     __syncthreads();
-    if (t < 32) { sh.bm[t] = 0u; sh.bmB[t] = 0u; }  // ready for the next sample (read only above)
     if (warp == CW - 1 && e + gridDim.x < W) load_stat(p, work, e + gridDim.x, sh.st[sb ^ 1], lane);
     if (!sh.skip) {
       const int nq = sh.nq, nj4 = 4 * nq;
@@ -271,19 +267,23 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
         Pm[m * JS + j] = c >= 0 ? expf(rows[(size_t)m * p.ldc + c] - st.ls[m]) : 0.f;
       }
       __syncthreads();
-      // ---- S5: half-mask tables TA[h][j] = sum_{m in h} p[m][j] (ascending m), TB rows after TA ----
+      // ---- S5: half-mask tables TA[h][j] = sum_{m in h} p[m][j] (ascending m), TB rows after TA:
+      //      thread t owns row h = t mod 128 and every other column ---------------------------------
       {
-        const int KB = K - K1, TT = TAn + (1 << KB);
-        for (int i = t; i < TT * nj4; i += CT) {
-          const int h = i / nj4, j = i - h * nj4;
+        const int TT = TAn + (1 << (K - K1));
+        const int h = t & 127;
+        if (h < TT) {
           const bool lo = h < TAn;
           const uint32_t hm = lo ? (uint32_t)h : (uint32_t)(h - TAn);
-          const float* pc = Pm + (lo ? 0 : K1) * JS + j;
-          float s = 0.f;
+          const int mo = lo ? 0 : K1;
+          const float* pc = Pm + mo * JS;
+          for (int j = t >> 7; j < nj4; j += CT / 128) {
+            float s = 0.f;
 #pragma unroll
-          for (int b = 0; b < 6; ++b)
-            if ((hm >> b) & 1u) s += pc[b * JS];
-          TA[(size_t)h * JS + j] = s;
+            for (int b = 0; b < 6; ++b)
+              if ((hm >> b) & 1u) s += pc[b * JS + j];
+            TA[h * JS + j] = s;
+          }
         }
       }
       __syncthreads();
