@@ -163,9 +163,14 @@ __global__ void __launch_bounds__(WT, 4) vote_average_kernel(const VoteParams p,
     ws.bitmapB[lane] = 0u;
     __syncwarp();
     // ---- 1. candidate set R: one streaming pass over the sample's K rows ----------------------
+    const int64_t nnext = e + nw < W ? (int64_t)work[e + nw] : -1;
 #pragma unroll 1
     for (int m = 0; m < K; ++m) {
       const float* row = rowbase + (size_t)m * p.ldc;
+      {  // one-row-ahead L2 prefetch (the next row, or the next sample's first row): 128 B per lane
+        const float* nrow = m + 1 < K ? row + p.ldc : (nnext >= 0 ? p.logits + nnext * K * p.ldc : nullptr);
+        if (nrow && lane * 32 < p.ldc) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + lane * 32));
+      }
       float4 v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
