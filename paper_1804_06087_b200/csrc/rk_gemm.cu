@@ -359,14 +359,20 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (width - c0 >= 32) tmem_ld32(tbase + c0, v);
           else tmem_ld16(tbase + c0, v);
           const int colbase = j * BN + c0;  // column inside the model
-          const float* bptr = a.bias + (size_t)model * a.Cp + colbase;
+          const float4* bptr = reinterpret_cast<const float4*>(a.bias + (size_t)model * a.Cp + colbase);
           float cmax = -INFINITY;
           int carg = 0;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float b = (colbase + i < a.Cp) ? __ldg(bptr + i) : -INFINITY;
-            v[i] = fmaf(v[i], scale, b);  // scale is a power of two: exact product, one rounding
-            if (v[i] > cmax) { cmax = v[i]; carg = colbase + i; }
+          for (int i4 = 0; i4 < 8; ++i4) {  // bias: -inf on padding columns; groups of 4 never straddle Cp
+            const float4 b4 = colbase + 4 * i4 < a.Cp ? __ldg(bptr + i4)
+                                                      : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * i4 + e;
+              v[i] = fmaf(v[i], scale, bb[e]);  // scale is a power of two: exact product, one rounding
+              if (v[i] > cmax) { cmax = v[i]; carg = colbase + i; }
+            }
           }
           if (cmax > mx) {
             sum = sum * __expf(mx - cmax);
