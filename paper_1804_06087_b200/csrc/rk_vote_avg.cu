@@ -127,7 +127,7 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(WT, 4) vote_average_kernel(const VoteParams p, const int32_t* work,
+__global__ void __launch_bounds__(WT, 5) vote_average_kernel(const VoteParams p, const int32_t* work,
                                                               const unsigned int* work_count) {
   extern __shared__ __align__(16) char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

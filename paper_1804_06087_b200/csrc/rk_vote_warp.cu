@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
 
 size_t vote_warp_smem_per_warp(const VoteParams& p) { return vote_avg_smem_per_warp(p); }
 int vote_warp_threads() { return WT; }
-int vote_warp_min_blocks() { return 4; }
+int vote_warp_min_blocks() { return 5; }
 
 cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
                              int32_t* st_top, float* st_lse, float* st_max, int sm_count) {
