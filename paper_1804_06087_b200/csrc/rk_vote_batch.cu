@@ -9,9 +9,10 @@
 //   phase 1  warps build a compact record per sample of a batch (row statistics, distinct-class
 //            vote masks, flags; for the averaging kernel: the candidate set R, gathered
 //            probabilities, half-tables and the competitor bound) in shared memory;
-//   phase 2  every thread owns the fixed subsets v = t + 1 + 256k and sweeps the batch: all threads
-//            read the same record at the same time (smem broadcast, uniform control flow), counters
-//            live in registers, per-group counts are written once per group.
+//   phase 2  bit-sliced: a thread owns a word of 32 subsets (low 5 models <-> bit position) and
+//            sweeps its share of the batch's records; vote counts per class come from a constant
+//            "popcount >= c" table, comparisons and the tie race work on whole words, per-subset
+//            counts accumulate in vertical bit counters folded into shared memory per group.
 // Exactness arguments are those of rk_vote_warp.cu (unanimity I6, theta pruning, the y-dominance
 // filter, the competitor bound, fp64 recheck of near-ties).
 #include <cuda_runtime.h>
@@ -58,6 +59,15 @@ __device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int 
   return (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
 }
 
+// ragged-tail counts for the correct subsets of one word (samples past the last complete batch; rare)
+__device__ __noinline__ void tail_add_word(const VoteParams& p, uint32_t tm, uint32_t w, uint32_t ok) {
+  for (uint32_t o = ok; o; o &= o - 1) {
+    const uint32_t v = (w << 5) | (uint32_t)(__ffs(o) - 1);
+    for (int bi = 0; bi < p.nB; ++bi)
+      if ((tm >> bi) & 1u) atomicAdd(p.tail + (size_t)bi * p.S + (v - 1), 1ull);
+  }
+}
+
 __device__ __noinline__ void tail_add_b(const VoteParams& p, uint32_t tm, uint32_t v) {
   for (int bi = 0; bi < p.nB; ++bi)
     if ((tm >> bi) & 1u) atomicAdd(p.tail + (size_t)bi * p.S + (v - 1), 1ull);
@@ -97,7 +107,9 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
                                                                     float* st_lse, float* st_max) {
   __shared__ Rec rec[SB];
   __shared__ uint32_t uni[SB];
-  __shared__ uint8_t best_of[1 << KM];
+  __shared__ uint32_t GE[32 * 8];        // GE[L][c] = {lo in [0,32) : popc(lo & L) >= c}
+  __shared__ uint32_t gcnt[1 << KM];     // correct votes of the current group per subset v
+  __shared__ int8_t rorder[KM];          // models by rank (best first), BEST_MEMBER tie rule
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int K = p.K, S = p.S, C = p.C;
   const uint32_t kmask = (1u << K) - 1u;
@@ -106,12 +118,25 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
   const int64_t nbatch = (N + SB - 1) / SB;
   int64_t tail0 = N;
   for (int bi = 0; bi < p.nB; ++bi) tail0 = p.tail_start[bi] < tail0 ? p.tail_start[bi] : tail0;
-  if (p.tie == 0)
-    for (int i = t; i < (1 << K); i += BT) best_of[i] = p.best_of[i];
+  for (int i = t; i < 32 * 8; i += BT) {
+    const uint32_t L = (uint32_t)(i >> 3), c = (uint32_t)(i & 7);
+    uint32_t wd = 0;
+    for (uint32_t lo = 0; lo < 32; ++lo) wd |= ((uint32_t)__popc(lo & L) >= c ? 1u : 0u) << lo;
+    GE[i] = wd;
+  }
+  for (int i = t; i < (1 << K); i += BT) gcnt[i] = 0;
+  if (t == 0 && p.tie == 0) {
+    uint32_t rem = kmask;
+    for (int r = 0; r < K; ++r) {
+      const int m = p.best_of[rem];
+      rorder[r] = (int8_t)m;
+      rem &= ~(1u << m);
+    }
+  }
 
-  uint32_t cv[NK], ca[NK], gv[NK];
+  uint32_t cv[NK], ca[NK];
 #pragma unroll
-  for (int k = 0; k < NK; ++k) { cv[k] = 0; ca[k] = 0; gv[k] = 0; }
+  for (int k = 0; k < NK; ++k) { cv[k] = 0; ca[k] = 0; }
 
   for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
     const int64_t b0 = batch * SB;
@@ -197,64 +222,98 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
         work[base + __popc(wl & ((1u << lane) - 1u))] = (int32_t)(b0 + warp + NWB * lane);
     }
     __syncthreads();
-    // ---- phase 2: thread t owns subsets v = t + 1 + 256k and sweeps the batch ----------------
+    // ---- phase 2 (bit-sliced): thread t owns the 32-subset word w = t mod 2^(K-5) -- subsets
+    //      v = 32w + lo, the low 5 models <-> bits of lo, the high models <-> bits of w -- for the
+    //      samples b = t / 2^(K-5) (mod lanes) of each group. Per class, the member count over v is
+    //      popc(lo & L) + popc(w & H): the lo-part comes from the constant table GE, so a whole word
+    //      of comparisons costs a few logic ops. Per-subset counts accumulate in a vertical counter
+    //      and are folded into the shared per-subset group counts at each group end.
+    const int nwd = 1 << (K - 5), nsl = BT / nwd;
+    const uint32_t w = (uint32_t)t & (uint32_t)(nwd - 1);
+    const int sl = t / nwd;
+    const uint32_t validw = w == 0 ? ~1u : ~0u;  // v = 0 is not a subset
     const int ngroups = SB / gsz;
 #pragma unroll 1
     for (int g = 0; g < ngroups; ++g) {
+      uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;  // vertical counter (<= 16 samples per thread)
 #pragma unroll 1
-      for (int b = g * gsz; b < (g + 1) * gsz; ++b) {
-        if (!(rec[b].flags & R_EVAL)) continue;  // uniform across the CTA
-        // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|,
-        // y wins iff c_y > 0, no class has more votes, and the tie (if any) goes to y:
-        // LOWEST_CLASS -> no tied class below y; BEST_MEMBER -> the best-ranked member among all
-        // tied voters votes y (reading Q2).
-        const uint32_t my = rec[b].my, lt = rec[b].lt, tm = rec[b].tm;
+      for (int b = g * gsz + sl; b < (g + 1) * gsz; b += nsl) {
+        if (!(rec[b].flags & R_EVAL)) continue;
+        // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|, y wins iff
+        // c_y > 0, no class has more votes, and the tie (if any) goes to y: LOWEST_CLASS -> no tied
+        // class below y; BEST_MEMBER -> the best-ranked member among all tied voters votes y (Q2).
+        const uint32_t my = rec[b].my, lt = rec[b].lt, Ly = my & 31u;
+        const int hy = __popc(w & (my >> 5));
+        const int ny = __popc(Ly);
+        const uint32_t* GY = GE + Ly * 8;
+        uint32_t lose = hy == 0 ? ~GY[1] : 0u;  // c_y == 0
         const int no = rec[b].no;
-        uint32_t cy[NK], tied[NK], lose = 0;
-#pragma unroll
-        for (int k = 0; k < NK; ++k) {
-          const uint32_t v = (uint32_t)(t + 1 + BT * k);
-          tied[k] = v & my;
-          cy[k] = __popc(tied[k]);
-          lose |= (cy[k] == 0u) ? (1u << k) : 0u;
-        }
 #pragma unroll 1
         for (int j = 0; j < no; ++j) {
-          const uint32_t mj = rec[b].mo[j];
-          const bool ltj = (lt >> j) & 1u;
-#pragma unroll
-          for (int k = 0; k < NK; ++k) {
-            const uint32_t v = (uint32_t)(t + 1 + BT * k);
-            const uint32_t vm = v & mj;
-            const uint32_t cj = __popc(vm);
-            lose |= (cj > cy[k] || (p.tie != 0 && cj == cy[k] && ltj)) ? (1u << k) : 0u;
-            tied[k] |= (cj == cy[k]) ? vm : 0u;
+          const uint32_t Mj = rec[b].mo[j];
+          const uint32_t* GJ = GE + (Mj & 31u) * 8;
+          const int d = hy - __popc(w & (Mj >> 5));  // c_j > c_y  <=>  x_j >= x_y + d + 1
+          uint32_t gt = 0, eq = 0;
+#pragma unroll 1
+          for (int a = 0; a <= ny; ++a) {
+            const uint32_t ya = GY[a] & ~GY[a + 1];  // x_y == a
+            const int k = a + d + 1;
+            const uint32_t gk = k <= 0 ? ~0u : (k >= 8 ? 0u : GJ[k]);
+            const uint32_t ek = (k - 1 < 0 || k - 1 >= 8) ? 0u : (GJ[k - 1] & ~gk);
+            gt |= ya & gk;
+            eq |= ya & ek;
+          }
+          lose |= gt;
+          if (p.tie != 0) {
+            if ((lt >> j) & 1u) lose |= eq;
+          } else if (eq & ~lose) {  // tie race: is the best-ranked member of v ∩ (M_y ∪ M_j) a y voter?
+            uint32_t decided = 0, ywin = 0;
+#pragma unroll 1
+            for (int r = 0; r < K && decided != ~0u; ++r) {
+              const int m = rorder[r];
+              const uint32_t bit = 1u << m;
+              if (!((my | Mj) & bit)) continue;
+              const uint32_t mw = m < 5 ? GE[(1u << m) * 8 + 1] : (((w >> (m - 5)) & 1u) ? ~0u : 0u);
+              if (my & bit) ywin |= mw & ~decided;
+              decided |= mw;
+            }
+            lose |= eq & ~ywin;
           }
         }
-#pragma unroll
-        for (int k = 0; k < NK; ++k) {
-          const uint32_t v = (uint32_t)(t + 1 + BT * k);
-          if (v > (uint32_t)S) break;
-          uint32_t ok = !((lose >> k) & 1u);
-          if (p.tie == 0 && ok) ok = (my >> best_of[tied[k]]) & 1u;
-          gv[k] += ok;
-          if (ok && tm) tail_add_b(p, tm, v);
+        const uint32_t ok = ~lose & validw;
+        uint32_t c = ok, x;  // vertical counter += ok
+        x = k0 & c; k0 ^= c; c = x;
+        x = k1 & c; k1 ^= c; c = x;
+        x = k2 & c; k2 ^= c; c = x;
+        x = k3 & c; k3 ^= c; c = x;
+        k4 ^= c;
+        if (ok && rec[b].tm) tail_add_word(p, rec[b].tm, w, ok);
+      }
+      if (k0 | k1 | k2 | k3 | k4) {
+        for (uint32_t lo = 0; lo < 32; ++lo) {
+          const uint32_t cnt = ((k0 >> lo) & 1u) | (((k1 >> lo) & 1u) << 1) | (((k2 >> lo) & 1u) << 2) |
+                               (((k3 >> lo) & 1u) << 3) | (((k4 >> lo) & 1u) << 4);
+          if (cnt) atomicAdd(&gcnt[(w << 5) | lo], cnt);
         }
       }
+      __syncthreads();
       // group end: labelled-moment group counts and totals
       const int64_t gi = (b0 + (int64_t)g * gsz) / gsz;
-      const uint32_t u = uni[g * gsz / gsz];
+      const uint32_t u = uni[g];
 #pragma unroll
       for (int k = 0; k < NK; ++k) {
         const int v1 = t + BT * k;
-        if (v1 < S && b0 + (int64_t)g * gsz < N) {
-          const uint32_t tot = gv[k] + u;
-          if (p.grp) p.grp[gi * S + v1] = (uint8_t)tot;
-          cv[k] += tot;
-          ca[k] += u;
+        if (v1 < S) {
+          if (b0 + (int64_t)g * gsz < N) {
+            const uint32_t tot = gcnt[v1 + 1] + u;
+            if (p.grp) p.grp[gi * S + v1] = (uint8_t)tot;
+            cv[k] += tot;
+            ca[k] += u;
+          }
+          gcnt[v1 + 1] = 0;
         }
-        gv[k] = 0;
       }
+      __syncthreads();
     }
   }
 #pragma unroll

@@ -43,6 +43,9 @@ CASES = [  # (K, C, N, seed)
     (6, 1000, 300, 3),    # c3 shape
     (8, 1000, 150, 4),    # c4 shape
     (12, 100, 70, 5),     # c5 shape (4095 subsets)
+    (9, 50, 300, 8),      # K = 9..11: every word count of the bit-sliced vote (16..64 words)
+    (10, 20, 200, 9),
+    (11, 100, 150, 10),
     (1, 2, 33, 6),        # degenerate: one model, two classes
     (5, 37, 517, 7),      # odd sizes, ragged everything
 ]
