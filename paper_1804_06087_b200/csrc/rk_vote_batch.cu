@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
   __shared__ uint32_t uni[SB];
   __shared__ uint32_t GE[32 * 8];        // GE[L][c] = {lo in [0,32) : popc(lo & L) >= c}
   __shared__ uint32_t gcnt[1 << KM];     // correct votes of the current group per subset v
-  __shared__ int8_t rorder[KM];          // models by rank (best first), BEST_MEMBER tie rule
+  __shared__ uint32_t LW[32 * 32];       // LW[A][B] = {lo : best-ranked member of lo ∩ (A ∪ B) is in A}
+  __shared__ uint8_t LR[KM + 1];         // LR[r] = low models (m < 5) ranked better than r
+  __shared__ int8_t rnk[KM];             // rank of each model (0 = best), BEST_MEMBER tie rule
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int K = p.K, S = p.S, C = p.C;
   const uint32_t kmask = (1u << K) - 1u;
@@ -125,15 +127,34 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
     GE[i] = wd;
   }
   for (int i = t; i < (1 << K); i += BT) gcnt[i] = 0;
-  if (t == 0 && p.tie == 0) {
-    uint32_t rem = kmask;
-    for (int r = 0; r < K; ++r) {
-      const int m = p.best_of[rem];
-      rorder[r] = (int8_t)m;
-      rem &= ~(1u << m);
+  if (p.tie == 0) {
+    if (t == 0) {
+      uint32_t rem = kmask;
+      for (int r = 0; r < K; ++r) {
+        const int m = p.best_of[rem];
+        rnk[m] = (int8_t)r;
+        rem &= ~(1u << m);
+      }
+    }
+    __syncthreads();
+    if (t <= K) {
+      uint32_t lr = 0;
+      for (int m = 0; m < 5; ++m) lr |= (rnk[m] < t ? 1u : 0u) << m;
+      LR[t] = (uint8_t)lr;
+    }
+    for (int i = t; i < 32 * 32; i += BT) {
+      const uint32_t A = (uint32_t)i >> 5, B = (uint32_t)i & 31u;
+      uint32_t wd = 0;
+      for (uint32_t lo = 1; lo < 32; ++lo) {
+        const uint32_t s2 = lo & (A | B);
+        int best = -1, br = 1 << 30;
+        for (int m = 0; m < 5; ++m)
+          if (((s2 >> m) & 1u) && rnk[m] < br) { br = rnk[m]; best = m; }
+        if (best >= 0 && ((A >> best) & 1u)) wd |= 1u << lo;
+      }
+      LW[i] = wd;
     }
   }
-
   uint32_t cv[NK], ca[NK];
 #pragma unroll
   for (int k = 0; k < NK; ++k) { cv[k] = 0; ca[k] = 0; }
@@ -266,17 +287,15 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
           lose |= gt;
           if (p.tie != 0) {
             if ((lt >> j) & 1u) lose |= eq;
-          } else if (eq & ~lose) {  // tie race: is the best-ranked member of v ∩ (M_y ∪ M_j) a y voter?
-            uint32_t decided = 0, ywin = 0;
-#pragma unroll 1
-            for (int r = 0; r < K && decided != ~0u; ++r) {
-              const int m = rorder[r];
-              const uint32_t bit = 1u << m;
-              if (!((my | Mj) & bit)) continue;
-              const uint32_t mw = m < 5 ? GE[(1u << m) * 8 + 1] : (((w >> (m - 5)) & 1u) ? ~0u : 0u);
-              if (my & bit) ywin |= mw & ~decided;
-              decided |= mw;
-            }
+          } else if (eq & ~lose) {
+            // tie race: is the best-ranked member of v ∩ (M_y ∪ M_j) a y voter? The high members are
+            // fixed by w: the best of them (rank rh) wins unless a low member ranked better is in lo.
+            int rh = K, hiy = 0;
+            for (int m = 5; m < K; ++m)
+              if (((w >> (m - 5)) & 1u) && (((my | Mj) >> m) & 1u) && rnk[m] < rh) { rh = rnk[m]; hiy = (my >> m) & 1u; }
+            const uint32_t lr = LR[rh];
+            const uint32_t A = Ly & lr, Bm = Mj & 31u & lr;
+            const uint32_t ywin = LW[(A << 5) | Bm] | (hiy ? ~GE[(A | Bm) * 8 + 1] : 0u);
             lose |= eq & ~ywin;
           }
         }
