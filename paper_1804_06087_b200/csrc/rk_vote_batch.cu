@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
   __shared__ uint32_t LW[32 * 32];       // LW[A][B] = {lo : best-ranked member of lo ∩ (A ∪ B) is in A}
   __shared__ uint8_t LR[KM + 1];         // LR[r] = low models (m < 5) ranked better than r
   __shared__ int8_t rnk[KM];             // rank of each model (0 = best), BEST_MEMBER tie rule
+  __shared__ uint16_t RS[2][64];         // model mask -> rank-order mask, 6 models per half
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int K = p.K, S = p.S, C = p.C;
   const uint32_t kmask = (1u << K) - 1u;
@@ -137,6 +138,13 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
       }
     }
     __syncthreads();
+    if (t < 128) {
+      const int hf = t >> 6, x = t & 63;
+      uint32_t r = 0;
+      for (int b = 0; b < 6; ++b)
+        if (((x >> b) & 1) && 6 * hf + b < K) r |= 1u << rnk[6 * hf + b];
+      RS[hf][x] = (uint16_t)r;
+    }
     if (t <= K) {
       uint32_t lr = 0;
       for (int m = 0; m < 5; ++m) lr |= (rnk[m] < t ? 1u : 0u) << m;
@@ -253,6 +261,10 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
     const uint32_t w = (uint32_t)t & (uint32_t)(nwd - 1);
     const int sl = t / nwd;
     const uint32_t validw = w == 0 ? ~1u : ~0u;  // v = 0 is not a subset
+    uint32_t hwr = 0;  // this word's high models, in rank order
+    if (p.tie == 0)
+      for (int m = 5; m < K; ++m)
+        if ((w >> (m - 5)) & 1u) hwr |= 1u << rnk[m];
     const int ngroups = SB / gsz;
 #pragma unroll 1
     for (int g = 0; g < ngroups; ++g) {
@@ -290,9 +302,10 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
           } else if (eq & ~lose) {
             // tie race: is the best-ranked member of v ∩ (M_y ∪ M_j) a y voter? The high members are
             // fixed by w: the best of them (rank rh) wins unless a low member ranked better is in lo.
-            int rh = K, hiy = 0;
-            for (int m = 5; m < K; ++m)
-              if (((w >> (m - 5)) & 1u) && (((my | Mj) >> m) & 1u) && rnk[m] < rh) { rh = rnk[m]; hiy = (my >> m) & 1u; }
+            const uint32_t myr = RS[0][my & 63u] | RS[1][my >> 6];
+            const uint32_t hr = (myr | RS[0][Mj & 63u] | RS[1][Mj >> 6]) & hwr;
+            const int rh = hr ? __ffs(hr) - 1 : K;
+            const bool hiy = hr && ((myr >> rh) & 1u);
             const uint32_t lr = LR[rh];
             const uint32_t A = Ly & lr, Bm = Mj & 31u & lr;
             const uint32_t ywin = LW[(A << 5) | Bm] | (hiy ? ~GE[(A | Bm) * 8 + 1] : 0u);
