@@ -321,9 +321,20 @@ def main():
         "rank0_check": {"N": int(t["N"]), "a_full_set": float(t["cnt_vote"][-1]) / max(1, int(t["N"])),
                         "a_best_single": float(t["cnt_vote"][0]) / max(1, int(t["N"]))},
     }
-    if vote_ms > gemm_ms:  # the vote stage dominates (K >= 9): it is the roofline kernel
-        line["roofline"], line["gemm_stage"] = line["vote_stage"], line["roofline"]
-        del line["vote_stage"]
+    if vote_ms > gemm_ms:  # the vote stage dominates (K >= 9): an ALU-bound roofline kernel
+        # algorithmic ops: one per (sample, subset, member) for the vote count and one for the
+        # probability sum = 2 * sum_v |v| = K * 2^K per sample; peak: 148 SMs x 128 int32/fp32 lanes
+        # x the SM clock (B200_PROFILING.md unit counts)
+        sm_mhz = clk.get("sm_max_mhz") or 1965.0
+        ops = Ntot * K * (1 << K) / world
+        alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9
+        alu = ops / (vote_ms / 1e3) / 1e9
+        line["gemm_stage"] = line["roofline"]
+        line["roofline"] = {"bound": "alu", "kernel": "vote_subsets", "achieved": alu, "peak": alu_peak,
+                            "unit": "Gop/s", "frac": alu / alu_peak, "traffic": vtraffic,
+                            "share_of_step": vote_ms / ms_step,
+                            "peak_source": f"148 SMs x 128 lanes x {sm_mhz:.0f} MHz (B200 unit counts)",
+                            "algorithmic": "K*2^K ops per sample (vote count + probability sum per subset member)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfgname, cfg)
     if rank == 0:
