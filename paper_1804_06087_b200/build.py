@@ -41,6 +41,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
               "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", inc]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += os.environ.get("RK_NVCC_FLAGS", "").split()  # development experiments only
     objs, procs = [], []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
