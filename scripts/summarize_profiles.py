@@ -24,7 +24,7 @@ for r in rows:
     d = per.setdefault(k, [0, 0.0])
     d[0] += 1
     d[1] += float(r[14]) / 1e6
-ours = {"gemm_heads_kernel", "vote_classify_kernel", "vote_average_kernel", "vote_batch", "overdue_kernel",
+ours = {"gemm_heads_kernel", "vote_classify_kernel", "vote_average_kernel", "vote_batch", "vote_cta", "overdue_kernel",
         "merge_kernel", "q_kernel", "fold_kernel"}
 tot_ours = sum(v[1] for k, v in per.items() if any(k.startswith(o) for o in ours))
 lines = [f"# {R} launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of",
@@ -58,7 +58,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "smsp__inst_executed.sum", "launch__grid_size", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
 summary = {}
-for tag in ("gemm", "vote"):
+for tag in ("gemm", "vote", "k12"):
     try:
         recs = raw(f"gpurun_out/{R}_{tag}.ncu-rep")
     except Exception as e:  # noqa: BLE001
@@ -80,10 +80,12 @@ for k, d in summary.items():
         print("   ", kk, vv)
 
 # ---- DRAM traffic per launch for bench.py's roofline.traffic (scaled linearly in N to c4) ----------
-CAPN = {"gemm": 65536, "vote": 200000}  # N of the captures in scripts/profile_round.sh
+CAPN = {"gemm": 65536, "vote": 200000, "k12": 250000}  # N of the captures in scripts/profile_round.sh
 per_sample = {}
 for key, d in summary.items():
     tag, name = key.split(":", 1)
+    if tag == "k12":
+        continue  # c5 shape: reported in the summary, not part of the c4 traffic figure
     rd = float(d.get("dram__bytes_read.sum", "0 byte").split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[
         d.get("dram__bytes_read.sum", "0 byte").split()[1]]
     wr = float(d.get("dram__bytes_write.sum", "0 byte").split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[
