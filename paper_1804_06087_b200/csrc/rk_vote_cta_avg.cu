@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
   };
   if (t == 0 && (int64_t)blockIdx.x < W) issue(blockIdx.x, 0);
   if (warp == 0 && (int64_t)blockIdx.x < W) load_stat(p, work, blockIdx.x, sh.st[0], lane);
+  __syncthreads();  // the first sample's statistics
 
   uint32_t ca[NSUB];
 #pragma unroll
@@ -209,9 +210,8 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
     const float* rows = reinterpret_cast<const float*>(dyn + L.rows + buf * rowbytes);
     const int sb = (int)(it & 1);
     const Stat& st = sh.st[sb];
-    mbar_wait(&sh.bar[buf], par);  // the sample's rows have landed
-    __syncthreads();                // (and warp 0's statistics of this sample, loaded last iteration)
-    const int y = st.y;
+    mbar_wait(&sh.bar[buf], par);  // every thread: the sample's rows have landed (the statistics were
+    const int y = st.y;            // loaded last iteration, before its final barrier)
     // ---- S2: R ∪ {y} as a bitmap: warp w owns 32-class words, ORs ballots over the K rows of
     //      S_c (l >= θ-threshold) and of {c : l[m][c] >= l[m][y]}, then stores their AND -------------
     {
