@@ -41,7 +41,8 @@ def build(force: bool = False) -> str:
 class _Cfg(ctypes.Structure):
     _fields_ = [("nB", ctypes.c_int), ("B", ctypes.c_void_p), ("beta", ctypes.c_double),
                 ("tau_ns", ctypes.c_int64), ("lat_ns", ctypes.c_void_p), ("nR", ctypes.c_int),
-                ("rates", ctypes.c_void_p), ("arrival_ns", ctypes.c_void_p), ("want_exceed", ctypes.c_int)]
+                ("rates", ctypes.c_void_p), ("arrival_ns", ctypes.c_void_p), ("want_exceed", ctypes.c_int),
+                ("queue", ctypes.c_int)]
 
 
 class _Table(ctypes.Structure):
@@ -143,6 +144,7 @@ class RewardCfg:
     rates: list | None = None   # req/s
     arrival_ns: np.ndarray | None = None
     want_exceed: bool = True
+    queue: bool = False         # reading Q15: FIFO ensemble server, batch j waits for batch j-1
 
 
 @dataclass
@@ -196,7 +198,8 @@ def table(logits, labels, K: int, C: int, tie: int = TIE_BEST_MEMBER, rank=None,
             rates = np.ascontiguousarray(cfg.rates, dtype=np.float64)
             nR = rates.size
         keep += [Bv, lat, arr, rates]
-        cc = _Cfg(nB, _p(Bv), cfg.beta, cfg.tau_ns, _p(lat), nR, _p(rates), _p(arr), int(cfg.want_exceed))
+        cc = _Cfg(nB, _p(Bv), cfg.beta, cfg.tau_ns, _p(lat), nR, _p(rates), _p(arr), int(cfg.want_exceed),
+                  int(cfg.queue))
     t = Table(np.zeros(S, np.uint64), np.zeros(S, np.uint64), np.zeros(S, np.uint64))
     if cfg is not None:
         t.corr = np.zeros((nB, S), np.uint64)

@@ -166,6 +166,8 @@ typedef struct {
   const int* rank;
   int tie;
   const or_cfg* cfg;
+  const int64_t* fin;  /* queue mode: finish time of every complete batch [nR][nB][S][nbmax] */
+  int64_t nbmax;
   int status;
   /* thread-local accumulators */
   uint64_t *cnt_vote, *cnt_avg, *n_amb, *corr, *O, *Q, *E;
@@ -229,6 +231,7 @@ static void* table_thr(void* arg) {
       /* batch complete: latency of each request l(s) = wait + c(v,b),
        * wait = t_last - t_s (dispatch when the batch is full), c(v,b) = max over members
        * (straggler); overdue <=> l(s) > tau, strict (reading Q10) */
+      /* queue mode (reading Q15): l(s) = finish_j - t_s, finish_j from the FIFO recurrence */
       const int64_t s0 = jb * b, s1 = s0 + b;
       for (int r = 0; r < nR; ++r) {
         const int64_t tlast = arrival(cfg, r, s1 - 1);
@@ -236,9 +239,11 @@ static void* table_thr(void* arg) {
           int64_t c = 0;
           for (int m = 0; m < K; ++m)
             if (((v >> m) & 1u) && cfg->lat_ns[m * nB + bi] > c) c = cfg->lat_ns[m * nB + bi];
+          const int64_t done = cfg->queue ? j->fin[(((int64_t)r * nB + bi) * S + (v - 1)) * j->nbmax + jb]
+                                          : tlast + c;
           uint64_t o = 0, e = 0;
           for (int64_t s = s0; s < s1; ++s) {
-            int64_t lat = (tlast - arrival(cfg, r, s)) + c;
+            int64_t lat = done - arrival(cfg, r, s);
             if (lat > cfg->tau_ns) { o++; e += (uint64_t)(lat - cfg->tau_ns); }
           }
           const int64_t idx = ((int64_t)r * nB + bi) * S + (v - 1);
@@ -276,6 +281,31 @@ int or_table_build(const float* logits_f32, int ldc, const double* logits_f64, i
   int64_t units = (N + L - 1) / L;
   if (threads > units) threads = (int)(units > 0 ? units : 1);
   int64_t per = (units + threads - 1) / threads;
+  /* queue mode: the FIFO recurrence over the whole stream, in batch order, for every (r, b, v):
+   * start_j = max(t_last(j), finish_{j-1}), finish_j = start_j + c(v,b) (Q15) */
+  int64_t* fin = NULL;
+  int64_t nbmax = 0;
+  if (cfg && cfg->queue && nB > 0 && nR > 0) {
+    for (int bi = 0; bi < nB; ++bi) if (N / cfg->B[bi] > nbmax) nbmax = N / cfg->B[bi];
+    fin = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nT ? nT : 1) * (size_t)(nbmax ? nbmax : 1));
+    if (!fin) return OR_EINVAL;
+    for (int r = 0; r < nR; ++r)
+      for (int bi = 0; bi < nB; ++bi) {
+        const int64_t b = cfg->B[bi];
+        for (uint32_t v = 1; v <= (uint32_t)S; ++v) {
+          int64_t c = 0;
+          for (int m = 0; m < K; ++m)
+            if (((v >> m) & 1u) && cfg->lat_ns[m * nB + bi] > c) c = cfg->lat_ns[m * nB + bi];
+          int64_t prev = INT64_MIN;
+          for (int64_t jb = 0; jb < N / b; ++jb) {
+            const int64_t ready = arrival(cfg, r, (jb + 1) * b - 1);
+            const int64_t start = (prev == INT64_MIN || ready > prev) ? ready : prev;
+            prev = start + c;
+            fin[(((int64_t)r * nB + bi) * S + (v - 1)) * nbmax + jb] = prev;
+          }
+        }
+      }
+  }
   pthread_t th[256];
   table_job* jobs = (table_job*)calloc((size_t)threads, sizeof(table_job));
   int nt = 0;
@@ -286,6 +316,7 @@ int or_table_build(const float* logits_f32, int ldc, const double* logits_f64, i
     table_job* j = &jobs[t];
     j->lf = logits_f32; j->ldc = ldc; j->ld = logits_f64; j->N = N; j->a = a; j->b = b;
     j->K = K; j->C = C; j->labels = labels; j->rank = rank; j->tie = tie; j->cfg = cfg;
+    j->fin = fin; j->nbmax = nbmax;
     j->cnt_vote = (uint64_t*)calloc((size_t)S, 8);
     j->cnt_avg = (uint64_t*)calloc((size_t)S, 8);
     j->n_amb = (uint64_t*)calloc((size_t)S, 8);
@@ -324,6 +355,7 @@ int or_table_build(const float* logits_f32, int ldc, const double* logits_f64, i
     free(j->cnt_vote); free(j->cnt_avg); free(j->n_amb); free(j->corr); free(j->O); free(j->Q); free(j->E);
   }
   free(jobs);
+  free(fin);
   if (status != OR_OK) return status;
   /* A7: eq. `multi_acc_reward` a(M[v]) * (b - beta*|{s in batch : l(s) > tau}|),
    * summed over the n_b complete batches. Surrogate a(v) = validation accuracy of the vote

@@ -36,6 +36,9 @@ typedef struct {
   const double* rates;    /* [nR] req/s; t_s = floor(s*1e9/r) (reading Q9)                */
   const int64_t* arrival_ns; /* [N] or NULL: caller arrivals (then nR must be 1)          */
   int want_exceed;        /* also compute E (eq. `eq:single`)           */
+  int queue;              /* 0: batch j dispatched when full (reading Q8); 1: one ensemble
+                             server, FIFO: start_j = max(t_last(j), finish_{j-1}), "the next
+                             batch has to wait" (reading Q15)                */
 } or_cfg;
 
 /* Output table (host, caller-allocated). S = 2^K-1, index v-1. */

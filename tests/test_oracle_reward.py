@@ -112,3 +112,36 @@ def test_arrival_closed_form():
     assert oracle.arrival_ns(3, 572.0) == int(np.floor(3e9 / 572.0))
     # exact integer-ns comparison avoids 0.1+0.2 > 0.3 style miscounts (reading Q10)
     assert 0.2 + 0.1 > 0.3 and oracle.arrival_ns(3, 10.0) - oracle.arrival_ns(1, 10.0) == 200_000_000
+
+
+def test_R6_queue_aware_worked_example():
+    """Reading Q15: FIFO ensemble server, start_j = max(t_last(j), finish_{j-1})."""
+    g = gold()["R6"]
+    L, y = _single_model(6, 6)
+    for queue, tag in ((False, "noqueue"), (True, "queue")):
+        cfg = oracle.RewardCfg(B=[2], beta=1.0, tau_ns=300, lat_ns=np.array([[250]]), rates=[1e7], queue=queue)
+        t = oracle.table(L, y, 1, 2, cfg=cfg)
+        assert t.O[0, 0, 0] == g[f"O_{tag}"]
+        assert t.E[0, 0, 0] == g[f"E_{tag}"]
+        assert t.Q[0, 0, 0] == g[f"Q_{tag}"]
+
+
+def test_queue_invariants():
+    """Backlog only delays: O, E (queue) >= O, E (no queue) everywhere; with arrivals far apart
+    (no batch ever waits) the two modes agree exactly."""
+    rng = np.random.default_rng(5)
+    K, C, N = 3, 5, 480
+    y = rng.integers(0, C, N).astype(np.int32)
+    L = rng.normal(size=(N, K, C))
+    lat = np.array([[40_000_000, 70_000_000], [25_000_000, 50_000_000], [60_000_000, 90_000_000]], np.int64)
+    for rates, equal in (([400.0, 1000.0], False), ([0.5], True)):
+        t = {}
+        for q in (False, True):
+            cfg = oracle.RewardCfg(B=[16, 48], beta=1.0, tau_ns=200_000_000, lat_ns=lat, rates=rates, queue=q)
+            t[q] = oracle.table(L, y, K, C, cfg=cfg)
+        assert (t[True].O >= t[False].O).all() and (t[True].E >= t[False].E).all()
+        if equal:
+            np.testing.assert_array_equal(t[True].O, t[False].O)
+            np.testing.assert_array_equal(t[True].E, t[False].E)
+        else:
+            assert (t[True].O > t[False].O).any()
