@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="rk", choices=["rk", "reference"])
     ap.add_argument("--tie", default="best_member", choices=["best_member", "lowest_class"])
+    ap.add_argument("--queue", action="store_true", help="queue-aware latency (reading Q15, PAPER.md:410)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -217,7 +218,7 @@ def main():
     gen.dev_features(1, off, n, D, C, psig, False, X.data_ptr(), labels.data_ptr(), stream.cuda_stream)
     lat = lat_profile(K, cfg["B"])
     rcfg = rk.RewardCfg(B=cfg["B"], beta=BETA, tau_ns=TAU_NS, lat_ns=lat, rates=cfg["rates"], want_exceed=True,
-                        want_labelled=True)
+                        want_labelled=True, queue=args.queue)
     torch.cuda.synchronize()
 
     def step():
@@ -300,7 +301,7 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfgname, "K": K, "C": C, "N": Ntot, "D": D, "B": cfg["B"], "rates": cfg["rates"],
-                   "tie": args.tie, "subsets": S, "parallelism": f"samples sharded over {world} GPU(s)",
+                   "tie": args.tie, "queue": bool(args.queue), "subsets": S, "parallelism": f"samples sharded over {world} GPU(s)",
                    "l2": "inputs larger than L2 (X %.1f GB, logits %.1f GB)" % (Ntot * D * 2 / 1e9, Ntot * K * C * 4 / 1e9)},
         "roofline": {"bound": "tensor", "kernel": "gemm_heads_tcgen05", "achieved": gemm_tfs,
                      "peak": peak_t, "unit": "TFLOP/s", "frac": gemm_tfs / peak_t, "traffic": traffic,

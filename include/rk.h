@@ -98,6 +98,13 @@ typedef struct {
                                 if non-NULL, nR must be 1 and rates is ignored                   */
   int want_exceed;         /* also accumulate E = sum max(0, l(s) - tau) (eq. `eq:single`)      */
   int want_labelled;       /* also accumulate Q = sum_j corr_j * o_j (labelled reward variant)  */
+  int queue;               /* 0: batch j is dispatched when full, l(s) = t_last(j) - t_s + c(v,b)
+                              (reading Q8). 1: one ensemble server runs the batches of (v,b) in FIFO
+                              order, "the next batch has to wait" (reading Q15):
+                              finish_j = max(t_last(j), finish_{j-1}) + c(v,b), l(s) = finish_j - t_s.
+                              Chunks must then arrive in global order; a rank whose first chunk
+                              starts after sample 0 derives the backlog from `rates` (arrival_ns
+                              with a non-zero first offset -> RK_EUNSUPPORTED).                     */
 } rk_reward_cfg;
 
 /* Result table (host arrays, caller-allocated; any pointer may be NULL to skip it). */

@@ -90,6 +90,12 @@ struct rk_ctx {
   size_t grp_cap = 0;
   uint16_t* d_ovd = nullptr;  // per-batch overdue counts (labelled moments)
   size_t ovd_cap = 0;
+  int queue = 0;               // reading Q15 (FIFO ensemble server)
+  int64_t* d_fin = nullptr;    // queue mode: finish times of the chunk's batches
+  size_t fin_cap = 0;
+  int64_t* d_qcarry = nullptr; // queue mode: running max of t_last(i) - i c per (b, r, m)
+  bool q_started = false;
+  int64_t q_next_off = 0;
   int32_t* d_labels = nullptr;
   int64_t labels_cap = 0;
   int32_t* d_work = nullptr;  // vote worklist [N] + count
@@ -225,7 +231,7 @@ void rk_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
   void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_max, ctx->ws_x,
-                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
+                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -390,6 +396,9 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
   ctx->gs = 0;
   ctx->arrival_user = nullptr;
   ctx->beta = 0; ctx->tau = 0;
+  ctx->queue = 0;
+  ctx->q_started = false;
+  ctx->q_next_off = 0;
   if (cfg) {
     if (cfg->nB < 0 || cfg->nB > kMaxB || (cfg->nB > 0 && (!cfg->B || !cfg->lat_ns))) return fail(ctx, RK_EINVAL, "nB in [0,8] with B and lat_ns");
     if (cfg->arrival_ns && cfg->nR != 1) return fail(ctx, RK_EINVAL, "arrival_ns requires nR == 1");
@@ -402,6 +411,7 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
     ctx->want_exceed = cfg->want_exceed ? 1 : 0;
     ctx->want_labelled = cfg->want_labelled ? 1 : 0;
     ctx->arrival_user = cfg->arrival_ns;
+    ctx->queue = cfg->queue ? 1 : 0;
     int64_t g = 0;
     for (int i = 0; i < cfg->nB; ++i) {
       if (cfg->B[i] < 1 || cfg->B[i] > 4096) return fail(ctx, RK_EINVAL, "batch sizes in [1,4096]");
@@ -464,6 +474,13 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
     if (ctx->d_slow) cudaFree(ctx->d_slow);
     CK(cudaMalloc(&ctx->d_slow, slow.size()));
     CK(cudaMemcpy(ctx->d_slow, slow.data(), slow.size(), cudaMemcpyHostToDevice));
+  }
+  if (ctx->queue && nB > 0 && nR > 0) {  // backlog carry per (b, r, m): empty server
+    std::vector<int64_t> c0((size_t)nB * nR * K, INT64_MIN / 4);
+    if (ctx->d_qcarry) cudaFree(ctx->d_qcarry);
+    ctx->d_qcarry = nullptr;
+    CK(cudaMalloc(&ctx->d_qcarry, c0.size() * 8));
+    CK(cudaMemcpy(ctx->d_qcarry, c0.data(), c0.size() * 8, cudaMemcpyHostToDevice));
   }
   ctx->reset_done = true;
   ctx->final_seen = false;
@@ -607,6 +624,29 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
         mp.ovd_nrp = ovd_nrp(nR);
       }
       ProfScope ps(ctx, KK_OVERDUE, st, 0, 0);
+      if (ctx->queue) {  // reading Q15: FIFO finish times, carried across chunks in global order
+        int seed = 0;
+        if (!ctx->q_started) {
+          if (ctx->cur_off > 0) {
+            if (ctx->arrival_user)
+              return fail(ctx, RK_EUNSUPPORTED, "queue mode with arrival_ns needs the stream to start at sample 0");
+            seed = 1;
+          }
+          ctx->q_started = true;
+        } else if (ctx->cur_off != ctx->q_next_off) {
+          return fail(ctx, RK_EINVAL, "queue mode: chunks must be contiguous and in global order");
+        }
+        ctx->q_next_off = ctx->cur_off + N;
+        const size_t need = (size_t)fin_elems(nB, ctx->B, nR, K, N, mp.fin_off) * sizeof(int64_t);
+        if (ctx->fin_cap < need) {
+          if (ctx->d_fin) cudaFree(ctx->d_fin);
+          ctx->d_fin = nullptr;
+          CK(cudaMalloc(&ctx->d_fin, need ? need : 8));
+          ctx->fin_cap = need;
+        }
+        mp.fin = ctx->d_fin;
+        CK(launch_queue_scan(mp, ctx->d_fin, ctx->d_qcarry, seed, st));
+      }
       CK(launch_overdue(mp, st));
     }
     // ---- merge chunk counters into the table ----

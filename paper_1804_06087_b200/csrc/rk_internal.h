@@ -97,6 +97,8 @@ struct MomentParams {
   int want_exceed;
   unsigned long long* osum;       // [nR][nB][K] overdue counts per slowest model
   unsigned long long* esum;       // [nR][nB][K]
+  const int64_t* fin;             // queue mode: finish time of local batch j: fin[fin_off[bi] + (r*K + m)*nb + j]
+  int64_t fin_off[kMaxB];
   uint16_t* ovd;                  // per-batch overdue counts: ovd[ovd_off[bi] + (j*K + m)*ovd_nrp + r], or null
   int64_t ovd_off[kMaxB];
   int ovd_nrp;                    // rates padded to 4 or 8 (ovd_nrp(nR))
@@ -105,6 +107,11 @@ struct MomentParams {
 int ovd_nrp(int nR);
 int64_t ovd_elems(int nB, const int* B, int nR, int K, int64_t N, int64_t* off /*[kMaxB] or null*/);
 cudaError_t launch_overdue(const MomentParams& p, cudaStream_t st);  // err flags follow esum
+// queue mode (reading Q15): finish times of this chunk's complete batches per (b, r, slowest model m)
+// by a prefix-max scan, finish_j = (J+1) c + max(carry, max_{i<=j} (t_last(i) - i c)), J global;
+// carry [nB][nR][K] holds the running max over earlier chunks (derived from rates when seed_rates).
+int64_t fin_elems(int nB, const int* B, int nR, int K, int64_t N, int64_t* off /*[kMaxB] or null*/);
+cudaError_t launch_queue_scan(const MomentParams& p, int64_t* fin, int64_t* carry, int seed_rates, cudaStream_t st);
 
 struct QParams {
   int K, S, nB, nR, gs;

@@ -55,9 +55,13 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
         if (p.arrival[s0 + i] < p.arrival[s0 + i - 1]) { atomicOr(err + 2, 1u); break; }
     }
     int cnt[kMaxK];
+    int64_t fm[kMaxK];  // completion time of the batch when m is the slowest member
+    for (int m = 0; m < p.K; ++m)
+      fm[m] = p.fin ? p.fin[p.fin_off[bi] + ((int64_t)r * p.K + m) * nb + jl] : tl + p.lat[m * p.nB + bi];
     for (int m = 0; m < p.K; ++m) {
-      // overdue <=> (tl - t_s) + c > tau <=> t_s < tl + c - tau ; t_s non-decreasing in s
-      const int64_t thr = tl + p.lat[m * p.nB + bi] - p.tau;
+      // overdue <=> l(s) = F - t_s > tau <=> t_s < F - tau ; t_s non-decreasing in s. F = t_last + c
+      // (reading Q8) or the FIFO finish time (queue mode, reading Q15)
+      const int64_t thr = fm[m] - p.tau;
       int lo = 0, hi = b;  // first i with t_i >= thr
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -76,8 +80,7 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
       for (int i = 0; i <= maxc; ++i) {
         for (int m = 0; m < p.K; ++m)
           if (cnt[m] == i) {
-            const int64_t c = p.lat[m * p.nB + bi];
-            const unsigned long long e = (unsigned long long)((int64_t)i * (tl + c - p.tau) - pre);
+            const unsigned long long e = (unsigned long long)((int64_t)i * (fm[m] - p.tau) - pre);
             atomicAdd(&se[(r * p.nB + bi) * p.K + m], e);
           }
         if (i < maxc) pre += arrival_at(p.arrival, s0 + i, p.goff + s0 + i, rate);
@@ -89,6 +92,64 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
     if (so[i]) atomicAdd(p.osum + i, so[i]);
     if (p.want_exceed && se[i]) atomicAdd(p.esum + i, se[i]);
   }
+}
+
+// ---- queue mode (reading Q15): FIFO finish times by a prefix-max scan --------------------------
+// finish_j = max(t_last(j), finish_{j-1}) + c unrolls to finish_j = (j+1) c + max_{i<=j} (t_last(i) - i c)
+// (global batch indices). One CTA per (b, r, m); tiles of QS batches, block-wide inclusive max-scan.
+constexpr int QS = 256;
+constexpr int64_t kNegInf = INT64_MIN / 4;
+__device__ __forceinline__ int64_t block_max_i64(int64_t x, int64_t* sm) {
+  for (int off = 16; off; off >>= 1) x = max(x, (int64_t)__shfl_xor_sync(0xffffffffu, x, off));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = x;
+  __syncthreads();
+  int64_t r = kNegInf;
+  for (int i = 0; i < QS / 32; ++i) r = max(r, sm[i]);
+  return r;
+}
+__global__ void __launch_bounds__(QS) queue_scan_kernel(const MomentParams p, int64_t* fin, int64_t* carry,
+                                                        int seed_rates) {
+  __shared__ int64_t sm[QS / 32];
+  __shared__ int64_t wsum[QS / 32];
+  const int tri = blockIdx.x;  // (bi, r, m)
+  const int m = tri % p.K, r = (tri / p.K) % p.nR, bi = tri / (p.K * p.nR);
+  const int64_t b = p.B[bi], c = p.lat[m * p.nB + bi];
+  const int64_t nb = p.N / b, J0 = p.goff / b;
+  const double rate = p.rates[r];
+  int64_t* cy = carry + ((int64_t)bi * p.nR + r) * p.K + m;
+  int64_t M = *cy;
+  if (seed_rates) {  // backlog from the global batches before this rank's first chunk (rates only)
+    int64_t x = kNegInf;
+    for (int64_t i = threadIdx.x; i < J0; i += QS) x = max(x, arrival_at(nullptr, 0, (i + 1) * b - 1, rate) - i * c);
+    M = max(M, block_max_i64(x, sm));
+  }
+  int64_t* out = fin + p.fin_off[bi] + ((int64_t)r * p.K + m) * nb;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int64_t t0 = 0; t0 < nb; t0 += QS) {
+    const int64_t jl = t0 + threadIdx.x;
+    int64_t u = kNegInf;
+    if (jl < nb) {
+      const int64_t s = (jl + 1) * b - 1;
+      u = arrival_at(p.arrival, s, p.goff + s, rate) - (J0 + jl) * c;
+    }
+    for (int off = 1; off < 32; off <<= 1) {  // warp inclusive max-scan
+      const int64_t o = __shfl_up_sync(0xffffffffu, u, off);
+      if (l >= off) u = max(u, o);
+    }
+    __syncthreads();
+    if (l == 31) wsum[w] = u;
+    __syncthreads();
+    int64_t pre = M;
+    for (int i = 0; i < w; ++i) pre = max(pre, wsum[i]);
+    const int64_t incl = max(pre, u);
+    if (jl < nb) out[jl] = (J0 + jl + 1) * c + incl;
+    int64_t tile = M;
+    for (int i = 0; i < QS / 32; ++i) tile = max(tile, wsum[i]);
+    M = tile;
+  }
+  if (threadIdx.x == 0) *cy = M;
 }
 
 // ---- chunk counters -> table ------------------------------------------------------------------
@@ -272,6 +333,21 @@ cudaError_t launch_overdue(const MomentParams& p, cudaStream_t st) {
   if (blocks > 148 * 8) blocks = 148 * 8;
   // err flags live right after the sums (see rk_api.cpp chunk layout)
   overdue_kernel<<<(int)blocks, 256, 0, st>>>(p, reinterpret_cast<unsigned int*>(p.esum + (size_t)p.nR * p.nB * p.K));
+  return cudaGetLastError();
+}
+
+int64_t fin_elems(int nB, const int* B, int nR, int K, int64_t N, int64_t* off) {
+  int64_t tot = 0;
+  for (int bi = 0; bi < nB; ++bi) {
+    if (off) off[bi] = tot;
+    tot += (N / B[bi]) * nR * K;
+  }
+  return tot;
+}
+
+cudaError_t launch_queue_scan(const MomentParams& p, int64_t* fin, int64_t* carry, int seed_rates, cudaStream_t st) {
+  if (p.nB == 0 || p.nR == 0) return cudaSuccess;
+  queue_scan_kernel<<<p.nB * p.nR * p.K, QS, 0, st>>>(p, fin, carry, seed_rates);
   return cudaGetLastError();
 }
 

@@ -36,7 +36,8 @@ class RkError(RuntimeError):
 class _Cfg(ctypes.Structure):
     _fields_ = [("nB", ctypes.c_int), ("B", ctypes.c_void_p), ("beta", ctypes.c_double), ("tau_ns", ctypes.c_int64),
                 ("lat_ns", ctypes.c_void_p), ("nR", ctypes.c_int), ("rates", ctypes.c_void_p),
-                ("arrival_ns", ctypes.c_void_p), ("want_exceed", ctypes.c_int), ("want_labelled", ctypes.c_int)]
+                ("arrival_ns", ctypes.c_void_p), ("want_exceed", ctypes.c_int), ("want_labelled", ctypes.c_int),
+                ("queue", ctypes.c_int)]
 
 
 class _Table(ctypes.Structure):
@@ -127,6 +128,7 @@ class RewardCfg:
     arrival_ns: object = None
     want_exceed: bool = True
     want_labelled: bool = True
+    queue: bool = False  # reading Q15: FIFO ensemble server, batch j waits for batch j-1
 
 
 class Context:
@@ -185,7 +187,7 @@ class Context:
         nR = 1 if arr is not None else (0 if rates is None else rates.size)
         self._keep = [B, lat, rates, arr]
         return _Cfg(B.size, _ptr(B), cfg.beta, int(cfg.tau_ns), _ptr(lat), nR, _ptr(rates), _ptr(arr),
-                    int(cfg.want_exceed), int(cfg.want_labelled))
+                    int(cfg.want_exceed), int(cfg.want_labelled), int(cfg.queue))
 
     def subset_reset(self, cfg: RewardCfg | None = None):
         c = self._cfg(cfg)

@@ -12,12 +12,13 @@ def lat_profile(K, B):
     return np.array([[int(round(f[m] * (16.67e6 + 3.333e6 * b))) for b in B] for m in range(K)], np.int64)
 
 
-def default_cfg(K, B=(16, 32, 64), rates=(64.0, 128.0, 572.0, 1144.0), beta=1.0, tau_ns=560_000_000):
+def default_cfg(K, B=(16, 32, 64), rates=(64.0, 128.0, 572.0, 1144.0), beta=1.0, tau_ns=560_000_000, queue=False):
     import paper_1804_06087_b200 as rk
     lat = lat_profile(K, B)
     g = rk.RewardCfg(B=list(B), beta=beta, tau_ns=tau_ns, lat_ns=lat, rates=list(rates), want_exceed=True,
-                     want_labelled=True)
-    o = oracle.RewardCfg(B=list(B), beta=beta, tau_ns=tau_ns, lat_ns=lat, rates=list(rates), want_exceed=True)
+                     want_labelled=True, queue=queue)
+    o = oracle.RewardCfg(B=list(B), beta=beta, tau_ns=tau_ns, lat_ns=lat, rates=list(rates), want_exceed=True,
+                         queue=queue)
     return g, o
 
 

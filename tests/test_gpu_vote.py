@@ -196,3 +196,65 @@ def test_errors(rk):
     ctx.score_logits(None, 12, 0)
     t = ctx.subset_stats(None)
     assert t["N"] == 0 and t["cnt_vote"].sum() == 0
+
+
+QUEUE_CASES = [(3, 10, 1000, 11), (8, 1000, 300, 12), (12, 100, 200, 13), (5, 37, 517, 14)]
+
+
+@pytest.mark.parametrize("K,C,N,seed", QUEUE_CASES)
+def test_queue_mode_parity(rk, K, C, N, seed):
+    """Reading Q15: FIFO finish times; the rates span under- and overload."""
+    y = gen.labels(seed, 0, N, C)
+    L = gen.logits(seed, 0, N, K, C, y=y)
+    gcfg, ocfg = default_cfg(K, rates=(64.0, 572.0, 4000.0), queue=True)
+    t, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    compare_tables(t, o, K=K)
+    _, onq = default_cfg(K, rates=(64.0, 572.0, 4000.0))
+    o0 = oracle.table(L, y, K, C, cfg=onq)
+    assert (o.O > o0.O).any()  # the backlog matters in this workload
+
+
+def test_queue_mode_chunks_and_shards(rk):
+    """Backlog carried across in-order chunks; a shard starting at sample 512 derives the backlog of
+    the earlier batches from the rates; shards add up to the one-shot table."""
+    K, C, N = 4, 100, 1000
+    y = gen.labels(22, 0, N, C)
+    L = gen.logits(22, 0, N, K, C, y=y)
+    gcfg, ocfg = default_cfg(K, B=(16, 32, 64), rates=(300.0, 2000.0), queue=True)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C)
+    ctx.subset_reset(gcfg)
+    keep = []
+    for off, n in [(0, 256), (256, 512), (768, 232)]:
+        keep.append(dev(L[off:off + n]))
+        ctx.score_logits(keep[-1], L.shape[2], n, off)
+        ctx.subset_accumulate(dev(y[off:off + n]))
+    compare_tables(ctx.subset_finalize(), o, K=K)
+    parts = []
+    for off, n in [(0, 512), (512, 488)]:
+        c2 = rk.Context(0)
+        c2.load_ensemble(K, C)
+        keep.append(dev(L[off:off + n]))
+        c2.score_logits(keep[-1], L.shape[2], n, off)
+        parts.append(c2.subset_stats(dev(y[off:off + n]), gcfg))
+    for k in ("O", "Q", "E"):
+        np.testing.assert_array_equal(parts[0][k] + parts[1][k], getattr(o, k), err_msg=k)
+    # out-of-order chunks are rejected; caller arrivals need the stream to start at sample 0
+    ctx.subset_reset(gcfg)
+    ctx.score_logits(keep[1], L.shape[2], 512, 256)
+    ctx.subset_accumulate(dev(y[256:768]))
+    ctx.score_logits(keep[0], L.shape[2], 256, 0)
+    with pytest.raises(rk.RkError):
+        ctx.subset_accumulate(dev(y[:256]))
+    import paper_1804_06087_b200 as m
+    arr = np.arange(N, dtype=np.int64) * 1_000_000
+    acfg = m.RewardCfg(B=[16], beta=1.0, tau_ns=10_000_000, lat_ns=gcfg.lat_ns[:, :1].copy(), arrival_ns=arr[512:],
+                       queue=True)
+    c3 = rk.Context(0)
+    c3.load_ensemble(K, C)
+    c3.score_logits(keep[-1], L.shape[2], 488, 512)
+    with pytest.raises(rk.RkError) as e:
+        c3.subset_stats(dev(y[512:]), acfg)
+    assert e.value.status == 8  # RK_EUNSUPPORTED
