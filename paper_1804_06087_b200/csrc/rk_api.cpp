@@ -63,7 +63,7 @@ struct rk_ctx {
   int64_t ws_cap = 0, ws_top1_cap = 0, ws_lse_cap = 0, ws_max_cap = 0;
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
-  alignas(64) uint8_t tmaps[3 * 128];
+  alignas(64) uint8_t tmaps[4 * 128];
   int gemm_cluster = 2;                // head GEMM: 2 = CTA pair (tcgen05 cta_group::2, M = 256), 1 = single CTA (env RK_GEMM_CLUSTER)
   cudaStream_t copy_stream = nullptr;  // H2D of host X, overlapped with the GEMM
   cudaEvent_t ev_start = nullptr;

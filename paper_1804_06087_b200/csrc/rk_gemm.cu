@@ -34,8 +34,10 @@ namespace {
 constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB: this CTA's 128 rows of X
 constexpr int EPI_WARPS = 4;
-constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging box
+constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging box (packed mode: two 32x16 boxes)
 constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int EPI_PACK = 8;              // packed mode: two epilogue warps per TMEM lane quarter
+constexpr int XCH_BYTES = 4 * 32 * 12;   // packed mode: (max, sum, argmax) hand-over per quarter
 // CL = 1: one CTA computes a 128 x 256 tile (W tile 256 rows in its smem, 4 stages of 48 KB).
 // CL = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256): each CTA
 // holds its 128 X rows and HALF of the W tile (128 rows), 6 stages of 32 KB.
@@ -45,7 +47,8 @@ struct Tile {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NS = CL == 1 ? 4 : 6;
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + NS * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 256;
+  static constexpr int SMEM_BYTES =
+      1024 /*align slack*/ + NS * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 256 + XCH_BYTES;
 };
 static_assert(Tile<1>::SMEM_BYTES <= 232448 && Tile<2>::SMEM_BYTES <= 232448, "smem");
 
@@ -155,6 +158,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[32]) {
 struct GemmArgs {
   int64_t N;
   int K, C, Cp, D, nt, scale_log2;
+  int ng, gcols;  // work-unit column groups: K groups of Cp columns, or (packed) 1 group of K*Cp
   const float* bias;
   int32_t* top1;
   float* lse;
@@ -220,10 +224,130 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // operand byte crosses L2 -> smem once per pair instead of once per CTA (B traffic halved, smem
 // stage 32 KB instead of 48 KB -> 6 stages). Each CTA's TMEM receives its own 128 rows x N
 // accumulator and its epilogue is unchanged.
+// Packed-mode epilogue (see gemm_heads_kernel): 16-column blocks of the flattened column space; the
+// two warps of a TMEM lane quarter (half h) take alternating blocks and keep per-model online
+// (max, lowest argmax, sum-exp); at each model boundary half 1 hands its part to half 0 (named
+// barrier per quarter), which merges and writes top1/lse/max. Logits leave through a 32-row x
+// 16-column staging box (64-byte rows, 16-byte chunks XOR (row >> 1) & 3: the 64B TMA swizzle)
+// and a 3-D TMA store (class, model, row).
 template <int CL>
-__global__ void __launch_bounds__(THREADS, 1)
+__device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtensorMap& tmo16, uint64_t* tfull,
+                                                uint64_t* tempty, uint32_t tmem_base, int q, int h, int lane,
+                                                uint8_t* stg, float* xch, int64_t ucl0, int64_t units, int64_t ucls,
+                                                int crank, float scale, uint64_t store_policy) {
+  constexpr int SBOX = 32 * 16 * 4;
+  uint32_t tc = 0, nstore = 0, nclose = 0;
+  const int row_in_tile = q * 32 + lane;
+  float* xb = xch + q * 96;
+  for (int64_t u = ucl0; u < units; u += ucls) {
+    const int mt = (int)(u / a.ng) * CL + crank;
+    const int64_t row = (int64_t)mt * BM + row_in_tile;
+    float mx = -INFINITY, sum = 0.f;
+    int arg = 0x7fffffff, cur = -1;
+    auto close = [&](int m) {  // both halves call this at the same model boundaries
+      if (m < 0) return;
+      if (h == 1) {
+        if (nclose > 0) asm volatile("bar.sync %0, 64;" ::"r"(5 + q) : "memory");  // half 0 read the last one
+        xb[lane] = mx; xb[32 + lane] = sum; xb[64 + lane] = __int_as_float(arg);
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      if (h == 0) {
+        const float mx1 = xb[lane], s1 = xb[32 + lane];
+        const int a1 = __float_as_int(xb[64 + lane]);
+        asm volatile("bar.arrive %0, 64;" ::"r"(5 + q) : "memory");
+        const float M = fmaxf(mx, mx1);
+        float S = 0.f;
+        if (mx != -INFINITY) S += sum * __expf(mx - M);
+        if (mx1 != -INFINITY) S += s1 * __expf(mx1 - M);
+        int A = arg;
+        if (mx1 > mx || (mx1 == mx && a1 < arg)) A = a1;
+        if (row < a.N) {
+          a.top1[row * a.K + m] = A;
+          a.lse[row * a.K + m] = M + logf(S);
+          a.rmax[row * a.K + m] = M;
+        }
+      }
+      ++nclose;
+    };
+    uint32_t blk = 0;  // global 16-column block counter of this unit (alternates between the halves)
+    for (int j = 0; j < a.nt; ++j, ++tc) {
+      const int width = min(BN, a.gcols - j * BN);
+      const uint32_t as = tc & 1;
+      mbar_wait(&tfull[as], (tc >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      for (int c0 = 0; c0 < width; c0 += 16, ++blk) {
+        const int gc = j * BN + c0;
+        const int model = gc / a.Cp, cm = gc - model * a.Cp;
+        if (model != cur) {  // first block of the next model: close the previous one
+          close(cur);
+          mx = -INFINITY; sum = 0.f; arg = 0x7fffffff; cur = model;
+        }
+        if ((int)(blk & 1u) != h) continue;
+        float v[32];
+        tmem_ld16(tbase + c0, v);
+        const float4* bptr = reinterpret_cast<const float4*>(a.bias + (size_t)model * a.Cp + cm);
+        float cmax = -INFINITY;
+        int carg = 0;
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) {
+          const float4 b4 = __ldg(bptr + i4);  // -inf on padding columns
+          const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = 4 * i4 + e;
+            v[i] = fmaf(v[i], scale, bb[e]);
+            if (v[i] > cmax) { cmax = v[i]; carg = cm + i; }
+          }
+        }
+        if (cmax > mx) {
+          sum = sum * __expf(mx - cmax);
+          mx = cmax;
+          arg = carg;
+        }
+        if (mx != -INFINITY) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sum += __expf(v[i] - mx);
+        }
+        uint8_t* buf = stg + (nstore & 1) * SBOX;
+        if (lane == 0 && nstore >= 2) tma_store_wait_read1();
+        __syncwarp();
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int phys = c4 ^ ((lane >> 1) & 3);
+          *reinterpret_cast<float4*>(buf + lane * 64 + phys * 16) =
+              make_float4(v[c4 * 4], v[c4 * 4 + 1], v[c4 * 4 + 2], v[c4 * 4 + 3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmo16, buf, cm, model, (int)(mt * BM + q * 32), store_policy);
+          tma_store_commit();
+        }
+        ++nstore;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CL == 1) mbar_arrive(&tempty[as]);
+        else mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[as]), 0));
+      }
+    }
+    close(cur);
+  }
+  if (lane == 0) tma_store_wait_all();
+  __syncwarp();
+}
+
+// PACK (Cp <= 128): a work unit covers ALL K models -- the tiles walk the flattened [K*Cp] column
+// space, so each X tile is staged once per 256 columns instead of once per model; the epilogue works
+// in 16-column blocks (each inside one model, Cp % 16 == 0) and closes a model's online statistics
+// when the next model's first block arrives.
+template <int CL, bool PACK>
+__global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
     gemm_heads_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
-                      const __grid_constant__ CUtensorMap tmo, const GemmArgs a) {
+                      const __grid_constant__ CUtensorMap tmo, const __grid_constant__ CUtensorMap tmo16,
+                      const GemmArgs a) {
   using T = Tile<CL>;
   constexpr int NS = T::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -236,23 +360,26 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tfull = bars + 2 * NS;  // [2]
   uint64_t* tempty = bars + 2 * NS + 2;  // [2]  (CL = 2: the leader's counts both epilogues)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 4);
+  float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [4][3][32] (packed mode)
+  constexpr int EPI = PACK ? EPI_PACK : EPI_WARPS;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mtiles = (a.N + BM - 1) / BM;
   // work unit = (group of CL adjacent row tiles, model); CTA `crank` of the pair takes row tile
   // CL * (u / K) + crank. Both CTAs of a pair walk the same unit sequence.
-  const int64_t units = ((mtiles + CL - 1) / CL) * a.K;
+  const int64_t units = ((mtiles + CL - 1) / CL) * a.ng;
   const int64_t ucl0 = blockIdx.x / CL, ucls = gridDim.x / CL;
   const int crank = CL > 1 ? (int)cluster_rank() : 0;
   const int kblocks = a.D / BK;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI_WARPS * CL); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI * CL); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmx) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmw) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmo) : "memory");
+    if (PACK) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmo16) : "memory");
   }
   if (warp == 1) {  // CL = 2: both CTAs allocate collectively (same warp id, same smem slot)
     if (CL == 1) {
@@ -278,10 +405,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t pol_x = policy_evict_normal();
       uint32_t it = 0;
       for (int64_t u = ucl0; u < units; u += ucls) {
-        const int mt = (int)(u / a.K) * CL + crank, model = (int)(u % a.K);
+        const int mt = (int)(u / a.ng) * CL + crank, grp = (int)(u % a.ng);
         for (int j = 0; j < a.nt; ++j) {
-          const int width = min(BN, a.Cp - j * BN);
-          const int col0 = model * a.Cp + j * BN + crank * (width / CL);
+          const int width = min(BN, a.gcols - j * BN);
+          const int col0 = grp * a.gcols + j * BN + crank * (width / CL);
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
             const int s = it % NS;
             const uint32_t ph = (it / NS) & 1;
@@ -308,7 +435,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t it = 0, tc = 0;
       for (int64_t u = ucl0; u < units; u += ucls) {
         for (int j = 0; j < a.nt; ++j, ++tc) {
-          const int width = min(BN, a.Cp - j * BN);
+          const int width = min(BN, a.gcols - j * BN);
           const uint32_t idesc = umma_idesc(width, BM * CL);
           const uint32_t as = tc & 1;
           mbar_wait(&tempty[as], ((tc >> 1) & 1) ^ 1);
@@ -339,12 +466,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ===== epilogue: TMEM -> registers -> (stats, swizzled smem) -> TMA store =====
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     const int row_in_tile = q * 32 + lane;
-    uint8_t* stg = staging + (warp - 2) * 2 * STG_BYTES;
+    uint8_t* stg = staging + (warp - 2) * 2 * (STG_BYTES * EPI_WARPS / EPI);
     const float scale = ldexpf(1.0f, a.scale_log2);
     const uint64_t store_policy = policy_evict_first();
     uint32_t tc = 0, nstore = 0;
+    if (PACK) {
+      epilogue_packed<CL>(a, tmo16, tfull, tempty, tmem_base, q, (warp - 2) >> 2, lane, stg, xch, ucl0, units, ucls,
+                          crank, scale, store_policy);
+    } else
     for (int64_t u = ucl0; u < units; u += ucls) {
-      const int mt = (int)(u / a.K) * CL + crank, model = (int)(u % a.K);
+      const int mt = (int)(u / a.ng) * CL + crank, model = (int)(u % a.ng);
       const int64_t row = (int64_t)mt * BM + row_in_tile;
       float mx = -INFINITY, sum = 0.f;
       int arg = 0;
@@ -480,39 +611,45 @@ int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return -4;
   }
+  {  // 16-column store boxes for the packed mode (64-byte rows, 64B swizzle)
+    cuuint64_t dims[3] = {(cuuint64_t)p.C, (cuuint64_t)p.K, (cuuint64_t)p.N};
+    cuuint64_t strides[2] = {(cuuint64_t)p.ldc * 4, (cuuint64_t)p.K * p.ldc * 4};
+    cuuint32_t box[3] = {16, 1, 32};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&maps[3], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, logits, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -5;
+  }
   p.tmap_x = &maps[0];
   p.tmap_w = &maps[1];
   p.tmap_out = &maps[2];
+  p.tmap_out16 = &maps[3];
   return 0;
 }
 
-cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
-  if (p.N <= 0) return cudaSuccess;
-  GemmArgs a;
-  a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D; a.nt = (p.Cp + BN - 1) / BN;
-  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lse = p.lse; a.rmax = p.rmax;
+template <int CL, bool PACK>
+static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count, cudaStream_t st) {
   const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(p.tmap_x);
   const CUtensorMap& mw = *reinterpret_cast<const CUtensorMap*>(p.tmap_w);
   const CUtensorMap& mo = *reinterpret_cast<const CUtensorMap*>(p.tmap_out);
-  if (p.cluster <= 1) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_heads_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tile<1>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    const int64_t units = ((p.N + BM - 1) / BM) * p.K;
+  const CUtensorMap& m16 = *reinterpret_cast<const CUtensorMap*>(p.tmap_out16);
+  cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<CL, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Tile<CL>::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int64_t units = ((p.N + CL * BM - 1) / (CL * BM)) * a.ng;
+  if (CL == 1) {
     const int grid = (int)(units < sm_count ? units : sm_count);
-    gemm_heads_kernel<1><<<grid, THREADS, Tile<1>::SMEM_BYTES, st>>>(mx, mw, mo, a);
+    gemm_heads_kernel<CL, PACK><<<grid, 64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), Tile<CL>::SMEM_BYTES, st>>>(
+        mx, mw, mo, m16, a);
     return cudaGetLastError();
   }
-  // 2-CTA clusters: the grid is a multiple of 2 (one CTA per SM, SM pairs share the W tile)
-  cudaError_t e =
-      cudaFuncSetAttribute(gemm_heads_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tile<2>::SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  const int64_t units = ((p.N + 2 * BM - 1) / (2 * BM)) * p.K;
-  int64_t clusters = units < sm_count / 2 ? units : sm_count / 2;
+  // CTA pairs: clusters of 2 (one CTA per SM)
+  const int64_t clusters = units < sm_count / 2 ? units : sm_count / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * clusters));
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = Tile<2>::SMEM_BYTES;
+  cfg.blockDim = dim3(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS));
+  cfg.dynamicSmemBytes = Tile<CL>::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -521,9 +658,22 @@ cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, gemm_heads_kernel<2>, mx, mw, mo, a);
+  e = cudaLaunchKernelEx(&cfg, gemm_heads_kernel<CL, PACK>, mx, mw, mo, m16, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
+  if (p.N <= 0) return cudaSuccess;
+  GemmArgs a;
+  a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D;
+  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lse = p.lse; a.rmax = p.rmax;
+  const bool pack = p.Cp <= 128;  // small heads: tiles span several models
+  a.ng = pack ? 1 : p.K;
+  a.gcols = pack ? p.K * p.Cp : p.Cp;
+  a.nt = (a.gcols + BN - 1) / BN;
+  if (p.cluster <= 1) return pack ? launch_t<1, true>(a, p, sm_count, st) : launch_t<1, false>(a, p, sm_count, st);
+  return pack ? launch_t<2, true>(a, p, sm_count, st) : launch_t<2, false>(a, p, sm_count, st);
 }
 
 }  // namespace rk

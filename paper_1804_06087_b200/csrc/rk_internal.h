@@ -155,6 +155,7 @@ struct GemmParams {
   const void* tmap_x;    // CUtensorMap* (host copy passed by value via __grid_constant__)
   const void* tmap_w;
   const void* tmap_out;
+  const void* tmap_out16;  // 16-column store boxes (packed mode, Cp <= 128)
   int64_t N;             // rows
   int K, C, Cp, D, ldc;  // Cp = per-model padded columns (multiple of 16)
   int scale_log2;
@@ -167,6 +168,6 @@ struct GemmParams {
   int cluster;           // 1 = one CTA per 128-row tile; 2 = CTA pair, tcgen05.mma.cta_group::2 on 256-row tiles
 };
 cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st);
-int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits, void* storage /*3*128B*/);
+int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits, void* storage /*4*128B*/);
 
 }  // namespace rk
