@@ -238,3 +238,34 @@ def predict(logits, K: int, C: int, v: int, tie: int = TIE_BEST_MEMBER, rank=Non
     if rc != OK:
         raise OracleError(rc)
     return pv, pa, ap, t1, ls
+
+
+# ---- NEXT-1: Algorithm 3 greedy batching ------------------------------------------------------
+class _Serve(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("served", "overdue", "exceed_ns", "batches", "unserved")]
+
+
+def greedy_serve(cfg: RewardCfg, K: int, N: int, delta_ns: int) -> dict:
+    """Algorithm 3 per (rate, subset): arrays [nR][S] of served, overdue,
+    exceed_ns, batches, unserved (reading S1)."""
+    nB = len(cfg.B)
+    Bv = np.ascontiguousarray(cfg.B, dtype=np.int32)
+    lat = np.ascontiguousarray(cfg.lat_ns, dtype=np.int64).reshape(K, nB)
+    if cfg.arrival_ns is not None:
+        arr, rates, nR = np.ascontiguousarray(cfg.arrival_ns, dtype=np.int64), None, 1
+    else:
+        arr, rates = None, np.ascontiguousarray(cfg.rates, dtype=np.float64)
+        nR = rates.size
+    cc = _Cfg(nB, _p(Bv), cfg.beta, cfg.tau_ns, _p(lat), nR, _p(rates), _p(arr), int(cfg.want_exceed),
+              int(cfg.queue))
+    S = (1 << K) - 1
+    out = (_Serve * (nR * S))()
+    L = lib()
+    L.or_greedy_serve.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+    rc = L.or_greedy_serve(ctypes.byref(cc), K, N, delta_ns, out)
+    if rc != OK:
+        raise OracleError(rc)
+    res = {}
+    for name in ("served", "overdue", "exceed_ns", "batches", "unserved"):
+        res[name] = np.array([getattr(o, name) for o in out], dtype=np.uint64).reshape(nR, S)
+    return res

@@ -406,3 +406,63 @@ out:
   free(l); free(p);
   return status;
 }
+
+/* ---- NEXT-1: Algorithm 3 greedy batching (reading S1) ------------------------ */
+int or_greedy_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, or_serve* out) {
+  if (!cfg || K < 1 || K > 12 || N < 0 || cfg->nB < 1 || !cfg->B || !cfg->lat_ns || cfg->nR < 1) return OR_EINVAL;
+  if (!cfg->rates && !cfg->arrival_ns) return OR_EINVAL;
+  const int S = (1 << K) - 1, nB = cfg->nB;
+  int bmax = 0, bmin = 1 << 30;
+  for (int bi = 0; bi < nB; ++bi) {
+    if (cfg->B[bi] > bmax) bmax = cfg->B[bi];
+    if (cfg->B[bi] < bmin) bmin = cfg->B[bi];
+  }
+  for (int r = 0; r < cfg->nR; ++r)
+    for (uint32_t v = 1; v <= (uint32_t)S; ++v) {
+      or_serve o = {0, 0, 0, 0, 0};
+      int64_t t = 0, head = 0, tail = 0;
+      while (head < N) {
+        while (tail < N && arrival(cfg, r, tail) <= t) ++tail;
+        const int64_t qlen = tail - head;
+        int b = 0;  /* the batch size to infer now, 0 = wait */
+        int bsel = 0;
+        for (int bi = 0; bi < nB; ++bi)
+          if (cfg->B[bi] <= qlen && cfg->B[bi] > bsel) bsel = cfg->B[bi];
+        int64_t c = 0;
+        if (bsel > 0) {
+          int bi_sel = 0;
+          for (int bi = 0; bi < nB; ++bi) if (cfg->B[bi] == bsel) bi_sel = bi;
+          for (int m = 0; m < K; ++m)
+            if (((v >> m) & 1u) && cfg->lat_ns[m * nB + bi_sel] > c) c = cfg->lat_ns[m * nB + bi_sel];
+        }
+        if (qlen >= bmax) {
+          b = bmax;  /* bsel == bmax */
+        } else if (bsel > 0 && c + (t - arrival(cfg, r, head)) + delta_ns >= cfg->tau_ns) {
+          b = bsel;
+        }
+        if (b > 0) {
+          const int64_t done = t + c;
+          for (int64_t s = head; s < head + b; ++s) {
+            const int64_t l = done - arrival(cfg, r, s);
+            o.served++;
+            if (l > cfg->tau_ns) { o.overdue++; o.exceed_ns += (uint64_t)(l - cfg->tau_ns); }
+          }
+          o.batches++;
+          head += b;
+          t = done;
+        } else if (tail == N) {
+          if (bsel == 0) { o.unserved = (uint64_t)qlen; break; }
+          t = arrival(cfg, r, head) + cfg->tau_ns - delta_ns - c; /* the condition becomes true */
+        } else {
+          int64_t tn = arrival(cfg, r, tail);
+          if (bsel > 0) {
+            const int64_t tthr = arrival(cfg, r, head) + cfg->tau_ns - delta_ns - c;
+            if (tthr < tn) tn = tthr;
+          }
+          t = tn;
+        }
+      }
+      out[(int64_t)r * S + (v - 1)] = o;
+    }
+  return OR_OK;
+}

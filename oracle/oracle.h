@@ -89,6 +89,20 @@ int or_predict(const float* logits_f32, int ldc, const double* logits_f64, int64
 /* Arrival time of global request s at rate r (reading Q9): floor((double)s*1e9/r) ns. */
 int64_t or_arrival_ns(int64_t s, double rate);
 
+/* NEXT-1: Algorithm 3, Inference(Queue q, Model m), greedy batching of one
+ * synchronous ensemble v (c(v,b) = max over members of c(m,b)) on a request stream,
+ * single server, inference blocks the loop (reading S1): whenever the server is idle at time t,
+ * with q the arrived, unserved requests (oldest first):
+ *   len(q) >= max B                                   -> infer the oldest max B at t;
+ *   b = max{b in B : b <= len(q)} exists and
+ *     c(v,b) + (t - t_q0) + delta >= tau              -> infer the oldest b at t;
+ *   otherwise wait until the next arrival or until that condition becomes true.
+ * A batch inferred at t completes at t + c(v,b); l(s) = completion - t_s; overdue iff l(s) > tau.
+ * Requests still queued (fewer than min B) after the last arrival are unserved.
+ * Output per (rate r, subset v): out[r*S + v-1]. */
+typedef struct { uint64_t served, overdue, exceed_ns, batches, unserved; } or_serve;
+int or_greedy_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, or_serve* out);
+
 #ifdef __cplusplus
 }
 #endif

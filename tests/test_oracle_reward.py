@@ -145,3 +145,28 @@ def test_queue_invariants():
             np.testing.assert_array_equal(t[True].E, t[False].E)
         else:
             assert (t[True].O > t[False].O).any()
+
+
+def test_S1_greedy_batching_worked_example():
+    """NEXT-1: Algorithm 3 by hand (tests/golden/r_reward_examples.txt, S1)."""
+    for key in ("S1", "S1b"):
+        g = gold()[key]
+        cfg = oracle.RewardCfg(B=[2, 4], beta=1.0, tau_ns=1000, lat_ns=np.array([[600, 900]]), rates=[1e7])
+        r = oracle.greedy_serve(cfg, 1, int(g["N"]), 50)
+        for k, name in (("served", "served"), ("overdue", "overdue"), ("exceed", "exceed_ns"), ("batches", "batches"),
+                        ("unserved", "unserved")):
+            assert r[name][0, 0] == g[k], (key, k)
+
+
+def test_greedy_batching_properties():
+    """served + unserved = N; unserved < min B (after the last arrival the rule keeps dispatching
+    while min B requests wait); no batch exceeds max B."""
+    K, N = 3, 700
+    lat = np.array([[4_000_000, 7_000_000, 9_000_000], [2_000_000, 3_000_000, 5_000_000],
+                    [8_000_000, 12_000_000, 15_000_000]], np.int64)
+    cfg = oracle.RewardCfg(B=[16, 32, 48], beta=1.0, tau_ns=100_000_000, lat_ns=lat, rates=[300.0, 3000.0])
+    for delta in (0, 10_000_000, 100_000_000):
+        r = oracle.greedy_serve(cfg, K, N, delta)
+        assert ((r["served"] + r["unserved"]) == N).all()
+        assert (r["unserved"] < 16).all()
+        assert (r["batches"] >= r["served"] // 48).all()
