@@ -135,6 +135,26 @@ rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream);
 rk_status rk_subset_stats(rk_ctx* ctx, const int32_t* labels, const rk_reward_cfg* cfg, rk_table* out,
                           void* stream);
 
+/* NEXT-1 serving policy: Algorithm 3 greedy batching of EVERY subset v run as a
+ * synchronous ensemble (c(v,b) = max over members of c(m,b)) on N requests whose
+ * arrivals are those of cfg (rates, or arrival_ns [N] host/device with nR = 1), per rate and subset
+ * (reading S1): when the server is idle at t, infer max B if that many requests wait,
+ * else the largest b in B not above the queue length once c(v,b) + w(q0) + delta >= tau; a batch
+ * inferred at t completes at t + c(v,b). Uses cfg->B, lat_ns, tau_ns, beta and the arrivals
+ * (queue, want_* ignored). acc: [S] host a(v) (e.g. cnt_vote / N from rk_subset_stats) or NULL;
+ * reward = a(v) * (served - beta * overdue), eq. `multi_acc_reward` summed over the greedy batches.
+ * Output arrays are host [nR][S], each may be NULL. Blocks on `stream`. Needs rk_load_ensemble. */
+typedef struct {
+  uint64_t* served;        /* requests inferred                                               */
+  uint64_t* overdue;       /* requests with l(s) > tau                                        */
+  uint64_t* exceed_ns;     /* sum of max(0, l(s) - tau) (eq. `eq:single`)                     */
+  uint64_t* batches;       /* batches inferred                                                */
+  uint64_t* unserved;      /* requests left in the queue (< min B) after the last arrival     */
+  double* reward;          /* a(v) * (served - beta * overdue)          (needs acc)           */
+} rk_serve_out;
+rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
+                          rk_serve_out* out, void* stream);
+
 /* Serving of one action (NEXT-1) and parity hook: per-sample predictions of subset v on the
  * last rk_score* batch. pred_vote, pred_avg: [N] int32; avgprob: [N][C] fp32 averaged
  * probabilities. Device pointers; each may be NULL. v == 0 -> RK_EINVAL. */

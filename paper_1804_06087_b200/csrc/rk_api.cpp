@@ -23,9 +23,9 @@ using namespace rk;
 
 namespace {
 
-enum KernelKind { KK_GEMM = 0, KK_VOTE, KK_OVERDUE, KK_MERGE, KK_Q, KK_FOLD, KK_PREDICT, KK_ALLREDUCE, KK_COUNT };
+enum KernelKind { KK_GEMM = 0, KK_VOTE, KK_OVERDUE, KK_MERGE, KK_Q, KK_FOLD, KK_PREDICT, KK_ALLREDUCE, KK_SERVE, KK_COUNT };
 const char* kKernelNames[KK_COUNT] = {"gemm_heads_tcgen05", "vote_subsets", "overdue_moments", "merge_table",
-                                      "labelled_moments", "reward_fold", "predict", "nccl_allreduce"};
+                                      "labelled_moments", "reward_fold", "predict", "nccl_allreduce", "greedy_serve"};
 
 struct Prof {
   bool on = false;
@@ -94,6 +94,8 @@ struct rk_ctx {
   int64_t* d_fin = nullptr;    // queue mode: finish times of the chunk's batches
   size_t fin_cap = 0;
   int64_t* d_qcarry = nullptr; // queue mode: running max of t_last(i) - i c per (b, r, m)
+  uint64_t* d_serve = nullptr; // greedy serving outputs
+  int64_t serve_cap = 0;
   bool q_started = false;
   int64_t q_next_off = 0;
   int32_t* d_labels = nullptr;
@@ -231,7 +233,7 @@ void rk_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
   void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_max, ctx->ws_x,
-                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
+                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -756,6 +758,64 @@ rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_
   pp.pred_vote = pred_vote; pp.pred_avg = pred_avg; pp.avgprob = avgprob;
   ProfScope ps(ctx, KK_PREDICT, st, 0, 0);
   CK(launch_predict(pp, st));
+  return RK_OK;
+}
+
+rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
+                          rk_serve_out* out, void* stream) {
+  if (!ctx || !cfg || !out) return RK_EINVAL;
+  if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
+  if (N < 0) return fail(ctx, RK_EINVAL, "N >= 0");
+  if (cfg->nB < 1 || cfg->nB > kMaxB || !cfg->B || !cfg->lat_ns) return fail(ctx, RK_EINVAL, "nB in [1,8] with B and lat_ns");
+  if (cfg->arrival_ns ? cfg->nR != 1 : (cfg->nR < 1 || cfg->nR > kMaxR || !cfg->rates))
+    return fail(ctx, RK_EINVAL, "rates (nR in [1,8]) or arrival_ns with nR == 1");
+  if (cfg->tau_ns < 0 || !(cfg->beta == cfg->beta)) return fail(ctx, RK_EINVAL, "tau >= 0, finite beta");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int K = ctx->K, S = ctx->S;
+  ServeParams sp{};
+  sp.K = K; sp.S = S; sp.nB = cfg->nB; sp.nR = cfg->nR; sp.N = N; sp.tau = cfg->tau_ns; sp.delta = delta_ns;
+  sp.beta = cfg->beta;
+  for (int bi = 0; bi < cfg->nB; ++bi) {
+    if (cfg->B[bi] < 1) return fail(ctx, RK_EINVAL, "batch sizes >= 1");
+    sp.B[bi] = cfg->B[bi];
+    for (int m = 0; m < K; ++m) {
+      if (cfg->lat_ns[m * cfg->nB + bi] < 0) return fail(ctx, RK_EINVAL, "latencies must be >= 0");
+      sp.lat[m * cfg->nB + bi] = cfg->lat_ns[m * cfg->nB + bi];
+    }
+  }
+  for (int r = 0; r < sp.nR; ++r) {
+    sp.rates[r] = cfg->arrival_ns ? 1.0 : cfg->rates[r];
+    if (!(sp.rates[r] > 0) || sp.rates[r] > 1e12) return fail(ctx, RK_EINVAL, "rates must be > 0");
+  }
+  rk_status s;
+  const int64_t n = (int64_t)sp.nR * S;
+  if (cfg->arrival_ns) {
+    if (is_device_ptr(cfg->arrival_ns)) sp.arrival = cfg->arrival_ns;
+    else {
+      if ((s = ensure(ctx, &ctx->d_arr, &ctx->arr_cap, std::max<int64_t>(N, 1))) != RK_OK) return s;
+      CK(cudaMemcpyAsync(ctx->d_arr, cfg->arrival_ns, N * 8, cudaMemcpyHostToDevice, st));
+      sp.arrival = ctx->d_arr;
+    }
+  }
+  // device scratch: 5 counter arrays + reward + acc
+  const size_t words = 5 * (size_t)n + (size_t)n + (size_t)S;
+  if ((s = ensure(ctx, &ctx->d_serve, &ctx->serve_cap, (int64_t)words)) != RK_OK) return s;
+  sp.out = reinterpret_cast<unsigned long long*>(ctx->d_serve);
+  if (acc) {
+    sp.reward = reinterpret_cast<double*>(ctx->d_serve + 5 * n);
+    sp.acc = reinterpret_cast<const double*>(ctx->d_serve + 6 * n);
+    CK(cudaMemcpyAsync(ctx->d_serve + 6 * n, acc, (size_t)S * 8, cudaMemcpyHostToDevice, st));
+  }
+  {
+    ProfScope ps(ctx, KK_SERVE, st, 0, 0);
+    CK(launch_greedy_serve(sp, st));
+  }
+  uint64_t* dst[5] = {out->served, out->overdue, out->exceed_ns, out->batches, out->unserved};
+  for (int k = 0; k < 5; ++k)
+    if (dst[k]) CK(cudaMemcpyAsync(dst[k], ctx->d_serve + k * n, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  if (out->reward && acc) CK(cudaMemcpyAsync(out->reward, ctx->d_serve + 5 * n, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return RK_OK;
 }
 

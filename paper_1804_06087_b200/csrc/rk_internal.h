@@ -150,6 +150,21 @@ struct FoldParams {
 };
 cudaError_t launch_fold(const FoldParams& p, cudaStream_t st);
 
+// ---- NEXT-1: Algorithm 3 greedy batching per (rate, subset) (rk_serve.cu) -----------------------
+struct ServeParams {
+  int K, S, nB, nR;
+  int B[kMaxB];
+  int64_t lat[kMaxK * kMaxB];
+  double rates[kMaxR];
+  const int64_t* arrival;          // [N] device or null (rates)
+  int64_t N, tau, delta;
+  double beta;
+  const double* acc;               // [S] device a(v) or null
+  unsigned long long* out;         // [5][nR][S]: served, overdue, exceed_ns, batches, unserved
+  double* reward;                  // [nR][S] or null
+};
+cudaError_t launch_greedy_serve(const ServeParams& p, cudaStream_t st);
+
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {
   const void* tmap_x;    // CUtensorMap* (host copy passed by value via __grid_constant__)

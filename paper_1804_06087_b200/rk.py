@@ -23,7 +23,7 @@ RK_OK, RK_EINVAL, RK_ESTATE, RK_ENOMEM, RK_ECUDA, RK_ENCCL, RK_ELABEL, RK_ENONFI
 TIE_BEST_MEMBER, TIE_LOWEST_CLASS = 0, 1
 
 EXPORTS = ["rk_create", "rk_nccl_unique_id", "rk_load_ensemble", "rk_score", "rk_score_logits", "rk_subset_reset",
-           "rk_subset_accumulate", "rk_subset_finalize", "rk_subset_stats", "rk_predict", "rk_outputs",
+           "rk_subset_accumulate", "rk_subset_finalize", "rk_subset_stats", "rk_predict", "rk_greedy_serve", "rk_outputs",
            "rk_set_profiling", "rk_kernel_stats", "rk_last_error", "rk_status_string", "rk_destroy"]
 
 
@@ -44,6 +44,10 @@ class _Table(ctypes.Structure):
     _fields_ = [("N", ctypes.c_int64)] + [(n, ctypes.c_void_p) for n in
                                           ("cnt_vote", "cnt_avg", "n_recheck", "corr", "O", "Q", "E",
                                            "reward_sur", "reward_lab")]
+
+
+class _Serve(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("served", "overdue", "exceed_ns", "batches", "unserved", "reward")]
 
 
 class _KStat(ctypes.Structure):
@@ -69,6 +73,7 @@ def load_library(path: str | None = None):
     L.rk_subset_finalize.argtypes = [vp, ctypes.POINTER(_Table), vp]
     L.rk_subset_stats.argtypes = [vp, vp, ctypes.POINTER(_Cfg), ctypes.POINTER(_Table), vp]
     L.rk_predict.argtypes = [vp, u32, vp, vp, vp, vp]
+    L.rk_greedy_serve.argtypes = [vp, ctypes.POINTER(_Cfg), i64, i64, vp, ctypes.POINTER(_Serve), vp]
     L.rk_outputs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i32), ctypes.POINTER(vp), ctypes.POINTER(vp),
                              ctypes.POINTER(i64)]
     L.rk_set_profiling.argtypes = [vp, i32]
@@ -230,6 +235,21 @@ class Context:
     def predict(self, v, pred_vote=None, pred_avg=None, avgprob=None, stream=None):
         self._chk(self._L.rk_predict(self._p, v, _ptr(pred_vote), _ptr(pred_avg), _ptr(avgprob), _stream(stream)),
                   "rk_predict")
+
+    def greedy_serve(self, cfg: RewardCfg, N: int, delta_ns: int, acc=None, stream=None) -> dict:
+        """NEXT-1: Algorithm 3 greedy batching of every subset, per rate: arrays
+        [nR][S] of served, overdue, exceed_ns, batches, unserved and (with acc [S]) reward."""
+        c = self._cfg(cfg)
+        nR = c.nR
+        res = {k: np.zeros((nR, self.S), np.uint64) for k in ("served", "overdue", "exceed_ns", "batches", "unserved")}
+        res["reward"] = np.zeros((nR, self.S), np.float64)
+        a = None if acc is None else np.ascontiguousarray(acc, dtype=np.float64)
+        o = _Serve(*[res[k].ctypes.data for k in ("served", "overdue", "exceed_ns", "batches", "unserved", "reward")])
+        self._chk(self._L.rk_greedy_serve(self._p, ctypes.byref(c), N, delta_ns, _ptr(a), ctypes.byref(o),
+                                          _stream(stream)), "rk_greedy_serve")
+        if a is None:
+            del res["reward"]
+        return res
 
     def outputs(self):
         lg, t1, ls = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()

@@ -1,0 +1,80 @@
+"""GPU parity of NEXT-1's greedy batching policy (Algorithm 3; reading S1):
+rk_greedy_serve against oracle.greedy_serve, every (rate, subset) scenario, integer-exact."""
+import numpy as np
+import pytest
+
+import oracle
+from bench import lat_profile
+from test_oracle_reward import gold
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+KEYS = ("served", "overdue", "exceed_ns", "batches", "unserved")
+
+
+@pytest.fixture(scope="module")
+def rk():
+    import paper_1804_06087_b200 as m
+    m.load_library()
+    return m
+
+
+def ctx_for(rk, K, C=10):
+    c = rk.Context(0)
+    c.load_ensemble(K, C)
+    return c
+
+
+def compare(g, o):
+    for k in KEYS:
+        np.testing.assert_array_equal(g[k], o[k], err_msg=k)
+
+
+def test_worked_example(rk):
+    for key in ("S1", "S1b"):
+        gd = gold()[key]
+        cfg = rk.RewardCfg(B=[2, 4], beta=1.0, tau_ns=1000, lat_ns=np.array([[600, 900]]), rates=[1e7])
+        r = ctx_for(rk, 1).greedy_serve(cfg, int(gd["N"]), 50)
+        assert r["served"][0, 0] == gd["served"] and r["overdue"][0, 0] == gd["overdue"]
+        assert r["exceed_ns"][0, 0] == gd["exceed"] and r["batches"][0, 0] == gd["batches"]
+        assert r["unserved"][0, 0] == gd["unserved"]
+
+
+@pytest.mark.parametrize("K,B,rates,N,delta", [
+    (3, [16, 32, 48], [300.0, 3000.0], 700, 0),
+    (3, [16, 32, 48], [300.0, 3000.0], 700, 10_000_000),
+    (5, [16, 32, 48, 64], [128.0, 572.0], 2000, 56_000_000),   # paper's B, delta = 0.1 tau
+    (8, [16, 32, 64, 128, 256], [64.0, 572.0, 1144.0], 5000, 56_000_000),
+])
+def test_parity_rates(rk, K, B, rates, N, delta):
+    lat = lat_profile(K, B)
+    g = rk.RewardCfg(B=B, beta=0.5, tau_ns=560_000_000, lat_ns=lat, rates=rates)
+    o = oracle.RewardCfg(B=B, beta=0.5, tau_ns=560_000_000, lat_ns=lat, rates=rates)
+    acc = np.random.default_rng(K).uniform(0.5, 0.9, (1 << K) - 1)
+    r = ctx_for(rk, K).greedy_serve(g, N, delta, acc=acc)
+    ro = oracle.greedy_serve(o, K, N, delta)
+    compare(r, ro)
+    np.testing.assert_array_equal(r["reward"], acc[None, :] * (r["served"].astype(np.float64)
+                                                              - 0.5 * r["overdue"].astype(np.float64)))
+    assert (ro["overdue"] > 0).any() and (ro["batches"] > 0).all()
+
+
+def test_parity_caller_arrivals(rk):
+    K, B, N = 4, [8, 24], 1500
+    arr = np.cumsum(np.random.default_rng(2).integers(0, 3_000_000, N)).astype(np.int64)
+    lat = lat_profile(K, B) // 20
+    for on_device in (False, True):
+        a = torch.from_numpy(arr).cuda() if on_device else arr
+        g = rk.RewardCfg(B=B, beta=1.0, tau_ns=40_000_000, lat_ns=lat, arrival_ns=a)
+        r = ctx_for(rk, K).greedy_serve(g, N, 2_000_000)
+        o = oracle.RewardCfg(B=B, beta=1.0, tau_ns=40_000_000, lat_ns=lat, arrival_ns=arr)
+        compare(r, oracle.greedy_serve(o, K, N, 2_000_000))
+
+
+def test_errors(rk):
+    c = ctx_for(rk, 2)
+    with pytest.raises(rk.RkError):
+        c.greedy_serve(rk.RewardCfg(B=[], beta=1.0, tau_ns=10, lat_ns=np.zeros((2, 0), np.int64), rates=[1.0]), 10, 0)
+    with pytest.raises(rk.RkError):
+        c.greedy_serve(rk.RewardCfg(B=[4], beta=1.0, tau_ns=10, lat_ns=np.zeros((2, 1), np.int64), rates=[0.0]), 10, 0)
