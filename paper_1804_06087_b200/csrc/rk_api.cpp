@@ -790,13 +790,13 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
   }
   rk_status s;
   const int64_t n = (int64_t)sp.nR * S;
-  if (cfg->arrival_ns) {
-    if (is_device_ptr(cfg->arrival_ns)) sp.arrival = cfg->arrival_ns;
-    else {
-      if ((s = ensure(ctx, &ctx->d_arr, &ctx->arr_cap, std::max<int64_t>(N, 1))) != RK_OK) return s;
-      CK(cudaMemcpyAsync(ctx->d_arr, cfg->arrival_ns, N * 8, cudaMemcpyHostToDevice, st));
-      sp.arrival = ctx->d_arr;
-    }
+  if (cfg->arrival_ns && is_device_ptr(cfg->arrival_ns)) {
+    sp.arrival = cfg->arrival_ns;
+  } else {  // [nR][N] arrival times on the device: the caller's, or filled from the rates
+    if ((s = ensure(ctx, &ctx->d_arr, &ctx->arr_cap, std::max<int64_t>(N * sp.nR, 1))) != RK_OK) return s;
+    if (cfg->arrival_ns) CK(cudaMemcpyAsync(ctx->d_arr, cfg->arrival_ns, N * 8, cudaMemcpyHostToDevice, st));
+    else CK(launch_arrival_fill(sp, ctx->d_arr, st));
+    sp.arrival = ctx->d_arr;
   }
   // device scratch: 5 counter arrays + reward + acc
   const size_t words = 5 * (size_t)n + (size_t)n + (size_t)S;

@@ -156,7 +156,7 @@ struct ServeParams {
   int B[kMaxB];
   int64_t lat[kMaxK * kMaxB];
   double rates[kMaxR];
-  const int64_t* arrival;          // [N] device or null (rates)
+  const int64_t* arrival;          // [nR][N] device arrival times (launch_arrival_fill for rates)
   int64_t N, tau, delta;
   double beta;
   const double* acc;               // [S] device a(v) or null
@@ -164,6 +164,7 @@ struct ServeParams {
   double* reward;                  // [nR][S] or null
 };
 cudaError_t launch_greedy_serve(const ServeParams& p, cudaStream_t st);
+cudaError_t launch_arrival_fill(const ServeParams& p, int64_t* out /*[nR][N]*/, cudaStream_t st);
 
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {

@@ -11,7 +11,9 @@
 // Requests still queued (fewer than min B) after the last arrival are unserved.
 //
 // The policy is sequential in time but independent across (rate, subset), so one thread simulates
-// one scenario (thousands of scenarios per launch); integer nanoseconds throughout (exact).
+// one scenario (thousands of scenarios per launch) over arrival arrays computed once per rate by a
+// parallel fill (the fp64 division of reading Q9 is off the sequential path); integer nanoseconds
+// throughout (exact).
 // The reward of eq. `multi_acc_reward` summed over the greedy batches,
 // a(v) * (served - beta * overdue), is folded in fp64 in the same thread.
 #include <cuda_runtime.h>
@@ -23,9 +25,13 @@
 namespace rk {
 namespace {
 
-__device__ __forceinline__ int64_t arrival_ns(const int64_t* arr, int64_t s, double rate) {
-  if (arr) return arr[s];
-  return (int64_t)floor(__ddiv_rn(__dmul_rn((double)s, 1e9), rate));  // reading Q9, two roundings
+// arrival times of every rate, computed once (reading Q9: t_s = floor(s * 1e9 / r), two roundings)
+__global__ void arrival_fill_kernel(int64_t* out, int64_t N, int nR, const ServeParams p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N * nR) return;
+  const int r = (int)(i / N);
+  const int64_t s = i - (int64_t)r * N;
+  out[i] = (int64_t)floor(__ddiv_rn(__dmul_rn((double)s, 1e9), p.rates[r]));
 }
 
 __global__ void greedy_serve_kernel(const ServeParams p) {
@@ -33,7 +39,7 @@ __global__ void greedy_serve_kernel(const ServeParams p) {
   if (i >= p.nR * p.S) return;
   const int r = i / p.S;
   const uint32_t v = (uint32_t)(i % p.S) + 1u;
-  const double rate = p.rates[r];
+  const int64_t* arr = p.arrival + (int64_t)r * p.N;  // this rate's arrival times
   int64_t cb[kMaxB];
   int bmax = 0, bmin = 1 << 30;
   for (int bi = 0; bi < p.nB; ++bi) {
@@ -48,32 +54,44 @@ __global__ void greedy_serve_kernel(const ServeParams p) {
   int64_t t = 0, head = 0, tail = 0;
   const int64_t N = p.N;
   while (head < N) {
-    while (tail < N && arrival_ns(p.arrival, tail, rate) <= t) ++tail;
+    while (tail < N) {  // arrivals up to t: 8 independent loads per step (sorted, so the count is the advance)
+      int adv = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) adv += (tail + i < N && arr[tail + i] <= t) ? 1 : 0;
+      tail += adv;
+      if (adv < 8) break;
+    }
     const int64_t qlen = tail - head;
     int bsel = 0;
     int64_t c = 0;
     for (int bi = 0; bi < p.nB; ++bi)
       if (p.B[bi] <= qlen && p.B[bi] > bsel) { bsel = p.B[bi]; c = cb[bi]; }
     int b = 0;
-    const int64_t t0 = head < N ? arrival_ns(p.arrival, head, rate) : 0;
+    const int64_t t0 = head < N ? arr[head] : 0;
     if (qlen >= bmax) b = bmax;
     else if (bsel > 0 && c + (t - t0) + p.delta >= p.tau) b = bsel;
     if (b > 0) {
       const int64_t done = t + c;
+#pragma unroll 8
       for (int64_t s = head; s < head + b; ++s) {
-        const int64_t l = done - arrival_ns(p.arrival, s, rate);
+        const int64_t l = done - arr[s];
         ++served;
         if (l > p.tau) { ++overdue; exceed += (unsigned long long)(l - p.tau); }
       }
       ++batches;
       head += b;
       t = done;
-    } else if (tail == N) {
-      if (bsel == 0) { unserved = (unsigned long long)qlen; break; }
-      t = t0 + p.tau - p.delta - c;
     } else {
-      int64_t tn = arrival_ns(p.arrival, tail, rate);
+      // wait: the decision can only change when the queue reaches the next batch size above len(q)
+      // or when c(v,b) + w(q0) + delta reaches tau for the current b -- jump to the earlier of the two
+      // (equivalent to re-evaluating at every arrival, as the oracle does)
+      int bnext = 0x7fffffff;
+      for (int bi = 0; bi < p.nB; ++bi)
+        if (p.B[bi] > qlen && p.B[bi] < bnext) bnext = p.B[bi];
+      int64_t tn = INT64_MAX;
+      if (bnext != 0x7fffffff && head + bnext - 1 < N) tn = arr[head + bnext - 1];
       if (bsel > 0) tn = min(tn, t0 + p.tau - p.delta - c);
+      if (tn == INT64_MAX) { unserved = (unsigned long long)(N - head); break; }  // never reaches min B
       t = tn;
     }
   }
@@ -88,6 +106,13 @@ __global__ void greedy_serve_kernel(const ServeParams p) {
 }
 
 }  // namespace
+
+cudaError_t launch_arrival_fill(const ServeParams& p, int64_t* out, cudaStream_t st) {
+  const int64_t n = p.N * p.nR;
+  if (n <= 0) return cudaSuccess;
+  arrival_fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, p.N, p.nR, p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_greedy_serve(const ServeParams& p, cudaStream_t st) {
   const int n = p.nR * p.S;
