@@ -84,7 +84,7 @@ __global__ void greedy_serve_kernel(const ServeParams p) {
     } else {
       // wait: the decision can only change when the queue reaches the next batch size above len(q)
       // or when c(v,b) + w(q0) + delta reaches tau for the current b -- jump to the earlier of the two
-      // (equivalent to re-evaluating at every arrival, as the oracle does)
+      // (equivalent to re-evaluating the rule at every arrival, reading S1)
       int bnext = 0x7fffffff;
       for (int bi = 0; bi < p.nB; ++bi)
         if (p.B[bi] > qlen && p.B[bi] < bnext) bnext = p.B[bi];
