@@ -77,7 +77,8 @@ rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16,
 /* A1+A2: run the K heads on N feature rows. X_bf16: [N][D] bfloat16 bits, host or device.
  * global_offset = index of row 0 in the global request stream (fixes batch ids and arrival
  * times). Produces the context's logits workspace [N][K][ldc] fp32 (ldc = C rounded up to 4),
- * per-(row, model) top-1 and log-sum-exp, fused in the GEMM epilogue. */
+ * per-(row, model) top-1 and log-sum-exp, fused in the GEMM epilogue. N < 2^31 per call
+ * (larger streams go in chunks; RK_EINVAL otherwise). */
 rk_status rk_score(rk_ctx* ctx, const void* X_bf16, int64_t N, int64_t global_offset, void* stream);
 
 /* Vote-stage entry on caller-provided logits: [N][K][ldc] fp32 DEVICE memory, ldc % 4 == 0,

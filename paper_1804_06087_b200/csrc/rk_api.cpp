@@ -313,6 +313,7 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
   if (!ctx) return RK_EINVAL;
   if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
   if (N < 0 || goff < 0 || (N > 0 && !X)) return fail(ctx, RK_EINVAL, "bad X / N / offset");
+  if (N > INT32_MAX) return fail(ctx, RK_EINVAL, "N per call must be < 2^31 (stream larger sets in chunks)");
   CK(cudaSetDevice(ctx->dev));
   cudaStream_t st = (cudaStream_t)stream;
   rk_status s;
@@ -376,6 +377,7 @@ rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, 
   if (!ctx) return RK_EINVAL;
   if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
   if (N < 0 || goff < 0 || ldc < ctx->C || ldc % 4 != 0) return fail(ctx, RK_EINVAL, "bad ldc / N / offset (ldc % 4 == 0, ldc >= C)");
+  if (N > INT32_MAX) return fail(ctx, RK_EINVAL, "N per call must be < 2^31 (stream larger sets in chunks)");
   if (N > 0 && (!logits || (reinterpret_cast<uintptr_t>(logits) & 15))) return fail(ctx, RK_EINVAL, "logits must be 16-byte aligned");
   if (N > 0 && !is_device_ptr(logits)) return fail(ctx, RK_EINVAL, "logits must be device memory");
   ctx->cur_logits = logits;
