@@ -46,6 +46,8 @@ CASES = [  # (K, C, N, seed)
     (9, 50, 300, 8),      # K = 9..11: every word count of the bit-sliced vote (16..64 words)
     (10, 20, 200, 9),
     (11, 100, 150, 10),
+    (12, 1000, 40, 15),   # K = 12 with C = 1000: rows do not fit twice, single-buffered CTA kernel
+    (10, 1024, 50, 16),   # the largest C of this build
     (1, 2, 33, 6),        # degenerate: one model, two classes
     (5, 37, 517, 7),      # odd sizes, ragged everything
 ]
