@@ -190,6 +190,10 @@ __global__ void merge_kernel(const MergeParams p, int64_t N, int64_t off_N) {
 // accumulators [NRP][b], spilled to u64 shared accumulators every `flush` chunks (no u32 overflow:
 // a chunk adds at most L * max(B)); one atomic per (v, r, b) per block.
 constexpr int QT = 128;
+#ifndef RK_QG
+#define RK_QG 8
+#endif
+constexpr int QG = RK_QG;  // group counts loaded ahead per thread
 constexpr int kQStageBytes = 32 * 1024;
 constexpr int kQBlocksPerSM = 6;  // STAGED: the chunk's o values staged in shared memory
 template <int NRP>
@@ -259,26 +263,32 @@ __global__ void __launch_bounds__(QT, kQBlocksPerSM)
 #pragma unroll
     for (int bi = 0; bi < NBX; ++bi) { lj[bi] = qc.bg[bi]; part[bi] = 0; }
     const int64_t ga = q * gpc, gb = min(ngroups, ga + gpc);
-#pragma unroll 4
-    for (int64_t g = ga; g < gb; ++g) {
-      const unsigned int c = gp[g * p.S];
+    for (int64_t g0 = ga; g0 < gb; g0 += QG) {
+      unsigned int cc[QG];  // QG independent loads in flight before the dependent batch bookkeeping
 #pragma unroll
-      for (int bi = 0; bi < NBX; ++bi) {
-        if (NB == 0 && bi >= nB) break;
-        part[bi] += c;
-        if (((--lj[bi]) & 0xFFFF) == 0) {  // end of batch (lj >> 16) of size B[bi] in this chunk
-          const int jj = lj[bi] >> 16;
-          const int m = (mpack >> (4 * bi)) & 15;
-          if (part[bi] && (STAGED || q * qc.nbc[bi] + jj < qc.nbat[bi])) {
-            const uint16_t* ob = STAGED ? so + (qc.soff[bi] + jj) * KR
-                                        : p.ovd + p.ovd_off[bi] + (q * qc.nbc[bi] + jj) * KR;
-            union { V v; uint16_t h[NRP]; } o;
-            o.v = *reinterpret_cast<const V*>(ob + m * NRP);
+      for (int i = 0; i < QG; ++i) cc[i] = g0 + i < gb ? gp[(g0 + i) * p.S] : 0u;
 #pragma unroll
-            for (int r = 0; r < NRP; ++r) acc[r][bi] += part[bi] * o.h[r];
+      for (int i = 0; i < QG; ++i) {
+        if (g0 + i >= gb) break;
+        const unsigned int c = cc[i];
+#pragma unroll
+        for (int bi = 0; bi < NBX; ++bi) {
+          if (NB == 0 && bi >= nB) break;
+          part[bi] += c;
+          if (((--lj[bi]) & 0xFFFF) == 0) {  // end of batch (lj >> 16) of size B[bi] in this chunk
+            const int jj = lj[bi] >> 16;
+            const int m = (mpack >> (4 * bi)) & 15;
+            if (part[bi] && (STAGED || q * qc.nbc[bi] + jj < qc.nbat[bi])) {
+              const uint16_t* ob = STAGED ? so + (qc.soff[bi] + jj) * KR
+                                          : p.ovd + p.ovd_off[bi] + (q * qc.nbc[bi] + jj) * KR;
+              union { V v; uint16_t h[NRP]; } o;
+              o.v = *reinterpret_cast<const V*>(ob + m * NRP);
+#pragma unroll
+              for (int r = 0; r < NRP; ++r) acc[r][bi] += part[bi] * o.h[r];
+            }
+            part[bi] = 0;
+            lj[bi] += (1 << 16) + qc.bg[bi];
           }
-          part[bi] = 0;
-          lj[bi] += (1 << 16) + qc.bg[bi];
         }
       }
     }
