@@ -55,10 +55,11 @@ typedef enum {
   RK_TIE_LOWEST_CLASS = 1 /* north_star: lowest class index among the tied classes              */
 } rk_tie_mode;
 
-/* Create a context on `cuda_device`. world == 1: nccl_unique_id may be NULL. world > 1: every
- * rank passes the same 128-byte ncclUniqueId (from rk_nccl_unique_id on rank 0, broadcast by
- * the caller, e.g. through torch.distributed) and its rank; the table all-reduce (A6) then
- * runs over NCCL (NVLink/NVSwitch). */
+/* Create a context on `cuda_device`. world > 1: every rank passes the same 128-byte
+ * ncclUniqueId (from rk_nccl_unique_id on rank 0, broadcast by the caller, e.g. through
+ * torch.distributed) and its rank; the table all-reduce (A6) then runs over NCCL (NVLink /
+ * NVSwitch). world == 1: nccl_unique_id may be NULL (no communicator); a non-NULL id creates a
+ * one-rank communicator and runs the same all-reduce code path (used by the tests). */
 rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, int rank, int world);
 /* Fill `out128` with a fresh ncclUniqueId (rank 0 only). */
 rk_status rk_nccl_unique_id(void* out128);

@@ -219,7 +219,7 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
   if (e != cudaSuccess) { delete ctx; return RK_ECUDA; }
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
   if (const char* gc = getenv("RK_GEMM_CLUSTER")) ctx->gemm_cluster = atoi(gc) == 1 ? 1 : 2;
-  if (world > 1) {
+  if (nccl_unique_id) {  // world ranks (world may be 1: a one-rank communicator, same code path)
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
     if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) { delete ctx; return RK_ENCCL; }
@@ -688,7 +688,7 @@ rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int S = ctx->S, nB = ctx->nB, nR = ctx->nR;
   // A6: one all-reduce of the whole integer table (order-free, bit-exact)
-  if (ctx->world > 1) {
+  if (ctx->comm) {
     ProfScope ps(ctx, KK_ALLREDUCE, st, (double)ctx->table_words * 8, 0);
     if (ncclAllReduce(ctx->d_table, ctx->d_table, ctx->table_words, ncclUint64, ncclSum, ctx->comm, st) != ncclSuccess)
       return fail(ctx, RK_ENCCL, "ncclAllReduce failed");

@@ -260,3 +260,23 @@ def test_queue_mode_chunks_and_shards(rk):
     with pytest.raises(rk.RkError) as e:
         c3.subset_stats(dev(y[512:]), acfg)
     assert e.value.status == 8  # RK_EUNSUPPORTED
+
+
+def test_nccl_path_single_rank(rk):
+    """A6 over NCCL with a one-rank communicator: the all-reduce code path runs (profiled launch) and
+    the table equals the communicator-free one (this environment exposes one GPU per call)."""
+    K, C, N = 5, 100, 768
+    y = gen.labels(41, 0, N, C)
+    L = gen.logits(41, 0, N, K, C, y=y)
+    gcfg, ocfg = default_cfg(K)
+    t0, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    c = rk.Context(0, 0, 1, rk.nccl_unique_id())
+    c.load_ensemble(K, C)
+    dl = dev(L)
+    c.score_logits(dl, L.shape[2], N)
+    c.set_profiling(True)
+    t1 = c.subset_stats(dev(y), gcfg)
+    assert c.kernel_stats()["nccl_allreduce"]["launches"] == 1
+    for k in ("cnt_vote", "cnt_avg", "corr", "O", "Q", "E", "reward_sur", "reward_lab"):
+        np.testing.assert_array_equal(t1[k], t0[k], err_msg=k)
+    compare_tables(t1, oracle.table(L, y, K, C, cfg=ocfg), K=K)
