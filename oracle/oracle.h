@@ -11,9 +11,11 @@
  * passages are the SURVEY.md §8(c) Q-readings, listed in DESIGN.md.
  *
  * Pins (tests/test_oracle_*.py, tests/golden/): hand-computed examples W1-W4,
- * invariants I1-I8, reward examples R1-R5, brute force against an
- * independently written pairwise formulation, library pins (numpy argmax/bincount,
- * torch.softmax). Parity unpinned: the paper's Fig. `fig:ensemble` values (images only).
+ * invariants I1-I8, reward examples R1-R5, R6 (queue-aware latency,
+ * reading Q15) and S1 (Algorithm 3 greedy batching, reading S1) worked by hand, brute force
+ * against an independently written pairwise formulation, library pins (numpy
+ * argmax/bincount, torch.softmax). Parity unpinned: the paper's Fig. `fig:ensemble` values
+ * (images only).
  */
 #ifndef RK_ORACLE_H
 #define RK_ORACLE_H
