@@ -124,6 +124,12 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2 (what __expf uses after its multiply)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kL2E = 1.4426950408889634f;
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -294,20 +300,21 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
           const float4 b4 = __ldg(bptr + i4);  // -inf on padding columns
           const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int i = 4 * i4 + e;
-            v[i] = fmaf(v[i], scale, bb[e]);
-            if (v[i] > cmax) { cmax = v[i]; carg = cm + i; }
-          }
+          for (int e = 0; e < 4; ++e) v[4 * i4 + e] = fmaf(v[4 * i4 + e], scale, bb[e]);
         }
-        if (cmax > mx) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cmax = fmaxf(cmax, v[i]);
+        if (cmax > mx) {  // new running max of this model: its lowest column (Q4)
+#pragma unroll
+          for (int i = 15; i >= 0; --i) carg = v[i] == cmax ? cm + i : carg;
           sum = sum * __expf(mx - cmax);
           mx = cmax;
           arg = carg;
         }
         if (mx != -INFINITY) {
+          const float nml = -mx * kL2E;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) sum += __expf(v[i] - mx);
+          for (int i = 0; i < 16; ++i) sum += ex2_approx(fmaf(v[i], kL2E, nml));
         }
         uint8_t* buf = stg + (nstore & 1) * SBOX;
         if (lane == 0 && nstore >= 2) tma_store_wait_read1();
@@ -499,20 +506,21 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
                                                       : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = 4 * i4 + e;
-              v[i] = fmaf(v[i], scale, bb[e]);  // scale is a power of two: exact product, one rounding
-              if (v[i] > cmax) { cmax = v[i]; carg = colbase + i; }
-            }
+            for (int e = 0; e < 4; ++e) v[4 * i4 + e] = fmaf(v[4 * i4 + e], scale, bb[e]);  // exact product, one rounding
           }
-          if (cmax > mx) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cmax = fmaxf(cmax, v[i]);
+          if (cmax > mx) {  // new running max (rare after the first chunks): its lowest column (Q4)
+#pragma unroll
+            for (int i = 31; i >= 0; --i) carg = v[i] == cmax ? colbase + i : carg;
             sum = sum * __expf(mx - cmax);
             mx = cmax;
             arg = carg;
           }
           if (mx != -INFINITY) {
+            const float nml = -mx * kL2E;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sum += __expf(v[i] - mx);
+            for (int i = 0; i < 32; ++i) sum += ex2_approx(fmaf(v[i], kL2E, nml));
           }
           // stage 32 rows x 32 cols (128B-swizzled) and store with TMA. (Coalesced st.global.cs
           // from the same staging box measured 18% slower for the whole kernel: DESIGN.md §6.)
