@@ -284,12 +284,12 @@ def main():
     vote_bytes = v["bytes"] / max(1, v["launches"])
     gemm_tfs = gemm_flops / (gemm_ms / 1e3) / 1e12
     vote_gbs = vote_bytes / (vote_ms / 1e3) / 1e9
-    # Denominator by clock regime: the sustained cuBLAS figure was measured at ~1.34 GHz under the
-    # power cap; a step whose SM clock stays near max (the GEMM alternates with memory-bound vote
-    # kernels) is in the burst regime, so it is held to the burst figure.
-    burst = bool(clk.get("sm_mhz")) and clk["sm_mhz"] >= 0.9 * (clk.get("sm_max_mhz") or 1965.0)
-    peak_key = "bf16_tflops" if burst else "bf16_tflops_sustained"
-    peak_t = peaks.get(peak_key, peaks.get("bf16_tflops"))
+    # Denominator: the measured BURST cuBLAS bf16 figure, always. The sustained one was measured over a
+    # 4 s back-to-back loop at ~1.34 GHz under the power cap; a bench step alternates tensor-bound and
+    # memory-bound kernels and its timed region is far shorter, so the clock stays well above that
+    # regime (see `clocks`). The burst figure is the larger, i.e. conservative, denominator.
+    peak_key = "bf16_tflops"
+    peak_t = peaks.get(peak_key, peaks.get("bf16_tflops_sustained"))
     traffic = vtraffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):  # ncu dram bytes per launch of this workload (scripts/summarize_profiles.py)
@@ -306,8 +306,7 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "gemm_heads_tcgen05", "achieved": gemm_tfs,
                      "peak": peak_t, "unit": "TFLOP/s", "frac": gemm_tfs / peak_t, "traffic": traffic,
                      "share_of_step": gemm_ms / ms_step,
-                     "peak_source": f"{peak_src} {peak_key} (" + ("SM clock stayed >= 90% of max in the timed "
-                                    "region: burst regime" if burst else "kernel timed inside a long step") + ")",
+                     "peak_source": f"{peak_src} {peak_key} (burst cuBLAS bf16; conservative, see DESIGN.md §9)",
                      "algorithmic": "2*D*K*C flop per sample"},
         "vote_stage": {"bound": "hbm", "kernel": "vote_subsets", "achieved": vote_gbs, "peak": peaks["hbm_gbs"],
                        "unit": "GB/s", "frac": vote_gbs / peaks["hbm_gbs"], "traffic": vtraffic,
