@@ -58,7 +58,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 struct Lay {  // dynamic shared memory layout
-  size_t rows, tab, pm, pend, total;
+  size_t rows, tab, pm, pend, cnt, total;
   int nbuf;
 };
 __host__ __device__ inline Lay layout(const VoteParams& p) {
@@ -70,7 +70,8 @@ __host__ __device__ inline Lay layout(const VoteParams& p) {
   L.tab = L.rows + L.nbuf * rowbytes;
   L.pm = L.tab + a128((size_t)TT * JS * 4);
   L.pend = L.pm + a128((size_t)p.K * JS * 4);
-  L.total = L.pend + a128((size_t)(p.S + 1) * 2);
+  L.cnt = L.pend + a128((size_t)(p.S + 1) * 2);
+  L.total = L.cnt + a128((size_t)((p.S + CT) / CT) * CT * 4);
   return L;
 }
 
@@ -109,58 +110,51 @@ __device__ __forceinline__ void load_stat(const VoteParams& p, const int32_t* wo
 // S6 for the subsets v = t + 256k of this thread. Because 2^K1 divides 256, the low half a = v mod 2^K1
 // is the same for all k: its table row stays in registers (NQ float4 column groups; NQ = 0: runtime
 // count, row re-read). The high half b = v >> K1 is uniform across a warp (K1 <= 5) or shared by
-// groups of lanes, so its row is a broadcast read.
+// groups of lanes, so its row is a broadcast read. Branch-free: bit k of okm = subset t + 256k clearly
+// won by y, bit k of pm = near-tie (fp64 recheck); singletons and invalid slots are fixed by the caller.
 template <int NSUB, int NQ>
-__device__ __forceinline__ void decide_subsets(const VoteParams& p, const float* TA, const float* TB, const Stat& st,
-                                               int y, uint32_t (&ca)[NSUB], int& npend, uint16_t* pend,
-                                               int nq_rt = 0) {
+__device__ __forceinline__ void decide_subsets(const VoteParams& p, const float* TA, const float* TB, uint32_t& okm,
+                                               uint32_t& pm, int nq_rt = 0) {
   const int t = threadIdx.x;
-  const int K1 = p.K1, TAn = 1 << K1, S = p.S;
+  const int K1 = p.K1, TAn = 1 << K1;
   const uint32_t a = (uint32_t)t & (uint32_t)(TAn - 1);
   const float4* A = reinterpret_cast<const float4*>(TA + a * JS);
+  const float bh = 1.f + p.band, bl = 1.f - p.band;
   float4 ar[NQ > 0 ? NQ : 1];
 #pragma unroll
   for (int q = 0; q < (NQ > 0 ? NQ : 1); ++q) ar[q] = A[q];
+  const float4* B0 = reinterpret_cast<const float4*>(TB + (t >> K1) * JS);
+  const int bstep = (CT >> K1) * (JS / 4);  // float4 stride of b between k and k + 1
+  uint32_t w = 0, n = 0;
 #pragma unroll
   for (int k = 0; k < NSUB; ++k) {
-    const uint32_t v = (uint32_t)(t + CT * k);
-    if (v == 0 || v > (uint32_t)S) continue;
-    uint32_t ok = 0;
-    if (__popc(v) == 1) {
-      ok = st.top[__ffs(v) - 1] == y;  // softmax is monotone (invariant I1)
-    } else {
-      const float4* B = reinterpret_cast<const float4*>(TB + (v >> K1) * JS);
-      float4 b4 = B[0];
-      const float sy = ar[0].x + b4.x;
-      float mc = fmaxf(ar[0].y + b4.y, fmaxf(ar[0].z + b4.z, ar[0].w + b4.w));
-      if (NQ > 0) {
+    const float4* B = B0 + k * bstep;
+    float4 b4 = B[0];
+    const float sy = ar[0].x + b4.x;
+    float mc = fmaxf(ar[0].y + b4.y, fmaxf(ar[0].z + b4.z, ar[0].w + b4.w));
+    if (NQ > 0) {
 #pragma unroll
-        for (int q = 1; q < NQ; ++q) {
-          b4 = B[q];
-          mc = fmaxf(mc, fmaxf(fmaxf(ar[q].x + b4.x, ar[q].y + b4.y), fmaxf(ar[q].z + b4.z, ar[q].w + b4.w)));
-        }
-      } else {
-        for (int q = 1; q < nq_rt; ++q) {
-          const float4 a4 = A[q];
-          b4 = B[q];
-          mc = fmaxf(mc, fmaxf(fmaxf(a4.x + b4.x, a4.y + b4.y), fmaxf(a4.z + b4.z, a4.w + b4.w)));
-        }
+      for (int q = 1; q < NQ; ++q) {
+        b4 = B[q];
+        mc = fmaxf(mc, fmaxf(fmaxf(ar[q].x + b4.x, ar[q].y + b4.y), fmaxf(ar[q].z + b4.z, ar[q].w + b4.w)));
       }
-      bool beat, near;
-      if (sy >= 1e-30f) {  // positive sums: relative error << band
-        beat = mc > sy * (1.f + p.band);
-        near = mc >= sy * (1.f - p.band);
-      } else {  // y's sum is (nearly) subnormal: only a clearly larger competitor is decisive
-        beat = mc > 2e-30f;
-        near = !beat;
-      }
-      if (!beat) {
-        if (near) pend[atomicAdd(&npend, 1)] = (uint16_t)v;
-        else ok = 1;
+    } else {
+      for (int q = 1; q < nq_rt; ++q) {
+        const float4 a4 = A[q];
+        b4 = B[q];
+        mc = fmaxf(mc, fmaxf(fmaxf(a4.x + b4.x, a4.y + b4.y), fmaxf(a4.z + b4.z, a4.w + b4.w)));
       }
     }
-    ca[k] += ok;
+    // positive sums: relative error << band; y's sum (nearly) subnormal: only a clearly larger
+    // competitor is decisive, everything else is rechecked
+    const bool pos = sy >= 1e-30f;
+    const bool beat = pos ? mc > sy * bh : mc > 2e-30f;
+    const bool near = pos ? mc >= sy * bl : true;
+    w |= (uint32_t)(!near) << k;
+    n |= (uint32_t)(near && !beat) << k;
   }
+  okm = w;
+  pm = n;
 }
 
 template <int NSUB>
@@ -198,9 +192,30 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
   if (warp == 0 && (int64_t)blockIdx.x < W) load_stat(p, work, blockIdx.x, sh.st[0], lane);
   __syncthreads();  // the first sample's statistics
 
-  uint32_t ca[NSUB];
+  uint32_t* ca = reinterpret_cast<uint32_t*>(dyn + L.cnt);  // ca[t + CT*k]: this thread's subsets only
 #pragma unroll
-  for (int k = 0; k < NSUB; ++k) ca[k] = 0;
+  for (int k = 0; k < NSUB; ++k) ca[t + CT * k] = 0;
+  // per-sample decision words (bit k <-> subset t + 256k) accumulate in a 6-plane vertical counter,
+  // folded into ca every 63 samples
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
+  int nadd = 0;
+  uint32_t validm = 0, singm = 0;  // slots k holding a subset 1..S; singleton subsets (handled apart)
+#pragma unroll
+  for (int k = 0; k < NSUB; ++k) {
+    const uint32_t v = (uint32_t)(t + CT * k);
+    const bool valid = v >= 1 && v <= (uint32_t)S;
+    validm |= (uint32_t)valid << k;
+    singm |= (uint32_t)(valid && __popc(v) == 1) << k;
+  }
+  validm &= ~singm;
+  auto fold = [&]() {
+#pragma unroll
+    for (int k = 0; k < NSUB; ++k)
+      ca[t + CT * k] += ((c0 >> k) & 1u) | (((c1 >> k) & 1u) << 1) | (((c2 >> k) & 1u) << 2) | (((c3 >> k) & 1u) << 3) |
+               (((c4 >> k) & 1u) << 4) | (((c5 >> k) & 1u) << 5);
+    c0 = c1 = c2 = c3 = c4 = c5 = 0;
+    nadd = 0;
+  };
 
   int64_t it = 0;
   for (int64_t e = blockIdx.x; e < W; e += gridDim.x, ++it) {
@@ -288,16 +303,32 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       }
       __syncthreads();
       // ---- S6: every subset: sum of y's column and the largest competitor, branch-free ----------
-      if (nq <= 5) {
-        switch (nq) {
-          case 1: decide_subsets<NSUB, 1>(p, TA, TB, st, y, ca, sh.npend, pend); break;
-          case 2: decide_subsets<NSUB, 2>(p, TA, TB, st, y, ca, sh.npend, pend); break;
-          case 3: decide_subsets<NSUB, 3>(p, TA, TB, st, y, ca, sh.npend, pend); break;
-          case 4: decide_subsets<NSUB, 4>(p, TA, TB, st, y, ca, sh.npend, pend); break;
-          default: decide_subsets<NSUB, 5>(p, TA, TB, st, y, ca, sh.npend, pend); break;
-        }
-      } else {
-        decide_subsets<NSUB, 0>(p, TA, TB, st, y, ca, sh.npend, pend, nq);
+      uint32_t okm, pm;
+      switch (nq) {
+        case 1: decide_subsets<NSUB, 1>(p, TA, TB, okm, pm); break;
+        case 2: decide_subsets<NSUB, 2>(p, TA, TB, okm, pm); break;
+        case 3: decide_subsets<NSUB, 3>(p, TA, TB, okm, pm); break;
+        case 4: decide_subsets<NSUB, 4>(p, TA, TB, okm, pm); break;
+        default: decide_subsets<NSUB, 0>(p, TA, TB, okm, pm, nq); break;
+      }
+      okm &= validm;
+      pm &= validm;
+      for (uint32_t sm = singm; sm; sm &= sm - 1) {  // singletons: softmax is monotone (invariant I1)
+        const int k = __ffs(sm) - 1;
+        const uint32_t v = (uint32_t)(t + CT * k);
+        okm |= (uint32_t)(st.top[__ffs(v) - 1] == y) << k;
+      }
+      for (uint32_t q = pm; q; q &= q - 1)  // rare: near-ties to the fp64 recheck
+        pend[atomicAdd(&sh.npend, 1)] = (uint16_t)(t + CT * (__ffs(q) - 1));
+      {
+        uint32_t c = okm, x;
+        x = c0 & c; c0 ^= c; c = x;
+        x = c1 & c; c1 ^= c; c = x;
+        x = c2 & c; c2 ^= c; c = x;
+        x = c3 & c; c3 ^= c; c = x;
+        x = c4 & c; c4 ^= c; c = x;
+        c5 ^= c;
+        if (++nadd == 63) fold();
       }
       __syncthreads();
       // ---- S7 (rare): fp64 recheck of the pending subsets from the rows in shared memory --------
@@ -344,10 +375,11 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       if (L.nbuf == 1 && e + gridDim.x < W) issue(e + gridDim.x, 0);
     }
   }
+  fold();
 #pragma unroll
   for (int k = 0; k < NSUB; ++k) {
     const int v1 = t + CT * k - 1;
-    if (v1 >= 0 && v1 < S && ca[k]) atomicAdd(p.cnt_avg + v1, (unsigned long long)ca[k]);
+    if (v1 >= 0 && v1 < S && ca[t + CT * k]) atomicAdd(p.cnt_avg + v1, (unsigned long long)ca[t + CT * k]);
   }
 }
 
