@@ -64,6 +64,7 @@ struct rk_ctx {
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[4 * 128];
+  int cta_cols = 52;                   // K >= 9 CTA averaging: column capacity (env RK_CTA_AVG_COLS, tests)
   int gemm_cluster = 2;                // head GEMM: 2 = CTA pair (tcgen05 cta_group::2, M = 256), 1 = single CTA (env RK_GEMM_CLUSTER)
   cudaStream_t copy_stream = nullptr;  // H2D of host X, overlapped with the GEMM
   cudaEvent_t ev_start = nullptr;
@@ -219,6 +220,9 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
   if (e != cudaSuccess) { delete ctx; return RK_ECUDA; }
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
   if (const char* gc = getenv("RK_GEMM_CLUSTER")) ctx->gemm_cluster = atoi(gc) == 1 ? 1 : 2;
+  // tests only: a smaller column capacity of the K >= 9 CTA averaging kernel routes more samples through
+  // the overflow kernel (rk_vote_batch_avg.cu), so both paths stay covered
+  if (const char* cc = getenv("RK_CTA_AVG_COLS")) ctx->cta_cols = std::max(4, std::min(52, atoi(cc) / 4 * 4));
   if (nccl_unique_id) {  // world ranks (world may be 1: a one-rank communicator, same code path)
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
@@ -534,6 +538,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     vp.CAP = warp_path ? 96 : 64;
     vp.TCAP = warp_path ? std::min(vp.CAP, (int)(6272 / (4 * TT))) : std::min(vp.CAP, (int)(16384 / (4 * TT)) - 1);
     vp.band = 2e-5f;
+    vp.cta_cols = ctx->cta_cols;
     vp.best_of = ctx->d_best_of;
     vp.nB = nB;
     for (int bi = 0; bi < nB; ++bi) vp.tail_start[bi] = (N / ctx->B[bi]) * ctx->B[bi];

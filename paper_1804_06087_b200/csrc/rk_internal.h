@@ -30,6 +30,7 @@ struct VoteParams {
   int TCAP;                  // candidate capacity of the subset-sum tables in smem
   int K1;                    // low half of the models for the subset-sum tables
   float band;                // relative fp32 near-tie band -> fp64 recheck
+  int cta_cols;              // K >= 9: most table columns (y + competitors) of the CTA averaging kernel
   const uint8_t* best_of;    // [2^K] best-ranked model in a mask (device)
   int nB;
   int64_t tail_start[kMaxB]; // local sample index from which a sample is in the tail of B[b]
@@ -42,7 +43,7 @@ struct VoteParams {
   float* scratch;                 // per-CTA overflow P [gridDim][G][C][K]
   int32_t* scratch_cls;           // per-CTA overflow class list [gridDim][G][C]
   unsigned int* err;              // [0] non-finite logits, [1] bad label
-  int32_t* ovf_work;              // K >= 9: worklist samples with |R| > 32 (rk_vote_cta_avg.cu) [N]
+  int32_t* ovf_work;              // K >= 9: worklist samples whose columns exceed cta_cols (rk_vote_cta_avg.cu) [N]
   unsigned int* ovf_count;
 };
 

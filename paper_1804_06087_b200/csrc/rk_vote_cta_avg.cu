@@ -15,7 +15,7 @@
 // sm_100a layout: the K logit rows of a sample are contiguous ([N][K][ldc]); the CTA fetches them with
 // one cp.async.bulk (TMA, mbarrier complete_tx), prefetching the next sample while it decides the
 // current one (double buffer when two copies fit). 256 threads: thread t decides subsets t + 256k.
-// Samples whose columns do not fit 36 slots are appended to an overflow worklist for rk_vote_batch_avg.cu.
+// Samples whose columns do not fit p.cta_cols (<= JS) slots are appended to an overflow worklist for rk_vote_batch_avg.cu.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -28,8 +28,8 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int CT = 256;            // threads per CTA
 constexpr int CW = CT / 32;
-constexpr int JS = 36;             // table columns: y + up to 35 competitors, padded to float4; 144 B rows:
-                                   // 128-bit loads from 8 distinct rows hit distinct bank groups
+constexpr int JS = 52;             // table columns: y + up to 51 competitors, padded to float4; 208 B rows
+                                   // (13 x 16 B, odd): 128-bit loads from 8 distinct rows hit distinct bank groups
 constexpr int KM = 12;
 
 __host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       }
       const int nr = __shfl_sync(FULL, incl, 31);
       const int nq = (nr + 1 + 3) >> 2;
-      const bool fits = 4 * nq <= JS;
+      const bool fits = 4 * nq <= p.cta_cols;
       if (fits) {
         if (lane < 4) sh.cols[4 * nq - 4 + lane] = -1;
         __syncwarp();

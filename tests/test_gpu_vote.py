@@ -95,6 +95,21 @@ def test_overflow_candidates_all_equal_rows(rk, K):
     compare_tables(t, o, K=K, check_moments=False)
 
 
+@pytest.mark.parametrize("cols", [4, 8])
+def test_cta_average_overflow_route(rk, monkeypatch, cols):
+    """K >= 9: samples whose table columns exceed the CTA averaging kernel's capacity go to the batch
+    averaging kernel; a small capacity (RK_CTA_AVG_COLS, read at context creation) routes most worklist
+    samples there on the c5 shape, so both kernels are held to the oracle on the same data."""
+    K, C, N, seed = 12, 100, 120, 25
+    monkeypatch.setenv("RK_CTA_AVG_COLS", str(cols))
+    y = gen.labels(seed, 0, N, C)
+    L = gen.logits(seed, 0, N, K, C, y=y)
+    gcfg, ocfg = default_cfg(K)
+    t, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    compare_tables(t, o, K=K)
+
+
 def test_chunked_and_sharded_equal_one_shot(rk):
     """Streaming chunks (multiples of lcm(B)) and disjoint shards sum to the one-shot table (I7, P5)."""
     K, C, N = 4, 100, 1000
