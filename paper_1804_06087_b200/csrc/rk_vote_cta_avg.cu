@@ -87,7 +87,7 @@ struct Shared {  // static shared state
   int32_t cols[JS];  // 0 = y, 1..nr = R ascending, -1 = unused
   Stat st[2];
   double lse64[KM];
-  int32_t nq, npend, skip;
+  int32_t nq, npend, skip, tiny;
 };
 
 // warp 0: labels, top-1, log-sum-exp, row max of worklist entry e; θ threshold per model
@@ -112,9 +112,28 @@ __device__ __forceinline__ void load_stat(const VoteParams& p, const int32_t* wo
 // count, row re-read). The high half b = v >> K1 is uniform across a warp (K1 <= 5) or shared by
 // groups of lanes, so its row is a broadcast read. Branch-free: bit k of okm = subset t + 256k clearly
 // won by y, bit k of pm = near-tie (fp64 recheck); singletons and invalid slots are fixed by the caller.
+__device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3 (sm_100)
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// one float4 column group of the row pair: y's sum (group 0 only) and the running competitor max; the
+// four sums as two packed FADD2 (sm_100 add.rn.f32x2), the max as FMNMX3
+__device__ __forceinline__ void group_sum(const float4& a, const float4& b, float& sy, float& mc, bool first) {
+  const float2 s01 = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+  const float2 s23 = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
+  if (first) {
+    sy = s01.x;
+    mc = max3f(s01.y, s23.x, s23.y);
+  } else {
+    mc = max3f(mc, s01.x, s01.y);
+    mc = max3f(mc, s23.x, s23.y);
+  }
+}
+
 template <int NSUB, int NQ>
 __device__ __forceinline__ void decide_subsets(const VoteParams& p, const float* TA, const float* TB, uint32_t& okm,
-                                               uint32_t& pm, int nq_rt = 0) {
+                                               uint32_t& pm, int nq_rt = 0, bool tiny = false) {
   const int t = threadIdx.x;
   const int K1 = p.K1, TAn = 1 << K1;
   const uint32_t a = (uint32_t)t & (uint32_t)(TAn - 1);
@@ -129,32 +148,27 @@ __device__ __forceinline__ void decide_subsets(const VoteParams& p, const float*
 #pragma unroll
   for (int k = 0; k < NSUB; ++k) {
     const float4* B = B0 + k * bstep;
-    float4 b4 = B[0];
-    const float sy = ar[0].x + b4.x;
-    float mc = fmaxf(ar[0].y + b4.y, fmaxf(ar[0].z + b4.z, ar[0].w + b4.w));
+    float sy, mc;
+    group_sum(ar[0], B[0], sy, mc, true);
     if (NQ > 0) {
 #pragma unroll
-      for (int q = 1; q < NQ; ++q) {
-        b4 = B[q];
-        mc = fmaxf(mc, fmaxf(fmaxf(ar[q].x + b4.x, ar[q].y + b4.y), fmaxf(ar[q].z + b4.z, ar[q].w + b4.w)));
-      }
+      for (int q = 1; q < NQ; ++q) group_sum(ar[q], B[q], sy, mc, false);
     } else {
-      for (int q = 1; q < nq_rt; ++q) {
-        const float4 a4 = A[q];
-        b4 = B[q];
-        mc = fmaxf(mc, fmaxf(fmaxf(a4.x + b4.x, a4.y + b4.y), fmaxf(a4.z + b4.z, a4.w + b4.w)));
-      }
+      for (int q = 1; q < nq_rt; ++q) group_sum(A[q], B[q], sy, mc, false);
     }
-    // positive sums: relative error << band; y's sum (nearly) subnormal: only a clearly larger
-    // competitor is decisive, everything else is rechecked
-    const bool pos = sy >= 1e-30f;
-    const bool beat = pos ? mc > sy * bh : mc > 2e-30f;
-    const bool near = pos ? mc >= sy * bl : true;
-    w |= (uint32_t)(!near) << k;
-    n |= (uint32_t)(near && !beat) << k;
+    // r < 0: every competitor below y by more than the band (clear win); r >= 0 and r2 < 0: near-tie
+    // (fp64 recheck); r2 >= 0: clear loss. Positive sums: relative error << band. A sample with a
+    // (nearly) subnormal y probability (tiny, runtime-count variant only) decides only clear losses.
+    float r = fmaf(-sy, bl, mc), r2 = fmaf(-sy, bh, mc);
+    if (NQ == 0 && tiny && !(sy >= 1e-30f)) {
+      r = 1.f;
+      r2 = mc > 2e-30f ? 1.f : -1.f;
+    }
+    w = __funnelshift_l(__float_as_uint(r), w, 1);  // w = w << 1 | sign(r)
+    n = __funnelshift_l(~__float_as_uint(r) & __float_as_uint(r2), n, 1);
   }
-  okm = w;
-  pm = n;
+  okm = __brev(w) >> (32 - NSUB);  // bit k <-> subset t + 256k
+  pm = __brev(n) >> (32 - NSUB);
 }
 
 template <int NSUB>
@@ -258,6 +272,8 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       const int nr = __shfl_sync(FULL, incl, 31);
       const int nq = (nr + 1 + 3) >> 2;
       const bool fits = 4 * nq <= p.cta_cols;
+      // p[m][y] < e^-68 (~3e-30) for some model: y's subset sums may be (nearly) subnormal
+      const bool tiny = __any_sync(FULL, lane < K && rows[(size_t)lane * p.ldc + y] - st.ls[lane] < -68.f);
       if (fits) {
         if (lane < 4) sh.cols[4 * nq - 4 + lane] = -1;
         __syncwarp();
@@ -268,6 +284,7 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
         sh.cols[0] = y;
         sh.nq = nq;
         sh.skip = !fits;
+        sh.tiny = tiny;
         if (!fits) ovf_work[atomicAdd(ovf_count, 1u)] = (int32_t)st.n;  // rk_vote_batch_avg.cu
       }
     }
@@ -304,12 +321,12 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       __syncthreads();
       // ---- S6: every subset: sum of y's column and the largest competitor, branch-free ----------
       uint32_t okm, pm;
-      switch (nq) {
+      switch (sh.tiny ? 0 : nq) {
         case 1: decide_subsets<NSUB, 1>(p, TA, TB, okm, pm); break;
         case 2: decide_subsets<NSUB, 2>(p, TA, TB, okm, pm); break;
         case 3: decide_subsets<NSUB, 3>(p, TA, TB, okm, pm); break;
         case 4: decide_subsets<NSUB, 4>(p, TA, TB, okm, pm); break;
-        default: decide_subsets<NSUB, 0>(p, TA, TB, okm, pm, nq); break;
+        default: decide_subsets<NSUB, 0>(p, TA, TB, okm, pm, nq, sh.tiny); break;
       }
       okm &= validm;
       pm &= validm;

@@ -110,6 +110,20 @@ def test_cta_average_overflow_route(rk, monkeypatch, cols):
     compare_tables(t, o, K=K)
 
 
+@pytest.mark.parametrize("K", [8, 12])
+def test_tiny_label_probabilities(rk, K):
+    """Steep logits (x40 on every third sample): p[m][y] underflows fp32 for some models, so subset sums
+    of y can be (nearly) subnormal; those decisions must still match the fp64 oracle."""
+    C, N, seed = 100, 90, 26
+    y = gen.labels(seed, 0, N, C)
+    L = gen.logits(seed, 0, N, K, C, y=y)
+    L[::3] *= 40.0
+    gcfg, ocfg = default_cfg(K)
+    t, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    compare_tables(t, o, K=K)
+
+
 def test_chunked_and_sharded_equal_one_shot(rk):
     """Streaming chunks (multiples of lcm(B)) and disjoint shards sum to the one-shot table (I7, P5)."""
     K, C, N = 4, 100, 1000
