@@ -103,6 +103,8 @@ struct rk_ctx {
   int64_t labels_cap = 0;
   int32_t* d_work = nullptr;  // vote worklist [N] + count
   int64_t work_cap = 0;
+  uint64_t* d_pairs = nullptr;  // K >= 9: near-tie (sample, subset) pairs for the fp64 recheck kernel
+  int64_t pairs_cap = 0;
   int64_t* d_arr = nullptr;
   int64_t arr_cap = 0;
   float* d_scratch = nullptr;
@@ -237,7 +239,7 @@ void rk_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
   void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_max, ctx->ws_x,
-                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_arr, ctx->d_scratch,
+                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_pairs, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -584,8 +586,15 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     vp.scratch = ctx->d_scratch;
     vp.scratch_cls = ctx->d_scratch_cls;
     {
-      // worklist [N] + count, then (K >= 9) the overflow worklist [N] + count
-      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, 2 * N + 2)) != RK_OK) return s;
+      // worklist [N] + count, then (K >= 9) the overflow and the CTA-kernel worklists, [N] + count each,
+      // and the near-tie pair count
+      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, 3 * N + 4)) != RK_OK) return s;
+      if (!warp_path) {  // near-tie pairs of the warp averaging kernel (a full list sends samples to the CTA kernel)
+        if ((s = ensure(ctx, &ctx->d_pairs, &ctx->pairs_cap, N / 2 + 65536)) != RK_OK) return s;
+        vp.pairs = ctx->d_pairs;
+        vp.pair_cap = ctx->pairs_cap;
+        vp.pair_count = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 3);
+      }
       int32_t* st_top = nullptr;
       float *st_lse = nullptr, *st_max = nullptr;
       if (!ctx->batch_stats) {  // the classify kernel writes row statistics for the averaging kernel
@@ -597,6 +606,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       unsigned int* wc = reinterpret_cast<unsigned int*>(ctx->d_work + N);
       vp.ovf_work = ctx->d_work + N + 1;
       vp.ovf_count = reinterpret_cast<unsigned int*>(ctx->d_work + 2 * N + 1);
+      vp.cta_work = ctx->d_work + 2 * N + 2;  // K >= 9: warp averaging kernel -> CTA kernel
+      vp.cta_count = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 2);
       const double bytes = (double)N * ((double)K * C * 4 + 4);
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
       if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lse, st_max, ctx->sm_count));

@@ -45,6 +45,11 @@ struct VoteParams {
   unsigned int* err;              // [0] non-finite logits, [1] bad label
   int32_t* ovf_work;              // K >= 9: worklist samples whose columns exceed cta_cols (rk_vote_cta_avg.cu) [N]
   unsigned int* ovf_count;
+  int32_t* cta_work;              // K >= 9, ldc <= 128: samples the warp kernel hands to the CTA kernel [N]
+  unsigned int* cta_count;
+  uint64_t* pairs;                // K >= 9, ldc <= 128: near-tie pairs (n << 16 | v) for the fp64 recheck kernel
+  unsigned int* pair_count;
+  int64_t pair_cap;
 };
 
 // warp-per-sample variant for K <= 8, C <= 1024 (rk_vote_warp.cu); uses CAP, TCAP, K1, gs, scratch
@@ -69,6 +74,15 @@ cudaError_t launch_vote_batch_avg(const VoteParams& q, int sm_count, cudaStream_
 size_t vote_cta_avg_smem(const VoteParams& q);
 cudaError_t launch_vote_cta_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
                                 const unsigned int* work_count, int32_t* ovf_work, unsigned int* ovf_count);
+
+// Warp-per-sample averaging for K = 9..12 with ldc <= 128 (rk_vote_wsample_avg.cu): samples with more
+// than 7 competitors, a near-subnormal label probability or a near-tie go, untouched, to cta_work.
+// Near-tie subsets of its samples are appended as (sample, subset) pairs to q.pairs and decided by
+// launch_vote_pair_recheck (fp64, one warp per pair, from the definition).
+bool vote_wsample_avg_supported(const VoteParams& q);
+cudaError_t launch_vote_pair_recheck(const VoteParams& q, int sm_count, cudaStream_t st);
+cudaError_t launch_vote_wsample_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
+                                    const unsigned int* work_count, int32_t* cta_work, unsigned int* cta_count);
 
 // Two kernels: classify+votes over all samples, then averages over the worklist of samples whose
 // label is an averaging candidate. work: [N] int32, work_count: 1 uint; st_*: [N][K] statistics

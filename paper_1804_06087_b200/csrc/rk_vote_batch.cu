@@ -372,7 +372,15 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
   {  // averages on the worklist, from statistics (the GEMM's or the classify kernel's)
     VoteParams q = p;
     if (!p.lse_in) { q.top1_in = st_top; q.lse_in = st_lse; q.rmax_in = st_max; }
-    if ((e = launch_vote_cta_avg(q, sm_count, st, work, work_count, p.ovf_work, p.ovf_count)) != cudaSuccess) return e;
+    if (vote_wsample_avg_supported(q)) {  // few competitors: warp per sample; the rest -> CTA kernel
+      if ((e = launch_vote_wsample_avg(q, sm_count, st, work, work_count, p.cta_work, p.cta_count)) != cudaSuccess)
+        return e;
+      if ((e = launch_vote_pair_recheck(q, sm_count, st)) != cudaSuccess) return e;
+      if ((e = launch_vote_cta_avg(q, sm_count, st, p.cta_work, p.cta_count, p.ovf_work, p.ovf_count)) != cudaSuccess)
+        return e;
+    } else if ((e = launch_vote_cta_avg(q, sm_count, st, work, work_count, p.ovf_work, p.ovf_count)) != cudaSuccess) {
+      return e;
+    }
     if ((e = launch_vote_batch_avg(q, sm_count, st, p.ovf_work, p.ovf_count)) != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -386,6 +394,8 @@ cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st
   if (p.N <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(work_count, 0, sizeof(unsigned int), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(p.ovf_count, 0, sizeof(unsigned int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.cta_count, 0, sizeof(unsigned int), st);
+  if (e == cudaSuccess && p.pair_count) e = cudaMemsetAsync(p.pair_count, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
   const int nk = (p.S + BT - 1) / BT;
   if (nk <= 2) return launch_nk<2>(p, sm_count, st, work, work_count, st_top, st_lse, st_max);

@@ -60,7 +60,7 @@ def load_library(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    so = path or _build.build()
+    so = path or os.environ.get("RK_LIB") or _build.build()  # RK_LIB: another build of librk.so (experiments)
     L = ctypes.CDLL(so)
     vp, i32, i64, u32, c = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, ctypes.c_char_p
     L.rk_create.argtypes = [ctypes.POINTER(vp), i32, vp, i32, i32]
