@@ -70,6 +70,7 @@ struct Geo {
 
 struct WarpSmem {
   float P[KM * WC];    // p[m][j] of the sample's columns (j = 0: y), zero-padded
+  int32_t cols[WC];    // c_j (j = 0: y, then R ascending)
 };
 
 template <int K>
@@ -91,7 +92,7 @@ __device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NG], const 
     uint32_t w[G::NA], n[G::NA];
 #pragma unroll
     for (int s = 0; s < G::NA; ++s) w[s] = n[s] = 0;
-#pragma unroll 8
+#pragma unroll 4
     for (int j = 0; j < G::NBW; ++j) {
       const int b = b0 + G::LPA * (ws * G::NBW + j);
       const float4* B = reinterpret_cast<const float4*>(TB + b * WC);
@@ -236,23 +237,26 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
       continue;
     }
     const int nq = (nr + 1 + 3) >> 2;  // 1..NG float4 column groups
-    // ---- probabilities of the columns: the owning lane computes its K values ---------------------
-    __syncwarp();  // the previous sample's readers of P / TB are done
+    // ---- probabilities of the columns: column j's K logits are shuffled from the lane holding the
+    //      class to lanes m < K, which compute p[m][j] = exp(l[m][c_j] - lse_m) (one expf per lane) -----
+    __syncwarp();  // the previous sample's readers of P / TB / cols are done
     for (int i = lane; i < K * WC / 4; i += 32) reinterpret_cast<float4*>(P)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncwarp();
     {
-      int jq[4];
       int j = 1 + incl - cnt_l;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) jq[q] = ((nib >> q) & 1u) ? j++ : -1;
-      if (lane == yl) jq[yq] = 0;
+      for (uint32_t q = nib; q; q &= q - 1) wsm[warp].cols[j++] = cls0 + __ffs(q) - 1;
+      if (lane == 0) wsm[warp].cols[0] = y;
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j <= nr; ++j) {
+      const int c = wsm[warp].cols[j], src = c >> 2, q = c & 3;
+      float mine = 0.f;
 #pragma unroll
       for (int m = 0; m < K; ++m) {
-        const float lsm = __shfl_sync(FULL, ls, m);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (jq[q] >= 0) P[m * WC + jq[q]] = expf(f4c(x[m], q) - lsm);
+        const float v = __shfl_sync(FULL, f4c(x[m], q), src);
+        if (lane == m) mine = v;
       }
+      if (lane < K) P[lane * WC + j] = expf(mine - ls);
     }
     __syncwarp();
     // ---- tables: TB rows b = lane + 32r in shared memory, the lane's TA row(s) in registers -------
