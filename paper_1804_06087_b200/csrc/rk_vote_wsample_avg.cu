@@ -36,13 +36,6 @@ constexpr int NG = 3;        // float4 column groups
 constexpr int WC = 4 * NG;   // table columns: y + up to 11 competitors
 constexpr int KM = 12;
 
-__device__ __forceinline__ float4 ldg_stream(const float* p) {
-  float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p));
-  return r;
-}
 __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 __device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3 (sm_100)
   float r;
@@ -71,6 +64,7 @@ struct Geo {
 struct WarpSmem {
   float P[KM * WC];    // p[m][j] of the sample's columns (j = 0: y), zero-padded
   int32_t cols[WC];    // c_j (j = 0: y, then R ascending)
+  float ls[KM];        // lse per model
 };
 
 template <int K>
@@ -201,12 +195,14 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
     const float lth = logf(th / (float)K);
     const float thr = (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
     const uint32_t ymask = __ballot_sync(FULL, lane < K && tp == y);  // models whose top-1 is y
-    // ---- the K rows in registers: lane holds classes 4*lane .. 4*lane+3 --------------------------
+    // ---- the K rows in registers (L1-allocating: the column pass re-reads a few values) -----------
+    //      lane holds classes 4*lane .. 4*lane+3
     const float* rb = p.logits + n * K * ldc;
     float4 x[K];
 #pragma unroll
     for (int m = 0; m < K; ++m)
-      x[m] = lane_ok ? ldg_stream(rb + m * ldc + 4 * lane) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      x[m] = lane_ok ? __ldg(reinterpret_cast<const float4*>(rb + m * ldc + 4 * lane))
+                     : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     // ---- R: S_c (x >= θ threshold of some model) ∩ {x >= l[m][y] for some model}, minus y -------
     uint32_t b1 = 0, b2 = 0;
     float myly = 0.f;
@@ -237,26 +233,20 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
       continue;
     }
     const int nq = (nr + 1 + 3) >> 2;  // 1..NG float4 column groups
-    // ---- probabilities of the columns: column j's K logits are shuffled from the lane holding the
-    //      class to lanes m < K, which compute p[m][j] = exp(l[m][c_j] - lse_m) (one expf per lane) -----
+    // ---- probabilities of the columns: lane i handles (m, j) = (i mod K, i div K), re-reading l[m][c_j]
+    //      (an L1 hit: the rows were just loaded) -> p[m][j] = exp(l[m][c_j] - lse_m) -------------------
     __syncwarp();  // the previous sample's readers of P / TB / cols are done
     for (int i = lane; i < K * WC / 4; i += 32) reinterpret_cast<float4*>(P)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     {
       int j = 1 + incl - cnt_l;
       for (uint32_t q = nib; q; q &= q - 1) wsm[warp].cols[j++] = cls0 + __ffs(q) - 1;
       if (lane == 0) wsm[warp].cols[0] = y;
+      if (lane < K) wsm[warp].ls[lane] = ls;
     }
     __syncwarp();
-#pragma unroll 1
-    for (int j = 0; j <= nr; ++j) {
-      const int c = wsm[warp].cols[j], src = c >> 2, q = c & 3;
-      float mine = 0.f;
-#pragma unroll
-      for (int m = 0; m < K; ++m) {
-        const float v = __shfl_sync(FULL, f4c(x[m], q), src);
-        if (lane == m) mine = v;
-      }
-      if (lane < K) P[lane * WC + j] = expf(mine - ls);
+    for (int i = lane; i < K * (nr + 1); i += 32) {
+      const int j = i / K, m = i - j * K;
+      P[m * WC + j] = expf(__ldg(rb + m * ldc + wsm[warp].cols[j]) - wsm[warp].ls[m]);
     }
     __syncwarp();
     // ---- tables: TB rows b = lane + 32r in shared memory, the lane's TA row(s) in registers -------
