@@ -16,6 +16,7 @@
 // merge kernel.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "rk_internal.h"
 
@@ -377,6 +378,119 @@ int64_t ovd_elems(int nB, const int* B, int nR, int K, int64_t N, int64_t* off) 
   return tot;
 }
 
+// Fast path for doubling batch sizes B = {gs, 2gs, ..., 2^(NB-1) gs} (the configs' {16, ..., 256}): a
+// chunk (L = B[NB-1] samples) holds G0 = 2^(NB-1) groups, so a thread loads its subset's G0 group counts
+// into registers once and forms every batch size's correct counts as a pairwise-sum tree, each batch
+// end costing one 128-bit shared load of the staged overdue counts (u32 per rate) and NRP multiply-adds.
+// QC chunks are staged per pair of barriers.
+constexpr int QC = 4;
+constexpr int kQNestedBlocksPerSM = 4;
+template <int NRP, int NB>
+__global__ void __launch_bounds__(QT, kQNestedBlocksPerSM)
+    q_nested_kernel(const QParams p, const QConst qc, int64_t chunks_per_block, int flush) {
+  constexpr int G0 = 1 << (NB - 1);   // groups (= smallest batches) per chunk
+  constexpr int TOT = 2 * G0 - 1;     // batches of every size per chunk
+  extern __shared__ unsigned long long qacc[];  // [nR * NB][QT], then u32 [QC][TOT][K][NRP]
+  uint32_t* so = reinterpret_cast<uint32_t*>(qacc + (size_t)p.nR * NB * QT);
+  const int K = p.K, KR = K * NRP;
+  const int v1 = blockIdx.x * QT + threadIdx.x;
+  const bool own = v1 < p.S;
+  for (int i = 0; i < p.nR * NB; ++i) qacc[i * QT + threadIdx.x] = 0;
+  const int64_t ngroups = (p.N + p.gs - 1) / p.gs;
+  const int64_t nch = (p.N + p.L - 1) / p.L;
+  const int64_t q0 = blockIdx.y * chunks_per_block;
+  const int64_t q1 = min(nch, q0 + chunks_per_block);
+  int mo[NB];  // slowest member of v per batch size -> offset of its rates in a staged batch
+#pragma unroll
+  for (int bi = 0; bi < NB; ++bi) mo[bi] = (own ? p.slow[(size_t)bi * p.S + v1] : 0) * NRP;
+  unsigned int acc[NRP][NB];
+#pragma unroll
+  for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+    for (int r = 0; r < NRP; ++r) acc[r][bi] = 0;
+  const uint8_t* gp = p.grp + (own ? v1 : 0);
+  int since = 0;
+  for (int64_t qq = q0; qq < q1; qq += QC) {
+    __syncthreads();
+    {  // stage overdue counts of chunks qq .. qq+QC-1 as u32 (one NRP-vector per (batch, model)); a level's
+       // batches of a chunk are contiguous in ovd; incomplete batches contribute 0 (reading Q13)
+      using V = typename OVec<NRP>::T;
+      int base = 0;
+#pragma unroll
+      for (int bi = 0; bi < NB; ++bi) {
+        const int nb = G0 >> bi;
+        for (int w = threadIdx.x; w < QC * nb * K; w += QT) {
+          const int c = w / (nb * K), rem = w - c * nb * K;  // rem = j * K + m
+          const int64_t jg = (qq + c) * (int64_t)nb + rem / K;
+          union { V v; uint16_t h[NRP]; } o;
+          if (qq + c < q1 && jg < qc.nbat[bi]) o.v = reinterpret_cast<const V*>(p.ovd + p.ovd_off[bi] + jg * KR)[rem % K];
+          else o.v = V{};
+          uint32_t* d = so + ((size_t)c * TOT + base) * KR + (size_t)rem * NRP;
+#pragma unroll
+          for (int r = 0; r < NRP; r += 4) *reinterpret_cast<uint4*>(d + r) = make_uint4(o.h[r], o.h[r + 1], o.h[r + 2], o.h[r + 3]);
+        }
+        base += nb;
+      }
+    }
+    __syncthreads();
+    if (!own) continue;
+    unsigned int nx[G0];  // group counts of the next chunk, loaded one chunk ahead
+#pragma unroll
+    for (int i = 0; i < G0; ++i) {
+      const int64_t g = qq * G0 + i;
+      nx[i] = g < ngroups ? gp[g * p.S] : 0u;
+    }
+#pragma unroll 1
+    for (int c = 0; c < QC; ++c) {
+      const int64_t q = qq + c;
+      if (q >= q1) break;
+      unsigned int sv[G0];
+#pragma unroll
+      for (int i = 0; i < G0; ++i) {
+        sv[i] = nx[i];
+        const int64_t g = (q + 1) * G0 + i;
+        nx[i] = (c + 1 < QC && g < ngroups) ? gp[g * p.S] : 0u;
+      }
+      const uint32_t* sc = so + (size_t)c * TOT * KR;
+      int base = 0;
+#pragma unroll
+      for (int bi = 0; bi < NB; ++bi) {
+        const int nb = G0 >> bi;
+#pragma unroll
+        for (int j = 0; j < nb; ++j) {
+          if (NRP == 4) {
+            const uint4 o = *reinterpret_cast<const uint4*>(sc + (base + j) * KR + mo[bi]);
+            acc[0][bi] += sv[j] * o.x; acc[1][bi] += sv[j] * o.y;
+            acc[2][bi] += sv[j] * o.z; acc[3][bi] += sv[j] * o.w;
+          } else {
+#pragma unroll
+            for (int r = 0; r < NRP; ++r) acc[r][bi] += sv[j] * sc[(base + j) * KR + mo[bi] + r];
+          }
+        }
+        base += nb;
+#pragma unroll
+        for (int j = 0; j < nb / 2; ++j) sv[j] = sv[2 * j] + sv[2 * j + 1];  // next batch size
+      }
+      if (++since == flush || q + 1 == q1) {  // spill the u32 accumulators
+        since = 0;
+#pragma unroll
+        for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+          for (int r = 0; r < NRP; ++r) {
+            if (r < p.nR) qacc[(r * NB + bi) * QT + threadIdx.x] += acc[r][bi];
+            acc[r][bi] = 0;
+          }
+      }
+    }
+  }
+  if (!own) return;
+  for (int r = 0; r < p.nR; ++r)
+    for (int bi = 0; bi < NB; ++bi) {
+      const unsigned long long x = qacc[(r * NB + bi) * QT + threadIdx.x];
+      if (x) atomicAdd(p.Q + ((size_t)r * NB + bi) * p.S + v1, x);
+    }
+}
+
 template <int NRP, int NB, bool STAGED>
 static cudaError_t launch_q_t(const QParams& p, const QConst& qc, dim3 grid, size_t smem, int64_t cpb, int tot,
                               int flush, cudaStream_t st) {
@@ -434,6 +548,35 @@ cudaError_t launch_q(const QParams& p, int sm_count, cudaStream_t st) {
   const unsigned long long fl = 0xFFFFFFFFull / ((unsigned long long)p.L * bmax);
   const int flush = (int)(fl < 1024 ? fl : 1024);
   const dim3 grid((unsigned)slices, (unsigned)ranges);
+  // doubling batch sizes starting at the group size, at most 16 groups per chunk: the tree kernel
+  bool nested = p.B[0] == p.gs && p.nB <= 5 && p.L == p.B[p.nB - 1];
+  for (int bi = 1; bi < p.nB; ++bi) nested = nested && p.B[bi] == 2 * p.B[bi - 1];
+  if (nested && !getenv("RK_Q_GENERIC")) {  // env: tests compare against the generic kernel
+    const int G0 = 1 << (p.nB - 1);
+    const size_t nsmem = acc + sizeof(uint32_t) * (size_t)QC * (2 * G0 - 1) * p.K * nrp;
+    int nper = (int)((200 * 1024) / (nsmem + 1024));
+    nper = nper < 1 ? 1 : (nper > kQNestedBlocksPerSM ? kQNestedBlocksPerSM : nper);
+    int64_t nr_ = ((int64_t)sm_count * nper) / slices;
+    nr_ = nr_ < 1 ? 1 : (nr_ > nch ? nch : (nr_ > 65535 ? 65535 : nr_));
+    int64_t ncpb = (nch + nr_ - 1) / nr_;
+    ncpb = (ncpb + QC - 1) / QC * QC;  // whole staging rounds per block
+    nr_ = (nch + ncpb - 1) / ncpb;
+    const dim3 ngrid((unsigned)slices, (unsigned)nr_);
+    switch (p.nB * 16 + nrp) {
+#define RK_QN(NBV, NRV)                                                                                      \
+  case NBV * 16 + NRV: {                                                                                    \
+    cudaError_t e = cudaFuncSetAttribute(q_nested_kernel<NRV, NBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         (int)nsmem);                                                       \
+    if (e != cudaSuccess) return e;                                                                         \
+    q_nested_kernel<NRV, NBV><<<ngrid, QT, nsmem, st>>>(p, qc, ncpb, flush);                                \
+    return cudaGetLastError();                                                                              \
+  }
+      RK_QN(1, 4) RK_QN(2, 4) RK_QN(3, 4) RK_QN(4, 4) RK_QN(5, 4)
+      RK_QN(1, 8) RK_QN(2, 8) RK_QN(3, 8) RK_QN(4, 8) RK_QN(5, 8)
+#undef RK_QN
+      default: break;
+    }
+  }
   return nrp == 4 ? launch_q_nb<4>(p, qc, staged, grid, smem, cpb, tot, flush, st)
                   : launch_q_nb<8>(p, qc, staged, grid, smem, cpb, tot, flush, st);
 }

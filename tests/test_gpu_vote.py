@@ -167,6 +167,20 @@ def test_labelled_moments_batch_sets(rk, B, N):
     assert o.Q.sum() > 0  # the labelled moments are exercised
 
 
+@pytest.mark.parametrize("K,rates", [(5, (64.0, 128.0, 572.0, 1144.0)),
+                                     (9, (40.0, 64.0, 128.0, 300.0, 572.0, 1144.0))])  # 6 rates: 8-wide vectors
+def test_labelled_moments_doubling_batches(rk, K, rates):
+    """The bench's doubling batch sizes {16, ..., 256} take the pairwise-sum tree kernel for Q; ragged N."""
+    C, N = 40, 2000
+    B = (16, 32, 64, 128, 256)
+    y = gen.labels(41, 0, N, C)
+    L = gen.logits(41, 0, N, K, C, y=y)
+    gcfg, ocfg = default_cfg(K, B=B, rates=rates)
+    t, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    compare_tables(t, o, K=K)
+
+
 def test_arrival_ns_input(rk):
     K, C, N = 3, 10, 640
     y = gen.labels(5, 0, N, C)
