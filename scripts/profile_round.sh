@@ -10,6 +10,6 @@ echo "gemm rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:vote -c 2 -o gpurun_out/${R}_vote \
   python scripts/prof_vote.py --K 8 --C 1000 --N 200000 --gemm 2048 --reps 1 > gpurun_out/${R}_vote.log 2>&1
 echo "vote rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:vote -c 3 -o gpurun_out/${R}_k12 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:vote -c 5 -o gpurun_out/${R}_k12 \
   python scripts/prof_vote.py --K 12 --C 100 --N 250000 --gemm 1024 --reps 1 > gpurun_out/${R}_k12.log 2>&1
 echo "k12 rc=$?"
