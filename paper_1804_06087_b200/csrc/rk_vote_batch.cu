@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "rk_internal.h"
 
@@ -358,6 +359,270 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VotePa
   }
 }
 
+// ======================= kernel A': classify + votes, one warp per 16-sample chunk =================
+// Same per-sample records and the same bit-sliced word evaluation as vote_batch_classify_kernel, but a
+// warp owns 16 consecutive samples (whole count groups, gs | 16) and lane l owns the 32-subset words
+// w = l + 32 i of every one of them: no block barrier at all; per-group counts leave the vertical bit
+// counters through a multiply-spread bit->byte transposition into the warp's staging row, which is
+// copied out coalesced (grp) and added to the CTA's per-subset totals.
+constexpr int CH = 16;  // samples per warp chunk
+struct WRec {  // one sample's vote record (warp-private)
+  uint32_t my, lt, tm;
+  int32_t no;
+  uint32_t mo[KM];
+};
+template <int NWL, bool STATS>
+__global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VoteParams p, int32_t* work,
+                                                                    unsigned int* work_count, int32_t* st_top,
+                                                                    float* st_lse, float* st_max) {
+  __shared__ uint32_t GE[32 * 8];        // GE[L][c] = {lo in [0,32) : popc(lo & L) >= c}
+  __shared__ uint32_t LW[32 * 32];       // LW[A][B] = {lo : best-ranked member of lo ∩ (A ∪ B) is in A}
+  __shared__ uint8_t LR[KM + 1];         // LR[r] = low models (m < 5) ranked better than r
+  __shared__ int8_t rnk[KM];             // rank of each model (0 = best), BEST_MEMBER tie rule
+  __shared__ uint16_t RS[2][64];         // model mask -> rank-order mask, 6 models per half
+  __shared__ uint32_t cnt[1 << KM];      // per-subset correct votes of this CTA (index v)
+  __shared__ uint32_t utot;              // unanimous-correct samples of this CTA
+  __shared__ WRec wrec[NWB];
+  extern __shared__ __align__(16) uint8_t stage_dyn[];  // [NWB][2^K] per-warp group counts, index v
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int K = p.K, S = p.S, C = p.C;
+  const uint32_t kmask = (1u << K) - 1u;
+  const int gsz = p.gs > 0 ? p.gs : CH;
+  const int64_t N = p.N;
+  int64_t tail0 = N;
+  for (int bi = 0; bi < p.nB; ++bi) tail0 = p.tail_start[bi] < tail0 ? p.tail_start[bi] : tail0;
+  for (int i = t; i < 32 * 8; i += BT) {
+    const uint32_t L = (uint32_t)(i >> 3), c = (uint32_t)(i & 7);
+    uint32_t wd = 0;
+    for (uint32_t lo = 0; lo < 32; ++lo) wd |= ((uint32_t)__popc(lo & L) >= c ? 1u : 0u) << lo;
+    GE[i] = wd;
+  }
+  for (int i = t; i < (1 << K); i += BT) cnt[i] = 0;
+  if (t == 0) utot = 0;
+  if (p.tie == 0) {
+    if (t == 0) {
+      uint32_t rem = kmask;
+      for (int r = 0; r < K; ++r) {
+        const int m = p.best_of[rem];
+        rnk[m] = (int8_t)r;
+        rem &= ~(1u << m);
+      }
+    }
+    __syncthreads();
+    if (t < 128) {
+      const int hf = t >> 6, x = t & 63;
+      uint32_t r = 0;
+      for (int b = 0; b < 6; ++b)
+        if (((x >> b) & 1) && 6 * hf + b < K) r |= 1u << rnk[6 * hf + b];
+      RS[hf][x] = (uint16_t)r;
+    }
+    if (t <= K) {
+      uint32_t lr = 0;
+      for (int m = 0; m < 5; ++m) lr |= (rnk[m] < t ? 1u : 0u) << m;
+      LR[t] = (uint8_t)lr;
+    }
+    for (int i = t; i < 32 * 32; i += BT) {
+      const uint32_t A = (uint32_t)i >> 5, B = (uint32_t)i & 31u;
+      uint32_t wd = 0;
+      for (uint32_t lo = 1; lo < 32; ++lo) {
+        const uint32_t s2 = lo & (A | B);
+        int best = -1, br = 1 << 30;
+        for (int m = 0; m < 5; ++m)
+          if (((s2 >> m) & 1u) && rnk[m] < br) { br = rnk[m]; best = m; }
+        if (best >= 0 && ((A >> best) & 1u)) wd |= 1u << lo;
+      }
+      LW[i] = wd;
+    }
+  }
+  __syncthreads();
+  const int nwd = 1 << (K - 5);
+  uint32_t hwr[NWL];  // each owned word's high models, in rank order
+#pragma unroll
+  for (int i = 0; i < NWL; ++i) {
+    const uint32_t w = (uint32_t)(lane + 32 * i);
+    hwr[i] = 0;
+    if (p.tie == 0)
+      for (int m = 5; m < K; ++m)
+        if ((w >> (m - 5)) & 1u) hwr[i] |= 1u << rnk[m];
+  }
+  WRec& rc = wrec[warp];
+  uint8_t* stg = stage_dyn + (size_t)warp * (1 << K);
+  uint32_t uw = 0;  // this warp's unanimous-correct samples (lane 0's count is authoritative)
+  const int64_t nch = (N + CH - 1) / CH;
+  for (int64_t ch = (int64_t)blockIdx.x * NWB + warp; ch < nch; ch += (int64_t)gridDim.x * NWB) {
+    const int64_t n0 = ch * CH;
+    uint32_t k0[NWL], k1[NWL], k2[NWL], k3[NWL], k4[NWL];
+#pragma unroll
+    for (int i = 0; i < NWL; ++i) k0[i] = k1[i] = k2[i] = k3[i] = k4[i] = 0;
+    uint32_t u = 0, wl = 0;
+#pragma unroll 1
+    for (int i = 0; i < CH; ++i) {
+      const int64_t n = n0 + i;
+      if (n < N) {
+        // ---- phase 1: the sample's record (as in vote_batch_classify_kernel) -----------------------
+        bool eval = false;
+        const int y = p.labels[n];
+        if (y < 0 || y >= C) {
+          if (lane == 0) atomicOr(p.err + 1, 1u);
+        } else {
+          const float* rowbase = p.logits + n * K * p.ldc;
+          int tp = 0;
+          float mx = 0.f, ls = 0.f;
+          bool bad = false;
+          if (STATS) {
+            if (lane < K) {
+              tp = p.top1_in[n * K + lane];
+              ls = p.lse_in[n * K + lane];
+              mx = p.rmax_in[n * K + lane];
+              bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
+            }
+          } else {
+            row_stats(p, rowbase, lane, tp, mx, ls, bad);
+            if (lane < K) { st_top[n * K + lane] = tp; st_lse[n * K + lane] = ls; st_max[n * K + lane] = mx; }
+          }
+          if (__any_sync(FULL, bad)) {
+            if (lane == 0) atomicOr(p.err, 1u);
+          } else {
+            const int c = lane < K ? tp : -1 - lane;
+            const uint32_t mm = __match_any_sync(FULL, c);
+            uint32_t tm = 0;
+            if (n >= tail0)
+              for (int bi = 0; bi < p.nB; ++bi)
+                if (n >= p.tail_start[bi]) tm |= 1u << bi;
+            if (__shfl_sync(FULL, mm, 0) == kmask) {  // unanimous (invariant I6)
+              if (__shfl_sync(FULL, c, 0) == y) {
+                ++u;
+                if (tm)
+                  for (int bi = 0; bi < p.nB; ++bi)
+                    if ((tm >> bi) & 1u)
+                      for (int v1 = lane; v1 < S; v1 += 32) atomicAdd(p.tail + (size_t)bi * S + v1, 1ull);
+              }
+            } else {
+              const float thr = theta_threshold(mx, ls, K, lane);
+              if (__any_sync(FULL, lane < K && rowbase[(size_t)lane * p.ldc + y] >= thr)) wl |= 1u << i;
+              if (__any_sync(FULL, lane < K && c == y)) {
+                eval = true;
+                const bool other = lane < K && (__ffs(mm) - 1) == lane && c != y;  // one lane per other class
+                const uint32_t ob = __ballot_sync(FULL, other);
+                const uint32_t ltb = __ballot_sync(FULL, other && c < y);
+                __syncwarp();  // the previous sample's readers of rc are done
+                if (other) rc.mo[__popc(ob & ((1u << lane) - 1u))] = mm;
+                if (lane < K && c == y && (__ffs(mm) - 1) == lane) rc.my = mm;
+                if (lane == 0) {
+                  rc.no = __popc(ob);
+                  rc.tm = tm;
+                  uint32_t lt = 0;  // lt bit j refers to the j-th other class in lane order
+                  for (uint32_t w = ob, j = 0; w; w &= w - 1, ++j)
+                    if ((ltb >> (__ffs(w) - 1)) & 1u) lt |= 1u << j;
+                  rc.lt = lt;
+                }
+                __syncwarp();
+              }
+            }
+          }
+        }
+        // ---- phase 2: the lane's words of this sample (bit-sliced A3) -----------------
+        if (eval) {
+          const uint32_t my = rc.my, lt = rc.lt, Ly = my & 31u, tmr = rc.tm;
+          const int no = rc.no, ny = __popc(Ly);
+          const uint32_t* GY = GE + Ly * 8;
+#pragma unroll
+          for (int wi = 0; wi < NWL; ++wi) {
+            const uint32_t w = (uint32_t)(lane + 32 * wi);
+            if ((int)w >= nwd) break;
+            const int hy = __popc(w & (my >> 5));
+            uint32_t lose = hy == 0 ? ~GY[1] : 0u;  // c_y == 0
+#pragma unroll 1
+            for (int j = 0; j < no; ++j) {
+              const uint32_t Mj = rc.mo[j];
+              const uint32_t* GJ = GE + (Mj & 31u) * 8;
+              const int d = hy - __popc(w & (Mj >> 5));  // c_j > c_y  <=>  x_j >= x_y + d + 1
+              uint32_t gt = 0, eq = 0;
+#pragma unroll 1
+              for (int a = 0; a <= ny; ++a) {
+                const uint32_t ya = GY[a] & ~GY[a + 1];  // x_y == a
+                const int k = a + d + 1;
+                const uint32_t gk = k <= 0 ? ~0u : (k >= 8 ? 0u : GJ[k]);
+                const uint32_t ek = (k - 1 < 0 || k - 1 >= 8) ? 0u : (GJ[k - 1] & ~gk);
+                gt |= ya & gk;
+                eq |= ya & ek;
+              }
+              lose |= gt;
+              if (p.tie != 0) {
+                if ((lt >> j) & 1u) lose |= eq;
+              } else if (eq & ~lose) {  // tie race (reading Q2), as in vote_batch_classify_kernel
+                const uint32_t myr = RS[0][my & 63u] | RS[1][my >> 6];
+                const uint32_t hr = (myr | RS[0][Mj & 63u] | RS[1][Mj >> 6]) & hwr[wi];
+                const int rh = hr ? __ffs(hr) - 1 : K;
+                const bool hiy = hr && ((myr >> rh) & 1u);
+                const uint32_t lr = LR[rh];
+                const uint32_t A = Ly & lr, Bm = Mj & 31u & lr;
+                const uint32_t ywin = LW[(A << 5) | Bm] | (hiy ? ~GE[(A | Bm) * 8 + 1] : 0u);
+                lose |= eq & ~ywin;
+              }
+            }
+            const uint32_t ok = ~lose & (w == 0 ? ~1u : ~0u);  // v = 0 is not a subset
+            uint32_t cc = ok, x;  // vertical counter += ok
+            x = k0[wi] & cc; k0[wi] ^= cc; cc = x;
+            x = k1[wi] & cc; k1[wi] ^= cc; cc = x;
+            x = k2[wi] & cc; k2[wi] ^= cc; cc = x;
+            x = k3[wi] & cc; k3[wi] ^= cc; cc = x;
+            k4[wi] ^= cc;
+            if (ok && tmr) tail_add_word(p, tmr, w, ok);
+          }
+        }
+      }
+      // ---- group end: per-subset counts (+ unanimous) -> staging row -> grp and the CTA totals -----
+      if ((i + 1) % gsz == 0) {
+        const int64_t gstart = n0 + i + 1 - gsz;
+        if (gstart < N) {
+          const uint32_t ub = u * 0x01010101u;
+#pragma unroll
+          for (int wi = 0; wi < NWL; ++wi) {
+            const int w = lane + 32 * wi;
+            if (w >= nwd) break;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(stg + 32 * w);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {  // subsets 4q..4q+3 of the word: bit b of each count -> byte
+              uint32_t o = ub;
+              o += (((k0[wi] >> (4 * q)) & 0xfu) * 0x00204081u & 0x01010101u);
+              o += (((k1[wi] >> (4 * q)) & 0xfu) * 0x00204081u & 0x01010101u) << 1;
+              o += (((k2[wi] >> (4 * q)) & 0xfu) * 0x00204081u & 0x01010101u) << 2;
+              o += (((k3[wi] >> (4 * q)) & 0xfu) * 0x00204081u & 0x01010101u) << 3;
+              o += (((k4[wi] >> (4 * q)) & 0xfu) * 0x00204081u & 0x01010101u) << 4;
+              dst[q] = o;
+            }
+            k0[wi] = k1[wi] = k2[wi] = k3[wi] = k4[wi] = 0;
+          }
+          __syncwarp();
+          const int64_t gi = gstart / gsz;
+          for (int v1 = lane; v1 < S; v1 += 32) {
+            const uint32_t tot = stg[v1 + 1];
+            if (p.grp) p.grp[gi * S + v1] = (uint8_t)tot;
+            if (tot) atomicAdd(&cnt[v1 + 1], tot);
+          }
+          __syncwarp();
+          uw += u;
+        }
+        u = 0;
+      }
+    }
+    if (wl) {  // worklist append: one atomic per warp per chunk
+      unsigned int base = 0;
+      if (lane == 0) base = atomicAdd(work_count, (unsigned int)__popc(wl));
+      base = __shfl_sync(FULL, base, 0);
+      if (lane < CH && ((wl >> lane) & 1u)) work[base + __popc(wl & ((1u << lane) - 1u))] = (int32_t)(n0 + lane);
+    }
+  }
+  if (lane == 0 && uw) atomicAdd(&utot, uw);
+  __syncthreads();
+  const uint32_t ua = utot;
+  for (int v1 = t; v1 < S; v1 += BT) {
+    if (cnt[v1 + 1]) atomicAdd(p.cnt_vote + v1, (unsigned long long)cnt[v1 + 1]);
+    if (ua) atomicAdd(p.cnt_avg + v1, (unsigned long long)ua);
+  }
+}
+
 template <int NK>
 cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work, unsigned int* work_count,
                       int32_t* st_top, float* st_lse, float* st_max) {
@@ -365,8 +630,25 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
   {
     const int64_t nb = (p.N + SB - 1) / SB;
     const int grid = (int)(nb < (int64_t)sm_count * 2 ? nb : (int64_t)sm_count * 2);
-    if (p.lse_in) vote_batch_classify_kernel<NK, true><<<grid, BT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
-    else vote_batch_classify_kernel<NK, false><<<grid, BT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+    constexpr int NWL = NK / 4 > 0 ? NK / 4 : 1;  // words per lane: 2^(K-5) / 32 (K = 9: half the lanes idle)
+    if (!getenv("RK_VOTE_BATCHED")) {             // env: the older batch-transposed kernel (comparison)
+      const int dsm = NWB << p.K;
+      if (p.lse_in) {
+        if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, dsm)) != cudaSuccess)
+          return e;
+        vote_group_classify_kernel<NWL, true><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
+      } else {
+        if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, dsm)) != cudaSuccess)
+          return e;
+        vote_group_classify_kernel<NWL, false><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
+      }
+    } else if (p.lse_in) {
+      vote_batch_classify_kernel<NK, true><<<grid, BT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+    } else {
+      vote_batch_classify_kernel<NK, false><<<grid, BT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   {  // averages on the worklist, from statistics (the GEMM's or the classify kernel's)
