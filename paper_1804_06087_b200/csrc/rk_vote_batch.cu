@@ -522,35 +522,44 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
           }
         }
         // ---- phase 2: the lane's words of this sample (bit-sliced A3) -----------------
+        // For class j, with x(lo) = low-model votes and h = high-model votes of word w: j beats y iff
+        // x_y - x_j < h_j - h_y =: -d, ties iff equal. The 32-lane ballots of (x_y - x_j >= t) for
+        // t = -7..8 (lane = lo) give DG_j[t]; lane t + 7 keeps it and each lane fetches DG_j[-d] and
+        // DG_j[-d + 1] for its words by shuffle: no per-word loop over vote counts.
         if (eval) {
           const uint32_t my = rc.my, lt = rc.lt, Ly = my & 31u, tmr = rc.tm;
-          const int no = rc.no, ny = __popc(Ly);
-          const uint32_t* GY = GE + Ly * 8;
+          const int no = rc.no;
+          const uint32_t gy1 = GE[Ly * 8 + 1];  // lo with x_y >= 1
+          uint32_t lose[NWL];
+          int hy[NWL];
 #pragma unroll
           for (int wi = 0; wi < NWL; ++wi) {
             const uint32_t w = (uint32_t)(lane + 32 * wi);
-            if ((int)w >= nwd) break;
-            const int hy = __popc(w & (my >> 5));
-            uint32_t lose = hy == 0 ? ~GY[1] : 0u;  // c_y == 0
+            hy[wi] = __popc(w & (my >> 5));
+            lose[wi] = hy[wi] == 0 ? ~gy1 : 0u;  // c_y == 0
+          }
+          const int xy = __popc((uint32_t)lane & Ly);
 #pragma unroll 1
-            for (int j = 0; j < no; ++j) {
-              const uint32_t Mj = rc.mo[j];
-              const uint32_t* GJ = GE + (Mj & 31u) * 8;
-              const int d = hy - __popc(w & (Mj >> 5));  // c_j > c_y  <=>  x_j >= x_y + d + 1
-              uint32_t gt = 0, eq = 0;
-#pragma unroll 1
-              for (int a = 0; a <= ny; ++a) {
-                const uint32_t ya = GY[a] & ~GY[a + 1];  // x_y == a
-                const int k = a + d + 1;
-                const uint32_t gk = k <= 0 ? ~0u : (k >= 8 ? 0u : GJ[k]);
-                const uint32_t ek = (k - 1 < 0 || k - 1 >= 8) ? 0u : (GJ[k - 1] & ~gk);
-                gt |= ya & gk;
-                eq |= ya & ek;
-              }
-              lose |= gt;
+          for (int j = 0; j < no; ++j) {
+            const uint32_t Mj = rc.mo[j];
+            const int dif = xy - __popc((uint32_t)lane & Mj & 31u);  // x_y - x_j at lo = lane
+            uint32_t dg = lane <= 2 ? ~0u : 0u;                   // t <= -5: always; t >= 6: never
+#pragma unroll
+            for (int tt = 3; tt <= 12; ++tt) {
+              const uint32_t bb = __ballot_sync(FULL, dif >= tt - 7);
+              if (lane == tt) dg = bb;
+            }
+#pragma unroll
+            for (int wi = 0; wi < NWL; ++wi) {
+              const uint32_t w = (uint32_t)(lane + 32 * wi);
+              const int d = hy[wi] - __popc(w & (Mj >> 5));  // in [-7, 7]
+              const uint32_t g = __shfl_sync(FULL, dg, 7 - d);      // x_y - x_j >= -d
+              const uint32_t g1 = __shfl_sync(FULL, dg, 8 - d);     // x_y - x_j >= -d + 1
+              const uint32_t eq = g & ~g1;
+              lose[wi] |= ~g;
               if (p.tie != 0) {
-                if ((lt >> j) & 1u) lose |= eq;
-              } else if (eq & ~lose) {  // tie race (reading Q2), as in vote_batch_classify_kernel
+                if ((lt >> j) & 1u) lose[wi] |= eq;
+              } else if (eq & ~lose[wi]) {  // tie race (reading Q2), as in vote_batch_classify_kernel
                 const uint32_t myr = RS[0][my & 63u] | RS[1][my >> 6];
                 const uint32_t hr = (myr | RS[0][Mj & 63u] | RS[1][Mj >> 6]) & hwr[wi];
                 const int rh = hr ? __ffs(hr) - 1 : K;
@@ -558,10 +567,15 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
                 const uint32_t lr = LR[rh];
                 const uint32_t A = Ly & lr, Bm = Mj & 31u & lr;
                 const uint32_t ywin = LW[(A << 5) | Bm] | (hiy ? ~GE[(A | Bm) * 8 + 1] : 0u);
-                lose |= eq & ~ywin;
+                lose[wi] |= eq & ~ywin;
               }
             }
-            const uint32_t ok = ~lose & (w == 0 ? ~1u : ~0u);  // v = 0 is not a subset
+          }
+#pragma unroll
+          for (int wi = 0; wi < NWL; ++wi) {
+            const uint32_t w = (uint32_t)(lane + 32 * wi);
+            if ((int)w >= nwd) break;
+            const uint32_t ok = ~lose[wi] & (w == 0 ? ~1u : ~0u);  // v = 0 is not a subset
             uint32_t cc = ok, x;  // vertical counter += ok
             x = k0[wi] & cc; k0[wi] ^= cc; cc = x;
             x = k1[wi] & cc; k1[wi] ^= cc; cc = x;
