@@ -4,21 +4,16 @@
 // (RK_TIE_BEST_MEMBER; RK_TIE_LOWEST_CLASS = north_star), :72 averaged softmax (readings Q5, Q6),
 // :429 every non-empty subset v of the model list is an action (2^|M| - 1 of them).
 //
-// With thousands of subsets per sample the work is the (sample, subset) sweep, so the layout is
-// transposed relative to rk_vote_warp.cu:
-//   phase 1  warps build a compact record per sample of a batch (row statistics, distinct-class
-//            vote masks, flags; for the averaging kernel: the candidate set R, gathered
-//            probabilities, half-tables and the competitor bound) in shared memory;
-//   phase 2  bit-sliced: a thread owns a word of 32 subsets (low 5 models <-> bit position) and
-//            sweeps its share of the batch's records; vote counts per class come from a constant
-//            "popcount >= c" table, comparisons and the tie race work on whole words, per-subset
-//            counts accumulate in vertical bit counters folded into shared memory per group.
+// With thousands of subsets per sample the work is the (sample, subset) sweep, evaluated bit-sliced:
+// 32 subsets per word, vote counts per class from a constant "popcount >= c" table and per-class
+// difference masks, the tie race on whole words, per-subset counts in vertical bit counters (kernel A
+// below, one warp per 16-sample chunk). The averages go to the kernels of rk_vote_wsample_avg.cu,
+// rk_vote_cta_avg.cu and rk_vote_batch_avg.cu over the worklist kernel A builds.
 // Exactness arguments are those of rk_vote_warp.cu (unanimity I6, theta pruning, the y-dominance
 // filter, the competitor bound, fp64 recheck of near-ties).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include "rk_internal.h"
 
@@ -28,20 +23,9 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int BT = 256;          // threads per CTA
 constexpr int NWB = BT / 32;
-constexpr int SB = 128;          // samples per batch (kernel A)
-constexpr int SBW = NWB;         // worklist samples per batch (kernel B): one per warp
+constexpr int SB = 128;          // samples per grid-sizing unit (kernel A)
 constexpr int KM = 12;
 
-constexpr uint32_t R_EVAL = 1u, R_UNAN = 2u;
-
-struct Rec {  // per-sample vote record (kernel A), relative to the label y
-  uint32_t flags;
-  uint32_t tm;      // ragged-tail membership per batch size
-  uint32_t my;      // members voting y
-  int32_t no;       // number of other predicted classes
-  uint32_t lt;      // bit j: other class j < y (LOWEST_CLASS tie rule)
-  uint32_t mo[KM];  // members voting each other class
-};
 
 __device__ __forceinline__ float4 ldg_stream(const float* p) {
   float4 r;
@@ -69,10 +53,6 @@ __device__ __noinline__ void tail_add_word(const VoteParams& p, uint32_t tm, uin
   }
 }
 
-__device__ __noinline__ void tail_add_b(const VoteParams& p, uint32_t tm, uint32_t v) {
-  for (int bi = 0; bi < p.nB; ++bi)
-    if ((tm >> bi) & 1u) atomicAdd(p.tail + (size_t)bi * p.S + (v - 1), 1ull);
-}
 
 // Row statistics of model `lane` for caller logits: one pass over every row (lanes stride a row).
 __device__ void row_stats(const VoteParams& p, const float* rowbase, int lane, int& tp, float& mx, float& ls,
@@ -101,270 +81,15 @@ __device__ void row_stats(const VoteParams& p, const float* rowbase, int lane, i
   }
 }
 
-// =============================== kernel A: classify + votes (batched) ==========================
-template <int NK, bool STATS>
-__global__ void __launch_bounds__(BT, 2) vote_batch_classify_kernel(const VoteParams p, int32_t* work,
-                                                                    unsigned int* work_count, int32_t* st_top,
-                                                                    float* st_lse, float* st_max) {
-  __shared__ Rec rec[SB];
-  __shared__ uint32_t uni[SB];
-  __shared__ uint32_t GE[32 * 8];        // GE[L][c] = {lo in [0,32) : popc(lo & L) >= c}
-  __shared__ uint32_t gcnt[1 << KM];     // correct votes of the current group per subset v
-  __shared__ uint32_t LW[32 * 32];       // LW[A][B] = {lo : best-ranked member of lo ∩ (A ∪ B) is in A}
-  __shared__ uint8_t LR[KM + 1];         // LR[r] = low models (m < 5) ranked better than r
-  __shared__ int8_t rnk[KM];             // rank of each model (0 = best), BEST_MEMBER tie rule
-  __shared__ uint16_t RS[2][64];         // model mask -> rank-order mask, 6 models per half
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int K = p.K, S = p.S, C = p.C;
-  const uint32_t kmask = (1u << K) - 1u;
-  const int gsz = p.gs > 0 ? p.gs : 16;
-  const int64_t N = p.N;
-  const int64_t nbatch = (N + SB - 1) / SB;
-  int64_t tail0 = N;
-  for (int bi = 0; bi < p.nB; ++bi) tail0 = p.tail_start[bi] < tail0 ? p.tail_start[bi] : tail0;
-  for (int i = t; i < 32 * 8; i += BT) {
-    const uint32_t L = (uint32_t)(i >> 3), c = (uint32_t)(i & 7);
-    uint32_t wd = 0;
-    for (uint32_t lo = 0; lo < 32; ++lo) wd |= ((uint32_t)__popc(lo & L) >= c ? 1u : 0u) << lo;
-    GE[i] = wd;
-  }
-  for (int i = t; i < (1 << K); i += BT) gcnt[i] = 0;
-  if (p.tie == 0) {
-    if (t == 0) {
-      uint32_t rem = kmask;
-      for (int r = 0; r < K; ++r) {
-        const int m = p.best_of[rem];
-        rnk[m] = (int8_t)r;
-        rem &= ~(1u << m);
-      }
-    }
-    __syncthreads();
-    if (t < 128) {
-      const int hf = t >> 6, x = t & 63;
-      uint32_t r = 0;
-      for (int b = 0; b < 6; ++b)
-        if (((x >> b) & 1) && 6 * hf + b < K) r |= 1u << rnk[6 * hf + b];
-      RS[hf][x] = (uint16_t)r;
-    }
-    if (t <= K) {
-      uint32_t lr = 0;
-      for (int m = 0; m < 5; ++m) lr |= (rnk[m] < t ? 1u : 0u) << m;
-      LR[t] = (uint8_t)lr;
-    }
-    for (int i = t; i < 32 * 32; i += BT) {
-      const uint32_t A = (uint32_t)i >> 5, B = (uint32_t)i & 31u;
-      uint32_t wd = 0;
-      for (uint32_t lo = 1; lo < 32; ++lo) {
-        const uint32_t s2 = lo & (A | B);
-        int best = -1, br = 1 << 30;
-        for (int m = 0; m < 5; ++m)
-          if (((s2 >> m) & 1u) && rnk[m] < br) { br = rnk[m]; best = m; }
-        if (best >= 0 && ((A >> best) & 1u)) wd |= 1u << lo;
-      }
-      LW[i] = wd;
-    }
-  }
-  uint32_t cv[NK], ca[NK];
-#pragma unroll
-  for (int k = 0; k < NK; ++k) { cv[k] = 0; ca[k] = 0; }
-
-  for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
-    const int64_t b0 = batch * SB;
-    __syncthreads();
-    for (int i = t; i < SB; i += BT) uni[i] = 0;
-    __syncthreads();
-    // ---- phase 1: per-sample records (warp per sample) --------------------------------------
-    uint32_t wl = 0;  // this warp's worklist samples (bit i <-> b = warp + NWB * i)
-#pragma unroll 1
-    for (int i = 0; i < SB / NWB; ++i) {
-      const int b = warp + NWB * i;
-      const int64_t n = b0 + b;
-      uint32_t fl = 0;
-      if (n < N) {
-        const int y = p.labels[n];
-        if (y < 0 || y >= C) {
-          if (lane == 0) atomicOr(p.err + 1, 1u);
-        } else {
-          const float* rowbase = p.logits + n * K * p.ldc;
-          int tp = 0;
-          float mx = 0.f, ls = 0.f;
-          bool bad = false;
-          if (STATS) {
-            if (lane < K) {
-              tp = p.top1_in[n * K + lane];
-              ls = p.lse_in[n * K + lane];
-              mx = p.rmax_in[n * K + lane];
-              bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
-            }
-          } else {
-            row_stats(p, rowbase, lane, tp, mx, ls, bad);
-            if (lane < K) { st_top[n * K + lane] = tp; st_lse[n * K + lane] = ls; st_max[n * K + lane] = mx; }
-          }
-          if (__any_sync(FULL, bad)) {
-            if (lane == 0) atomicOr(p.err, 1u);
-          } else {
-            const int c = lane < K ? tp : -1 - lane;
-            const uint32_t mm = __match_any_sync(FULL, c);
-            uint32_t tm = 0;
-            if (n >= tail0)
-              for (int bi = 0; bi < p.nB; ++bi)
-                if (n >= p.tail_start[bi]) tm |= 1u << bi;
-            if (__shfl_sync(FULL, mm, 0) == kmask) {  // unanimous (invariant I6)
-              fl = R_UNAN;
-              if (__shfl_sync(FULL, c, 0) == y) {
-                if (lane == 0) atomicAdd(&uni[b / gsz], 1u);
-                if (tm)
-                  for (int bi = 0; bi < p.nB; ++bi)
-                    if ((tm >> bi) & 1u)
-                      for (int v1 = lane; v1 < S; v1 += 32) atomicAdd(p.tail + (size_t)bi * S + v1, 1ull);
-              }
-            } else {
-              const float thr = theta_threshold(mx, ls, K, lane);
-              if (__any_sync(FULL, lane < K && rowbase[(size_t)lane * p.ldc + y] >= thr)) wl |= 1u << i;
-              if (__any_sync(FULL, lane < K && c == y)) {
-                fl = R_EVAL;
-                const bool other = lane < K && (__ffs(mm) - 1) == lane && c != y;  // one lane per other class
-                const uint32_t ob = __ballot_sync(FULL, other);
-                const uint32_t ltb = __ballot_sync(FULL, other && c < y);
-                if (other) rec[b].mo[__popc(ob & ((1u << lane) - 1u))] = mm;
-                if (lane < K && c == y && (__ffs(mm) - 1) == lane) rec[b].my = mm;
-                if (lane == 0) {
-                  rec[b].no = __popc(ob);
-                  rec[b].tm = tm;
-                  // lt bit j refers to the j-th other class in lane order
-                  uint32_t lt = 0;
-                  for (uint32_t w = ob, j = 0; w; w &= w - 1, ++j)
-                    if ((ltb >> (__ffs(w) - 1)) & 1u) lt |= 1u << j;
-                  rec[b].lt = lt;
-                }
-              }
-            }
-          }
-        }
-      }
-      if (lane == 0) rec[b].flags = fl;
-    }
-    if (wl) {  // worklist append: one atomic per warp per batch
-      unsigned int base = 0;
-      if (lane == 0) base = atomicAdd(work_count, (unsigned int)__popc(wl));
-      base = __shfl_sync(FULL, base, 0);
-      if (lane < SB / NWB && ((wl >> lane) & 1u))
-        work[base + __popc(wl & ((1u << lane) - 1u))] = (int32_t)(b0 + warp + NWB * lane);
-    }
-    __syncthreads();
-    // ---- phase 2 (bit-sliced): thread t owns the 32-subset word w = t mod 2^(K-5) -- subsets
-    //      v = 32w + lo, the low 5 models <-> bits of lo, the high models <-> bits of w -- for the
-    //      samples b = t / 2^(K-5) (mod lanes) of each group. Per class, the member count over v is
-    //      popc(lo & L) + popc(w & H): the lo-part comes from the constant table GE, so a whole word
-    //      of comparisons costs a few logic ops. Per-subset counts accumulate in a vertical counter
-    //      and are folded into the shared per-subset group counts at each group end.
-    const int nwd = 1 << (K - 5), nsl = BT / nwd;
-    const uint32_t w = (uint32_t)t & (uint32_t)(nwd - 1);
-    const int sl = t / nwd;
-    const uint32_t validw = w == 0 ? ~1u : ~0u;  // v = 0 is not a subset
-    uint32_t hwr = 0;  // this word's high models, in rank order
-    if (p.tie == 0)
-      for (int m = 5; m < K; ++m)
-        if ((w >> (m - 5)) & 1u) hwr |= 1u << rnk[m];
-    const int ngroups = SB / gsz;
-#pragma unroll 1
-    for (int g = 0; g < ngroups; ++g) {
-      uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;  // vertical counter (<= 16 samples per thread)
-#pragma unroll 1
-      for (int b = g * gsz + sl; b < (g + 1) * gsz; b += nsl) {
-        if (!(rec[b].flags & R_EVAL)) continue;
-        // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|, y wins iff
-        // c_y > 0, no class has more votes, and the tie (if any) goes to y: LOWEST_CLASS -> no tied
-        // class below y; BEST_MEMBER -> the best-ranked member among all tied voters votes y (Q2).
-        const uint32_t my = rec[b].my, lt = rec[b].lt, Ly = my & 31u;
-        const int hy = __popc(w & (my >> 5));
-        const int ny = __popc(Ly);
-        const uint32_t* GY = GE + Ly * 8;
-        uint32_t lose = hy == 0 ? ~GY[1] : 0u;  // c_y == 0
-        const int no = rec[b].no;
-#pragma unroll 1
-        for (int j = 0; j < no; ++j) {
-          const uint32_t Mj = rec[b].mo[j];
-          const uint32_t* GJ = GE + (Mj & 31u) * 8;
-          const int d = hy - __popc(w & (Mj >> 5));  // c_j > c_y  <=>  x_j >= x_y + d + 1
-          uint32_t gt = 0, eq = 0;
-#pragma unroll 1
-          for (int a = 0; a <= ny; ++a) {
-            const uint32_t ya = GY[a] & ~GY[a + 1];  // x_y == a
-            const int k = a + d + 1;
-            const uint32_t gk = k <= 0 ? ~0u : (k >= 8 ? 0u : GJ[k]);
-            const uint32_t ek = (k - 1 < 0 || k - 1 >= 8) ? 0u : (GJ[k - 1] & ~gk);
-            gt |= ya & gk;
-            eq |= ya & ek;
-          }
-          lose |= gt;
-          if (p.tie != 0) {
-            if ((lt >> j) & 1u) lose |= eq;
-          } else if (eq & ~lose) {
-            // tie race: is the best-ranked member of v ∩ (M_y ∪ M_j) a y voter? The high members are
-            // fixed by w: the best of them (rank rh) wins unless a low member ranked better is in lo.
-            const uint32_t myr = RS[0][my & 63u] | RS[1][my >> 6];
-            const uint32_t hr = (myr | RS[0][Mj & 63u] | RS[1][Mj >> 6]) & hwr;
-            const int rh = hr ? __ffs(hr) - 1 : K;
-            const bool hiy = hr && ((myr >> rh) & 1u);
-            const uint32_t lr = LR[rh];
-            const uint32_t A = Ly & lr, Bm = Mj & 31u & lr;
-            const uint32_t ywin = LW[(A << 5) | Bm] | (hiy ? ~GE[(A | Bm) * 8 + 1] : 0u);
-            lose |= eq & ~ywin;
-          }
-        }
-        const uint32_t ok = ~lose & validw;
-        uint32_t c = ok, x;  // vertical counter += ok
-        x = k0 & c; k0 ^= c; c = x;
-        x = k1 & c; k1 ^= c; c = x;
-        x = k2 & c; k2 ^= c; c = x;
-        x = k3 & c; k3 ^= c; c = x;
-        k4 ^= c;
-        if (ok && rec[b].tm) tail_add_word(p, rec[b].tm, w, ok);
-      }
-      if (k0 | k1 | k2 | k3 | k4) {
-        for (uint32_t lo = 0; lo < 32; ++lo) {
-          const uint32_t cnt = ((k0 >> lo) & 1u) | (((k1 >> lo) & 1u) << 1) | (((k2 >> lo) & 1u) << 2) |
-                               (((k3 >> lo) & 1u) << 3) | (((k4 >> lo) & 1u) << 4);
-          if (cnt) atomicAdd(&gcnt[(w << 5) | lo], cnt);
-        }
-      }
-      __syncthreads();
-      // group end: labelled-moment group counts and totals
-      const int64_t gi = (b0 + (int64_t)g * gsz) / gsz;
-      const uint32_t u = uni[g];
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const int v1 = t + BT * k;
-        if (v1 < S) {
-          if (b0 + (int64_t)g * gsz < N) {
-            const uint32_t tot = gcnt[v1 + 1] + u;
-            if (p.grp) p.grp[gi * S + v1] = (uint8_t)tot;
-            cv[k] += tot;
-            ca[k] += u;
-          }
-          gcnt[v1 + 1] = 0;
-        }
-      }
-      __syncthreads();
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NK; ++k) {
-    const int v1 = t + BT * k;
-    if (v1 < S) {
-      if (cv[k]) atomicAdd(p.cnt_vote + v1, (unsigned long long)cv[k]);
-      if (ca[k]) atomicAdd(p.cnt_avg + v1, (unsigned long long)ca[k]);
-    }
-  }
-}
-
-// ======================= kernel A': classify + votes, one warp per 16-sample chunk =================
-// Same per-sample records and the same bit-sliced word evaluation as vote_batch_classify_kernel, but a
-// warp owns 16 consecutive samples (whole count groups, gs | 16) and lane l owns the 32-subset words
-// w = l + 32 i of every one of them: no block barrier at all; per-group counts leave the vertical bit
-// counters through a multiply-spread bit->byte transposition into the warp's staging row, which is
-// copied out coalesced (grp) and added to the CTA's per-subset totals.
+// ======================= kernel A: classify + votes, one warp per 16-sample chunk ==================
+// A warp owns 16 consecutive samples (whole count groups, gs | 16): it builds each sample's vote record
+// (row statistics, distinct-class voter masks) and lane l evaluates the 32-subset words w = l + 32 i
+// (subsets v = 32w + lo: the low 5 models <-> bits of lo, the high models <-> bits of w) of every one
+// of them -- no block barrier. Per-subset correct counts accumulate in vertical bit counters and leave
+// them at each group end through a multiply-spread bit->byte transposition into the warp's staging
+// row, which is copied out coalesced (grp, labelled moments) and added to the CTA's per-subset totals.
+// (An earlier batch-transposed layout -- threads owning a word across a 128-sample batch in shared
+// memory, two block barriers per 16 samples -- measured 5 ms per 1M samples at K = 12 against 2.5.)
 constexpr int CH = 16;  // samples per warp chunk
 struct WRec {  // one sample's vote record (warp-private)
   uint32_t my, lt, tm;
@@ -459,7 +184,7 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
     for (int i = 0; i < CH; ++i) {
       const int64_t n = n0 + i;
       if (n < N) {
-        // ---- phase 1: the sample's record (as in vote_batch_classify_kernel) -----------------------
+        // ---- phase 1: the sample's record ----------------------------------------------------------
         bool eval = false;
         const int y = p.labels[n];
         if (y < 0 || y >= C) {
@@ -559,7 +284,9 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
               lose[wi] |= ~g;
               if (p.tie != 0) {
                 if ((lt >> j) & 1u) lose[wi] |= eq;
-              } else if (eq & ~lose[wi]) {  // tie race (reading Q2), as in vote_batch_classify_kernel
+              } else if (eq & ~lose[wi]) {
+                // tie race (reading Q2): is the best-ranked member of v ∩ (M_y ∪ M_j) a y voter? The high
+                // members are fixed by w: the best of them (rank rh) wins unless a better low member is in lo
                 const uint32_t myr = RS[0][my & 63u] | RS[1][my >> 6];
                 const uint32_t hr = (myr | RS[0][Mj & 63u] | RS[1][Mj >> 6]) & hwr[wi];
                 const int rh = hr ? __ffs(hr) - 1 : K;
@@ -645,23 +372,17 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
     const int64_t nb = (p.N + SB - 1) / SB;
     const int grid = (int)(nb < (int64_t)sm_count * 2 ? nb : (int64_t)sm_count * 2);
     constexpr int NWL = NK / 4 > 0 ? NK / 4 : 1;  // words per lane: 2^(K-5) / 32 (K = 9: half the lanes idle)
-    if (!getenv("RK_VOTE_BATCHED")) {             // env: the older batch-transposed kernel (comparison)
-      const int dsm = NWB << p.K;
-      if (p.lse_in) {
-        if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, dsm)) != cudaSuccess)
-          return e;
-        vote_group_classify_kernel<NWL, true><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
-      } else {
-        if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, dsm)) != cudaSuccess)
-          return e;
-        vote_group_classify_kernel<NWL, false><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
-      }
-    } else if (p.lse_in) {
-      vote_batch_classify_kernel<NK, true><<<grid, BT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+    const int dsm = NWB << p.K;
+    if (p.lse_in) {
+      if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dsm)) != cudaSuccess)
+        return e;
+      vote_group_classify_kernel<NWL, true><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
     } else {
-      vote_batch_classify_kernel<NK, false><<<grid, BT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+      if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dsm)) != cudaSuccess)
+        return e;
+      vote_group_classify_kernel<NWL, false><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

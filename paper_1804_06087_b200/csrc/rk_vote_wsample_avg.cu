@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(WT) vote_pair_recheck_kernel(const VoteParams 
     const int y = p.labels[n];
     const float* rb = p.logits + n * K * p.ldc;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (uint32_t mm = v; mm; mm &= mm - 1) {  // ascending member order, as the oracle sums
+    for (uint32_t mm = v; mm; mm &= mm - 1) {  // ascending member order
       const int m = __ffs(mm) - 1;
       const float4 x = lane_ok ? *reinterpret_cast<const float4*>(rb + m * p.ldc + 4 * lane)
                                : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
