@@ -32,8 +32,8 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WT = 256;      // threads per CTA
 constexpr int WWARPS = WT / 32;
-constexpr int NG = 3;        // float4 column groups
-constexpr int WC = 4 * NG;   // table columns: y + up to 11 competitors
+constexpr int NGR = 3;       // column groups whose TA values stay in registers (the rest: the warp's TAX slice)
+constexpr int NGMAX = 5;
 constexpr int KM = 12;
 
 __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
@@ -59,9 +59,16 @@ struct Geo {
   static constexpr int NWS = NB / NBW;                  // words per a-slot
   static constexpr int NW = NA * NWS;                   // decision words per lane
   static constexpr int S = (1 << K) - 1;
+  // float4 column groups: y + up to 4*NG - 1 competitors. K = 12 keeps 3 (two a-slots per lane; a
+  // 4th/5th group measured slower there: register pressure), K <= 11 takes 5 (fewer CTA-kernel samples)
+  static constexpr int NG = K == 12 ? 3 : NGMAX;
+  static constexpr int WC = 4 * NG;
 };
 
+template <int NG>
 struct WarpSmem {
+  static constexpr int WC = 4 * NG;
+  float4 TAX[NG > NGR ? 64 * (NG - NGR) : 1];  // TA rows' column groups NGR.. (a < 2^K1 <= 64)
   float P[KM * WC];    // p[m][j] of the sample's columns (j = 0: y), zero-padded
   int32_t cols[WC];    // c_j (j = 0: y, then R ascending)
   float ls[KM];        // lse per model
@@ -75,11 +82,12 @@ __device__ __forceinline__ uint32_t subset_of(int lane, int s, int bi) {
   return a | (b << G::K1);
 }
 
-// the lane's decision sweep over b for one column-group count NQ (1..NG)
+// the lane's decision sweep over b for one column-group count NQ (1..G::NG)
 template <int K, int NQ>
-__device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NG], const float* TB, int lane, float bl, float bh,
-                                      uint32_t (&win)[Geo<K>::NW], uint32_t (&pen)[Geo<K>::NW]) {
+__device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NGR], const float4* TAX, const float* TB, int lane,
+                                      float bl, float bh, uint32_t (&win)[Geo<K>::NW], uint32_t (&pen)[Geo<K>::NW]) {
   using G = Geo<K>;
+  constexpr int NG = G::NG, WC = G::WC;
   const int b0 = G::TAn < 32 ? lane / G::TAn : 0;
 #pragma unroll
   for (int ws = 0; ws < G::NWS; ++ws) {
@@ -108,6 +116,13 @@ __device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NG], const 
           mc = max3f(mc, s2.x, s2.y);
           mc = max3f(mc, s2.z, s2.w);
         }
+#pragma unroll
+        for (int g = NGR; g < NQ; ++g) {  // groups 3..: TA values from the warp's shared slice
+          const uint32_t a = G::TAn >= 32 ? (uint32_t)(lane + 32 * s) : (uint32_t)(lane & (G::TAn - 1));
+          const float4 sg = add4(TAX[a * (NG - NGR) + (g - NGR)], B[g]);
+          mc = max3f(mc, sg.x, sg.y);
+          mc = max3f(mc, sg.z, sg.w);
+        }
         const float sy = s0.x;
         // r < 0: clear win; r >= 0 > r2: near-tie; r2 >= 0: clear loss (sums are >= 1e-30 here)
         const float r = fmaf(-sy, bl, mc), r2 = fmaf(-sy, bh, mc);
@@ -128,6 +143,8 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
                                                                      const unsigned int* work_count,
                                                                      int32_t* cta_work, unsigned int* cta_count) {
   using G = Geo<K>;
+  constexpr int NG = G::NG, WC = G::WC;
+  using WarpSmem = rk::WarpSmem<NG>;
   extern __shared__ __align__(16) char dyn[];
   uint32_t* cnt = reinterpret_cast<uint32_t*>(dyn);                       // [2^K] per-CTA counts
   float* TBall = reinterpret_cast<float*>(dyn + (size_t)(G::S + 1) * 4);  // [warps][TBn][WC]
@@ -137,6 +154,7 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
   const int64_t ldc = p.ldc;
   float* TB = TBall + (size_t)warp * G::TBn * WC;
   float* P = wsm[warp].P;
+  float4* TAX = wsm[warp].TAX;
   const float bh = 1.f + p.band, bl = 1.f - p.band;
   for (int i = t; i <= G::S; i += WT) cnt[i] = 0;
   __syncthreads();
@@ -264,7 +282,7 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
         reinterpret_cast<float4*>(TB + b * WC)[g] = s;
       }
     }
-    float4 ar[G::NA][NG];
+    float4 ar[G::NA][NGR];
 #pragma unroll
     for (int s = 0; s < G::NA; ++s) {
       const uint32_t a = G::TAn >= 32 ? (uint32_t)(lane + 32 * s) : (uint32_t)(lane & (G::TAn - 1));
@@ -276,15 +294,20 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
           for (int i = 0; i < G::K1; ++i)
             if ((a >> i) & 1u) acc = add4(acc, P4[i * NG + g]);
         }
-        ar[s][g] = acc;
+        if (g < NGR) ar[s][g] = acc;
+        else if (g < nq && (G::TAn >= 32 || lane < G::TAn)) TAX[a * (NG - NGR) + (g - NGR)] = acc;
       }
     }
     __syncwarp();
     // ---- S6: every subset of the lane ------------------------------------------------------------
     uint32_t win[G::NW], pen[G::NW];
-    if (nq == 1) sweep<K, 1>(ar, TB, lane, bl, bh, win, pen);
-    else if (nq == 2) sweep<K, 2>(ar, TB, lane, bl, bh, win, pen);
-    else sweep<K, 3>(ar, TB, lane, bl, bh, win, pen);
+    switch (nq) {
+      case 1: sweep<K, 1>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      case 2: sweep<K, 2>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      case 3: sweep<K, 3>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      case 4: sweep<K, NG >= 4 ? 4 : NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      default: sweep<K, NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+    }
     uint32_t pq[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int i = 0; i < G::NW; ++i) pq[i] = pen[i] & valid[i];
@@ -401,7 +424,7 @@ __global__ void __launch_bounds__(WT) vote_pair_recheck_kernel(const VoteParams 
 template <int K>
 size_t smem_bytes() {
   using G = Geo<K>;
-  return (size_t)(G::S + 1) * 4 + (size_t)WWARPS * G::TBn * WC * 4 + (size_t)WWARPS * sizeof(WarpSmem);
+  return (size_t)(G::S + 1) * 4 + (size_t)WWARPS * G::TBn * G::WC * 4 + (size_t)WWARPS * sizeof(WarpSmem<G::NG>);
 }
 
 template <int K>
