@@ -81,8 +81,11 @@ cudaError_t launch_vote_cta_avg(const VoteParams& q, int sm_count, cudaStream_t 
 // launch_vote_pair_recheck (fp64, one warp per pair, from the definition).
 bool vote_wsample_avg_supported(const VoteParams& q);
 cudaError_t launch_vote_pair_recheck(const VoteParams& q, int sm_count, cudaStream_t st);
-cudaError_t launch_vote_wsample_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
-                                    const unsigned int* work_count, int32_t* cta_work, unsigned int* cta_count);
+// The samples left for the CTA kernel are returned in (*rest, *rest_count): cta_work, or (K = 12, after
+// a second wide pass that consumes cta_work) the reused worklist buffer.
+cudaError_t launch_vote_wsample_avg(const VoteParams& q, int sm_count, cudaStream_t st, int32_t* work,
+                                    unsigned int* work_count, int32_t* cta_work, unsigned int* cta_count,
+                                    const int32_t** rest, const unsigned int** rest_count);
 
 // Two kernels: classify+votes over all samples, then averages over the worklist of samples whose
 // label is an averaging candidate. work: [N] int32, work_count: 1 uint; st_*: [N][K] statistics

@@ -390,11 +390,13 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
     VoteParams q = p;
     if (!p.lse_in) { q.top1_in = st_top; q.lse_in = st_lse; q.rmax_in = st_max; }
     if (vote_wsample_avg_supported(q)) {  // few competitors: warp per sample; the rest -> CTA kernel
-      if ((e = launch_vote_wsample_avg(q, sm_count, st, work, work_count, p.cta_work, p.cta_count)) != cudaSuccess)
+      const int32_t* rest = nullptr;
+      const unsigned int* rest_count = nullptr;
+      if ((e = launch_vote_wsample_avg(q, sm_count, st, work, work_count, p.cta_work, p.cta_count, &rest,
+                                       &rest_count)) != cudaSuccess)
         return e;
       if ((e = launch_vote_pair_recheck(q, sm_count, st)) != cudaSuccess) return e;
-      if ((e = launch_vote_cta_avg(q, sm_count, st, p.cta_work, p.cta_count, p.ovf_work, p.ovf_count)) != cudaSuccess)
-        return e;
+      if ((e = launch_vote_cta_avg(q, sm_count, st, rest, rest_count, p.ovf_work, p.ovf_count)) != cudaSuccess) return e;
     } else if ((e = launch_vote_cta_avg(q, sm_count, st, work, work_count, p.ovf_work, p.ovf_count)) != cudaSuccess) {
       return e;
     }

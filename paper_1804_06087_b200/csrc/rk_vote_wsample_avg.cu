@@ -32,8 +32,10 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WT = 256;      // threads per CTA
 constexpr int WWARPS = WT / 32;
-constexpr int NGR = 3;       // column groups whose TA values stay in registers (the rest: the warp's TAX slice)
-constexpr int NGMAX = 5;
+// Column groups (float4 each): y + up to 4*NG - 1 competitors; the first NR groups of the lane's TA
+// rows stay in registers, the rest are read from the warp's TAX slice. Instantiations: K <= 11 <5, 3>;
+// K = 12 (two a-slots per lane) <3, 3>, then a second pass <5, 0> over the samples it handed on (a
+// 4th/5th register group measured slower at K = 12: register pressure).
 constexpr int KM = 12;
 
 __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
@@ -59,16 +61,12 @@ struct Geo {
   static constexpr int NWS = NB / NBW;                  // words per a-slot
   static constexpr int NW = NA * NWS;                   // decision words per lane
   static constexpr int S = (1 << K) - 1;
-  // float4 column groups: y + up to 4*NG - 1 competitors. K = 12 keeps 3 (two a-slots per lane; a
-  // 4th/5th group measured slower there: register pressure), K <= 11 takes 5 (fewer CTA-kernel samples)
-  static constexpr int NG = K == 12 ? 3 : NGMAX;
-  static constexpr int WC = 4 * NG;
 };
 
-template <int NG>
+template <int NG, int NR>
 struct WarpSmem {
   static constexpr int WC = 4 * NG;
-  float4 TAX[NG > NGR ? 64 * (NG - NGR) : 1];  // TA rows' column groups NGR.. (a < 2^K1 <= 64)
+  float4 TAX[NG > NR ? 64 * (NG - NR) : 1];  // TA rows' column groups NR.. (a < 2^K1 <= 64)
   float P[KM * WC];    // p[m][j] of the sample's columns (j = 0: y), zero-padded
   int32_t cols[WC];    // c_j (j = 0: y, then R ascending)
   float ls[KM];        // lse per model
@@ -82,12 +80,13 @@ __device__ __forceinline__ uint32_t subset_of(int lane, int s, int bi) {
   return a | (b << G::K1);
 }
 
-// the lane's decision sweep over b for one column-group count NQ (1..G::NG)
-template <int K, int NQ>
-__device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NGR], const float4* TAX, const float* TB, int lane,
-                                      float bl, float bh, uint32_t (&win)[Geo<K>::NW], uint32_t (&pen)[Geo<K>::NW]) {
+// the lane's decision sweep over b for one column-group count NQ (1..NG)
+template <int K, int NG, int NR, int NQ>
+__device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NR > 0 ? NR : 1], const float4* TAX, const float* TB,
+                                      int lane, float bl, float bh, uint32_t (&win)[Geo<K>::NW],
+                                      uint32_t (&pen)[Geo<K>::NW]) {
   using G = Geo<K>;
-  constexpr int NG = G::NG, WC = G::WC;
+  constexpr int WC = 4 * NG, NX = NG - NR;
   const int b0 = G::TAn < 32 ? lane / G::TAn : 0;
 #pragma unroll
   for (int ws = 0; ws < G::NWS; ++ws) {
@@ -98,32 +97,25 @@ __device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NGR], const
     for (int j = 0; j < G::NBW; ++j) {
       const int b = b0 + G::LPA * (ws * G::NBW + j);
       const float4* B = reinterpret_cast<const float4*>(TB + b * WC);
-      const float4 b0v = B[0];
-      float4 b1v, b2v;
-      if (NQ > 1) b1v = B[1];
-      if (NQ > 2) b2v = B[2];
+      float4 bv[NQ];
+#pragma unroll
+      for (int g = 0; g < NQ; ++g) bv[g] = B[g];
 #pragma unroll
       for (int s = 0; s < G::NA; ++s) {
-        const float4 s0 = add4(ar[s][0], b0v);
-        float mc = max3f(s0.y, s0.z, s0.w);
-        if (NQ > 1) {
-          const float4 s1 = add4(ar[s][1], b1v);
-          mc = max3f(mc, s1.x, s1.y);
-          mc = max3f(mc, s1.z, s1.w);
-        }
-        if (NQ > 2) {
-          const float4 s2 = add4(ar[s][2], b2v);
-          mc = max3f(mc, s2.x, s2.y);
-          mc = max3f(mc, s2.z, s2.w);
-        }
+        const uint32_t a = G::TAn >= 32 ? (uint32_t)(lane + 32 * s) : (uint32_t)(lane & (G::TAn - 1));
+        float sy = 0.f, mc = 0.f;
 #pragma unroll
-        for (int g = NGR; g < NQ; ++g) {  // groups 3..: TA values from the warp's shared slice
-          const uint32_t a = G::TAn >= 32 ? (uint32_t)(lane + 32 * s) : (uint32_t)(lane & (G::TAn - 1));
-          const float4 sg = add4(TAX[a * (NG - NGR) + (g - NGR)], B[g]);
-          mc = max3f(mc, sg.x, sg.y);
-          mc = max3f(mc, sg.z, sg.w);
+        for (int g = 0; g < NQ; ++g) {
+          const float4 av = g < NR ? ar[s][g < NR ? g : 0] : TAX[a * NX + (g - NR)];
+          const float4 sg = add4(av, bv[g]);
+          if (g == 0) {
+            sy = sg.x;
+            mc = max3f(sg.y, sg.z, sg.w);
+          } else {
+            mc = max3f(mc, sg.x, sg.y);
+            mc = max3f(mc, sg.z, sg.w);
+          }
         }
-        const float sy = s0.x;
         // r < 0: clear win; r >= 0 > r2: near-tie; r2 >= 0: clear loss (sums are >= 1e-30 here)
         const float r = fmaf(-sy, bl, mc), r2 = fmaf(-sy, bh, mc);
         w[s] = __funnelshift_l(__float_as_uint(r), w[s], 1);
@@ -138,13 +130,13 @@ __device__ __forceinline__ void sweep(const float4 (&ar)[Geo<K>::NA][NGR], const
   }
 }
 
-template <int K>
+template <int K, int NG, int NR>
 __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteParams p, const int32_t* work,
                                                                      const unsigned int* work_count,
                                                                      int32_t* cta_work, unsigned int* cta_count) {
   using G = Geo<K>;
-  constexpr int NG = G::NG, WC = G::WC;
-  using WarpSmem = rk::WarpSmem<NG>;
+  constexpr int WC = 4 * NG;
+  using WarpSmem = rk::WarpSmem<NG, NR>;
   extern __shared__ __align__(16) char dyn[];
   uint32_t* cnt = reinterpret_cast<uint32_t*>(dyn);                       // [2^K] per-CTA counts
   float* TBall = reinterpret_cast<float*>(dyn + (size_t)(G::S + 1) * 4);  // [warps][TBn][WC]
@@ -282,7 +274,7 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
         reinterpret_cast<float4*>(TB + b * WC)[g] = s;
       }
     }
-    float4 ar[G::NA][NGR];
+    float4 ar[G::NA][NR > 0 ? NR : 1];
 #pragma unroll
     for (int s = 0; s < G::NA; ++s) {
       const uint32_t a = G::TAn >= 32 ? (uint32_t)(lane + 32 * s) : (uint32_t)(lane & (G::TAn - 1));
@@ -294,19 +286,19 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
           for (int i = 0; i < G::K1; ++i)
             if ((a >> i) & 1u) acc = add4(acc, P4[i * NG + g]);
         }
-        if (g < NGR) ar[s][g] = acc;
-        else if (g < nq && (G::TAn >= 32 || lane < G::TAn)) TAX[a * (NG - NGR) + (g - NGR)] = acc;
+        if (g < NR) ar[s][g < NR ? g : 0] = acc;
+        else if (g < nq && (G::TAn >= 32 || lane < G::TAn)) TAX[a * (NG - NR) + (g - NR)] = acc;
       }
     }
     __syncwarp();
     // ---- S6: every subset of the lane ------------------------------------------------------------
     uint32_t win[G::NW], pen[G::NW];
     switch (nq) {
-      case 1: sweep<K, 1>(ar, TAX, TB, lane, bl, bh, win, pen); break;
-      case 2: sweep<K, 2>(ar, TAX, TB, lane, bl, bh, win, pen); break;
-      case 3: sweep<K, 3>(ar, TAX, TB, lane, bl, bh, win, pen); break;
-      case 4: sweep<K, NG >= 4 ? 4 : NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
-      default: sweep<K, NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      case 1: sweep<K, NG, NR, 1>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      case 2: sweep<K, NG, NR, NG >= 2 ? 2 : NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      case 3: sweep<K, NG, NR, NG >= 3 ? 3 : NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      case 4: sweep<K, NG, NR, NG >= 4 ? 4 : NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
+      default: sweep<K, NG, NR, NG>(ar, TAX, TB, lane, bl, bh, win, pen); break;
     }
     uint32_t pq[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -421,24 +413,20 @@ __global__ void __launch_bounds__(WT) vote_pair_recheck_kernel(const VoteParams 
   }
 }
 
-template <int K>
-size_t smem_bytes() {
-  using G = Geo<K>;
-  return (size_t)(G::S + 1) * 4 + (size_t)WWARPS * G::TBn * G::WC * 4 + (size_t)WWARPS * sizeof(WarpSmem<G::NG>);
-}
-
-template <int K>
+template <int K, int NG, int NR>
 cudaError_t launch_k(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
                      const unsigned int* work_count, int32_t* cta_work, unsigned int* cta_count) {
-  const size_t smem = smem_bytes<K>();
-  cudaError_t e = cudaFuncSetAttribute(vote_wsample_average_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  using G = Geo<K>;
+  const size_t smem =
+      (size_t)(G::S + 1) * 4 + (size_t)WWARPS * G::TBn * 4 * NG * 4 + (size_t)WWARPS * sizeof(WarpSmem<NG, NR>);
+  cudaError_t e = cudaFuncSetAttribute(vote_wsample_average_kernel<K, NG, NR>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vote_wsample_average_kernel<K>, WT, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vote_wsample_average_kernel<K, NG, NR>, WT, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  vote_wsample_average_kernel<K><<<sm_count * per_sm, WT, smem, st>>>(q, work, work_count, cta_work, cta_count);
+  vote_wsample_average_kernel<K, NG, NR><<<sm_count * per_sm, WT, smem, st>>>(q, work, work_count, cta_work, cta_count);
   return cudaGetLastError();
 }
 
@@ -453,13 +441,23 @@ cudaError_t launch_vote_pair_recheck(const VoteParams& q, int sm_count, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_vote_wsample_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
-                                    const unsigned int* work_count, int32_t* cta_work, unsigned int* cta_count) {
+cudaError_t launch_vote_wsample_avg(const VoteParams& q, int sm_count, cudaStream_t st, int32_t* work,
+                                    unsigned int* work_count, int32_t* cta_work, unsigned int* cta_count,
+                                    const int32_t** rest, const unsigned int** rest_count) {
+  *rest = cta_work;
+  *rest_count = cta_count;
   switch (q.K) {
-    case 9: return launch_k<9>(q, sm_count, st, work, work_count, cta_work, cta_count);
-    case 10: return launch_k<10>(q, sm_count, st, work, work_count, cta_work, cta_count);
-    case 11: return launch_k<11>(q, sm_count, st, work, work_count, cta_work, cta_count);
-    case 12: return launch_k<12>(q, sm_count, st, work, work_count, cta_work, cta_count);
+    case 9: return launch_k<9, 5, 3>(q, sm_count, st, work, work_count, cta_work, cta_count);
+    case 10: return launch_k<10, 5, 3>(q, sm_count, st, work, work_count, cta_work, cta_count);
+    case 11: return launch_k<11, 5, 3>(q, sm_count, st, work, work_count, cta_work, cta_count);
+    case 12: {  // 3 register groups, then the samples with 12..19 columns from shared-memory TA rows
+      cudaError_t e = launch_k<12, 3, 3>(q, sm_count, st, work, work_count, cta_work, cta_count);
+      if (e == cudaSuccess) e = cudaMemsetAsync(work_count, 0, sizeof(unsigned int), st);  // work is consumed
+      if (e == cudaSuccess) e = launch_k<12, 5, 0>(q, sm_count, st, cta_work, cta_count, work, work_count);
+      *rest = work;
+      *rest_count = work_count;
+      return e;
+    }
     default: return cudaErrorInvalidValue;
   }
 }
