@@ -65,6 +65,7 @@ struct rk_ctx {
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[4 * 128];
   int cta_cols = 52;                   // K >= 9 CTA averaging: column capacity (env RK_CTA_AVG_COLS, tests)
+  int64_t pair_cap_test = 0;           // K >= 9: near-tie pair list capacity override (env RK_PAIR_CAP, tests)
   int gemm_cluster = 2;                // head GEMM: 2 = CTA pair (tcgen05 cta_group::2, M = 256), 1 = single CTA (env RK_GEMM_CLUSTER)
   cudaStream_t copy_stream = nullptr;  // H2D of host X, overlapped with the GEMM
   cudaEvent_t ev_start = nullptr;
@@ -225,6 +226,8 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
   // tests only: a smaller column capacity of the K >= 9 CTA averaging kernel routes more samples through
   // the overflow kernel (rk_vote_batch_avg.cu), so both paths stay covered
   if (const char* cc = getenv("RK_CTA_AVG_COLS")) ctx->cta_cols = std::max(4, std::min(52, atoi(cc) / 4 * 4));
+  // tests only: a tiny near-tie pair list makes the warp averaging kernel hand whole samples to the CTA kernel
+  if (const char* pc = getenv("RK_PAIR_CAP")) ctx->pair_cap_test = std::max(1, atoi(pc));
   if (nccl_unique_id) {  // world ranks (world may be 1: a one-rank communicator, same code path)
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
@@ -592,7 +595,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       if (!warp_path) {  // near-tie pairs of the warp averaging kernel (a full list sends samples to the CTA kernel)
         if ((s = ensure(ctx, &ctx->d_pairs, &ctx->pairs_cap, N / 2 + 65536)) != RK_OK) return s;
         vp.pairs = ctx->d_pairs;
-        vp.pair_cap = ctx->pairs_cap;
+        vp.pair_cap = ctx->pair_cap_test > 0 ? std::min<int64_t>(ctx->pair_cap_test, ctx->pairs_cap) : ctx->pairs_cap;
         vp.pair_count = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 3);
       }
       int32_t* st_top = nullptr;

@@ -110,6 +110,23 @@ def test_cta_average_overflow_route(rk, monkeypatch, cols):
     compare_tables(t, o, K=K)
 
 
+@pytest.mark.parametrize("cap", [1, 5])
+def test_pair_list_full(rk, monkeypatch, cap):
+    """K >= 9, C <= 128: near-tie (sample, subset) pairs go to the fp64 pair kernel; when the list is full
+    the warp kernel hands the whole sample to the CTA kernel and marks its reserved slots as skipped
+    (RK_PAIR_CAP shrinks the list). Ties are forced with integer logits."""
+    K, C, N = 10, 8, 300
+    monkeypatch.setenv("RK_PAIR_CAP", str(cap))
+    rng = np.random.default_rng(27)
+    L = rng.integers(0, 3, size=(N, K, C)).astype(np.float32)
+    y = rng.integers(0, C, N).astype(np.int32)
+    gcfg, ocfg = default_cfg(K)
+    t, _ = run_vote(rk, L, y, K, C, cfg=gcfg)
+    o = oracle.table(L, y, K, C, cfg=ocfg)
+    compare_tables(t, o, K=K)
+    assert t["n_recheck"].sum() > 0
+
+
 @pytest.mark.parametrize("K", [8, 12])
 def test_tiny_label_probabilities(rk, K):
     """Steep logits (x40 on every third sample): p[m][y] underflows fp32 for some models, so subset sums
