@@ -240,6 +240,8 @@ def main():
         t = step()
     e1.record(stream)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     ms = e0.elapsed_time(e1)
     ks = ctx.kernel_stats()
     ctx.set_profiling(False)
