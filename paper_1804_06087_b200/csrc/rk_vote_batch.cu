@@ -180,27 +180,40 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
 #pragma unroll
     for (int i = 0; i < NWL; ++i) k0[i] = k1[i] = k2[i] = k3[i] = k4[i] = 0;
     uint32_t u = 0, wl = 0;
+    // the chunk's labels (lane i: sample n0 + i), and the next sample's statistics and l[m][y] loaded one
+    // sample ahead (STATS): the per-sample dependent load chain leaves the critical path
+    const int ylane = (lane < CH && n0 + lane < N) ? p.labels[n0 + lane] : 0;
+    int ntp = 0;
+    float nls = 0.f, nmx = 0.f, nly = 0.f;
+    auto prefetch = [&](int i) {
+      const int64_t n = n0 + i;
+      const int yy = __shfl_sync(FULL, ylane, i & (CH - 1));
+      if (STATS && i < CH && n < N && lane < K) {
+        ntp = p.top1_in[n * K + lane];
+        nls = p.lse_in[n * K + lane];
+        nmx = p.rmax_in[n * K + lane];
+        nly = (yy >= 0 && yy < C) ? p.logits[(n * K + lane) * p.ldc + yy] : 0.f;
+      }
+    };
+    prefetch(0);
 #pragma unroll 1
     for (int i = 0; i < CH; ++i) {
       const int64_t n = n0 + i;
+      int tp = ntp;
+      float mx = nmx, ls = nls;
+      const float lyv = nly;
+      prefetch(i + 1);
       if (n < N) {
         // ---- phase 1: the sample's record ----------------------------------------------------------
         bool eval = false;
-        const int y = p.labels[n];
+        const int y = __shfl_sync(FULL, ylane, i);
         if (y < 0 || y >= C) {
           if (lane == 0) atomicOr(p.err + 1, 1u);
         } else {
           const float* rowbase = p.logits + n * K * p.ldc;
-          int tp = 0;
-          float mx = 0.f, ls = 0.f;
           bool bad = false;
           if (STATS) {
-            if (lane < K) {
-              tp = p.top1_in[n * K + lane];
-              ls = p.lse_in[n * K + lane];
-              mx = p.rmax_in[n * K + lane];
-              bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
-            }
+            if (lane < K) bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
           } else {
             row_stats(p, rowbase, lane, tp, mx, ls, bad);
             if (lane < K) { st_top[n * K + lane] = tp; st_lse[n * K + lane] = ls; st_max[n * K + lane] = mx; }
@@ -224,7 +237,8 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
               }
             } else {
               const float thr = theta_threshold(mx, ls, K, lane);
-              if (__any_sync(FULL, lane < K && rowbase[(size_t)lane * p.ldc + y] >= thr)) wl |= 1u << i;
+              const float lym = STATS ? lyv : (lane < K ? rowbase[(size_t)lane * p.ldc + y] : 0.f);
+              if (__any_sync(FULL, lane < K && lym >= thr)) wl |= 1u << i;
               if (__any_sync(FULL, lane < K && c == y)) {
                 eval = true;
                 const bool other = lane < K && (__ffs(mm) - 1) == lane && c != y;  // one lane per other class
