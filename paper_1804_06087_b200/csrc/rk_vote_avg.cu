@@ -52,8 +52,7 @@ __device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int 
 struct WS {  // per-warp shared memory
   double* lse64;    // [8]
   int32_t* stop;    // [8] top-1 per model
-  uint32_t* bitmap; // [32] S_c (theta test)
-  uint32_t* bitmapB;// [32] classes not below y in some model
+  uint32_t* bitmap; // [32] R = S_c (theta test) ∩ classes not below y in some model
   int32_t* ccls;    // [CAP] candidate classes in ascending order
   float* P;         // [K][CAP+1]
   float* T;         // [32][DSTR] half-mask sums of the exact columns (col 0 = y, 1.. = D)
@@ -68,7 +67,6 @@ __host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS*
   char* l64 = take(8 * 8);
   char* st = take(4 * 8);
   char* bm = take(4 * 32);
-  char* bmB = take(4 * 32);
   char* cc = take(4ull * p.CAP);
   char* P = take(4ull * p.K * (p.CAP + 1));
   char* T = take(4ull * 32 * DSTR);
@@ -76,7 +74,7 @@ __host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS*
   char* Q = take(4 * 8);
   char* CN = take(4 * JMAX * 32);
   if (w) {
-    w->lse64 = (double*)l64; w->stop = (int32_t*)st; w->bitmap = (uint32_t*)bm; w->bitmapB = (uint32_t*)bmB;
+    w->lse64 = (double*)l64; w->stop = (int32_t*)st; w->bitmap = (uint32_t*)bm;
     w->ccls = (int32_t*)cc; w->P = (float*)P; w->T = (float*)T; w->QB = (float*)QB; w->Q = (float*)Q;
     w->cnt = (uint32_t*)CN;
   }
@@ -159,11 +157,12 @@ __global__ void __launch_bounds__(WT, 5) vote_average_kernel(const VoteParams p,
     const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;  // l[m][y]
     __syncwarp();
     if (lane < K) ws.stop[lane] = tp;
-    ws.bitmap[lane] = 0u;
-    ws.bitmapB[lane] = 0u;
     __syncwarp();
     // ---- 1. candidate set R: one streaming pass over the sample's K rows ----------------------
     const int64_t nnext = e + nw < W ? (int64_t)work[e + nw] : -1;
+    // candidate bits of the lane's classes (lane + 32 i) * 4 + q kept as nibble i of two registers:
+    // S_c (>= θ threshold) and "not below y" (>= l[m][y]), OR-ed over the models, no shared atomics
+    uint32_t B1 = 0, B2 = 0;
 #pragma unroll 1
     for (int m = 0; m < K; ++m) {
       const float* row = rowbase + (size_t)m * p.ldc;
@@ -193,13 +192,24 @@ __global__ void __launch_bounds__(WT, 5) vote_average_kernel(const VoteParams p,
             bits |= (x >= t_m && cb + q < C) ? (1u << q) : 0u;
             bitsB |= (x >= y_m && cb + q < C) ? (1u << q) : 0u;
           }
-          if (bits) atomicOr(&ws.bitmap[cb >> 5], bits << (cb & 31));
-          if (bitsB) atomicOr(&ws.bitmapB[cb >> 5], bitsB << (cb & 31));
+          B1 |= bits << (4 * i);
+          B2 |= bitsB << (4 * i);
         }
       }
     }
+    {  // R nibbles -> 32-class words: nibble i of lanes 8k..8k+7 forms word 4i + k
+      const uint32_t Rn = B1 & B2;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t wv = ((Rn >> (4 * i)) & 0xfu) << (4 * (lane & 7));
+        wv |= __shfl_xor_sync(FULL, wv, 1);
+        wv |= __shfl_xor_sync(FULL, wv, 2);
+        wv |= __shfl_xor_sync(FULL, wv, 4);
+        if ((lane & 7) == 0) ws.bitmap[(lane >> 3) + 4 * i] = wv;
+      }
+    }
     __syncwarp();
-    const uint32_t word = ws.bitmap[lane] & ws.bitmapB[lane];
+    const uint32_t word = ws.bitmap[lane];
     const int cnt = __popc(word);
     int incl = cnt;
     for (int off = 1; off < 32; off <<= 1) {
