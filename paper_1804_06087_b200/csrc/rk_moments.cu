@@ -28,6 +28,17 @@ __device__ __forceinline__ int64_t arrival_at(const int64_t* arr, int64_t local,
   const double num = __dmul_rn((double)global, 1e9);
   return (int64_t)floor(__ddiv_rn(num, rate));
 }
+// The same value as arrival_at(nullptr, ., global, rate) (reading Q9: floor of the correctly rounded
+// quotient), with the fp64 division replaced by a multiplication by inv = 1/rate whenever the product
+// is farther than its error bound (< 4e-16 relative, both roundings and inv's included) from an
+// integer: then both floors agree; otherwise (probability ~1e-5) the exact division decides.
+__device__ __forceinline__ int64_t arrival_uniform(int64_t global, double rate, double inv) {
+  const double num = __dmul_rn((double)global, 1e9);
+  const double x = __dmul_rn(num, inv);
+  const double q = floor(x), fr = x - q, d = 4e-16 * x + 1e-300;
+  if (fr > d && fr < 1.0 - d) return (int64_t)q;
+  return (int64_t)floor(__ddiv_rn(num, rate));
+}
 
 // ---- overdue / exceed sums per (r, b, slowest model) ------------------------------------------
 __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
@@ -50,6 +61,7 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
     const int b = p.B[bi];
     const int64_t s0 = jl * b;  // local index of the batch's first request
     const double rate = p.rates[r];
+    const double inv = __drcp_rn(rate);
     const int64_t tl = arrival_at(p.arrival, s0 + b - 1, p.goff + s0 + b - 1, rate);
     if (p.arrival && r == 0) {  // arrivals must be non-decreasing inside a batch (FIFO)
       for (int i = 1; i < b; ++i)
@@ -63,11 +75,20 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
       // overdue <=> l(s) = F - t_s > tau <=> t_s < F - tau ; t_s non-decreasing in s. F = t_last + c
       // (reading Q8) or the FIFO finish time (queue mode, reading Q15)
       const int64_t thr = fm[m] - p.tau;
-      int lo = 0, hi = b;  // first i with t_i >= thr
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const int64_t tm = arrival_at(p.arrival, s0 + mid, p.goff + s0 + mid, rate);
-        if (tm < thr) lo = mid + 1; else hi = mid;
+      int lo = 0;  // first i with t_i >= thr
+      if (p.arrival) {  // caller arrivals: binary search
+        int hi = b;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const int64_t tm = arrival_at(p.arrival, s0 + mid, p.goff + s0 + mid, rate);
+          if (tm < thr) lo = mid + 1; else hi = mid;
+        }
+      } else {  // uniform arrivals (reading Q9): closed-form guess, then exact local correction, so the
+                // result is the same first index the search finds (t non-decreasing in s)
+        const double est = ceil((double)thr * rate * 1e-9) - (double)(p.goff + s0);
+        lo = est <= 0.0 ? 0 : (est >= (double)b ? b : (int)est);
+        while (lo > 0 && arrival_uniform(p.goff + s0 + lo - 1, rate, inv) >= thr) --lo;
+        while (lo < b && arrival_uniform(p.goff + s0 + lo, rate, inv) < thr) ++lo;
       }
       cnt[m] = lo;
       atomicAdd(&so[(r * p.nB + bi) * p.K + m], (unsigned long long)lo);
@@ -77,14 +98,21 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
       // E = sum_{i < cnt} (tl - t_i + c - tau): one sweep with prefix sums of t_i
       int maxc = 0;
       for (int m = 0; m < p.K; ++m) maxc = cnt[m] > maxc ? cnt[m] : maxc;
+      int ord[kMaxK];  // models in increasing overdue count (insertion sort; K <= 12)
+      for (int m = 0; m < p.K; ++m) {
+        int k = m;
+        while (k > 0 && cnt[ord[k - 1]] > cnt[m]) { ord[k] = ord[k - 1]; --k; }
+        ord[k] = m;
+      }
       int64_t pre = 0;
+      int k = 0;
       for (int i = 0; i <= maxc; ++i) {
-        for (int m = 0; m < p.K; ++m)
-          if (cnt[m] == i) {
-            const unsigned long long e = (unsigned long long)((int64_t)i * (fm[m] - p.tau) - pre);
-            atomicAdd(&se[(r * p.nB + bi) * p.K + m], e);
-          }
-        if (i < maxc) pre += arrival_at(p.arrival, s0 + i, p.goff + s0 + i, rate);
+        for (; k < p.K && cnt[ord[k]] == i; ++k) {
+          const int m = ord[k];
+          const unsigned long long e = (unsigned long long)((int64_t)i * (fm[m] - p.tau) - pre);
+          atomicAdd(&se[(r * p.nB + bi) * p.K + m], e);
+        }
+        if (i < maxc) pre += p.arrival ? p.arrival[s0 + i] : arrival_uniform(p.goff + s0 + i, rate, inv);
       }
     }
   }
