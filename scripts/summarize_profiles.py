@@ -91,14 +91,24 @@ for key, d in summary.items():
     wr = float(d.get("dram__bytes_write.sum", "0 byte").split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[
         d.get("dram__bytes_write.sum", "0 byte").split()[1]]
     per_sample[name] = (rd + wr) / CAPN[tag]
+k12_ps = 0.0  # c5 shape (K = 12, C = 100): the vote stage's kernels, scaled to c5's N = 4M
+for key, d in summary.items():
+    tag, name = key.split(":", 1)
+    if tag != "k12":
+        continue
+    for mk in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        val, unit = d.get(mk, "0 byte").split()[:2]
+        k12_ps += float(val) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[unit] / CAPN["k12"]
 gemm_ps = sum(v for k, v in per_sample.items() if k.startswith("gemm_heads"))
 vote_ps = sum(v for k, v in per_sample.items() if k.startswith("vote_"))
 tj = {"_note": f"DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch from the `ncu --set full` "
                f"captures of {R} (profiles/{R}_ncu_full.json; GEMM at N={CAPN['gemm']}, vote kernels at N={CAPN['vote']}, "
-               f"K=8, C=1000, D=2048), scaled linearly in N to the c4 workload (N=1,000,000). vote_subsets = "
+               f"K=8, C=1000, D=2048), scaled linearly in N to the c4 workload (N=1,000,000); c5: the K=12 vote kernels of the k12 capture "
+               f"(N={CAPN['k12']}) scaled to N=4,000,000. vote_subsets = "
                f"classify + average kernels. Algorithmic: GEMM 36,096 B/sample (X 4,096 + fp32 logits 32,000), "
                f"vote 32,004 B/sample.",
       "c4": {"gemm_heads_tcgen05": round(gemm_ps * 1e6), "vote_subsets": round(vote_ps * 1e6)},
+      "c5": {"vote_subsets": round(k12_ps * 4e6)},
       "per_sample": {k: round(v, 1) for k, v in per_sample.items()}}
 json.dump(tj, open(f"{OUT}/traffic.json", "w"), indent=1)
 print(json.dumps(tj, indent=1))
