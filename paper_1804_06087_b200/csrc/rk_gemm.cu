@@ -36,21 +36,31 @@ constexpr int A_BYTES = BM * BK * 2;   // 16 KB: this CTA's 128 rows of X
 constexpr int EPI_WARPS = 4;
 constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging box (packed mode: two 32x16 boxes)
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr int EPI_PACK = 8;              // packed mode: two epilogue warps per TMEM lane quarter
-constexpr int XCH_BYTES = 4 * 32 * 12;   // packed mode: (max, sum, argmax) hand-over per quarter
+#ifndef RK_EPI_PACK
+#define RK_EPI_PACK 12
+#endif
+constexpr int EPI_PACK = RK_EPI_PACK;    // packed mode: EPI_PACK / 4 epilogue warps per TMEM lane quarter
+constexpr int NHP = EPI_PACK / 4;
+static_assert(EPI_PACK == 8 || EPI_PACK == 12, "packed epilogue: 2 or 3 warps per lane quarter");
+constexpr int XCH_BYTES = 4 * 32 * 12;   // (max, sum, argmax) hand-over per quarter and partner part
 // CL = 1: one CTA computes a 128 x 256 tile (W tile 256 rows in its smem, 4 stages of 48 KB).
 // CL = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256): each CTA
 // holds its 128 X rows and HALF of the W tile (128 rows), 6 stages of 32 KB.
-template <int CL>
+template <int CL, bool PACK = false>
 struct Tile {
   static constexpr int B_ROWS = BN / CL;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int NS = CL == 1 ? 4 : 6;
+  // packed mode with 3 warps per quarter: 12 x 4 KB of store staging; one operand stage makes room
+  static constexpr bool WIDE = PACK && NHP == 3;
+  static constexpr int NS = CL == 1 ? (WIDE ? 3 : 4) : (WIDE ? 5 : 6);
+  static constexpr int STG_TOTAL = WIDE ? EPI_PACK * 2 * (32 * 16 * 4) : EPI_WARPS * 2 * STG_BYTES;
   static constexpr int SMEM_BYTES =
-      1024 /*align slack*/ + NS * STAGE_BYTES + EPI_WARPS * 2 * STG_BYTES + 256 + XCH_BYTES;
+      1024 /*align slack*/ + NS * STAGE_BYTES + STG_TOTAL + 256 + XCH_BYTES * (PACK ? NHP - 1 : 1);
 };
-static_assert(Tile<1>::SMEM_BYTES <= 232448 && Tile<2>::SMEM_BYTES <= 232448, "smem");
+static_assert(Tile<1>::SMEM_BYTES <= 232448 && Tile<2>::SMEM_BYTES <= 232448 && Tile<1, true>::SMEM_BYTES <= 232448 &&
+                  Tile<2, true>::SMEM_BYTES <= 232448,
+              "smem");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -244,29 +254,41 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
   constexpr int SBOX = 32 * 16 * 4;
   uint32_t tc = 0, nstore = 0, nclose = 0;
   const int row_in_tile = q * 32 + lane;
-  float* xb = xch + q * 96;
+  float* xb = xch + q * 96 * (NHP - 1);
   for (int64_t u = ucl0; u < units; u += ucls) {
     const int mt = (int)(u / a.ng) * CL + crank;
     const int64_t row = (int64_t)mt * BM + row_in_tile;
     float mx = -INFINITY, sum = 0.f;
     int arg = 0x7fffffff, cur = -1;
-    auto close = [&](int m) {  // both halves call this at the same model boundaries
+    auto close = [&](int m) {  // every part calls this at the same model boundaries
       if (m < 0) return;
-      if (h == 1) {
-        if (nclose > 0) asm volatile("bar.sync %0, 64;" ::"r"(5 + q) : "memory");  // half 0 read the last one
-        xb[lane] = mx; xb[32 + lane] = sum; xb[64 + lane] = __int_as_float(arg);
+      constexpr int NT = 32 * NHP;  // threads of the quarter's warps (named barriers 1+q, 5+q)
+      if (h > 0) {
+        if (nclose > 0) asm volatile("bar.sync %0, %1;" ::"r"(5 + q), "n"(NT) : "memory");  // part 0 read the last one
+        float* xs = xb + (h - 1) * 96;
+        xs[lane] = mx; xs[32 + lane] = sum; xs[64 + lane] = __int_as_float(arg);
       }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "n"(NT) : "memory");
       if (h == 0) {
-        const float mx1 = xb[lane], s1 = xb[32 + lane];
-        const int a1 = __float_as_int(xb[64 + lane]);
-        asm volatile("bar.arrive %0, 64;" ::"r"(5 + q) : "memory");
-        const float M = fmaxf(mx, mx1);
+        float mk[NHP - 1], sk[NHP - 1];
+        int ak[NHP - 1];
+#pragma unroll
+        for (int k = 0; k < NHP - 1; ++k) {
+          mk[k] = xb[k * 96 + lane]; sk[k] = xb[k * 96 + 32 + lane]; ak[k] = __float_as_int(xb[k * 96 + 64 + lane]);
+        }
+        asm volatile("bar.arrive %0, %1;" ::"r"(5 + q), "n"(NT) : "memory");
+        float M = mx;
+        int A = arg;
+#pragma unroll
+        for (int k = 0; k < NHP - 1; ++k) {  // the lowest column among the parts' maxima (Q4)
+          if (mk[k] > M) { M = mk[k]; A = ak[k]; }
+          else if (mk[k] == M && ak[k] < A) A = ak[k];
+        }
         float S = 0.f;
         if (mx != -INFINITY) S += sum * __expf(mx - M);
-        if (mx1 != -INFINITY) S += s1 * __expf(mx1 - M);
-        int A = arg;
-        if (mx1 > mx || (mx1 == mx && a1 < arg)) A = a1;
+#pragma unroll
+        for (int k = 0; k < NHP - 1; ++k)
+          if (mk[k] != -INFINITY) S += sk[k] * __expf(mk[k] - M);
         if (row < a.N) {
           a.top1[row * a.K + m] = A;
           a.lse[row * a.K + m] = M + logf(S);
@@ -275,7 +297,7 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
       }
       ++nclose;
     };
-    uint32_t blk = 0;  // global 16-column block counter of this unit (alternates between the halves)
+    uint32_t blk = 0;  // global 16-column block counter of this unit (dealt round-robin to the parts)
     for (int j = 0; j < a.nt; ++j, ++tc) {
       const int width = min(BN, a.gcols - j * BN);
       const uint32_t as = tc & 1;
@@ -289,7 +311,7 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
           close(cur);
           mx = -INFINITY; sum = 0.f; arg = 0x7fffffff; cur = model;
         }
-        if ((int)(blk & 1u) != h) continue;
+        if ((int)(blk % NHP) != h) continue;
         float v[32];
         tmem_ld16(tbase + c0, v);
         const float4* bptr = reinterpret_cast<const float4*>(a.bias + (size_t)model * a.Cp + cm);
@@ -355,19 +377,19 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
     gemm_heads_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                       const __grid_constant__ CUtensorMap tmo, const __grid_constant__ CUtensorMap tmo16,
                       const GemmArgs a) {
-  using T = Tile<CL>;
+  using T = Tile<CL, PACK>;
   constexpr int NS = T::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
   uint8_t* staging = smem + NS * T::STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + EPI_WARPS * 2 * STG_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + T::STG_TOTAL);
   uint64_t* full = bars;            // [NS]  (CL = 2: only the leader's are waited on)
   uint64_t* empty = bars + NS;      // [NS]
   uint64_t* tfull = bars + 2 * NS;  // [2]
   uint64_t* tempty = bars + 2 * NS + 2;  // [2]  (CL = 2: the leader's counts both epilogues)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 4);
-  float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [4][3][32] (packed mode)
+  float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [4][NHP-1][3][32] (packed)
   constexpr int EPI = PACK ? EPI_PACK : EPI_WARPS;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -473,7 +495,7 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
     // ===== epilogue: TMEM -> registers -> (stats, swizzled smem) -> TMA store =====
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     const int row_in_tile = q * 32 + lane;
-    uint8_t* stg = staging + (warp - 2) * 2 * (STG_BYTES * EPI_WARPS / EPI);
+    uint8_t* stg = staging + (warp - 2) * (T::STG_TOTAL / EPI);
     const float scale = ldexpf(1.0f, a.scale_log2);
     const uint64_t store_policy = policy_evict_first();
     uint32_t tc = 0, nstore = 0;
@@ -643,12 +665,12 @@ static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count
   const CUtensorMap& mo = *reinterpret_cast<const CUtensorMap*>(p.tmap_out);
   const CUtensorMap& m16 = *reinterpret_cast<const CUtensorMap*>(p.tmap_out16);
   cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<CL, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Tile<CL>::SMEM_BYTES);
+                                       Tile<CL, PACK>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int64_t units = ((p.N + CL * BM - 1) / (CL * BM)) * a.ng;
   if (CL == 1) {
     const int grid = (int)(units < sm_count ? units : sm_count);
-    gemm_heads_kernel<CL, PACK><<<grid, 64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), Tile<CL>::SMEM_BYTES, st>>>(
+    gemm_heads_kernel<CL, PACK><<<grid, 64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), Tile<CL, PACK>::SMEM_BYTES, st>>>(
         mx, mw, mo, m16, a);
     return cudaGetLastError();
   }
@@ -657,7 +679,7 @@ static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * clusters));
   cfg.blockDim = dim3(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS));
-  cfg.dynamicSmemBytes = Tile<CL>::SMEM_BYTES;
+  cfg.dynamicSmemBytes = Tile<CL, PACK>::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
