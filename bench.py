@@ -163,6 +163,28 @@ def reference_arm(args, cfgname, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def kernels_per_step(K, C, cfg, queue):
+    """Our kernel launches in one step (rk_score + rk_subset_stats), mirroring the library's dispatch
+    (csrc/rk_api.cpp, rk_vote_batch.cu); cross-checked against the ncu launch list in profiles/."""
+    ldc = (C + 3) // 4 * 4
+    n = 1  # gemm_heads_kernel
+    if K <= 8:
+        n += 2  # vote_classify_kernel + vote_average_kernel
+    else:
+        n += 1  # vote_group_classify_kernel
+        if ldc <= 128:
+            n += (2 if K == 12 else 1) + 1  # vote_wsample_average_kernel pass(es) + vote_pair_recheck_kernel
+        n += 2  # vote_cta_average_kernel + vote_batch_average_kernel
+    labelled = bool(cfg["B"]) and bool(cfg["rates"])
+    if labelled:
+        n += 1 + (1 if queue else 0)  # overdue_kernel (+ queue_scan_kernel)
+    n += 1  # merge_kernel
+    if labelled:
+        n += 1  # q_nested_kernel / q_kernel
+    n += 1  # fold_kernel
+    return n
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -297,7 +319,7 @@ def main():
     if os.path.exists(tp):  # ncu dram bytes per launch of this workload (scripts/summarize_profiles.py)
         tj = json.load(open(tp)).get(cfgname, {})
         traffic, vtraffic = tj.get("gemm_heads_tcgen05"), tj.get("vote_subsets")
-    launches = sum(ks[k]["launches"] for k in ks if k != "nccl_allreduce")
+    launches = args.steps * kernels_per_step(K, C, cfg, args.queue)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
