@@ -13,3 +13,6 @@ echo "vote rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:vote -c 5 -o gpurun_out/${R}_k12 \
   python scripts/prof_vote.py --K 12 --C 100 --N 250000 --gemm 1024 --reps 1 > gpurun_out/${R}_k12.log 2>&1
 echo "k12 rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_heads -c 1 -o gpurun_out/${R}_gemm12 \
+  python scripts/prof_vote.py --K 12 --C 100 --N 131072 --gemm 1024 --reps 1 > gpurun_out/${R}_gemm12.log 2>&1
+echo "gemm12 rc=$?"

@@ -58,7 +58,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "smsp__inst_executed.sum", "launch__grid_size", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
 summary = {}
-for tag in ("gemm", "vote", "k12"):
+for tag in ("gemm", "vote", "k12", "gemm12"):
     try:
         recs = raw(f"gpurun_out/{R}_{tag}.ncu-rep")
     except Exception as e:  # noqa: BLE001
@@ -80,11 +80,11 @@ for k, d in summary.items():
         print("   ", kk, vv)
 
 # ---- DRAM traffic per launch for bench.py's roofline.traffic (scaled linearly in N to c4) ----------
-CAPN = {"gemm": 65536, "vote": 200000, "k12": 250000}  # N of the captures in scripts/profile_round.sh
+CAPN = {"gemm": 65536, "vote": 200000, "k12": 250000, "gemm12": 131072}  # N of the captures in scripts/profile_round.sh
 per_sample = {}
 for key, d in summary.items():
     tag, name = key.split(":", 1)
-    if tag == "k12":
+    if tag in ("k12", "gemm12"):
         continue  # c5 shape: reported in the summary, not part of the c4 traffic figure
     rd = float(d.get("dram__bytes_read.sum", "0 byte").split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[
         d.get("dram__bytes_read.sum", "0 byte").split()[1]]
@@ -95,7 +95,7 @@ k12_ps = 0.0  # c5 shape (K = 12, C = 100): the vote stage's kernels, scaled to 
 for key, d in summary.items():
     tag, name = key.split(":", 1)
     if tag != "k12":
-        continue
+        continue  # (the c5 GEMM capture gemm12 is summarised, its traffic not used by bench.py)
     for mk in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         val, unit = d.get(mk, "0 byte").split()[:2]
         k12_ps += float(val) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[unit] / CAPN["k12"]
