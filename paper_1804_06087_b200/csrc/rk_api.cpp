@@ -672,6 +672,19 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       }
       CK(launch_overdue(mp, st));
     }
+    // ---- labelled moments (before the merge: for K >= 9 this pass also adds the vote totals) ----
+    if (gs > 0) {
+      QParams qp{};
+      qp.K = K; qp.S = S; qp.nB = nB; qp.nR = nR; qp.gs = gs;
+      for (int bi = 0; bi < nB; ++bi) qp.B[bi] = ctx->B[bi];
+      qp.N = N; qp.L = ctx->L;
+      qp.grp = ctx->d_grp; qp.slow = ctx->d_slow; qp.Q = ctx->d_table + ctx->off_Q;
+      qp.ovd = ctx->d_ovd;
+      qp.cnt_vote = warp_path ? nullptr : ch;  // K >= 9: per-subset vote totals from the group counts
+      ovd_elems(nB, ctx->B, nR, K, N, qp.ovd_off);
+      ProfScope ps(ctx, KK_Q, st, 0, 0);
+      CK(launch_q(qp, ctx->sm_count, st));
+    }
     // ---- merge chunk counters into the table ----
     MergeParams gp{};
     gp.S = S; gp.nB = nB; gp.nR = nR; gp.K = K; gp.chunk = ch; gp.slow = ctx->d_slow; gp.table = ctx->d_table;
@@ -681,18 +694,6 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     {
       ProfScope ps(ctx, KK_MERGE, st, 0, 0);
       CK(launch_merge(gp, N, ctx->off_N, st));
-    }
-    // ---- labelled moments ----
-    if (gs > 0) {
-      QParams qp{};
-      qp.K = K; qp.S = S; qp.nB = nB; qp.nR = nR; qp.gs = gs;
-      for (int bi = 0; bi < nB; ++bi) qp.B[bi] = ctx->B[bi];
-      qp.N = N; qp.L = ctx->L;
-      qp.grp = ctx->d_grp; qp.slow = ctx->d_slow; qp.Q = ctx->d_table + ctx->off_Q;
-      qp.ovd = ctx->d_ovd;
-      ovd_elems(nB, ctx->B, nR, K, N, qp.ovd_off);
-      ProfScope ps(ctx, KK_Q, st, 0, 0);
-      CK(launch_q(qp, ctx->sm_count, st));
     }
   }
   if (N % ctx->L != 0) ctx->final_seen = true;

@@ -140,6 +140,8 @@ struct QParams {
   const uint16_t* ovd;            // per-batch overdue counts (MomentParams::ovd)
   int64_t ovd_off[kMaxB];
   unsigned long long* Q;          // [nR][nB][S] (table section)
+  unsigned long long* cnt_vote;   // [S] or null: also add sum_g grp[g][v] (K >= 9: the vote kernel leaves
+                                  // the per-subset totals to this pass when it writes group counts)
 };
 cudaError_t launch_q(const QParams& p, int sm_count, cudaStream_t st);
 

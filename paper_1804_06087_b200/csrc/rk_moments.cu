@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(QT, kQBlocksPerSM)
     for (int r = 0; r < NRP; ++r) acc[r][bi] = 0;
   const uint8_t* gp = p.grp + (own ? v1 : 0);
   int since = 0;
+  unsigned long long csum = 0;  // sum of the subset's group counts (p.cnt_vote)
   for (int64_t q = q0; q < q1; ++q) {
     if (STAGED) {
       __syncthreads();
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(QT, kQBlocksPerSM)
       for (int i = 0; i < QG; ++i) {
         if (g0 + i >= gb) break;
         const unsigned int c = cc[i];
+        csum += c;
 #pragma unroll
         for (int bi = 0; bi < NBX; ++bi) {
           if (NB == 0 && bi >= nB) break;
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(QT, kQBlocksPerSM)
     }
   }
   if (!own) return;
+  if (p.cnt_vote && csum) atomicAdd(p.cnt_vote + v1, csum);
   for (int r = 0; r < p.nR; ++r)
     for (int bi = 0; bi < nB; ++bi) {
       const unsigned long long x = qacc[(r * nB + bi) * QT + threadIdx.x];
@@ -438,6 +441,7 @@ __global__ void __launch_bounds__(QT, kQNestedBlocksPerSM)
     for (int r = 0; r < NRP; ++r) acc[r][bi] = 0;
   const uint8_t* gp = p.grp + (own ? v1 : 0);
   int since = 0;
+  unsigned long long csum = 0;  // sum of the subset's group counts (p.cnt_vote)
   for (int64_t qq = q0; qq < q1; qq += QC) {
     __syncthreads();
     {  // stage overdue counts of chunks qq .. qq+QC-1 as u32 (one NRP-vector per (batch, model)); a level's
@@ -499,6 +503,7 @@ __global__ void __launch_bounds__(QT, kQNestedBlocksPerSM)
 #pragma unroll
         for (int j = 0; j < nb / 2; ++j) sv[j] = sv[2 * j] + sv[2 * j + 1];  // next batch size
       }
+      csum += sv[0];  // the last level is the whole chunk
       if (++since == flush || q + 1 == q1) {  // spill the u32 accumulators
         since = 0;
 #pragma unroll
@@ -512,6 +517,7 @@ __global__ void __launch_bounds__(QT, kQNestedBlocksPerSM)
     }
   }
   if (!own) return;
+  if (p.cnt_vote && csum) atomicAdd(p.cnt_vote + v1, csum);
   for (int r = 0; r < p.nR; ++r)
     for (int bi = 0; bi < NB; ++bi) {
       const unsigned long long x = qacc[(r * NB + bi) * QT + threadIdx.x];

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
           for (int v1 = lane; v1 < S; v1 += 32) {
             const uint32_t tot = stg[v1 + 1];
             if (p.grp) p.grp[gi * S + v1] = (uint8_t)tot;
-            if (tot) atomicAdd(&cnt[v1 + 1], tot);
+            if (tot && !p.grp) atomicAdd(&cnt[v1 + 1], tot);  // with group counts: summed by the q pass
           }
           __syncwarp();
           uw += u;
