@@ -173,8 +173,9 @@ def test_chunked_and_sharded_equal_one_shot(rk):
 @pytest.mark.parametrize("B,N", [((16, 48, 80), 1000),   # non-nested sizes, L = 240, staged overdue table
                                  ((1, 4096), 9000),       # gs = 1, L = 4096: per-chunk table > 32 KB, global path
                                  ((3, 6, 12), 61)])       # ragged tail, gs = 1
-def test_labelled_moments_batch_sets(rk, B, N):
-    K, C = 4, 50
+@pytest.mark.parametrize("K", [4, 10])  # K = 10: warp-per-chunk vote kernel, vote totals summed by the q pass
+def test_labelled_moments_batch_sets(rk, B, N, K):
+    C = 50
     y = gen.labels(31, 0, N, C)
     L = gen.logits(31, 0, N, K, C, y=y)
     gcfg, ocfg = default_cfg(K, B=B, tau_ns=100_000_000)
