@@ -141,9 +141,10 @@ def test_tiny_label_probabilities(rk, K):
     compare_tables(t, o, K=K)
 
 
-def test_chunked_and_sharded_equal_one_shot(rk):
+@pytest.mark.parametrize("K", [4, 11])
+def test_chunked_and_sharded_equal_one_shot(rk, K):
     """Streaming chunks (multiples of lcm(B)) and disjoint shards sum to the one-shot table (I7, P5)."""
-    K, C, N = 4, 100, 1000
+    C, N = 100, 1000
     y = gen.labels(21, 0, N, C)
     L = gen.logits(21, 0, N, K, C, y=y)
     gcfg, ocfg = default_cfg(K, B=(16, 32, 64))
