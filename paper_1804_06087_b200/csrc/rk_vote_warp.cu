@@ -88,24 +88,36 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
     uint32_t uni = 0, wmask = 0;
     const int64_t u0 = unit * U;
     const int64_t s1 = u0 + U < N ? u0 + U : N;
+    // the unit's labels in one load (lane i: sample u0 + i); with STATS the next sample's statistics and
+    // l[m][y] are loaded one sample ahead, off the per-sample dependent load chain
+    const int ylane = (lane < U && u0 + lane < s1) ? p.labels[u0 + lane] : 0;
+    int ntp = 0;
+    float nls = 0.f, nmx = 0.f, nly = 0.f;
+    auto prefetch = [&](int64_t nn) {
+      const int yy = __shfl_sync(FULL, ylane, (int)(nn - u0) & 31);
+      if (STATS && nn < s1 && lane < K) {
+        ntp = p.top1_in[nn * K + lane];
+        nls = p.lse_in[nn * K + lane];
+        nmx = p.rmax_in[nn * K + lane];
+        nly = (yy >= 0 && yy < C) ? p.logits[(nn * K + lane) * p.ldc + yy] : 0.f;
+      }
+    };
+    prefetch(u0);
 #pragma unroll 1
     for (int64_t n = u0; n < s1; ++n) {
-      const int y = p.labels[n];
+      int tp = ntp;
+      float mx = nmx, ls = nls;
+      const float lyv = nly;
+      prefetch(n + 1);
+      const int y = __shfl_sync(FULL, ylane, (int)(n - u0));
       if (y < 0 || y >= C) {
         if (lane == 0) atomicOr(p.err + 1, 1u);
         continue;
       }
       const float* rowbase = p.logits + n * K * p.ldc;
-      int tp = 0;
-      float mx = 0.f, ls = 0.f;
       bool bad = false;
       if (STATS) {
-        if (lane < K) {
-          tp = p.top1_in[n * K + lane];
-          ls = p.lse_in[n * K + lane];
-          mx = p.rmax_in[n * K + lane];
-          bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
-        }
+        if (lane < K) bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
       } else {
 #pragma unroll 1
         for (int m = 0; m < K; ++m) {  // one pass over the row: max, lowest argmax, sum exp
@@ -179,7 +191,8 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
       }
       // averaging candidate test (theta pruning) for the label
       const float thr = theta_threshold(mx, ls, K, lane);
-      const bool ycand = __any_sync(FULL, lane < K && rowbase[(size_t)lane * p.ldc + y] >= thr);
+      const float lym = STATS ? lyv : (lane < K ? rowbase[(size_t)lane * p.ldc + y] : 0.f);
+      const bool ycand = __any_sync(FULL, lane < K && lym >= thr);
       if (ycand) wmask |= 1u << (int)(n - u0);
       // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|, y wins iff
       // c_y > 0, no class has more votes, and the tie (if any) goes to y: LOWEST_CLASS -> no tied
