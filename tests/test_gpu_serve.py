@@ -78,3 +78,28 @@ def test_errors(rk):
         c.greedy_serve(rk.RewardCfg(B=[], beta=1.0, tau_ns=10, lat_ns=np.zeros((2, 0), np.int64), rates=[1.0]), 10, 0)
     with pytest.raises(rk.RkError):
         c.greedy_serve(rk.RewardCfg(B=[4], beta=1.0, tau_ns=10, lat_ns=np.zeros((2, 1), np.int64), rates=[0.0]), 10, 0)
+
+
+def test_measured_latency_profile(rk):
+    """NEXT-1: c(m, b) measured from our own head GEMM + per-request prediction, in integer ns (the
+    unit of RewardCfg.lat_ns); positive, and a larger batch never takes less than a third of the time
+    of a batch 16x smaller (a loose monotonicity check that survives timer noise)."""
+    import torch
+
+    import gen
+    from paper_1804_06087_b200.latency import measure_lat_ns
+
+    K, C, D, B = 3, 100, 1024, [16, 256]
+    psig, f0, df, sh = gen.head_params(D, C, K)
+    W = gen.weights(1000, K, C, D, f0, df, False)
+    b = gen.bias(2000, K, C, False)
+    X = torch.empty((max(B), D), dtype=torch.uint16, device="cuda")
+    lab = torch.empty(max(B), dtype=torch.int32, device="cuda")
+    gen.dev_labels(1, 0, max(B), C, lab.data_ptr())
+    gen.dev_features(1, 0, max(B), D, C, psig, False, X.data_ptr(), lab.data_ptr())
+    lat = measure_lat_ns(W, b, sh, B, X, reps=5, warmup=2)
+    assert lat.shape == (K, len(B)) and lat.dtype == np.int64
+    assert (lat > 0).all() and (lat < 10**9).all()
+    assert (lat[:, 1] * 3 >= lat[:, 0]).all()
+    cfg = rk.RewardCfg(B=B, beta=1.0, tau_ns=560_000_000, lat_ns=lat, rates=[128.0])  # usable as the profile
+    assert cfg.lat_ns.shape == (K, len(B))
