@@ -351,10 +351,24 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
           }
           __syncwarp();
           const int64_t gi = gstart / gsz;
-          for (int v1 = lane; v1 < S; v1 += 32) {
-            const uint32_t tot = stg[v1 + 1];
-            if (p.grp) p.grp[gi * S + v1] = (uint8_t)tot;
-            if (tot && !p.grp) atomicAdd(&cnt[v1 + 1], tot);  // with group counts: summed by the q pass
+          if (p.grp) {  // group counts: 4-byte stores on the aligned interior of the row (bytes v1 = v - 1)
+            uint8_t* g = p.grp + gi * S;
+            const int head = (int)((4 - ((uintptr_t)g & 3)) & 3);
+            const int nword = (S - head) >> 2, tail0 = head + 4 * nword;
+            if (lane < head) g[lane] = stg[lane + 1];
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(stg);
+            const int sh = 8 * ((head + 1) & 3);  // stg byte offset of v1 = head + 4j is head + 4j + 1
+            for (int j = lane; j < nword; j += 32) {
+              const int o = (head + 4 * j + 1) >> 2;
+              const uint32_t lo = sw[o], hi = sw[o + 1];
+              reinterpret_cast<uint32_t*>(g + head)[j] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+            }
+            if (tail0 + lane < S) g[tail0 + lane] = stg[tail0 + lane + 1];
+          } else {  // no group counts: per-subset totals here (otherwise the q pass sums the groups)
+            for (int v1 = lane; v1 < S; v1 += 32) {
+              const uint32_t tot = stg[v1 + 1];
+              if (tot) atomicAdd(&cnt[v1 + 1], tot);
+            }
           }
           __syncwarp();
           uw += u;
@@ -386,7 +400,7 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
     const int64_t nb = (p.N + SB - 1) / SB;
     const int grid = (int)(nb < (int64_t)sm_count * 2 ? nb : (int64_t)sm_count * 2);
     constexpr int NWL = NK / 4 > 0 ? NK / 4 : 1;  // words per lane: 2^(K-5) / 32 (K = 9: half the lanes idle)
-    const int dsm = NWB << p.K;
+    const int dsm = (NWB << p.K) + 16;  // + padding: the copy-out reads one word past a row
     if (p.lse_in) {
       if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     dsm)) != cudaSuccess)
