@@ -20,8 +20,11 @@
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). Calls are
  *    stream-ordered; rk_subset_finalize / rk_subset_stats synchronise `stream` and return
  *    host results.
- *  - Pointers documented "host or device" are classified with cudaPointerGetAttributes;
- *    host buffers are staged through pinned bounce buffers inside the call.
+ *  - Pointers documented "host or device" are classified with cudaPointerGetAttributes; host
+ *    inputs are copied with cudaMemcpyAsync on the call's stream(s), so -- as with cudaMemcpyAsync --
+ *    a HOST INPUT MUST STAY VALID AND UNMODIFIED UNTIL `stream` HAS COMPLETED THE CALL'S WORK (e.g. the
+ *    next rk_subset_finalize / rk_subset_stats, which synchronise, or a cudaStreamSynchronize).
+ *    Page-locked buffers are then read by DMA asynchronously; pageable ones are staged by the driver.
  *  - Subset mask v in [1, 2^K): bit m selects model m. Tables are indexed v-1 (v fastest),
  *    then batch-size index, then rate index: T[r][b][v-1]. RL action index of (v, B[b]) is
  *    (v-1)*nB + b (index 0 <-> (v = 0b001, B[0])).
@@ -65,7 +68,8 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
 rk_status rk_nccl_unique_id(void* out128);
 
 /* Load the ensemble M (PAPER.md:337 Table tb:notation "M: model list").
- *  K in [1,12] models (S = 2^K-1 <= 4095 subsets), C in [2,65535] classes.
+ *  K in [1,12] models (S = 2^K-1 <= 4095 subsets), C in [2,65535] classes (rows wider than 1024
+ *  classes are averaged by a slower fp64 kernel, rk_vote_large.cu; no bench config needs it).
  *  W_bf16: [K][C][D] bfloat16 bit patterns, row-major (D contiguous), host or device; NULL
  *          loads a logits-only ensemble (rk_score then returns RK_ESTATE). D % 64 == 0, D <= 16384.
  *  bias:   [K][C] fp32 or NULL (= 0). logit = 2^logit_scale_log2 * sum_d x*w + bias.
@@ -114,8 +118,17 @@ typedef struct {
   int64_t N;               /* samples accumulated over all chunks and ranks                      */
   uint64_t* cnt_vote;      /* [S] majority-vote correct counts; a(M[v]) = cnt_vote/N */
   uint64_t* cnt_avg;       /* [S] averaged-probability correct counts                            */
-  uint64_t* n_recheck;     /* [S] (sample, v) pairs whose fp32 top-2 gap was within the band and
-                              were decided in fp64                                              */
+  uint64_t* n_recheck;     /* [S] (sample, v) pairs whose fp32 relative top-2 gap was within the band
+                              (2e-5) and were decided from the definition in fp64. This is the
+                              library's counterpart of SURVEY.md §8(b)'s n_ambiguous_avg, but not
+                              the same count: n_ambiguous_avg (the oracle's, any two classes) flags
+                              pairs whose fp64 top-2 gap is <= 1e-12, where fp64 itself cannot
+                              decide. Here every pair whose decision about the label could flip
+                              under fp32 rounding is redone in fp64, so cnt_avg can differ from the
+                              exact-arithmetic count only on rechecked pairs:
+                              |cnt_avg[v] - exact| <= n_recheck[v], a bound callers get from library
+                              output alone (singletons are exact: top-1, invariant I1). The tests
+                              hold cnt_avg to the tighter oracle bound n_ambiguous_avg.        */
   uint64_t* corr;          /* [nB][S] vote-correct samples inside complete batches of size B[b]   */
   uint64_t* O;             /* [nR][nB][S] overdue requests sum_j o_j(v,b,r)                      */
   uint64_t* Q;             /* [nR][nB][S] sum_j corr_j(v) * o_j(v,b,r)   (want_labelled)         */
@@ -131,7 +144,12 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg);
 /* A2-A5 on the last rk_score* batch. labels: [N] int32, host or device. */
 rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream);
 /* A6 (all-reduce when world > 1) + A7 (reward fold) + copy to `out`. Blocks on `stream`.
- * Returns RK_ENONFINITE / RK_ELABEL if any accumulated chunk had bad input (table zeroed). */
+ * Returns RK_ENONFINITE / RK_ELABEL if any accumulated chunk had bad input (table zeroed).
+ * The all-reduce runs once per reset: a repeated finalize returns the same global table, and
+ * rk_subset_accumulate after a finalize is RK_ESTATE until the next rk_subset_reset. The wait for the
+ * all-reduce is bounded: it polls ncclCommGetAsyncError and gives up after RK_NCCL_TIMEOUT_S seconds
+ * (environment, read at rk_create; default 600); either failure aborts the communicator and returns
+ * RK_ENCCL (the context can no longer all-reduce). */
 rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream);
 /* One-shot: reset + accumulate + finalize on the last rk_score* batch. */
 rk_status rk_subset_stats(rk_ctx* ctx, const int32_t* labels, const rk_reward_cfg* cfg, rk_table* out,
@@ -163,10 +181,21 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
 rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_avg, float* avgprob,
                      void* stream);
 
-/* Device pointers of the last rk_score* outputs: logits [N][K][ldc] fp32, top1 [N][K] int32,
- * lse [N][K] fp32 (top1/lse are NULL after rk_score_logits). Valid until the next rk_score*. */
-rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** lse,
-                     int64_t* N);
+/* Device pointers of the last rk_score* outputs: logits [N][K][ldc] fp32, top1 [N][K] int32 (A2),
+ * rmax [N][K] fp32 = max_c logit, lsum [N][K] fp32 = log sum_c exp(logit - rmax) -- the softmax
+ * normaliser RELATIVE to the row max, so p[n][m][c] = exp((logit - rmax) - lsum) and the log-sum-exp is
+ * rmax + lsum (kept apart: their fp32 sum would round at the magnitude of the logits). top1/rmax/lsum
+ * are NULL after rk_score_logits. Any pointer argument may be NULL. Valid until the next rk_score*. */
+rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** rmax,
+                     const float** lsum, int64_t* N);
+
+/* Parity hook for the labelled moments (A5): the per-(group, subset) majority-vote correct counts of the
+ * LAST rk_subset_accumulate chunk, out[g][v-1] = #{n in group g : vote of v correct} (uint8), groups of
+ * *gs consecutive samples (gs = the largest power of two <= 16 dividing gcd(B); the last group may be
+ * partial), *groups = ceil(N_chunk / gs). They exist only when cfg had want_labelled, nB > 0 and nR > 0
+ * (otherwise *gs = *groups = 0). out: host or device, cap >= groups * S bytes, may be NULL to query
+ * the sizes. Blocks on `stream`. RK_ESTATE before the first accumulate after a reset. */
+rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64_t* groups, void* stream);
 
 /* Per-kernel device time, measured with CUDA events on the launch stream when profiling is on. */
 typedef struct {

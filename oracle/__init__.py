@@ -47,7 +47,8 @@ class _Cfg(ctypes.Structure):
 
 class _Table(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
-                ("cnt_vote", "cnt_avg", "n_amb", "corr", "O", "Q", "E", "reward_sur", "reward_lab")]
+                ("cnt_vote", "cnt_avg", "n_amb", "corr", "O", "Q", "E", "reward_sur", "reward_lab", "vote_ok",
+                 "avg_ok")]
 
 
 def lib():
@@ -158,6 +159,8 @@ class Table:
     E: np.ndarray | None = None
     reward_sur: np.ndarray | None = None
     reward_lab: np.ndarray | None = None
+    vote_ok: np.ndarray | None = None   # [N][S] uint8 per-sample vote correctness (want_bits)
+    avg_ok: np.ndarray | None = None    # [N][S] uint8 per-sample average correctness (want_bits)
 
 
 class OracleError(RuntimeError):
@@ -167,8 +170,9 @@ class OracleError(RuntimeError):
 
 
 def table(logits, labels, K: int, C: int, tie: int = TIE_BEST_MEMBER, rank=None,
-          cfg: RewardCfg | None = None, threads: int | None = None) -> Table:
-    """Steps A2-A7 over the whole dataset. logits: fp32 [N][K][ldc] or fp64 [N][K][C]."""
+          cfg: RewardCfg | None = None, threads: int | None = None, want_bits: bool = False) -> Table:
+    """Steps A2-A7 over the whole dataset. logits: fp32 [N][K][ldc] or fp64 [N][K][C].
+    want_bits: also return the per-sample correctness bits vote_ok / avg_ok [N][S] (uint8)."""
     lg = np.ascontiguousarray(logits)
     N = lg.shape[0]
     lf = ld = None
@@ -208,8 +212,11 @@ def table(logits, labels, K: int, C: int, tie: int = TIE_BEST_MEMBER, rank=None,
         t.E = np.zeros((nR, nB, S), np.uint64) if cfg.want_exceed else None
         t.reward_sur = np.zeros((nR, nB, S), np.float64)
         t.reward_lab = np.zeros((nR, nB, S), np.float64)
+    if want_bits:
+        t.vote_ok = np.zeros((N, S), np.uint8)
+        t.avg_ok = np.zeros((N, S), np.uint8)
     ct = _Table(_p(t.cnt_vote), _p(t.cnt_avg), _p(t.n_amb), _p(t.corr), _p(t.O), _p(t.Q), _p(t.E),
-                _p(t.reward_sur), _p(t.reward_lab))
+                _p(t.reward_sur), _p(t.reward_lab), _p(t.vote_ok), _p(t.avg_ok))
     rc = lib().or_table_build(_p(lf), ldc, _p(ld), N, K, C, _p(y), _p(r), tie,
                               ctypes.byref(cc) if cc is not None else None, ctypes.byref(ct),
                               threads or _threads())

@@ -169,6 +169,7 @@ typedef struct {
   const int64_t* fin;  /* queue mode: finish time of every complete batch [nR][nB][S][nbmax] */
   int64_t nbmax;
   int status;
+  uint8_t *vote_bits, *avg_bits;  /* [N][S] per-sample outputs or NULL (shared, disjoint rows) */
   /* thread-local accumulators */
   uint64_t *cnt_vote, *cnt_avg, *n_amb, *corr, *O, *Q, *E;
 } table_job;
@@ -216,6 +217,8 @@ static void* table_thr(void* arg) {
       int amb = 0;
       int wa = or_avg(p, K, C, v, &amb, NULL);
       vote_ok[v - 1] = (uint8_t)(wv == y);
+      if (j->vote_bits) j->vote_bits[n * S + (v - 1)] = (uint8_t)(wv == y);
+      if (j->avg_bits) j->avg_bits[n * S + (v - 1)] = (uint8_t)(wa == y);
       j->cnt_vote[v - 1] += (uint64_t)(wv == y);
       j->cnt_avg[v - 1] += (uint64_t)(wa == y);
       j->n_amb[v - 1] += (uint64_t)amb;
@@ -317,6 +320,7 @@ int or_table_build(const float* logits_f32, int ldc, const double* logits_f64, i
     j->lf = logits_f32; j->ldc = ldc; j->ld = logits_f64; j->N = N; j->a = a; j->b = b;
     j->K = K; j->C = C; j->labels = labels; j->rank = rank; j->tie = tie; j->cfg = cfg;
     j->fin = fin; j->nbmax = nbmax;
+    j->vote_bits = out->vote_ok; j->avg_bits = out->avg_ok;
     j->cnt_vote = (uint64_t*)calloc((size_t)S, 8);
     j->cnt_avg = (uint64_t*)calloc((size_t)S, 8);
     j->n_amb = (uint64_t*)calloc((size_t)S, 8);

@@ -54,6 +54,9 @@ typedef struct {
   uint64_t* E;         /* [nR][nB][S] or NULL                                    */
   double* reward_sur;  /* [nR][nB][S]                                            */
   double* reward_lab;  /* [nR][nB][S]                                            */
+  uint8_t* vote_ok;    /* [N][S] or NULL: per-sample majority-vote correctness (parity of the
+                          per-(group, subset) counts behind the labelled moments)  */
+  uint8_t* avg_ok;     /* [N][S] or NULL: per-sample averaged-probability correctness */
 } or_table;
 
 /* Per-model top-1: smallest class index attaining the max (reading Q4). */

@@ -12,6 +12,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -58,9 +60,9 @@ struct rk_ctx {
   // GEMM workspaces
   float* ws_logits = nullptr;
   int32_t* ws_top1 = nullptr;
-  float* ws_lse = nullptr;
+  float* ws_lsum = nullptr;
   float* ws_max = nullptr;
-  int64_t ws_cap = 0, ws_top1_cap = 0, ws_lse_cap = 0, ws_max_cap = 0;
+  int64_t ws_cap = 0, ws_top1_cap = 0, ws_lsum_cap = 0, ws_max_cap = 0;
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[4 * 128];
@@ -72,6 +74,8 @@ struct rk_ctx {
   std::vector<cudaEvent_t> ev_chunks;
   // accumulation state
   bool reset_done = false, final_seen = false;
+  bool finalized = false;      // the table holds the global sum (A6 done): no more accumulate / all-reduce
+  double nccl_timeout_s = 600; // bounded wait on the all-reduce (env RK_NCCL_TIMEOUT_S)
   bool has_cfg = false;
   int nB = 0, nR = 0, want_exceed = 0, want_labelled = 0;
   int B[kMaxB] = {};
@@ -114,6 +118,8 @@ struct rk_ctx {
   double* d_rew = nullptr;
   size_t rew_cap = 0;
   int64_t chunks = 0;
+  int64_t grp_groups = 0;      // group counts of the last accumulated chunk: ceil(N/gs) rows of S bytes
+  int grp_gs = 0;
   Prof prof;
 };
 
@@ -182,6 +188,30 @@ void prof_collect(rk_ctx* c) {
   c->prof.pending.clear();
 }
 
+// Wait for `st` (which holds the table all-reduce) while polling the communicator: a peer failure
+// (ncclCommGetAsyncError) or a wait longer than nccl_timeout_s aborts the communicator -> RK_ENCCL.
+rk_status wait_nccl(rk_ctx* ctx, cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) return RK_OK;
+    if (q != cudaErrorNotReady) return fail(ctx, RK_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(ctx->comm, &ar) != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+      ncclCommAbort(ctx->comm);
+      ctx->comm = nullptr;
+      return fail(ctx, RK_ENCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > ctx->nccl_timeout_s) {
+      ncclCommAbort(ctx->comm);
+      ctx->comm = nullptr;
+      return fail(ctx, RK_ENCCL, "all-reduce did not complete within RK_NCCL_TIMEOUT_S (peer lost?)");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(el < 0.01 ? 5 : 200));
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -228,6 +258,7 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
   if (const char* cc = getenv("RK_CTA_AVG_COLS")) ctx->cta_cols = std::max(4, std::min(52, atoi(cc) / 4 * 4));
   // tests only: a tiny near-tie pair list makes the warp averaging kernel hand whole samples to the CTA kernel
   if (const char* pc = getenv("RK_PAIR_CAP")) ctx->pair_cap_test = std::max(1, atoi(pc));
+  if (const char* to = getenv("RK_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::max(0.001, atof(to));
   if (nccl_unique_id) {  // world ranks (world may be 1: a one-rank communicator, same code path)
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
@@ -241,7 +272,7 @@ void rk_destroy(rk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
-  void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lse, ctx->ws_max, ctx->ws_x,
+  void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lsum, ctx->ws_max, ctx->ws_x,
                   ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_pairs, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -270,34 +301,13 @@ rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16,
     seen[rk_[m]] = true;
   }
   CK(cudaSetDevice(ctx->dev));
-  ctx->K = K; ctx->C = C; ctx->D = W_bf16 ? D : 0; ctx->S = (1 << K) - 1; ctx->tie = tie;
-  ctx->ldc = (C + 3) / 4 * 4;
-  ctx->Cp = (C + 15) / 16 * 16;
-  ctx->scale_log2 = logit_scale_log2;
-  memcpy(ctx->member_rank, rk_, sizeof(rk_));
-  // best_of[mask] = member of `mask` with the smallest rank (PAPER.md:407 "the model with the best accuracy")
-  std::vector<uint8_t> best(size_t(1) << K, 0);
-  for (uint32_t msk = 1; msk < (1u << K); ++msk) {
-    int b = -1;
-    for (int m = 0; m < K; ++m)
-      if (((msk >> m) & 1u) && (b < 0 || rk_[m] < rk_[b])) b = m;
-    best[msk] = (uint8_t)b;
-  }
-  if (ctx->d_best_of) cudaFree(ctx->d_best_of);
-  CK(cudaMalloc(&ctx->d_best_of, best.size()));
-  CK(cudaMemcpy(ctx->d_best_of, best.data(), best.size(), cudaMemcpyHostToDevice));
-  if (ctx->d_W) { cudaFree(ctx->d_W); ctx->d_W = nullptr; }
-  if (ctx->d_bias) { cudaFree(ctx->d_bias); ctx->d_bias = nullptr; }
-  ctx->has_heads = W_bf16 != nullptr;
-  if (ctx->has_heads) {
-    // pad each model's C rows to Cp (zero rows) and its bias to -inf, so tiles never mix models
-    const size_t wrows = (size_t)K * ctx->Cp;
-    CK(cudaMalloc(&ctx->d_W, wrows * D * 2));
-    CK(cudaMemset(ctx->d_W, 0, wrows * D * 2));
-    const bool wdev = is_device_ptr(W_bf16);
-    CK(cudaMemcpy2D(ctx->d_W, (size_t)ctx->Cp * D * 2, W_bf16, (size_t)C * D * 2, (size_t)C * D * 2, K,
-                    wdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-    std::vector<float> hb(wrows, -INFINITY);
+  const int Cp = (C + 15) / 16 * 16;
+  const size_t wrows = (size_t)K * Cp;
+  // Validate and stage everything BEFORE touching the context: on any failure the previously loaded
+  // ensemble (and the state built on it) stays intact.
+  std::vector<float> hb;
+  if (W_bf16) {
+    hb.assign(wrows, -INFINITY);  // padding columns: -inf never wins the max, exp -> 0
     std::vector<float> ub;
     if (bias) {
       ub.resize((size_t)K * C);
@@ -307,14 +317,59 @@ rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16,
       for (int c = 0; c < C; ++c) {
         const float b = bias ? ub[(size_t)m * C + c] : 0.f;
         if (!(b == b) || b == INFINITY || b == -INFINITY) return fail(ctx, RK_ENONFINITE, "bias must be finite");
-        hb[(size_t)m * ctx->Cp + c] = b;
+        hb[(size_t)m * Cp + c] = b;
       }
-    CK(cudaMalloc(&ctx->d_bias, wrows * 4));
-    CK(cudaMemcpy(ctx->d_bias, hb.data(), wrows * 4, cudaMemcpyHostToDevice));
   }
+  // best_of[mask] = member of `mask` with the smallest rank (PAPER.md:407 "the model with the best accuracy")
+  std::vector<uint8_t> best(size_t(1) << K, 0);
+  for (uint32_t msk = 1; msk < (1u << K); ++msk) {
+    int b = -1;
+    for (int m = 0; m < K; ++m)
+      if (((msk >> m) & 1u) && (b < 0 || rk_[m] < rk_[b])) b = m;
+    best[msk] = (uint8_t)b;
+  }
+  uint8_t* n_best = nullptr;
+  uint16_t* n_W = nullptr;
+  float* n_bias = nullptr;
+  auto undo = [&](rk_status st, const std::string& msg) {
+    if (n_best) cudaFree(n_best);
+    if (n_W) cudaFree(n_W);
+    if (n_bias) cudaFree(n_bias);
+    return fail(ctx, st, msg);
+  };
+#define CKU(call)                                                                                  \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return undo(RK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+  CKU(cudaMalloc(&n_best, best.size()));
+  CKU(cudaMemcpy(n_best, best.data(), best.size(), cudaMemcpyHostToDevice));
+  if (W_bf16) {
+    // pad each model's C rows to Cp (zero rows) and its bias to -inf, so tiles never mix models
+    CKU(cudaMalloc(&n_W, wrows * D * 2));
+    CKU(cudaMemset(n_W, 0, wrows * D * 2));
+    const bool wdev = is_device_ptr(W_bf16);
+    CKU(cudaMemcpy2D(n_W, (size_t)Cp * D * 2, W_bf16, (size_t)C * D * 2, (size_t)C * D * 2, K,
+                     wdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    CKU(cudaMalloc(&n_bias, wrows * 4));
+    CKU(cudaMemcpy(n_bias, hb.data(), wrows * 4, cudaMemcpyHostToDevice));
+  }
+#undef CKU
+  // commit
+  if (ctx->d_best_of) cudaFree(ctx->d_best_of);
+  if (ctx->d_W) cudaFree(ctx->d_W);
+  if (ctx->d_bias) cudaFree(ctx->d_bias);
+  ctx->d_best_of = n_best; ctx->d_W = n_W; ctx->d_bias = n_bias;
+  ctx->K = K; ctx->C = C; ctx->D = W_bf16 ? D : 0; ctx->S = (1 << K) - 1; ctx->tie = tie;
+  ctx->ldc = (C + 3) / 4 * 4;
+  ctx->Cp = Cp;
+  ctx->scale_log2 = logit_scale_log2;
+  memcpy(ctx->member_rank, rk_, sizeof(rk_));
+  ctx->has_heads = W_bf16 != nullptr;
   ctx->loaded = true;
-  ctx->have_batch = false;
-  ctx->reset_done = false;
+  ctx->have_batch = false;   // workspaces and tables were sized for the old ensemble:
+  ctx->reset_done = false;   // rk_score* and rk_subset_reset must run again
+  ctx->finalized = false;
   return RK_OK;
 }
 
@@ -328,7 +383,7 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
   rk_status s;
   if ((s = ensure(ctx, &ctx->ws_logits, &ctx->ws_cap, std::max<int64_t>(N, 1) * ctx->K * ctx->ldc)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
-  if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
+  if ((s = ensure(ctx, &ctx->ws_lsum, &ctx->ws_lsum_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   ctx->cur_logits = ctx->ws_logits;
   ctx->cur_ldc = ctx->ldc;
@@ -370,7 +425,7 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
     gp.N = n; gp.K = ctx->K; gp.C = ctx->C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
     gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias;
     gp.cluster = ctx->gemm_cluster;
-    gp.top1 = ctx->ws_top1 + r0 * ctx->K; gp.lse = ctx->ws_lse + r0 * ctx->K; gp.rmax = ctx->ws_max + r0 * ctx->K;
+    gp.top1 = ctx->ws_top1 + r0 * ctx->K; gp.lsum = ctx->ws_lsum + r0 * ctx->K; gp.rmax = ctx->ws_max + r0 * ctx->K;
     gp.logits = ctx->ws_logits + r0 * ctx->K * ctx->ldc;
     int rc = gemm_build_tmaps(gp, Xd, ctx->d_W, gp.logits, ctx->tmaps);  // maps are passed by value
     if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
@@ -496,6 +551,7 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
     CK(cudaMemcpy(ctx->d_qcarry, c0.data(), c0.size() * 8, cudaMemcpyHostToDevice));
   }
   ctx->reset_done = true;
+  ctx->finalized = false;
   ctx->final_seen = false;
   ctx->chunks = 0;
   return RK_OK;
@@ -504,6 +560,7 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
 rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream) {
   if (!ctx) return RK_EINVAL;
   if (!ctx->reset_done) return fail(ctx, RK_ESTATE, "rk_subset_reset first");
+  if (ctx->finalized) return fail(ctx, RK_ESTATE, "table already finalized (all-reduced): rk_subset_reset first");
   if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "rk_score / rk_score_logits first");
   const int64_t N = ctx->cur_N;
   if (N > 0 && !labels) return fail(ctx, RK_EINVAL, "labels required");
@@ -524,10 +581,9 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     unsigned long long* ch = ctx->d_chunk;
     unsigned int* errp = reinterpret_cast<unsigned int*>(ch + 3 * (size_t)S + (size_t)nB * S + 2 * (size_t)nR * nB * K);
     // ---- A2-A5: vote / average / counts ----
-    if (ctx->cur_ldc > kMaxCFast) return fail(ctx, RK_EUNSUPPORTED, "ldc > 1024 not supported by this build's vote kernel");
     VoteParams vp{};
     vp.logits = ctx->cur_logits; vp.ldc = ctx->cur_ldc;
-    vp.lse_in = ctx->batch_stats ? ctx->ws_lse : nullptr;
+    vp.lsum_in = ctx->batch_stats ? ctx->ws_lsum : nullptr;
     vp.top1_in = ctx->batch_stats ? ctx->ws_top1 : nullptr;
     vp.labels = dl; vp.N = N; vp.K = K; vp.C = C; vp.S = S; vp.tie = ctx->tie;
     const int gs = (ctx->want_labelled && nB > 0 && nR > 0) ? ctx->gs : 0;
@@ -549,6 +605,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     for (int bi = 0; bi < nB; ++bi) vp.tail_start[bi] = (N / ctx->B[bi]) * ctx->B[bi];
     vp.cnt_vote = ch; vp.cnt_avg = ch + S; vp.n_recheck = ch + 2 * S; vp.tail = ch + 3 * S;
     vp.err = errp;
+    ctx->grp_gs = gs;
+    ctx->grp_groups = gs > 0 ? (N + gs - 1) / gs : 0;
     if (gs > 0) {
       const size_t need = (size_t)((N + gs - 1) / gs) * S;
       if (ctx->grp_cap < need) {
@@ -573,7 +631,9 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     // overflow scratch (candidate sets larger than CAP): one region per warp
     const size_t owners = warp_path ? (size_t)grid * (vote_warp_threads() / 32)
                                     : (size_t)ctx->sm_count * vote_batch_avg_ctas_samples();
-    const size_t sf = owners * C * K, si = owners * C;
+    // (rows wider than kMaxCFast go to rk_vote_large.cu, which needs no global scratch)
+    const bool wide = ctx->cur_ldc > kMaxCFast;
+    const size_t sf = wide ? 0 : owners * C * K, si = wide ? 0 : owners * C;
     if (ctx->scratch_floats < sf) {
       if (ctx->d_scratch) cudaFree(ctx->d_scratch);
       ctx->d_scratch = nullptr;
@@ -599,12 +659,12 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
         vp.pair_count = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 3);
       }
       int32_t* st_top = nullptr;
-      float *st_lse = nullptr, *st_max = nullptr;
+      float *st_lsum = nullptr, *st_max = nullptr;
       if (!ctx->batch_stats) {  // the classify kernel writes row statistics for the averaging kernel
         if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, N * K)) != RK_OK) return s;
-        if ((s = ensure(ctx, &ctx->ws_lse, &ctx->ws_lse_cap, N * K)) != RK_OK) return s;
+        if ((s = ensure(ctx, &ctx->ws_lsum, &ctx->ws_lsum_cap, N * K)) != RK_OK) return s;
         if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, N * K)) != RK_OK) return s;
-        st_top = ctx->ws_top1; st_lse = ctx->ws_lse; st_max = ctx->ws_max;
+        st_top = ctx->ws_top1; st_lsum = ctx->ws_lsum; st_max = ctx->ws_max;
       }
       unsigned int* wc = reinterpret_cast<unsigned int*>(ctx->d_work + N);
       vp.ovf_work = ctx->d_work + N + 1;
@@ -613,8 +673,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       vp.cta_count = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 2);
       const double bytes = (double)N * ((double)K * C * 4 + 4);
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
-      if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lse, st_max, ctx->sm_count));
-      else CK(launch_vote_batch(vp, ctx->sm_count, st, ctx->d_work, wc, st_top, st_lse, st_max));
+      if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lsum, st_max, ctx->sm_count));
+      else CK(launch_vote_batch(vp, ctx->sm_count, st, ctx->d_work, wc, st_top, st_lsum, st_max));
     }
     // ---- A5: batch latency moments (label independent) ----
     const int64_t* arr = nullptr;
@@ -707,12 +767,17 @@ rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream) {
   CK(cudaSetDevice(ctx->dev));
   cudaStream_t st = (cudaStream_t)stream;
   const int S = ctx->S, nB = ctx->nB, nR = ctx->nR;
-  // A6: one all-reduce of the whole integer table (order-free, bit-exact)
-  if (ctx->comm) {
+  // A6: one all-reduce of the whole integer table (order-free, bit-exact), at most once per reset: a
+  // repeated finalize returns the same global table instead of summing it again
+  if (ctx->comm && !ctx->finalized) {
     ProfScope ps(ctx, KK_ALLREDUCE, st, (double)ctx->table_words * 8, 0);
     if (ncclAllReduce(ctx->d_table, ctx->d_table, ctx->table_words, ncclUint64, ncclSum, ctx->comm, st) != ncclSuccess)
       return fail(ctx, RK_ENCCL, "ncclAllReduce failed");
+    // bounded wait before any blocking copy: a dead peer must not hang the caller (NCCL async error poll)
+    rk_status w = wait_nccl(ctx, st);
+    if (w != RK_OK) return w;
   }
+  ctx->finalized = true;
   // A7: reward fold on the device
   const size_t nrew = (size_t)nR * nB * S;
   if (nrew > 0) {
@@ -775,7 +840,7 @@ rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_
   CK(cudaSetDevice(ctx->dev));
   cudaStream_t st = (cudaStream_t)stream;
   PredictParams pp{};
-  pp.logits = ctx->cur_logits; pp.ldc = ctx->cur_ldc; pp.lse_in = ctx->batch_stats ? ctx->ws_lse : nullptr;
+  pp.logits = ctx->cur_logits; pp.ldc = ctx->cur_ldc;
   pp.N = ctx->cur_N; pp.K = ctx->K; pp.C = ctx->C; pp.tie = ctx->tie; pp.v = v; pp.best_of = ctx->d_best_of;
   pp.pred_vote = pred_vote; pp.pred_avg = pred_avg; pp.avgprob = avgprob;
   ProfScope ps(ctx, KK_PREDICT, st, 0, 0);
@@ -841,13 +906,30 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
   return RK_OK;
 }
 
-rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** lse, int64_t* N) {
+rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64_t* groups, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->reset_done || ctx->chunks == 0) return fail(ctx, RK_ESTATE, "no chunk accumulated since rk_subset_reset");
+  if (gs) *gs = ctx->grp_gs;
+  if (groups) *groups = ctx->grp_groups;
+  const int64_t bytes = ctx->grp_groups * ctx->S;
+  if (!out || bytes == 0) return RK_OK;
+  if (cap < bytes) return fail(ctx, RK_EINVAL, "out holds fewer than groups * S bytes");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(out, ctx->d_grp, (size_t)bytes, cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return RK_OK;
+}
+
+rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** rmax,
+                     const float** lsum, int64_t* N) {
   if (!ctx) return RK_EINVAL;
   if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "no batch scored yet");
   if (logits) *logits = ctx->cur_logits;
   if (ldc) *ldc = (int)ctx->cur_ldc;
   if (top1) *top1 = ctx->batch_stats ? ctx->ws_top1 : nullptr;
-  if (lse) *lse = ctx->batch_stats ? ctx->ws_lse : nullptr;
+  if (rmax) *rmax = ctx->batch_stats ? ctx->ws_max : nullptr;
+  if (lsum) *lsum = ctx->batch_stats ? ctx->ws_lsum : nullptr;
   if (N) *N = ctx->cur_N;
   return RK_OK;
 }

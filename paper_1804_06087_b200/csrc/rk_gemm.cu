@@ -3,7 +3,9 @@
 //
 //   logit[n][m][c] = 2^s * sum_d X[n][d] * W[m][c][d] + bias[m][c]
 //   top1[n][m]     = lowest c attaining max_c logit          (reading Q4)
-//   lse[n][m]      = log sum_c exp(logit[n][m][c])           (softmax normaliser)
+//   rmax[n][m]     = max_c logit[n][m][c]
+//   lsum[n][m]     = log sum_c exp(logit[n][m][c] - rmax[n][m])  (softmax normaliser, PAPER.md:72;
+//                    relative to the max so p = exp((l - rmax) - lsum) stays exact for any offset)
 // The heads stand in for the classifier layer of the paper's ConvNets (the
 // inference time "depends on the model complexity, hardware efficiency ... and the batch size",
 // PAPER.md:361).
@@ -19,7 +21,7 @@
 //     overlaps the MMAs of tile i+1.
 //   * a work unit is (128-row block (CL rows blocks for a pair), model): the CTA walks the model's column tiles in ascending
 //     order, so the epilogue keeps an ONLINE max / lowest-index argmax / rescaled sum-exp per row
-//     in registers and writes top1/lse once per unit; logits leave through swizzled smem staging
+//     in registers and writes top1/lsum/rmax once per unit; logits leave through swizzled smem staging
 //     and TMA bulk tensor stores (rows >= N and columns >= C are clipped by the tensor map).
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -177,7 +179,7 @@ struct GemmArgs {
   int ng, gcols;  // work-unit column groups: K groups of Cp columns, or (packed) 1 group of K*Cp
   const float* bias;
   int32_t* top1;
-  float* lse;
+  float* lsum;
   float* rmax;
 };
 
@@ -243,7 +245,7 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // Packed-mode epilogue (see gemm_heads_kernel): 16-column blocks of the flattened column space; the
 // two warps of a TMEM lane quarter (half h) take alternating blocks and keep per-model online
 // (max, lowest argmax, sum-exp); at each model boundary half 1 hands its part to half 0 (named
-// barrier per quarter), which merges and writes top1/lse/max. Logits leave through a 32-row x
+// barrier per quarter), which merges and writes top1/lsum/max. Logits leave through a 32-row x
 // 16-column staging box (64-byte rows, 16-byte chunks XOR (row >> 1) & 3: the 64B TMA swizzle)
 // and a 3-D TMA store (class, model, row).
 template <int CL>
@@ -291,7 +293,7 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
           if (mk[k] != -INFINITY) S += sk[k] * __expf(mk[k] - M);
         if (row < a.N) {
           a.top1[row * a.K + m] = A;
-          a.lse[row * a.K + m] = M + logf(S);
+          a.lsum[row * a.K + m] = logf(S);  // log-sum relative to the row max (exact p below)
           a.rmax[row * a.K + m] = M;
         }
       }
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
       }
       if (row < a.N) {
         a.top1[row * a.K + model] = arg;
-        a.lse[row * a.K + model] = mx + logf(sum);
+        a.lsum[row * a.K + model] = logf(sum);  // relative to the row max
         a.rmax[row * a.K + model] = mx;
       }
     }
@@ -697,7 +699,7 @@ cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
   if (p.N <= 0) return cudaSuccess;
   GemmArgs a;
   a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D;
-  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lse = p.lse; a.rmax = p.rmax;
+  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lsum = p.lsum; a.rmax = p.rmax;
   const bool pack = p.Cp <= 128;  // small heads: tiles span several models
   a.ng = pack ? 1 : p.K;
   a.gcols = pack ? p.K * p.Cp : p.Cp;

@@ -10,13 +10,28 @@ constexpr int kMaxK = 12;
 constexpr int kMaxB = 8;
 constexpr int kMaxR = 8;
 constexpr int kVoteThreads = 256;   // vote kernel block size (8 warps)
-constexpr int kMaxCFast = 1024;     // register-resident rows up to ldc <= 1024 (8 float4 / lane)
+constexpr int kMaxCFast = 1024;     // register/shared-resident rows up to ldc <= 1024; wider rows: rk_vote_large.cu
+
+#ifdef __CUDACC__
+// θ pruning threshold of model `lane`, from the row statistics
+// mx = max_c l[m][c] and ls = log sum_c exp(l[m][c] - mx): p[m][c] = exp((l - mx) - ls), so
+// p[m][top_m] = exp(-ls) and theta = min_j exp(-ls_j) / K. Returns the logit threshold
+// mx + ls + log(theta) of lane m minus a slack that can only ENLARGE the candidate set (fp32 rounding
+// of ls, of the sum with mx, and of the comparison). Lanes >= K return garbage and must not use it.
+__device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int lane) {
+  float th = lane < K ? __expf(-ls) : INFINITY;
+  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(0xffffffffu, th, off));
+  const float lth = logf(th / (float)K);
+  return mx + (ls + lth) - (1e-3f + 2e-6f * fabsf(mx) + 1e-6f * (fabsf(ls) + fabsf(lth)));
+}
+#endif
 
 // ---- vote / average / subset-count kernel (steps A2-A5) --------------------------------------
 struct VoteParams {
   const float* logits;       // [N][K][ldc]
   int64_t ldc;
-  const float* lse_in;       // [N][K] or null (then computed here)
+  const float* lsum_in;      // [N][K] log sum_c exp(l[c] - rmax), relative to the row max, or null
+                             // (then computed here); p[m][c] = exp((l - rmax_m) - lsum_m)
   const int32_t* top1_in;    // [N][K] or null
   const float* rmax_in;      // [N][K] or null (row max, from the GEMM epilogue)
   const int32_t* labels;     // [N] device
@@ -66,7 +81,7 @@ cudaError_t launch_vote_avg(const VoteParams& q, int grid, cudaStream_t st, cons
 size_t vote_batch_smem_per_sample(const VoteParams& p);
 int vote_batch_avg_ctas_samples();
 cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work,
-                              unsigned int* work_count, int32_t* st_top, float* st_lse, float* st_max);
+                              unsigned int* work_count, int32_t* st_top, float* st_lsum, float* st_max);
 cudaError_t launch_vote_batch_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
                                   const unsigned int* work_count);  // rk_vote_batch_avg.cu
 // CTA-per-sample averaging with exact tables over every competitor (rk_vote_cta_avg.cu); samples with
@@ -87,16 +102,21 @@ cudaError_t launch_vote_wsample_avg(const VoteParams& q, int sm_count, cudaStrea
                                     unsigned int* work_count, int32_t* cta_work, unsigned int* cta_count,
                                     const int32_t** rest, const unsigned int** rest_count);
 
+// A4 for rows wider than 1024 classes (any K; rk_vote_large.cu): one CTA per worklist sample, fp64
+// from the definition over the candidate set; used instead of the kernels above when ldc > kMaxCFast.
+bool vote_large_needed(const VoteParams& q);
+cudaError_t launch_vote_large_avg(const VoteParams& q, int sm_count, cudaStream_t st, const int32_t* work,
+                                  const unsigned int* work_count);
+
 // Two kernels: classify+votes over all samples, then averages over the worklist of samples whose
 // label is an averaging candidate. work: [N] int32, work_count: 1 uint; st_*: [N][K] statistics
 // scratch (written by kernel A when the logits came without statistics).
 cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
-                             int32_t* st_top, float* st_lse, float* st_max, int sm_count);
+                             int32_t* st_top, float* st_lsum, float* st_max, int sm_count);
 
 // ---- per-sample predictions for one action v (rk_predict) ---------------------------------------
 struct PredictParams {
   const float* logits; int64_t ldc;
-  const float* lse_in;
   int64_t N; int K, C, tie; uint32_t v;
   const uint8_t* best_of;
   int32_t* pred_vote; int32_t* pred_avg; float* avgprob;
@@ -197,7 +217,7 @@ struct GemmParams {
   int scale_log2;
   const float* bias;     // [K][Cp] (-inf on padding columns)
   int32_t* top1;         // [N][K]
-  float* lse;            // [N][K]
+  float* lsum;           // [N][K] log sum_c exp(l - rmax) (relative to the row max)
   float* rmax;           // [N][K] row max (theta of the candidate pruning)
   float* logits;         // [N][K][ldc]
   unsigned int* err;

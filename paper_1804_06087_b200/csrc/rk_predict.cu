@@ -20,7 +20,7 @@ __global__ void predict_kernel(const PredictParams p) {
   const int K = p.K, C = p.C;
   for (int64_t n = warp; n < p.N; n += nwarps) {
     int top[kMaxK];
-    float lse[kMaxK];
+    float mxs[kMaxK], lsum[kMaxK];
     for (int m = 0; m < K; ++m) {
       const float* row = p.logits + (n * K + m) * p.ldc;
       float mx = -INFINITY;
@@ -38,7 +38,8 @@ __global__ void predict_kernel(const PredictParams p) {
       for (int c = lane; c < C; c += 32) s += __expf(row[c] - mx);
       for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
       top[m] = arg;
-      lse[m] = p.lse_in ? p.lse_in[n * K + m] : mx + logf(s);
+      mxs[m] = mx;
+      lsum[m] = logf(s);  // relative to the row max: p = exp((l - mx) - lsum) is exact for any offset
     }
     // vote
     if (p.pred_vote && lane == 0) {
@@ -69,7 +70,7 @@ __global__ void predict_kernel(const PredictParams p) {
       for (int c = lane; c < C; c += 32) {
         float s = 0.f;
         for (int m = 0; m < K; ++m)
-          if ((p.v >> m) & 1u) s += expf(p.logits[(n * K + m) * p.ldc + c] - lse[m]);
+          if ((p.v >> m) & 1u) s += expf((p.logits[(n * K + m) * p.ldc + c] - mxs[m]) - lsum[m]);
         const float a = s * inv;
         if (p.avgprob) p.avgprob[n * C + c] = a;
         if (a > bm) { bm = a; bc = c; }

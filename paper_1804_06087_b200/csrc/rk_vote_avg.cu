@@ -10,7 +10,7 @@
 //      S_c = {c : exists m, p[m][c] >= theta}, theta = min_j p[j][top_j] / K (the averaged argmax of
 //      every subset lies in S_c); a class below y in EVERY model has
 //      avg_v[c] < avg_v[y] for all v and can never decide whether y wins;
-//   2. p[m][c] = exp(l - lse_m) is gathered for c in R (slots in class order, warp scan);
+//   2. p[m][c] = exp((l - mx_m) - lsum_m) is gathered for c in R (slots in class order, warp scan);
 //   3. the members' distinct top-1 classes other than y (D, at most K) are the natural competitors:
 //      their subset sums, and y's, come from half-mask tables (one add per subset and column);
 //      every other candidate is bounded by Q[v] = sum_{m in v} max_{c in R \ ({y} ∪ D)} p[m][c];
@@ -42,15 +42,9 @@ __device__ __forceinline__ float4 ldg_stream(const float* p) {
 __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int lane) {
-  float th = lane < K ? __expf(mx - ls) : INFINITY;
-  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
-  const float lth = logf(th / (float)K);
-  return (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
-}
 
 struct WS {  // per-warp shared memory
-  double* lse64;    // [8]
+  double* sum64;    // [16]: [0,8) sum_c exp(l - mx) in fp64, [8,16) the row max mx
   int32_t* stop;    // [8] top-1 per model
   uint32_t* bitmap; // [32] R = S_c (theta test) ∩ classes not below y in some model
   int32_t* ccls;    // [CAP] candidate classes in ascending order
@@ -64,7 +58,7 @@ struct WS {  // per-warp shared memory
 __host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS* w) {
   size_t o = 0;
   auto take = [&](size_t b) -> char* { char* r = base ? base + o : nullptr; o = a16(o + b); return r; };
-  char* l64 = take(8 * 8);
+  char* l64 = take(16 * 8);
   char* st = take(4 * 8);
   char* bm = take(4 * 32);
   char* cc = take(4ull * p.CAP);
@@ -74,7 +68,7 @@ __host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS*
   char* Q = take(4 * 8);
   char* CN = take(4 * JMAX * 32);
   if (w) {
-    w->lse64 = (double*)l64; w->stop = (int32_t*)st; w->bitmap = (uint32_t*)bm;
+    w->sum64 = (double*)l64; w->stop = (int32_t*)st; w->bitmap = (uint32_t*)bm;
     w->ccls = (int32_t*)cc; w->P = (float*)P; w->T = (float*)T; w->QB = (float*)QB; w->Q = (float*)Q;
     w->cnt = (uint32_t*)CN;
   }
@@ -83,7 +77,7 @@ __host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS*
 
 // fp64 recheck of near-ties (rare, out of line): warp-cooperative fp64 log-sum-exp of every row, then
 // each lane decides its pending subsets in fp64 per readings Q5-Q6 (avg = (sum_{m in v, asc}
-// exp(l - lse_m)) / |v|, lowest class on ties) over the candidates inside the band.
+// exp(l - mx_m) / sum_c exp(l - mx_m)) / |v|, lowest class on ties; softmax with max subtraction, reading Q5) over the candidates inside the band.
 __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t pending, const float* rowbase,
                                           float mx, const float* Pm, int ps, const int32_t* cls, int nc, int ys,
                                           int y, int lane) {
@@ -94,7 +88,7 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
     double s = 0.0;
     for (int cc = lane; cc < C; cc += 32) s += exp((double)row[cc] - m64);
     for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-    if (lane == 0) ws.lse64[m] = m64 + log(s);
+    if (lane == 0) { ws.sum64[m] = s; ws.sum64[8 + m] = m64; }
   }
   __syncwarp();
   for (int j = 0; j < JMAX; ++j) {
@@ -115,7 +109,7 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
       double s = 0.0;
       for (uint32_t a = v; a; a &= a - 1) {
         const int m = __ffs(a) - 1;
-        s += exp((double)rowbase[(size_t)m * p.ldc + cq] - ws.lse64[m]);
+        s += exp((double)rowbase[(size_t)m * p.ldc + cq] - ws.sum64[8 + m]) / ws.sum64[m];
       }
       const double a64 = s / (double)nv;
       if (a64 > best || (a64 == best && cq < bestc)) { best = a64; bestc = cq; }
@@ -150,7 +144,7 @@ __global__ void __launch_bounds__(WT, 5) vote_average_kernel(const VoteParams p,
     float mx = 0.f, ls = 0.f;
     if (lane < K) {
       tp = p.top1_in[n * K + lane];
-      ls = p.lse_in[n * K + lane];
+      ls = p.lsum_in[n * K + lane];
       mx = p.rmax_in[n * K + lane];
     }
     const float thr = theta_threshold(mx, ls, K, lane);
@@ -246,12 +240,15 @@ __global__ void __launch_bounds__(WT, 5) vote_average_kernel(const VoteParams p,
       }
     }
     __syncwarp();
-    // ---- 2. gather p[m][c] = exp(l - lse_m) for c in R ------------------------------------------
+    // ---- 2. gather p[m][c] = exp((l - mx_m) - lsum_m) for c in R ------------------------------------------
     float* P = ovf ? ovP : ws.P;
     const int ps = ovf ? C : CAPS;
-    float lsm[8];
+    float lsm[8], mxm[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) lsm[m] = __shfl_sync(FULL, ls, m < K ? m : 0);
+    for (int m = 0; m < 8; ++m) {
+      lsm[m] = __shfl_sync(FULL, ls, m < K ? m : 0);
+      mxm[m] = __shfl_sync(FULL, mx, m < K ? m : 0);
+    }
     for (int sl = lane; sl < nc; sl += 32) {
       const int cq = cls[sl];
       float l[8];
@@ -260,7 +257,7 @@ __global__ void __launch_bounds__(WT, 5) vote_average_kernel(const VoteParams p,
         l[m] = m < K ? __ldg(rowbase + (size_t)m * p.ldc + cq) : 0.f;
 #pragma unroll
       for (int m = 0; m < 8; ++m)
-        if (m < K) P[(size_t)m * ps + sl] = expf(l[m] - lsm[m]);
+        if (m < K) P[(size_t)m * ps + sl] = expf((l[m] - mxm[m]) - lsm[m]);  // exact l - mx near the max
     }
     __syncwarp();
     // ---- 3. bound for candidates outside {y} ∪ D, and the exact-column half tables ------------

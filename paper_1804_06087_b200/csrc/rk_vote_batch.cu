@@ -1,4 +1,4 @@
-// rk_vote_batch.cu — steps A2-A5 for K = 9..12 models (511..4095 subsets), C <= 1024 classes.
+// rk_vote_batch.cu — steps A2-A5 for K = 9..12 models (511..4095 subsets).
 //
 // PAPER.md passages: :153 top-1 (reading Q4), :407 majority vote with best-accuracy tie-break
 // (RK_TIE_BEST_MEMBER; RK_TIE_LOWEST_CLASS = north_star), :72 averaged softmax (readings Q5, Q6),
@@ -37,12 +37,6 @@ __device__ __forceinline__ float4 ldg_stream(const float* p) {
 __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int lane) {
-  float th = lane < K ? __expf(mx - ls) : INFINITY;
-  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
-  const float lth = logf(th / (float)K);
-  return (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
-}
 
 // ragged-tail counts for the correct subsets of one word (samples past the last complete batch; rare)
 __device__ __noinline__ void tail_add_word(const VoteParams& p, uint32_t tm, uint32_t w, uint32_t ok) {
@@ -63,7 +57,7 @@ __device__ void row_stats(const VoteParams& p, const float* rowbase, int lane, i
     const float* row = rowbase + (size_t)m * p.ldc;
     float bm = -INFINITY, sum = 0.f;
     int ba = 0x7fffffff;
-    for (int c = lane; c < C; c += 32) {  // C <= 1024: at most 32 values per lane
+    for (int c = lane; c < C; c += 32) {
       const float x = row[c];
       if (x > bm) { bm = x; ba = c; }
     }
@@ -75,7 +69,7 @@ __device__ void row_stats(const VoteParams& p, const float* rowbase, int lane, i
     for (int c = lane; c < C; c += 32) sum += __expf(row[c] - bm);
     for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(FULL, sum, off);
     if (lane == m) {
-      tp = ba; mx = bm; ls = bm + logf(sum);
+      tp = ba; mx = bm; ls = logf(sum);  // log-sum relative to the row max
       bad = !(sum == sum) || !(bm > -INFINITY) || bm == INFINITY;
     }
   }
@@ -99,7 +93,7 @@ struct WRec {  // one sample's vote record (warp-private)
 template <int NWL, bool STATS>
 __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VoteParams p, int32_t* work,
                                                                     unsigned int* work_count, int32_t* st_top,
-                                                                    float* st_lse, float* st_max) {
+                                                                    float* st_lsum, float* st_max) {
   __shared__ uint32_t GE[32 * 8];        // GE[L][c] = {lo in [0,32) : popc(lo & L) >= c}
   __shared__ uint32_t LW[32 * 32];       // LW[A][B] = {lo : best-ranked member of lo ∩ (A ∪ B) is in A}
   __shared__ uint8_t LR[KM + 1];         // LR[r] = low models (m < 5) ranked better than r
@@ -190,7 +184,7 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
       const int yy = __shfl_sync(FULL, ylane, i & (CH - 1));
       if (STATS && i < CH && n < N && lane < K) {
         ntp = p.top1_in[n * K + lane];
-        nls = p.lse_in[n * K + lane];
+        nls = p.lsum_in[n * K + lane];
         nmx = p.rmax_in[n * K + lane];
         nly = (yy >= 0 && yy < C) ? p.logits[(n * K + lane) * p.ldc + yy] : 0.f;
       }
@@ -216,7 +210,7 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
             if (lane < K) bad = !(ls > -INFINITY && ls < INFINITY) || !(mx > -INFINITY);
           } else {
             row_stats(p, rowbase, lane, tp, mx, ls, bad);
-            if (lane < K) { st_top[n * K + lane] = tp; st_lse[n * K + lane] = ls; st_max[n * K + lane] = mx; }
+            if (lane < K) { st_top[n * K + lane] = tp; st_lsum[n * K + lane] = ls; st_max[n * K + lane] = mx; }
           }
           if (__any_sync(FULL, bad)) {
             if (lane == 0) atomicOr(p.err, 1u);
@@ -394,29 +388,30 @@ __global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VotePa
 
 template <int NK>
 cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work, unsigned int* work_count,
-                      int32_t* st_top, float* st_lse, float* st_max) {
+                      int32_t* st_top, float* st_lsum, float* st_max) {
   cudaError_t e;
   {
     const int64_t nb = (p.N + SB - 1) / SB;
     const int grid = (int)(nb < (int64_t)sm_count * 2 ? nb : (int64_t)sm_count * 2);
     constexpr int NWL = NK / 4 > 0 ? NK / 4 : 1;  // words per lane: 2^(K-5) / 32 (K = 9: half the lanes idle)
     const int dsm = (NWB << p.K) + 16;  // + padding: the copy-out reads one word past a row
-    if (p.lse_in) {
+    if (p.lsum_in) {
       if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     dsm)) != cudaSuccess)
         return e;
-      vote_group_classify_kernel<NWL, true><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
+      vote_group_classify_kernel<NWL, true><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lsum, st_max);
     } else {
       if ((e = cudaFuncSetAttribute(vote_group_classify_kernel<NWL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     dsm)) != cudaSuccess)
         return e;
-      vote_group_classify_kernel<NWL, false><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lse, st_max);
+      vote_group_classify_kernel<NWL, false><<<grid, BT, dsm, st>>>(p, work, work_count, st_top, st_lsum, st_max);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   {  // averages on the worklist, from statistics (the GEMM's or the classify kernel's)
     VoteParams q = p;
-    if (!p.lse_in) { q.top1_in = st_top; q.lse_in = st_lse; q.rmax_in = st_max; }
+    if (!p.lsum_in) { q.top1_in = st_top; q.lsum_in = st_lsum; q.rmax_in = st_max; }
+    if (vote_large_needed(q)) return launch_vote_large_avg(q, sm_count, st, work, work_count);  // ldc > 1024
     if (vote_wsample_avg_supported(q)) {  // few competitors: warp per sample; the rest -> CTA kernel
       const int32_t* rest = nullptr;
       const unsigned int* rest_count = nullptr;
@@ -437,7 +432,7 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
 
 
 cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st, int32_t* work,
-                              unsigned int* work_count, int32_t* st_top, float* st_lse, float* st_max) {
+                              unsigned int* work_count, int32_t* st_top, float* st_lsum, float* st_max) {
   if (p.N <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(work_count, 0, sizeof(unsigned int), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(p.ovf_count, 0, sizeof(unsigned int), st);
@@ -445,10 +440,10 @@ cudaError_t launch_vote_batch(const VoteParams& p, int sm_count, cudaStream_t st
   if (e == cudaSuccess && p.pair_count) e = cudaMemsetAsync(p.pair_count, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
   const int nk = (p.S + BT - 1) / BT;
-  if (nk <= 2) return launch_nk<2>(p, sm_count, st, work, work_count, st_top, st_lse, st_max);
-  if (nk <= 4) return launch_nk<4>(p, sm_count, st, work, work_count, st_top, st_lse, st_max);
-  if (nk <= 8) return launch_nk<8>(p, sm_count, st, work, work_count, st_top, st_lse, st_max);
-  return launch_nk<16>(p, sm_count, st, work, work_count, st_top, st_lse, st_max);
+  if (nk <= 2) return launch_nk<2>(p, sm_count, st, work, work_count, st_top, st_lsum, st_max);
+  if (nk <= 4) return launch_nk<4>(p, sm_count, st, work, work_count, st_top, st_lsum, st_max);
+  if (nk <= 8) return launch_nk<8>(p, sm_count, st, work, work_count, st_top, st_lsum, st_max);
+  return launch_nk<16>(p, sm_count, st, work, work_count, st_top, st_lsum, st_max);
 }
 
 }  // namespace rk

@@ -35,12 +35,6 @@ __device__ __forceinline__ float4 ldg_stream(const float* p) {
 __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int lane) {
-  float th = lane < K ? __expf(mx - ls) : INFINITY;
-  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
-  const float lth = logf(th / (float)K);
-  return (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
-}
 
 struct SmpB {   // per-sample arrays in the CTA's dynamic smem
   float* P;     // [K][CAP+1]
@@ -72,7 +66,7 @@ struct HdrB {  // per-sample scalars
   int32_t dslot[KM];
   float mx[KM];
   float q[KM];
-  double lse64[KM];
+  double sum64[KM];
 };
 
 template <int NK>
@@ -105,7 +99,7 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_average_kernel(const VotePar
         const float* rowbase = p.logits + n * K * p.ldc;
         int tp = 0;
         float mx = 0.f, ls = 0.f;
-        if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lse_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
+        if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lsum_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
         const float thr = theta_threshold(mx, ls, K, lane);
         const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;
         sm.bm[lane] = 0u;
@@ -170,8 +164,9 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_average_kernel(const VotePar
         }
         __syncwarp();
         for (int m = 0; m < K; ++m) {
-          const float ls_m = __shfl_sync(FULL, ls, m);
-          for (int sl = lane; sl < nc; sl += 32) P[(size_t)m * ps + sl] = expf(__ldg(rowbase + (size_t)m * p.ldc + cls[sl]) - ls_m);
+          const float ls_m = __shfl_sync(FULL, ls, m), mx_m = __shfl_sync(FULL, mx, m);
+          for (int sl = lane; sl < nc; sl += 32)
+            P[(size_t)m * ps + sl] = expf((__ldg(rowbase + (size_t)m * p.ldc + cls[sl]) - mx_m) - ls_m);
         }
         __syncwarp();
         for (int m = 0; m < K; ++m) {  // bound for candidates outside {y} ∪ D
@@ -271,7 +266,7 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_average_kernel(const VotePar
         double s = 0.0;
         for (int c = lane; c < C; c += 32) s += exp((double)rowbase[(size_t)m * p.ldc + c] - m64);
         for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-        if (lane == 0) hd[warp].lse64[m] = m64 + log(s);
+        if (lane == 0) hd[warp].sum64[m] = s;  // sum_c exp(l - hd.mx[m])
       }
     }
     __syncthreads();
@@ -304,7 +299,7 @@ __global__ void __launch_bounds__(BT, 2) vote_batch_average_kernel(const VotePar
           double acc = 0.0;
           for (uint32_t m = v; m; m &= m - 1) {
             const int mi = __ffs(m) - 1;
-            acc += exp((double)rowbase[(size_t)mi * p.ldc + cq] - hd[s].lse64[mi]);
+            acc += exp((double)rowbase[(size_t)mi * p.ldc + cq] - (double)hd[s].mx[mi]) / hd[s].sum64[mi];
           }
           const double a64 = acc / (double)__popc(v);
           if (a64 > best || (a64 == best && cq < bestc)) { best = a64; bestc = cq; }

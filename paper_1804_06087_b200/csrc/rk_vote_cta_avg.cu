@@ -86,7 +86,7 @@ struct Shared {  // static shared state
   uint32_t bm[32];
   int32_t cols[JS];  // 0 = y, 1..nr = R ascending, -1 = unused
   Stat st[2];
-  double lse64[KM];
+  double sum64[KM];
   int32_t nq, npend, skip, tiny;
 };
 
@@ -96,14 +96,9 @@ __device__ __forceinline__ void load_stat(const VoteParams& p, const int32_t* wo
   const int64_t n = work[e];
   float mx = 0.f, ls = 0.f;
   int tp = 0;
-  if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lse_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
-  float th = lane < K ? __expf(mx - ls) : INFINITY;
-  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
-  const float lth = logf(th / (float)K);
-  if (lane < K) {
-    st.top[lane] = tp; st.ls[lane] = ls; st.mx[lane] = mx;
-    st.thr[lane] = (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
-  }
+  if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lsum_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
+  const float thr = theta_threshold(mx, ls, K, lane);
+  if (lane < K) { st.top[lane] = tp; st.ls[lane] = ls; st.mx[lane] = mx; st.thr[lane] = thr; }
   if (lane == 0) { st.n = n; st.y = p.labels[n]; }
 }
 
@@ -273,7 +268,7 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
       const int nq = (nr + 1 + 3) >> 2;
       const bool fits = 4 * nq <= p.cta_cols;
       // p[m][y] < e^-68 (~3e-30) for some model: y's subset sums may be (nearly) subnormal
-      const bool tiny = __any_sync(FULL, lane < K && rows[(size_t)lane * p.ldc + y] - st.ls[lane] < -68.f);
+      const bool tiny = __any_sync(FULL, lane < K && (rows[(size_t)lane * p.ldc + y] - st.mx[lane]) - st.ls[lane] < -68.f);
       if (fits) {
         if (lane < 4) sh.cols[4 * nq - 4 + lane] = -1;
         __syncwarp();
@@ -292,11 +287,11 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
     if (warp == CW - 1 && e + gridDim.x < W) load_stat(p, work, e + gridDim.x, sh.st[sb ^ 1], lane);
     if (!sh.skip) {
       const int nq = sh.nq, nj4 = 4 * nq;
-      // ---- S4: p[m][c] = exp(l - lse) for every column ------------------------------------------
+      // ---- S4: p[m][c] = exp((l - mx) - lsum) for every column ------------------------------------------
       for (int i = t; i < K * nj4; i += CT) {
         const int m = i / nj4, j = i - m * nj4;
         const int c = sh.cols[j];
-        Pm[m * JS + j] = c >= 0 ? expf(rows[(size_t)m * p.ldc + c] - st.ls[m]) : 0.f;
+        Pm[m * JS + j] = c >= 0 ? expf((rows[(size_t)m * p.ldc + c] - st.mx[m]) - st.ls[m]) : 0.f;
       }
       __syncthreads();
       // ---- S5: half-mask tables TA[h][j] = sum_{m in h} p[m][j] (ascending m), TB rows after TA:
@@ -356,7 +351,7 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
           double s = 0.0;
           for (int c = lane; c < C; c += 32) s += exp((double)rows[(size_t)m * p.ldc + c] - m64);
           for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-          if (lane == 0) sh.lse64[m] = m64 + log(s);
+          if (lane == 0) sh.sum64[m] = s;  // sum_c exp(l - st.mx[m])
         }
         __syncthreads();
         for (int i = warp; i < np; i += CW) {
@@ -369,7 +364,7 @@ __global__ void __launch_bounds__(CT, 3) vote_cta_average_kernel(const VoteParam
             double acc = 0.0;
             for (uint32_t mm = v; mm; mm &= mm - 1) {
               const int m = __ffs(mm) - 1;
-              acc += exp((double)rows[(size_t)m * p.ldc + c] - sh.lse64[m]);
+              acc += exp((double)rows[(size_t)m * p.ldc + c] - (double)st.mx[m]) / sh.sum64[m];
             }
             const double a64 = acc / (double)__popc(v);
             if (a64 > best || (a64 == best && c < bestc)) { best = a64; bestc = c; }

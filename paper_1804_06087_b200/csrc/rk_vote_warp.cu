@@ -1,4 +1,4 @@
-// rk_vote_warp.cu — steps A2-A5 for K <= 8 models, C <= 1024 classes. One WARP per sample, no
+// rk_vote_warp.cu — steps A2-A5 for K <= 8 models (caller rows are read in blocks of 1024 classes). One WARP per sample, no
 // block-level barriers, two kernels (rk_vote.cu holds the CTA-tile kernel used for K > 8).
 //
 // PAPER.md passages: :153 top-1 (reading Q4), :407 majority vote with best-accuracy tie-break
@@ -48,14 +48,6 @@ __device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// theta threshold of model m (lane m): candidate <=> l >= lse_m + log(theta), minus a slack that can
-// only enlarge the set (fp32 rounding of lse and of the comparison).
-__device__ __forceinline__ float theta_threshold(float mx, float ls, int K, int lane) {
-  float th = lane < K ? __expf(mx - ls) : INFINITY;
-  for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
-  const float lth = logf(th / (float)K);
-  return (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
-}
 
 // rare: a vote-correct sample in the ragged tail of the chunk (outside complete batches of B[b])
 __device__ __noinline__ void tail_add(const VoteParams& p, uint32_t tm, uint32_t v) {
@@ -67,7 +59,7 @@ __device__ __noinline__ void tail_add(const VoteParams& p, uint32_t tm, uint32_t
 template <bool STATS>
 __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p, int32_t* work,
                                                               unsigned int* work_count, int32_t* st_top,
-                                                              float* st_lse, float* st_max) {
+                                                              float* st_lsum, float* st_max) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.K, S = p.S, C = p.C;
   const int F = (int)(p.ldc >> 2);
@@ -97,7 +89,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
       const int yy = __shfl_sync(FULL, ylane, (int)(nn - u0) & 31);
       if (STATS && nn < s1 && lane < K) {
         ntp = p.top1_in[nn * K + lane];
-        nls = p.lse_in[nn * K + lane];
+        nls = p.lsum_in[nn * K + lane];
         nmx = p.rmax_in[nn * K + lane];
         nly = (yy >= 0 && yy < C) ? p.logits[(nn * K + lane) * p.ldc + yy] : 0.f;
       }
@@ -122,49 +114,59 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
 #pragma unroll 1
         for (int m = 0; m < K; ++m) {  // one pass over the row: max, lowest argmax, sum exp
           const float* row = rowbase + (size_t)m * p.ldc;
-          float4 v[8];
+          float bm = -INFINITY, sum = 0.f;
+          int ba = 0x7fffffff;
+#pragma unroll 1
+          for (int f0 = 0; f0 < F; f0 += 256) {  // blocks of 1024 classes (one block when ldc <= 1024)
+            float4 v[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int c4 = lane + 32 * i;
-            v[i] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-            if (c4 < F && c4 * 4 < C) {
-              v[i] = ldg_stream(row + c4 * 4);
-              if (c4 * 4 + 4 > C) {  // padding components of the last partial float4
-                const int valid = C - c4 * 4;
-                if (valid < 4) v[i].w = -INFINITY;
-                if (valid < 3) v[i].z = -INFINITY;
-                if (valid < 2) v[i].y = -INFINITY;
+            for (int i = 0; i < 8; ++i) {
+              const int c4 = f0 + lane + 32 * i;
+              v[i] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+              if (c4 < F && c4 * 4 < C) {
+                v[i] = ldg_stream(row + c4 * 4);
+                if (c4 * 4 + 4 > C) {  // padding components of the last partial float4
+                  const int valid = C - c4 * 4;
+                  if (valid < 4) v[i].w = -INFINITY;
+                  if (valid < 3) v[i].z = -INFINITY;
+                  if (valid < 2) v[i].y = -INFINITY;
+                }
               }
             }
-          }
-          float bm = -INFINITY;
-          int ba = 0x7fffffff;
+            float km = -INFINITY;
+            int ka = 0x7fffffff;
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float x = f4c(v[i], e);
-              if (x > bm) { bm = x; ba = (lane + 32 * i) * 4 + e; }
+              for (int e = 0; e < 4; ++e) {
+                const float x = f4c(v[i], e);
+                if (x > km) { km = x; ka = (f0 + lane + 32 * i) * 4 + e; }
+              }
+            for (int off = 16; off; off >>= 1) {
+              const float om = __shfl_xor_sync(FULL, km, off);
+              const int oa = __shfl_xor_sync(FULL, ka, off);
+              if (om > km || (om == km && oa < ka)) { km = om; ka = oa; }
             }
-          for (int off = 16; off; off >>= 1) {
-            const float om = __shfl_xor_sync(FULL, bm, off);
-            const int oa = __shfl_xor_sync(FULL, ba, off);
-            if (om > bm || (om == bm && oa < ba)) { bm = om; ba = oa; }
+            // running max / lowest argmax (earlier blocks hold lower classes) / rescaled sum
+            const float nm = fmaxf(bm, km);
+            if (km > bm) ba = ka;
+            float ks = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) ks += __expf(f4c(v[i], e) - nm);
+            for (int off = 16; off; off >>= 1) ks += __shfl_xor_sync(FULL, ks, off);
+            sum = (bm == -INFINITY ? 0.f : sum * __expf(bm - nm)) + ks;
+            bm = nm;
           }
-          float sum = 0.f;
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) sum += __expf(f4c(v[i], e) - bm);
-          for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(FULL, sum, off);
           if (lane == m) {
-            tp = ba; mx = bm; ls = bm + logf(sum);
+            tp = ba; mx = bm; ls = logf(sum);  // log-sum relative to the row max
             bad = !(sum == sum) || !(bm > -INFINITY) || bm == INFINITY;
           }
         }
         if (lane < K) {  // statistics for kernel B
           st_top[n * K + lane] = tp;
-          st_lse[n * K + lane] = ls;
+          st_lsum[n * K + lane] = ls;
           st_max[n * K + lane] = mx;
         }
       }
@@ -266,7 +268,7 @@ int vote_warp_threads() { return WT; }
 int vote_warp_min_blocks() { return 5; }
 
 cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
-                             int32_t* st_top, float* st_lse, float* st_max, int sm_count) {
+                             int32_t* st_top, float* st_lsum, float* st_max, int sm_count) {
   if (p.N <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(work_count, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
@@ -276,15 +278,17 @@ cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int
     const int64_t units = (p.N + U - 1) / U;
     int64_t ga = (units + WPC - 1) / WPC;
     if (ga > (int64_t)sm_count * 8) ga = (int64_t)sm_count * 8;
-    if (p.lse_in) vote_classify_kernel<true><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
-    else vote_classify_kernel<false><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lse, st_max);
+    if (p.lsum_in) vote_classify_kernel<true><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lsum, st_max);
+    else vote_classify_kernel<false><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lsum, st_max);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   // kernel B: averages on the worklist (always from statistics: the GEMM's or kernel A's)
   {
     VoteParams q = p;
-    if (!p.lse_in) { q.top1_in = st_top; q.lse_in = st_lse; q.rmax_in = st_max; }
-    if ((e = launch_vote_avg(q, grid, st, work, work_count)) != cudaSuccess) return e;
+    if (!p.lsum_in) { q.top1_in = st_top; q.lsum_in = st_lsum; q.rmax_in = st_max; }
+    if (vote_large_needed(q)) e = launch_vote_large_avg(q, sm_count, st, work, work_count);  // ldc > 1024
+    else e = launch_vote_avg(q, grid, st, work, work_count);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

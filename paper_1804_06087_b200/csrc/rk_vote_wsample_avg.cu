@@ -69,7 +69,8 @@ struct WarpSmem {
   float4 TAX[NG > NR ? 64 * (NG - NR) : 1];  // TA rows' column groups NR.. (a < 2^K1 <= 64)
   float P[KM * WC];    // p[m][j] of the sample's columns (j = 0: y), zero-padded
   int32_t cols[WC];    // c_j (j = 0: y, then R ascending)
-  float ls[KM];        // lse per model
+  float ls[KM];        // log sum_c exp(l - mx) per model
+  float mx[KM];        // row max per model
 };
 
 template <int K>
@@ -199,11 +200,8 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
     // ---- statistics and θ threshold, lane m < K holds model m ----------------------
     int tp = 0;
     float ls = 0.f, mx = 0.f;
-    if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lse_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
-    float th = lane < K ? __expf(mx - ls) : INFINITY;
-    for (int off = 16; off; off >>= 1) th = fminf(th, __shfl_xor_sync(FULL, th, off));
-    const float lth = logf(th / (float)K);
-    const float thr = (ls + lth) - (1e-3f + 1e-6f * fabsf(ls) + 1e-6f * fabsf(lth));
+    if (lane < K) { tp = p.top1_in[n * K + lane]; ls = p.lsum_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
+    const float thr = theta_threshold(mx, ls, K, lane);
     const uint32_t ymask = __ballot_sync(FULL, lane < K && tp == y);  // models whose top-1 is y
     // ---- the K rows in registers (L1-allocating: the column pass re-reads a few values) -----------
     //      lane holds classes 4*lane .. 4*lane+3
@@ -237,26 +235,26 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
     }
     const int nr = __shfl_sync(FULL, incl, 31);
     // p[m][y] < e^-68 for some model: y's sums may be (nearly) subnormal -> CTA kernel (guarded)
-    const bool tiny = __any_sync(FULL, lane < K && myly - ls < -68.f);
+    const bool tiny = __any_sync(FULL, lane < K && (myly - mx) - ls < -68.f);
     if (nr + 1 > WC || tiny) {
       if (lane == 0) cta_work[atomicAdd(cta_count, 1u)] = (int32_t)n;
       continue;
     }
     const int nq = (nr + 1 + 3) >> 2;  // 1..NG float4 column groups
     // ---- probabilities of the columns: lane i handles (m, j) = (i mod K, i div K), re-reading l[m][c_j]
-    //      (an L1 hit: the rows were just loaded) -> p[m][j] = exp(l[m][c_j] - lse_m) -------------------
+    //      (an L1 hit: the rows were just loaded) -> p[m][j] = exp((l[m][c_j] - mx_m) - lsum_m) -------------------
     __syncwarp();  // the previous sample's readers of P / TB / cols are done
     for (int i = lane; i < K * WC / 4; i += 32) reinterpret_cast<float4*>(P)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     {
       int j = 1 + incl - cnt_l;
       for (uint32_t q = nib; q; q &= q - 1) wsm[warp].cols[j++] = cls0 + __ffs(q) - 1;
       if (lane == 0) wsm[warp].cols[0] = y;
-      if (lane < K) wsm[warp].ls[lane] = ls;
+      if (lane < K) { wsm[warp].ls[lane] = ls; wsm[warp].mx[lane] = mx; }
     }
     __syncwarp();
     for (int i = lane; i < K * (nr + 1); i += 32) {
       const int j = i / K, m = i - j * K;
-      P[m * WC + j] = expf(__ldg(rb + m * ldc + wsm[warp].cols[j]) - wsm[warp].ls[m]);
+      P[m * WC + j] = expf((__ldg(rb + m * ldc + wsm[warp].cols[j]) - wsm[warp].mx[m]) - wsm[warp].ls[m]);
     }
     __syncwarp();
     // ---- tables: TB rows b = lane + 32r in shared memory, the lane's TA row(s) in registers -------
@@ -359,8 +357,8 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
 }
 
 // fp64 recheck of one near-tie (sample, subset) pair per warp, from the definition (reading
-// Q6): p[m][c] = exp(l[m][c] - lse64[m]) with lse64[m] = mx_m + log sum_c exp(l[m][c] - mx_m) (mx_m the
-// exact fp32 row max), avg[c] = sum_{m in v} p[m][c] / |v| over every class, argmax with the lowest
+// Q6): p[m][c] = exp(l[m][c] - mx_m) / sum_c exp(l[m][c] - mx_m) in fp64 (mx_m the exact fp32 row max: the
+// max-subtracted softmax of reading Q5), avg[c] = sum_{m in v} p[m][c] / |v| over every class, argmax with the lowest
 // class on ties; correct iff it is y. Lane l holds classes 4l..4l+3 (ldc <= 128).
 __global__ void __launch_bounds__(WT) vote_pair_recheck_kernel(const VoteParams p) {
   const int lane = threadIdx.x & 31;
@@ -388,10 +386,9 @@ __global__ void __launch_bounds__(WT) vote_pair_recheck_kernel(const VoteParams 
         s += e4[q];
       }
       for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-      const double lse = m64 + log(s);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (4 * lane + q < C) acc[q] += exp((double)f4c(x, q) - lse);
+        if (4 * lane + q < C) acc[q] += e4[q] / s;
     }
     const double inv = (double)__popc(v);
     double best = -1.0;

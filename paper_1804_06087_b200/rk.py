@@ -24,6 +24,7 @@ TIE_BEST_MEMBER, TIE_LOWEST_CLASS = 0, 1
 
 EXPORTS = ["rk_create", "rk_nccl_unique_id", "rk_load_ensemble", "rk_score", "rk_score_logits", "rk_subset_reset",
            "rk_subset_accumulate", "rk_subset_finalize", "rk_subset_stats", "rk_predict", "rk_greedy_serve", "rk_outputs",
+           "rk_group_counts",
            "rk_set_profiling", "rk_kernel_stats", "rk_last_error", "rk_status_string", "rk_destroy"]
 
 
@@ -75,7 +76,8 @@ def load_library(path: str | None = None):
     L.rk_predict.argtypes = [vp, u32, vp, vp, vp, vp]
     L.rk_greedy_serve.argtypes = [vp, ctypes.POINTER(_Cfg), i64, i64, vp, ctypes.POINTER(_Serve), vp]
     L.rk_outputs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i32), ctypes.POINTER(vp), ctypes.POINTER(vp),
-                             ctypes.POINTER(i64)]
+                             ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    L.rk_group_counts.argtypes = [vp, vp, i64, ctypes.POINTER(i32), ctypes.POINTER(i64), vp]
     L.rk_set_profiling.argtypes = [vp, i32]
     L.rk_kernel_stats.argtypes = [vp, ctypes.POINTER(_KStat), i32, ctypes.POINTER(i32)]
     for f in EXPORTS:
@@ -252,11 +254,23 @@ class Context:
         return res
 
     def outputs(self):
-        lg, t1, ls = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        lg, t1, mx, ls = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         ldc, n = ctypes.c_int(), ctypes.c_int64()
-        self._chk(self._L.rk_outputs(self._p, ctypes.byref(lg), ctypes.byref(ldc), ctypes.byref(t1), ctypes.byref(ls),
-                                     ctypes.byref(n)), "rk_outputs")
-        return {"logits": lg.value, "ldc": ldc.value, "top1": t1.value, "lse": ls.value, "N": n.value}
+        self._chk(self._L.rk_outputs(self._p, ctypes.byref(lg), ctypes.byref(ldc), ctypes.byref(t1), ctypes.byref(mx),
+                                     ctypes.byref(ls), ctypes.byref(n)), "rk_outputs")
+        return {"logits": lg.value, "ldc": ldc.value, "top1": t1.value, "rmax": mx.value, "lsum": ls.value,
+                "N": n.value}
+
+    def group_counts(self, stream=None):
+        """Per-(group, subset) vote-correct counts of the last accumulated chunk: (gs, uint8 [groups][S])."""
+        gs, ng = ctypes.c_int(), ctypes.c_int64()
+        self._chk(self._L.rk_group_counts(self._p, None, 0, ctypes.byref(gs), ctypes.byref(ng), _stream(stream)),
+                  "rk_group_counts")
+        out = np.zeros((ng.value, self.S), np.uint8)
+        if out.size:
+            self._chk(self._L.rk_group_counts(self._p, out.ctypes.data, out.size, None, None, _stream(stream)),
+                      "rk_group_counts")
+        return gs.value, out
 
     def set_profiling(self, on: bool):
         self._chk(self._L.rk_set_profiling(self._p, int(on)), "rk_set_profiling")

@@ -40,8 +40,9 @@ def run_gemm(rk, K, C, D, N, X, W, b, sh, tie=0):
     torch.cuda.synchronize()
     lg = dev_view(out["logits"], (N, K, ldc), "<f4")
     t1 = dev_view(out["top1"], (N, K), "<i4")
-    ls = dev_view(out["lse"], (N, K), "<f4")
-    return ctx, lg, t1, ls
+    mx = dev_view(out["rmax"], (N, K), "<f4")
+    ls = dev_view(out["lsum"], (N, K), "<f4")
+    return ctx, lg, t1, (mx, ls)
 
 
 class _CAI:
@@ -55,7 +56,7 @@ def dev_view(ptr, shape, typestr):
 
 
 @pytest.mark.parametrize("K,C,D,N", [(3, 10, 128, 200), (2, 100, 256, 300), (3, 1000, 512, 130),
-                                     (12, 100, 1024, 257), (1, 2, 64, 5), (4, 300, 192, 129)])
+                                     (12, 100, 1024, 257), (1, 2, 64, 5), (4, 300, 192, 129), (2, 2000, 256, 300)])
 @pytest.mark.parametrize("cluster", ["1", "2"])
 def test_int_mode_bit_exact(rk, K, C, D, N, cluster, monkeypatch):
     monkeypatch.setenv("RK_GEMM_CLUSTER", cluster)  # read by rk_create: 1 CTA or 2-CTA W multicast
@@ -64,8 +65,17 @@ def test_int_mode_bit_exact(rk, K, C, D, N, cluster, monkeypatch):
     ref = oracle.logits_gemm(X, W, b, sh)  # fp64, exact for these integer inputs
     np.testing.assert_array_equal(lg[:, :, :C], ref.astype(np.float32))
     np.testing.assert_array_equal(t1, np.argmax(ref, axis=2))
-    ref_lse = np.array([[oracle.lse(ref[n, m]) for m in range(K)] for n in range(N)])
-    np.testing.assert_allclose(ls, ref_lse, rtol=2e-6, atol=2e-6)
+    check_row_stats(ls, ref)
+
+
+def check_row_stats(stats, ref):
+    """rmax bit-exact (fp32 of the exact logits); lsum = log sum_c exp(l - max) = oracle lse - max within
+    2e-6 (fp32 sum of ex2 terms, relative to the max so the bound does not grow with the logits' offset)."""
+    mx, ls = stats
+    N, K = mx.shape
+    np.testing.assert_array_equal(mx, ref.max(axis=2).astype(np.float32))
+    ref_ls = np.array([[oracle.lse(ref[n, m]) - ref[n, m].max() for m in range(K)] for n in range(N)])
+    np.testing.assert_allclose(ls, ref_ls, rtol=2e-6, atol=2e-6)
 
 
 def test_real_mode_tolerance(rk):
@@ -84,7 +94,8 @@ def test_real_mode_tolerance(rk):
     np.testing.assert_array_equal(t1[clear], np.argmax(ref, axis=2)[clear])
 
 
-@pytest.mark.parametrize("K,C,D,N,tie", [(3, 1000, 512, 600, 0), (8, 1000, 256, 150, 1), (12, 100, 512, 64, 0)])
+@pytest.mark.parametrize("K,C,D,N,tie", [(3, 1000, 512, 600, 0), (8, 1000, 256, 150, 1), (12, 100, 512, 64, 0),
+                                         (3, 2000, 256, 300, 1)])
 def test_end_to_end_int_mode(rk, K, C, D, N, tie):
     """X -> tcgen05 heads -> vote/average/moments -> reward table equals the oracle on its own fp64 logits."""
     y, X, W, b, sh = make(K, C, D, N, 9, real=False)

@@ -47,7 +47,10 @@ CASES = [  # (K, C, N, seed)
     (10, 20, 200, 9),
     (11, 100, 150, 10),
     (12, 1000, 40, 15),   # K = 12 with C = 1000: rows do not fit twice, single-buffered CTA kernel
-    (10, 1024, 50, 16),   # the largest C of this build
+    (10, 1024, 50, 16),   # the widest rows of the register/shared-memory kernels
+    (3, 2000, 400, 17),   # C > 1024 (SURVEY.md §8(b) allows C <= 65535): fp64 CTA averaging kernel
+    (10, 1500, 80, 18),   # C > 1024 with K >= 9
+    (2, 65535, 24, 19),   # the largest C of the contract
     (1, 2, 33, 6),        # degenerate: one model, two classes
     (5, 37, 517, 7),      # odd sizes, ragged everything
 ]
@@ -80,11 +83,12 @@ def test_integer_logits_ties(rk):
         assert o.n_amb.sum() > 0  # the case is exercised
 
 
-@pytest.mark.parametrize("K", [4, 10])
-def test_overflow_candidates_all_equal_rows(rk, K):
+@pytest.mark.parametrize("K,C", [(4, 300), (10, 300), (4, 2000)])
+def test_overflow_candidates_all_equal_rows(rk, K, C):
     """Rows with equal logits make every class a candidate (smem overflow paths; K = 10: more than 32
-    competitors, the CTA kernel hands the sample to the batch kernel)."""
-    C, N = 300, 64
+    competitors, the CTA kernel hands the sample to the batch kernel; C = 2000: the wide-row kernel's
+    candidate list overflows and it sweeps every class)."""
+    N = 64
     rng = np.random.default_rng(3)
     L = gen.logits(3, 0, N, K, C)
     L[::2, 1:, :C] = 0.0  # half the samples: models 1.. flat

@@ -66,6 +66,18 @@ def test_w1_per_sample_bits_mask3():
         assert bits == exp[key].astype(int).tolist()
 
 
+def test_w1_table_bits_mask3():
+    """The table's per-sample vote bits (want_bits, used for the per-group parity of the GPU's group
+    counts) reproduce the hand-computed mask-3 bits, and every column sums to its cnt_vote."""
+    K, C, preds, y, exp = _w1()
+    L = onehot_logits(preds, C)
+    for tie, key in ((oracle.TIE_BEST_MEMBER, "mask3_best_member"), (oracle.TIE_LOWEST_CLASS, "mask3_lowest_class")):
+        t = oracle.table(L, y, K, C, tie=tie, want_bits=True)
+        assert t.vote_ok[:, 3 - 1].astype(int).tolist() == exp[key].astype(int).tolist()
+        assert t.vote_ok.sum(0).tolist() == t.cnt_vote.tolist()
+        assert t.avg_ok.sum(0).tolist() == t.cnt_avg.tolist()
+
+
 # ---------------------------------------------------------------- W2 (reading Q2)
 def test_w2_tied_voters_reading():
     # (7,3,3,5,5): tied-voters reading -> 3; best-overall would give 7 (not a majority class).
@@ -289,3 +301,53 @@ def test_nonfinite_and_label_errors():
     assert e.value.code == oracle.ELABEL
     ok = L.copy(); ok[3, 1, 2] = -np.inf  # -inf is a legal logit (probability 0)
     oracle.table(ok, y, 2, 5)
+
+
+# ---------------------------------------------------------------- A1 heads (or_logits_gemm)
+def _bf16_bits(vals):
+    """bf16 bit patterns through torch's own float -> bfloat16 conversion (independent of gen/oracle)."""
+    import torch
+    t = torch.tensor(np.asarray(vals, np.float32)).to(torch.bfloat16)
+    return t.view(torch.int16).numpy().view(np.uint16)
+
+
+def _bf16_values(bits):
+    """Exact widening through torch (bfloat16 -> float64), independent of the oracle's bit shifting."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(torch.float64).numpy()
+
+
+def test_a1_hand_worked_example():
+    """One row worked by hand: W indexing [m][c][d], scale 2^s applied to the dot only, then the bias."""
+    rows = {r[0]: r[1:] for r in _read("a1_heads_example.txt")}
+    s = int(rows["s"][0])
+    X = _bf16_bits([[float(v) for v in rows["X"]]])
+    W = _bf16_bits([[[float(v) for v in rows[f"W{m}{c}"]] for c in range(2)] for m in range(2)])
+    b = np.array([float(v) for v in rows["bias"]], np.float32).reshape(2, 2)
+    out = oracle.logits_gemm(X, W, b, s)
+    assert out.reshape(-1).tolist() == [float(v) for v in rows["logits"]]
+    # without bias: the scaled dots only
+    assert oracle.logits_gemm(X, W, None, s).reshape(-1).tolist() == [1.25, -1.0, 0.125, -1.25]
+
+
+@pytest.mark.parametrize("N,K,C,D,s", [(7, 3, 5, 64, -3), (5, 1, 2, 128, 0), (3, 4, 11, 192, 4)])
+def test_a1_matches_einsum(N, K, C, D, s):
+    """Random bf16 values with exponents in a narrow band (every product and partial sum exact in fp64, so
+    the summation order cannot matter): the oracle equals numpy's einsum over torch-widened operands,
+    scaled by an exact power of two, plus the bias. Non-square shapes catch transposed operands."""
+    rng = np.random.default_rng(N * 131 + C)
+    def vals(shape):
+        return rng.choice([-1.0, 1.0], size=shape) * rng.integers(1, 256, size=shape) * 2.0 ** rng.integers(-8, 2, size=shape)
+    X = _bf16_bits(vals((N, D)))
+    W = _bf16_bits(vals((K, C, D)))
+    b = (rng.integers(-64, 64, size=(K, C)) / 8.0).astype(np.float32)
+    ref = np.einsum("nd,mcd->nmc", _bf16_values(X), _bf16_values(W)) * 2.0 ** s + b.astype(np.float64)[None]
+    out = oracle.logits_gemm(X, W, b, s)
+    assert out.shape == (N, K, C)
+    np.testing.assert_array_equal(out, ref)
+    # the generator's integer heads widen to small integers (integer-exact mode P3)
+    psig, f0, df, sh = gen.head_params(D, C, K)
+    Xg = gen.features(3, 0, N, D, C, psig, False)
+    Wg = gen.weights(4, K, C, D, f0, df, False)
+    ref_g = np.einsum("nd,mcd->nmc", _bf16_values(Xg), _bf16_values(Wg)) * 2.0 ** sh
+    np.testing.assert_array_equal(oracle.logits_gemm(Xg, Wg, None, sh), ref_g)
