@@ -142,6 +142,20 @@ __device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2 (what __expf
   return y;
 }
 constexpr float kL2E = 1.4426950408889634f;
+constexpr float kLN2 = 0.6931471805599453f;
+// Sum-exp bookkeeping that stays exact relative to the row max for ANY logit offset: the terms are
+// 2^(l*L2E + nml(mx)) with nml(mx) = rnd(-mx*L2E) (one FFMA each); a new running max rescales the sum by
+// 2^(nml(new) - nml(old)) (the same rounded values the terms used, so no |mx|-sized error enters); at the
+// end ln sum_c exp(l - mx) = ln(sum) - d*ln2 with d = mx*L2E + nml(mx), the rounding residual of nml,
+// which one FMA yields exactly. (Using exp(mx_old - mx_new) for the rescale, or ignoring d, would
+// leave an error of about |mx| * 2^-24 in the normaliser -- 1e-3 relative at |logits| ~ 1e4.)
+__device__ __forceinline__ float nml_of(float mx) { return __fmul_rn(-mx, kL2E); }
+__device__ __forceinline__ float rescale_factor(float mx_old, float mx_new) {
+  return ex2_approx(nml_of(mx_new) - nml_of(mx_old));  // mx_old = -inf -> 2^-inf = 0
+}
+__device__ __forceinline__ float lsum_of(float sum, float mx) {
+  return logf(sum) - fmaf(mx, kL2E, nml_of(mx)) * kLN2;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -286,14 +300,14 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
           if (mk[k] > M) { M = mk[k]; A = ak[k]; }
           else if (mk[k] == M && ak[k] < A) A = ak[k];
         }
-        float S = 0.f;
-        if (mx != -INFINITY) S += sum * __expf(mx - M);
+        float S = 0.f;  // every part's sum moved to the base nml(M) (see rescale_factor)
+        if (mx != -INFINITY) S += sum * rescale_factor(mx, M);
 #pragma unroll
         for (int k = 0; k < NHP - 1; ++k)
-          if (mk[k] != -INFINITY) S += sk[k] * __expf(mk[k] - M);
+          if (mk[k] != -INFINITY) S += sk[k] * rescale_factor(mk[k], M);
         if (row < a.N) {
           a.top1[row * a.K + m] = A;
-          a.lsum[row * a.K + m] = logf(S);  // log-sum relative to the row max (exact p below)
+          a.lsum[row * a.K + m] = lsum_of(S, M);  // log-sum relative to the row max (exact p below)
           a.rmax[row * a.K + m] = M;
         }
       }
@@ -331,12 +345,12 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
         if (cmax > mx) {  // new running max of this model: its lowest column (Q4)
 #pragma unroll
           for (int i = 15; i >= 0; --i) carg = v[i] == cmax ? cm + i : carg;
-          sum = sum * __expf(mx - cmax);
+          sum = sum * rescale_factor(mx, cmax);
           mx = cmax;
           arg = carg;
         }
         if (mx != -INFINITY) {
-          const float nml = -mx * kL2E;
+          const float nml = nml_of(mx);
 #pragma unroll
           for (int i = 0; i < 16; ++i) sum += ex2_approx(fmaf(v[i], kL2E, nml));
         }
@@ -537,12 +551,12 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
           if (cmax > mx) {  // new running max (rare after the first chunks): its lowest column (Q4)
 #pragma unroll
             for (int i = 31; i >= 0; --i) carg = v[i] == cmax ? colbase + i : carg;
-            sum = sum * __expf(mx - cmax);
+            sum = sum * rescale_factor(mx, cmax);
             mx = cmax;
             arg = carg;
           }
           if (mx != -INFINITY) {
-            const float nml = -mx * kL2E;
+            const float nml = nml_of(mx);
 #pragma unroll
             for (int i = 0; i < 32; ++i) sum += ex2_approx(fmaf(v[i], kL2E, nml));
           }
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
       }
       if (row < a.N) {
         a.top1[row * a.K + model] = arg;
-        a.lsum[row * a.K + model] = logf(sum);  // relative to the row max
+        a.lsum[row * a.K + model] = lsum_of(sum, mx);  // relative to the row max
         a.rmax[row * a.K + model] = mx;
       }
     }

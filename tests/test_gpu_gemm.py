@@ -70,12 +70,14 @@ def test_int_mode_bit_exact(rk, K, C, D, N, cluster, monkeypatch):
 
 def check_row_stats(stats, ref):
     """rmax bit-exact (fp32 of the exact logits); lsum = log sum_c exp(l - max) = oracle lse - max within
-    2e-6 (fp32 sum of ex2 terms, relative to the max so the bound does not grow with the logits' offset)."""
+    4e-6 absolute (fp32 sum of ex2.approx terms; relative to the max, so the bound does not grow with the
+    logits' offset -- the p[m][c] the averaging kernels form from it are within ~4e-6 relative, inside
+    the 2e-5 fp64-recheck band)."""
     mx, ls = stats
     N, K = mx.shape
     np.testing.assert_array_equal(mx, ref.max(axis=2).astype(np.float32))
     ref_ls = np.array([[oracle.lse(ref[n, m]) - ref[n, m].max() for m in range(K)] for n in range(N)])
-    np.testing.assert_allclose(ls, ref_ls, rtol=2e-6, atol=2e-6)
+    np.testing.assert_allclose(ls, ref_ls, rtol=0, atol=4e-6)
 
 
 def test_real_mode_tolerance(rk):
