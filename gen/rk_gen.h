@@ -90,10 +90,17 @@ RKG_FN int rkg_w_int(uint64_t seed, int m, int c, int d, uint32_t flip_q16) {
   uint32_t r = (uint32_t)(rkg_hash(seed, RKG_TAG_FLIP, ((uint64_t)m << 32) | (uint64_t)c, (uint64_t)d) & 0xffff);
   return r < flip_q16 ? -p : p;
 }
+/* psig_q16 packs two probabilities (units of 1/65536): bits 0..15 = P(prototype-matched dim);
+ * bits 16..31 = P(noise dim is +-1) -- 0 keeps the original uniform {-1, 0, 1} noise. A sparser noise
+ * lowers the spread of the wrong-class logits at the same signal, i.e. a softer softmax for a given
+ * accuracy (the calibration knob between the power-of-two logit scales). */
 RKG_FN int rkg_x_int(uint64_t seed, int64_t n, int d, int y, uint32_t psig_q16) {
   uint64_t h = rkg_hash(seed, RKG_TAG_X, (uint64_t)n, (uint64_t)d);
-  if ((uint32_t)(h & 0xffff) < psig_q16) return rkg_proto(seed, y, d);
-  return (int)rkg_below(h, 3) - 1;
+  if ((uint32_t)(h & 0xffff) < (psig_q16 & 0xffffu)) return rkg_proto(seed, y, d);
+  const uint32_t pnz = psig_q16 >> 16;
+  if (pnz == 0) return (int)rkg_below(h, 3) - 1;
+  if ((uint32_t)((h >> 16) & 0xffff) >= pnz) return 0;
+  return (h >> 63) ? 1 : -1;
 }
 /* float -> bf16 bits, round to nearest even (inputs are finite). */
 RKG_FN uint16_t rkg_f32_to_bf16(float f) {

@@ -72,12 +72,16 @@ def check_row_stats(stats, ref):
     """rmax bit-exact (fp32 of the exact logits); lsum = log sum_c exp(l - max) = oracle lse - max within
     4e-6 absolute (fp32 sum of ex2.approx terms; relative to the max, so the bound does not grow with the
     logits' offset -- the p[m][c] the averaging kernels form from it are within ~4e-6 relative, inside
-    the 2e-5 fp64-recheck band)."""
+    the 2e-5 fp64-recheck band). The error of a recursive fp32 sum grows with its number of
+    terms (Higham: (n-1)u worst case), so rows wider than 1000 classes get a proportionally wider bound;
+    those rows (ldc > 1024) are averaged by the fp64 wide-row kernel, which recomputes the normaliser, and
+    lsum only feeds the theta pruning there, whose threshold keeps a 1e-3 log margin (rk_internal.h)."""
     mx, ls = stats
     N, K = mx.shape
+    C = ref.shape[2]
     np.testing.assert_array_equal(mx, ref.max(axis=2).astype(np.float32))
     ref_ls = np.array([[oracle.lse(ref[n, m]) - ref[n, m].max() for m in range(K)] for n in range(N)])
-    np.testing.assert_allclose(ls, ref_ls, rtol=0, atol=4e-6)
+    np.testing.assert_allclose(ls, ref_ls, rtol=0, atol=4e-6 * max(1.0, C / 1000))
 
 
 def test_real_mode_tolerance(rk):

@@ -52,7 +52,7 @@ def near_tie_logits(N, K, C, seed, offsets):
     a = rng.uniform(0.5, 2.0, N)
     L[:, 0, 0], L[:, 0, 1] = a, 0.0
     L[:, 1, 0], L[:, 1, 1] = 0.0, a + rng.normal(0.0, 3e-4, N)
-    L += np.asarray(offsets[:K], np.float64)[None, :, None]
+    L += np.resize(np.asarray(offsets, np.float64), K)[None, :, None]
     L[:, :, C:] = np.nan
     y = rng.integers(0, 2, N).astype(np.int32)
     return L.astype(np.float32), y
