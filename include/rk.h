@@ -175,6 +175,51 @@ typedef struct {
 rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
                           rk_serve_out* out, void* stream);
 
+/* NEXT-1 baseline: "runs all models asynchronously, one model per batch of requests" (r_u
+ * is the sum of the models' throughputs in this mode). Reading S2: K servers
+ * (one per model) share one FIFO queue; whenever a model is idle at t, the lowest-index idle model m
+ * applies Algorithm 3's rule with its own c(m, b) (len(q) >= max B -> the oldest max B; else the largest
+ * b <= len(q) once c(m,b) + w(q0) + delta >= tau); the batch occupies m until t + c(m, b) and another idle
+ * model may dispatch at the same t. Same cfg fields as rk_greedy_serve. acc: [K] host single-model
+ * accuracies a({m}) or NULL; reward = sum over batches of a(m) * (b - beta * overdue). Output arrays are
+ * host [nR] (out fields; each may be NULL), model_batches host [nR][K] or NULL. Blocks on `stream`. */
+rk_status rk_async_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
+                         rk_serve_out* out, uint64_t* model_batches, void* stream);
+
+/* NEXT-1 serving loop: serve N requests with features X ([N][D] bf16, DEVICE, request order = arrival
+ * order) under action v with Algorithm 3 batching (rk_greedy_serve's rule for subset v on the single
+ * arrival stream of cfg, nR == 1): every dispatched batch runs the K heads (A1+A2, tcgen05 GEMM) on its
+ * rows and the per-request prediction of v (rk_predict's kernel), one batch at a time, in dispatch order.
+ * pred_vote / pred_avg: [N] int32 DEVICE or NULL; requests never served (fewer than min B left at the end)
+ * get -1. out: host, one element per field (may be NULL); *n_batches = batches served (may be NULL).
+ * Needs heads (rk_load_ensemble with W). The context's rk_score workspaces are reused: call rk_score again
+ * before rk_subset_accumulate / rk_predict. Blocks on `stream`. */
+rk_status rk_serve_stream(rk_ctx* ctx, const void* X_bf16, int64_t N, const rk_reward_cfg* cfg, int64_t delta_ns,
+                          uint32_t v, int32_t* pred_vote, int32_t* pred_avg, rk_serve_out* out, int64_t* n_batches,
+                          void* stream);
+
+/* NEXT-4: the paper's request-arrival process (§7.2, eqs. `eq:r1`/`eq:r2`; reading Q16):
+ * rate(t) = k sin(2 pi t / T) + b with k = 0.1 ref / (1 - s0), b = 1.1 ref - k, s0 = sin(0.3 pi) =
+ * (1 + sqrt 5)/4 (the rate exceeds ref for 20 % of each period T and peaks at 1.1 ref).
+ * The simulator is invoked every delta_ns; invocation j adds n_j = floor(max(0, delta * rate(j delta) *
+ * (1 + phi_j)) + 0.5) requests ("delta x (gamma sin(t) + b) x (1 + phi), phi ~ N(0, 0.1)"), phi_j =
+ * noise_std * z_j, z_j the Irwin-Hall(4) unit normal sum of the four 16-bit fields of
+ * h = mix(mix(mix(seed ^ 0x51AE0A77) ^ j) + 0x2545F4914F6CDD1D) minus 131070, times 7 / 2^18 (mix = the
+ * SplitMix64 finalizer), and the n_j requests arrive evenly spaced inside the invocation:
+ * t = j delta + floor(i delta / n_j), i < n_j. Writes the arrival times (ns, non-decreasing) of global
+ * requests [n0, n0 + N) to out_ns ([N] int64, DEVICE memory; earlier requests are generated and skipped,
+ * so shards of one stream agree). Feeds rk_reward_cfg.arrival_ns and rk_greedy_serve. Blocks on `stream`
+ * (the chunk loop reads each chunk's request total). Errors: ref <= 0, period_ns <= 0, delta_ns <= 0,
+ * noise_std < 0 or non-finite, n0 < 0, N < 0 -> RK_EINVAL. */
+typedef struct {
+  double ref_rate;         /* r_u or r_l in req/s                                   */
+  int64_t period_ns;       /* T; the paper uses 500 * tau                           */
+  int64_t delta_ns;        /* invocation interval delta                                              */
+  double noise_std;        /* 0.1 in the paper ("phi ~ N(0, 0.1)", read as the standard deviation) */
+  uint64_t seed;
+} rk_sine_cfg;
+rk_status rk_sine_arrivals(rk_ctx* ctx, const rk_sine_cfg* cfg, int64_t n0, int64_t N, int64_t* out_ns, void* stream);
+
 /* Serving of one action (NEXT-1) and parity hook: per-sample predictions of subset v on the
  * last rk_score* batch. pred_vote, pred_avg: [N] int32; avgprob: [N][C] fp32 averaged
  * probabilities. Device pointers; each may be NULL. v == 0 -> RK_EINVAL. */

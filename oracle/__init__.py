@@ -69,6 +69,10 @@ def lib():
         L.or_predict.argtypes = [vp, i32, vp, i64, i32, i32, u32, vp, i32, vp, vp, vp, vp, vp, i32]
         L.or_predict.restype = i32
         L.or_arrival_ns.argtypes = [i64, dbl]; L.or_arrival_ns.restype = i64
+        L.or_sine_params.argtypes = [dbl, vp, vp]; L.or_sine_params.restype = None
+        L.or_sine_count.argtypes = [dbl, i64, i64, dbl, ctypes.c_uint64, i64]; L.or_sine_count.restype = i64
+        L.or_sine_arrivals.argtypes = [dbl, i64, i64, dbl, ctypes.c_uint64, i64, i64, vp]
+        L.or_sine_arrivals.restype = i32
         _lib = L
     return _lib
 
@@ -120,6 +124,27 @@ def avg(p, v: int):
 
 def arrival_ns(s: int, rate: float) -> int:
     return lib().or_arrival_ns(s, rate)
+
+
+def sine_params(ref: float):
+    """(k, b) of rate(t) = k sin(2 pi t / T) + b (eqs. eq:r1/eq:r2, reading Q16)."""
+    k, b = ctypes.c_double(), ctypes.c_double()
+    lib().or_sine_params(ref, ctypes.byref(k), ctypes.byref(b))
+    return k.value, b.value
+
+
+def sine_count(ref: float, period_ns: int, delta_ns: int, sigma: float, seed: int, j: int) -> int:
+    """Requests added by simulator invocation j (reading Q16)."""
+    return lib().or_sine_count(ref, period_ns, delta_ns, sigma, seed, j)
+
+
+def sine_arrivals(ref: float, period_ns: int, delta_ns: int, sigma: float, seed: int, n0: int, N: int) -> np.ndarray:
+    """Arrival times (ns) of global requests [n0, n0 + N) of the sine-plus-noise process (reading Q16)."""
+    out = np.zeros(N, np.int64)
+    rc = lib().or_sine_arrivals(ref, period_ns, delta_ns, sigma, seed, n0, N, _p(out))
+    if rc != OK:
+        raise ValueError(f"or_sine_arrivals failed ({rc})")
+    return out
 
 
 def logits_gemm(X_bits, W_bits, bias, scale_log2: int) -> np.ndarray:
@@ -275,4 +300,34 @@ def greedy_serve(cfg: RewardCfg, K: int, N: int, delta_ns: int) -> dict:
     res = {}
     for name in ("served", "overdue", "exceed_ns", "batches", "unserved"):
         res[name] = np.array([getattr(o, name) for o in out], dtype=np.uint64).reshape(nR, S)
+    return res
+
+
+def async_serve(cfg: RewardCfg, K: int, N: int, delta_ns: int, acc=None) -> dict:
+    """The asynchronous one-model-per-batch baseline (reading S2), per rate: arrays
+    [nR] of served, overdue, exceed_ns, batches, unserved, reward (with acc [K]) and batches per model [nR][K]."""
+    nB = len(cfg.B)
+    Bv = np.ascontiguousarray(cfg.B, dtype=np.int32)
+    lat = np.ascontiguousarray(cfg.lat_ns, dtype=np.int64).reshape(K, nB)
+    if cfg.arrival_ns is not None:
+        arr, rates, nR = np.ascontiguousarray(cfg.arrival_ns, dtype=np.int64), None, 1
+    else:
+        arr, rates = None, np.ascontiguousarray(cfg.rates, dtype=np.float64)
+        nR = rates.size
+    cc = _Cfg(nB, _p(Bv), cfg.beta, cfg.tau_ns, _p(lat), nR, _p(rates), _p(arr), int(cfg.want_exceed), 0)
+    out = (_Serve * nR)()
+    rew = np.zeros(nR, np.float64)
+    mb = np.zeros((nR, K), np.uint64)
+    a = None if acc is None else np.ascontiguousarray(acc, dtype=np.float64)
+    L = lib()
+    L.or_async_serve.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    rc = L.or_async_serve(ctypes.byref(cc), K, N, delta_ns, _p(a), out, _p(rew), _p(mb))
+    if rc != OK:
+        raise OracleError(rc)
+    res = {name: np.array([getattr(o, name) for o in out], dtype=np.uint64)
+           for name in ("served", "overdue", "exceed_ns", "batches", "unserved")}
+    res["model_batches"] = mb
+    if a is not None:
+        res["reward"] = rew
     return res

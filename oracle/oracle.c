@@ -9,6 +9,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
 /* ---- A2: per-model top-1 ("top-1"; reading Q4: lowest index on ties) ---- */
 int or_top1_f32(const float* row, int C) {
   int best = 0;
@@ -153,6 +157,52 @@ void or_logits_gemm(const uint16_t* X, const uint16_t* W, const float* bias, int
 int64_t or_arrival_ns(int64_t s, double rate) {
   volatile double num = (double)s * 1e9; /* two IEEE roundings, in this order */
   return (int64_t)floor(num / rate);
+}
+
+/* ---- NEXT-4: the sine-plus-noise arrival process (eqs. eq:r1/eq:r2; reading Q16) ----
+ * rate(t) = k sin(2 pi t / T) + b. Eq. eq:r1: the rate exceeds ref for 20 % of each period -> the
+ * threshold phase 0.3 pi, s0 = sin(0.3 pi); eq. eq:r2: peak k + b = 1.1 ref. Hence k (1 - s0) = 0.1 ref
+ * (SPEC.md:705). The simulator, invoked every delta, adds delta * rate * (1 + phi) requests (rounded
+ * half up, never negative), phi = sigma * z with z the counter-based Irwin-Hall(4) normal of invocation j;
+ * they arrive evenly spaced inside the invocation. */
+static uint64_t or_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void or_sine_params(double ref, double* k, double* b) {
+  const double s0 = sin(0.3 * M_PI);
+  *k = 0.1 * ref / (1.0 - s0);
+  *b = 1.1 * ref - *k;
+}
+
+int64_t or_sine_count(double ref, int64_t period_ns, int64_t delta_ns, double sigma, uint64_t seed, int64_t j) {
+  double k, b;
+  or_sine_params(ref, &k, &b);
+  const double t = (double)((j * delta_ns) % period_ns) / (double)period_ns; /* phase of t = j delta in [0, 1) */
+  const double rate = k * sin(2.0 * M_PI * t) + b;
+  const uint64_t h = or_mix64(or_mix64(or_mix64(seed ^ 0x51AE0A77ull) ^ (uint64_t)j) + 0x2545F4914F6CDD1Dull);
+  const int64_t ih = (int64_t)(h & 0xffff) + (int64_t)((h >> 16) & 0xffff) + (int64_t)((h >> 32) & 0xffff) +
+                     (int64_t)(h >> 48) - 131070;
+  const double z = (double)ih * 7.0 / 262144.0;
+  const double phi = sigma * z;
+  double y = ((double)delta_ns / 1e9) * rate * (1.0 + phi);
+  if (!(y > 0.0)) y = 0.0;
+  return (int64_t)floor(y + 0.5);
+}
+
+int or_sine_arrivals(double ref, int64_t period_ns, int64_t delta_ns, double sigma, uint64_t seed, int64_t n0,
+                     int64_t N, int64_t* out) {
+  if (!(ref > 0) || period_ns <= 0 || delta_ns <= 0 || !(sigma >= 0) || n0 < 0 || N < 0) return OR_EINVAL;
+  int64_t s = 0; /* global index of the next request */
+  for (int64_t j = 0; s < n0 + N; ++j) {
+    const int64_t n = or_sine_count(ref, period_ns, delta_ns, sigma, seed, j);
+    for (int64_t i = 0; i < n; ++i, ++s)
+      if (s >= n0 && s < n0 + N) out[s - n0] = j * delta_ns + (i * delta_ns) / n;
+  }
+  return OR_OK;
 }
 
 /* ---- A5-A7: table ------------------------------------------------------------------------- */
@@ -468,5 +518,78 @@ int or_greedy_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, or_se
       }
       out[(int64_t)r * S + (v - 1)] = o;
     }
+  return OR_OK;
+}
+
+/* ---- NEXT-1: the asynchronous baseline, one model per batch (reading S2) ----------
+ * K servers (one per model) share one FIFO queue; no ensemble. Whenever some model is idle at time t, the
+ * lowest-index idle model m evaluates Algorithm 3's rule with its own c(m, b): len(q) >= max B -> infer
+ * the oldest max B on m; else b = max{b in B : b <= len(q)} and c(m,b) + w(q0) + delta >= tau -> infer the
+ * oldest b on m; a dispatched batch occupies m until t + c(m,b) and the loop re-evaluates at the same t
+ * (another idle model may take the next batch). Otherwise time advances to the next arrival, the instant
+ * the rule becomes true for m, or the instant a lower-index model becomes idle -- the only events that
+ * can change the decision; with every model busy, to the earliest completion. Requests still queued
+ * (fewer than min B) after the last arrival are unserved. reward = sum over batches of
+ * a(m) * (b - beta * overdue) (eq. multi_acc_reward with v = {m}). Output per rate r. */
+int or_async_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, const double* acc, or_serve* out,
+                   double* reward, uint64_t* model_batches) {
+  if (!cfg || K < 1 || K > 12 || N < 0 || cfg->nB < 1 || !cfg->B || !cfg->lat_ns || cfg->nR < 1) return OR_EINVAL;
+  if (!cfg->rates && !cfg->arrival_ns) return OR_EINVAL;
+  const int nB = cfg->nB;
+  int bmax = 0;
+  for (int bi = 0; bi < nB; ++bi) if (cfg->B[bi] > bmax) bmax = cfg->B[bi];
+  for (int r = 0; r < cfg->nR; ++r) {
+    or_serve o = {0, 0, 0, 0, 0};
+    double rew = 0.0;
+    int64_t free_at[12];
+    for (int m = 0; m < K; ++m) { free_at[m] = 0; if (model_batches) model_batches[(int64_t)r * K + m] = 0; }
+    int64_t t = 0, head = 0, tail = 0;
+    while (head < N) {
+      while (tail < N && arrival(cfg, r, tail) <= t) ++tail;
+      int m = -1;
+      for (int i = 0; i < K && m < 0; ++i) if (free_at[i] <= t) m = i;
+      if (m < 0) { /* every model busy: the next completion */
+        int64_t tn = free_at[0];
+        for (int i = 1; i < K; ++i) if (free_at[i] < tn) tn = free_at[i];
+        t = tn;
+        continue;
+      }
+      const int64_t qlen = tail - head;
+      int bsel = 0, bi_sel = -1;
+      for (int bi = 0; bi < nB; ++bi)
+        if (cfg->B[bi] <= qlen && cfg->B[bi] > bsel) { bsel = cfg->B[bi]; bi_sel = bi; }
+      const int64_t c = bi_sel >= 0 ? cfg->lat_ns[m * nB + bi_sel] : 0;
+      int b = 0;
+      if (qlen >= bmax) b = bmax;
+      else if (bsel > 0 && c + (t - arrival(cfg, r, head)) + delta_ns >= cfg->tau_ns) b = bsel;
+      if (b > 0) {
+        const int64_t done = t + c;
+        uint64_t od = 0;
+        for (int64_t s = head; s < head + b; ++s) {
+          const int64_t l = done - arrival(cfg, r, s);
+          o.served++;
+          if (l > cfg->tau_ns) { od++; o.exceed_ns += (uint64_t)(l - cfg->tau_ns); }
+        }
+        o.overdue += od;
+        o.batches++;
+        if (model_batches) model_batches[(int64_t)r * K + m]++;
+        if (acc) rew += acc[m] * ((double)b - cfg->beta * (double)od);
+        free_at[m] = done;
+        head += b;
+        continue; /* same t: the next idle model may dispatch too */
+      }
+      int64_t tn = INT64_MAX;
+      if (tail < N) tn = arrival(cfg, r, tail);
+      if (bsel > 0) {
+        const int64_t tthr = arrival(cfg, r, head) + cfg->tau_ns - delta_ns - c;
+        if (tthr < tn) tn = tthr;
+      }
+      for (int i = 0; i < m; ++i) if (free_at[i] > t && free_at[i] < tn) tn = free_at[i];
+      if (tn == INT64_MAX) { o.unserved = (uint64_t)qlen; break; }
+      t = tn;
+    }
+    out[r] = o;
+    if (reward) reward[r] = rew;
+  }
   return OR_OK;
 }

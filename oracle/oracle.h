@@ -94,6 +94,14 @@ int or_predict(const float* logits_f32, int ldc, const double* logits_f64, int64
 /* Arrival time of global request s at rate r (reading Q9): floor((double)s*1e9/r) ns. */
 int64_t or_arrival_ns(int64_t s, double rate);
 
+/* NEXT-4: sine-plus-noise arrivals (eqs. eq:r1/eq:r2, reading Q16):
+ * k, b of rate(t) = k sin(2 pi t / T) + b for ref = r_u or r_l; the request count of simulator invocation j;
+ * the arrival times of global requests [n0, n0 + N) (invocation j's n_j requests evenly spaced inside it). */
+void or_sine_params(double ref, double* k, double* b);
+int64_t or_sine_count(double ref, int64_t period_ns, int64_t delta_ns, double sigma, uint64_t seed, int64_t j);
+int or_sine_arrivals(double ref, int64_t period_ns, int64_t delta_ns, double sigma, uint64_t seed, int64_t n0,
+                     int64_t N, int64_t* out);
+
 /* NEXT-1: Algorithm 3, Inference(Queue q, Model m), greedy batching of one
  * synchronous ensemble v (c(v,b) = max over members of c(m,b)) on a request stream,
  * single server, inference blocks the loop (reading S1): whenever the server is idle at time t,
@@ -107,6 +115,13 @@ int64_t or_arrival_ns(int64_t s, double rate);
  * Output per (rate r, subset v): out[r*S + v-1]. */
 typedef struct { uint64_t served, overdue, exceed_ns, batches, unserved; } or_serve;
 int or_greedy_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, or_serve* out);
+
+/* NEXT-1 baseline: all models asynchronously, one model per batch (reading S2): K
+ * servers, one FIFO queue, Algorithm 3's rule evaluated by the lowest-index idle model with its own
+ * c(m, b). acc: [K] single-model accuracies a(m) or NULL; per rate r: out[r], reward[r] (sum over batches
+ * of a(m) * (b - beta * overdue)) and model_batches[r][K] (each may be NULL except out). */
+int or_async_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, const double* acc, or_serve* out,
+                   double* reward, uint64_t* model_batches);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <thread>
 #include <cstdio>
@@ -848,9 +849,9 @@ rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_
   return RK_OK;
 }
 
-rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
-                          rk_serve_out* out, void* stream) {
-  if (!ctx || !cfg || !out) return RK_EINVAL;
+// Validate a serving configuration and fill ServeParams (+ the [nR][N] arrival times on the device).
+static rk_status serve_setup(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, ServeParams& sp,
+                      cudaStream_t st) {
   if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
   if (N < 0) return fail(ctx, RK_EINVAL, "N >= 0");
   if (cfg->nB < 1 || cfg->nB > kMaxB || !cfg->B || !cfg->lat_ns) return fail(ctx, RK_EINVAL, "nB in [1,8] with B and lat_ns");
@@ -858,10 +859,9 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
     return fail(ctx, RK_EINVAL, "rates (nR in [1,8]) or arrival_ns with nR == 1");
   if (cfg->tau_ns < 0 || !(cfg->beta == cfg->beta)) return fail(ctx, RK_EINVAL, "tau >= 0, finite beta");
   CK(cudaSetDevice(ctx->dev));
-  cudaStream_t st = (cudaStream_t)stream;
-  const int K = ctx->K, S = ctx->S;
-  ServeParams sp{};
-  sp.K = K; sp.S = S; sp.nB = cfg->nB; sp.nR = cfg->nR; sp.N = N; sp.tau = cfg->tau_ns; sp.delta = delta_ns;
+  const int K = ctx->K;
+  sp = ServeParams{};
+  sp.K = K; sp.S = ctx->S; sp.nB = cfg->nB; sp.nR = cfg->nR; sp.N = N; sp.tau = cfg->tau_ns; sp.delta = delta_ns;
   sp.beta = cfg->beta;
   for (int bi = 0; bi < cfg->nB; ++bi) {
     if (cfg->B[bi] < 1) return fail(ctx, RK_EINVAL, "batch sizes >= 1");
@@ -876,7 +876,6 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
     if (!(sp.rates[r] > 0) || sp.rates[r] > 1e12) return fail(ctx, RK_EINVAL, "rates must be > 0");
   }
   rk_status s;
-  const int64_t n = (int64_t)sp.nR * S;
   if (cfg->arrival_ns && is_device_ptr(cfg->arrival_ns)) {
     sp.arrival = cfg->arrival_ns;
   } else {  // [nR][N] arrival times on the device: the caller's, or filled from the rates
@@ -885,6 +884,18 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
     else CK(launch_arrival_fill(sp, ctx->d_arr, st));
     sp.arrival = ctx->d_arr;
   }
+  return RK_OK;
+}
+
+rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
+                          rk_serve_out* out, void* stream) {
+  if (!ctx || !cfg || !out) return RK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  ServeParams sp;
+  rk_status s = serve_setup(ctx, cfg, N, delta_ns, sp, st);
+  if (s != RK_OK) return s;
+  const int S = ctx->S;
+  const int64_t n = (int64_t)sp.nR * S;
   // device scratch: 5 counter arrays + reward + acc
   const size_t words = 5 * (size_t)n + (size_t)n + (size_t)S;
   if ((s = ensure(ctx, &ctx->d_serve, &ctx->serve_cap, (int64_t)words)) != RK_OK) return s;
@@ -904,6 +915,152 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
   if (out->reward && acc) CK(cudaMemcpyAsync(out->reward, ctx->d_serve + 5 * n, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return RK_OK;
+}
+
+rk_status rk_async_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
+                         rk_serve_out* out, uint64_t* model_batches, void* stream) {
+  if (!ctx || !cfg || !out) return RK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  ServeParams sp;
+  rk_status s = serve_setup(ctx, cfg, N, delta_ns, sp, st);
+  if (s != RK_OK) return s;
+  const int K = ctx->K, nR = sp.nR;
+  // device scratch: 5 x [nR] counters, [nR] reward, [nR][K] batches per model, [K] accuracies
+  const size_t words = 6 * (size_t)nR + (size_t)nR * K + (size_t)K;
+  if ((s = ensure(ctx, &ctx->d_serve, &ctx->serve_cap, (int64_t)words)) != RK_OK) return s;
+  sp.out = reinterpret_cast<unsigned long long*>(ctx->d_serve);
+  sp.reward = reinterpret_cast<double*>(ctx->d_serve + 5 * nR);
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(ctx->d_serve + 6 * nR);
+  const double* dacc = nullptr;
+  if (acc) {
+    CK(cudaMemcpyAsync(ctx->d_serve + 6 * nR + nR * K, acc, (size_t)K * 8, cudaMemcpyHostToDevice, st));
+    dacc = reinterpret_cast<const double*>(ctx->d_serve + 6 * nR + nR * K);
+  }
+  {
+    ProfScope ps(ctx, KK_SERVE, st, 0, 0);
+    CK(launch_async_serve(sp, dacc, mb, st));
+  }
+  uint64_t* dst[5] = {out->served, out->overdue, out->exceed_ns, out->batches, out->unserved};
+  for (int k = 0; k < 5; ++k)
+    if (dst[k]) CK(cudaMemcpyAsync(dst[k], ctx->d_serve + k * nR, (size_t)nR * 8, cudaMemcpyDeviceToHost, st));
+  if (out->reward && acc) CK(cudaMemcpyAsync(out->reward, ctx->d_serve + 5 * nR, (size_t)nR * 8, cudaMemcpyDeviceToHost, st));
+  if (model_batches) CK(cudaMemcpyAsync(model_batches, mb, (size_t)nR * K * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RK_OK;
+}
+
+rk_status rk_serve_stream(rk_ctx* ctx, const void* X, int64_t N, const rk_reward_cfg* cfg, int64_t delta_ns,
+                          uint32_t v, int32_t* pred_vote, int32_t* pred_avg, rk_serve_out* out, int64_t* n_batches,
+                          void* stream) {
+  if (!ctx || !cfg) return RK_EINVAL;
+  if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
+  if (v == 0 || v >= (1u << ctx->K)) return fail(ctx, RK_EINVAL, "v must be in [1, 2^K) (PAPER.md:429 excludes v = 0)");
+  if (cfg->nR != 1) return fail(ctx, RK_EINVAL, "rk_serve_stream serves one arrival stream (nR == 1)");
+  if (N > 0 && (!X || !is_device_ptr(X))) return fail(ctx, RK_EINVAL, "X must be device memory");
+  if ((pred_vote && !is_device_ptr(pred_vote)) || (pred_avg && !is_device_ptr(pred_avg)))
+    return fail(ctx, RK_EINVAL, "predictions must be device memory");
+  if (N > INT32_MAX) return fail(ctx, RK_EINVAL, "N < 2^31");
+  cudaStream_t st = (cudaStream_t)stream;
+  ServeParams sp;
+  rk_status s = serve_setup(ctx, cfg, N, delta_ns, sp, st);
+  if (s != RK_OK) return s;
+  // 1. Algorithm 3 for this one action: counters + the batch schedule
+  const int64_t n = (int64_t)sp.nR * ctx->S;  // counters [5][n], this scenario at index 0
+  if ((s = ensure(ctx, &ctx->d_serve, &ctx->serve_cap, 5 * n)) != RK_OK) return s;
+  int64_t* d_sched = nullptr;
+  CK(cudaMallocAsync((void**)&d_sched, (size_t)std::max<int64_t>(N, 1) * 16, st));
+  sp.out = reinterpret_cast<unsigned long long*>(ctx->d_serve);
+  sp.v_only = v;
+  sp.sched = d_sched;
+  {
+    ProfScope ps(ctx, KK_SERVE, st, 0, 0);
+    CK(launch_greedy_serve(sp, st));
+  }
+  uint64_t cnt[5];
+  for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(&cnt[k], ctx->d_serve + k * n, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> sched(2 * cnt[3]);
+  if (cnt[3]) CK(cudaMemcpyAsync(sched.data(), d_sched, sched.size() * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFreeAsync(d_sched, st);
+  if (out) {
+    uint64_t* dst[5] = {out->served, out->overdue, out->exceed_ns, out->batches, out->unserved};
+    for (int k = 0; k < 5; ++k) if (dst[k]) *dst[k] = cnt[k];
+  }
+  if (n_batches) *n_batches = (int64_t)cnt[3];
+  // 2. serve every batch through the heads (A1+A2) and the per-request prediction of v
+  if (pred_vote && N) CK(cudaMemsetAsync(pred_vote, 0xff, N * 4, st));  // unserved requests: -1
+  if (pred_avg && N) CK(cudaMemsetAsync(pred_avg, 0xff, N * 4, st));
+  int64_t bmax = 0;
+  for (size_t i = 0; i < cnt[3]; ++i) bmax = std::max(bmax, sched[2 * i + 1]);
+  if ((s = ensure(ctx, &ctx->ws_logits, &ctx->ws_cap, std::max<int64_t>(bmax, 1) * ctx->K * ctx->ldc)) != RK_OK) return s;
+  if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, std::max<int64_t>(bmax, 1) * ctx->K)) != RK_OK) return s;
+  if ((s = ensure(ctx, &ctx->ws_lsum, &ctx->ws_lsum_cap, std::max<int64_t>(bmax, 1) * ctx->K)) != RK_OK) return s;
+  if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, std::max<int64_t>(bmax, 1) * ctx->K)) != RK_OK) return s;
+  for (size_t i = 0; i < cnt[3]; ++i) {
+    const int64_t h = sched[2 * i], b = sched[2 * i + 1];
+    GemmParams gp{};
+    gp.N = b; gp.K = ctx->K; gp.C = ctx->C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
+    gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias; gp.cluster = ctx->gemm_cluster;
+    gp.top1 = ctx->ws_top1; gp.lsum = ctx->ws_lsum; gp.rmax = ctx->ws_max; gp.logits = ctx->ws_logits;
+    int rc = gemm_build_tmaps(gp, static_cast<const uint16_t*>(X) + h * ctx->D, ctx->d_W, gp.logits, ctx->tmaps);
+    if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
+    {
+      ProfScope ps(ctx, KK_GEMM, st, (double)b * ctx->D * 2 + (double)b * ctx->K * ctx->C * 4,
+                   2.0 * b * ctx->D * (double)ctx->K * ctx->C);
+      CK(launch_gemm(gp, ctx->sm_count, st));
+    }
+    PredictParams pp{};
+    pp.logits = ctx->ws_logits; pp.ldc = ctx->ldc; pp.N = b; pp.K = ctx->K; pp.C = ctx->C; pp.tie = ctx->tie; pp.v = v;
+    pp.best_of = ctx->d_best_of;
+    pp.pred_vote = pred_vote ? pred_vote + h : nullptr;
+    pp.pred_avg = pred_avg ? pred_avg + h : nullptr;
+    ProfScope ps(ctx, KK_PREDICT, st, 0, 0);
+    CK(launch_predict(pp, st));
+  }
+  ctx->have_batch = false;  // the workspaces hold the last served batch only
+  CK(cudaStreamSynchronize(st));
+  return RK_OK;
+}
+
+rk_status rk_sine_arrivals(rk_ctx* ctx, const rk_sine_cfg* cfg, int64_t n0, int64_t N, int64_t* out, void* stream) {
+  if (!ctx || !cfg) return RK_EINVAL;
+  if (!(cfg->ref_rate > 0) || cfg->ref_rate > 1e12 || cfg->period_ns <= 0 || cfg->delta_ns <= 0 ||
+      !(cfg->noise_std >= 0) || cfg->noise_std > 1e3 || n0 < 0 || N < 0 || (N > 0 && !out))
+    return fail(ctx, RK_EINVAL, "sine arrivals: ref > 0, period > 0, delta > 0, noise_std >= 0, n0, N >= 0");
+  if (N > 0 && !is_device_ptr(out)) return fail(ctx, RK_EINVAL, "out_ns must be device memory");
+  if (N == 0) return RK_OK;
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  SineParams sp{};
+  const double s0 = (1.0 + std::sqrt(5.0)) / 4.0;  // sin(0.3 pi)
+  sp.k = 0.1 * cfg->ref_rate / (1.0 - s0);
+  sp.b = 1.1 * cfg->ref_rate - sp.k;
+  sp.period = cfg->period_ns; sp.delta = cfg->delta_ns; sp.delta_s = (double)cfg->delta_ns / 1e9;
+  sp.sigma = cfg->noise_std; sp.seed = cfg->seed;
+  // chunks of invocations: about twice the expected count at the mean rate b, at least 64k
+  const double per = std::max(1e-9, sp.delta_s * sp.b);
+  const int64_t J = std::min<int64_t>(int64_t(1) << 26, std::max<int64_t>(65536, (int64_t)(2.0 * (n0 + N) / per) + 1024));
+  const int64_t nb = sine_chunk_blocks(J);
+  int64_t *d_cnt = nullptr, *d_bs = nullptr;
+  CK(cudaMallocAsync((void**)&d_cnt, (size_t)J * 8, st));
+  CK(cudaMallocAsync((void**)&d_bs, (size_t)(nb + 1) * 8, st));
+  rk_status status = RK_OK;
+  int64_t base = 0, j0 = 0;
+  for (int iter = 0; base < n0 + N; ++iter, j0 += J) {
+    if (iter > 4096) { status = fail(ctx, RK_EINVAL, "sine arrivals: the rate is (almost) zero"); break; }
+    cudaError_t e = launch_sine_counts(sp, j0, J, d_cnt, d_bs, st);
+    int64_t tot = 0;
+    if (e == cudaSuccess) e = launch_sine_scatter(sp, j0, J, d_cnt, d_bs, base, n0, N, out, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&tot, d_bs + nb, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { status = fail(ctx, RK_ECUDA, std::string("sine arrivals: ") + cudaGetErrorString(e)); break; }
+    base += tot;
+  }
+  cudaFreeAsync(d_cnt, st);
+  cudaFreeAsync(d_bs, st);
+  if (status == RK_OK) CK(cudaStreamSynchronize(st));
+  return status;
 }
 
 rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64_t* groups, void* stream) {

@@ -202,9 +202,32 @@ struct ServeParams {
   const double* acc;               // [S] device a(v) or null
   unsigned long long* out;         // [5][nR][S]: served, overdue, exceed_ns, batches, unserved
   double* reward;                  // [nR][S] or null
+  uint32_t v_only;                 // != 0: one scenario (rate 0, subset v_only), results at index 0
+  int64_t* sched;                  // v_only: the dispatched batches as (first request, size) pairs, or null
 };
 cudaError_t launch_greedy_serve(const ServeParams& p, cudaStream_t st);
 cudaError_t launch_arrival_fill(const ServeParams& p, int64_t* out /*[nR][N]*/, cudaStream_t st);
+// the asynchronous one-model-per-batch baseline (reading S2): one thread per rate; out [5][nR],
+// reward [nR] (acc_single [K] device or null), model_batches [nR][K] or null
+cudaError_t launch_async_serve(const ServeParams& p, const double* acc_single, unsigned long long* model_batches,
+                               cudaStream_t st);
+
+// ---- NEXT-4: the sine-plus-noise arrival process (rk_arrivals.cu, reading Q16) ------
+struct SineParams {
+  double k, b;          // rate(t) = k sin(2 pi t / T) + b, req/s (eqs. eq:r1 / eq:r2)
+  int64_t period;       // T in ns
+  int64_t delta;        // simulator invocation interval in ns
+  double delta_s;       // delta in seconds (delta / 1e9, one rounding on the host)
+  double sigma;         // noise std: phi = sigma * z
+  uint64_t seed;
+};
+int64_t sine_chunk_blocks(int64_t J);
+// counts of invocations [j0, j0 + J) into cnt [J], exclusive block offsets into bsum [blocks + 1]
+// (bsum[blocks] = the chunk's total)
+cudaError_t launch_sine_counts(const SineParams& p, int64_t j0, int64_t J, int64_t* cnt, int64_t* bsum,
+                               cudaStream_t st);
+cudaError_t launch_sine_scatter(const SineParams& p, int64_t j0, int64_t J, const int64_t* cnt, const int64_t* bsum,
+                                int64_t base, int64_t n0, int64_t N, int64_t* out, cudaStream_t st);
 
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {

@@ -24,6 +24,7 @@ TIE_BEST_MEMBER, TIE_LOWEST_CLASS = 0, 1
 
 EXPORTS = ["rk_create", "rk_nccl_unique_id", "rk_load_ensemble", "rk_score", "rk_score_logits", "rk_subset_reset",
            "rk_subset_accumulate", "rk_subset_finalize", "rk_subset_stats", "rk_predict", "rk_greedy_serve", "rk_outputs",
+           "rk_sine_arrivals", "rk_async_serve", "rk_serve_stream",
            "rk_group_counts",
            "rk_set_profiling", "rk_kernel_stats", "rk_last_error", "rk_status_string", "rk_destroy"]
 
@@ -49,6 +50,11 @@ class _Table(ctypes.Structure):
 
 class _Serve(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("served", "overdue", "exceed_ns", "batches", "unserved", "reward")]
+
+
+class _Sine(ctypes.Structure):
+    _fields_ = [("ref_rate", ctypes.c_double), ("period_ns", ctypes.c_int64), ("delta_ns", ctypes.c_int64),
+                ("noise_std", ctypes.c_double), ("seed", ctypes.c_uint64)]
 
 
 class _KStat(ctypes.Structure):
@@ -78,6 +84,10 @@ def load_library(path: str | None = None):
     L.rk_outputs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i32), ctypes.POINTER(vp), ctypes.POINTER(vp),
                              ctypes.POINTER(vp), ctypes.POINTER(i64)]
     L.rk_group_counts.argtypes = [vp, vp, i64, ctypes.POINTER(i32), ctypes.POINTER(i64), vp]
+    L.rk_async_serve.argtypes = [vp, ctypes.POINTER(_Cfg), i64, i64, vp, ctypes.POINTER(_Serve), vp, vp]
+    L.rk_serve_stream.argtypes = [vp, vp, i64, ctypes.POINTER(_Cfg), i64, u32, vp, vp, ctypes.POINTER(_Serve),
+                                  ctypes.POINTER(i64), vp]
+    L.rk_sine_arrivals.argtypes = [vp, ctypes.POINTER(_Sine), i64, i64, vp, vp]
     L.rk_set_profiling.argtypes = [vp, i32]
     L.rk_kernel_stats.argtypes = [vp, ctypes.POINTER(_KStat), i32, ctypes.POINTER(i32)]
     for f in EXPORTS:
@@ -252,6 +262,41 @@ class Context:
         if a is None:
             del res["reward"]
         return res
+
+    def async_serve(self, cfg: RewardCfg, N: int, delta_ns: int, acc=None, stream=None) -> dict:
+        """NEXT-1 baseline: all models asynchronously, one model per batch (reading S2): arrays
+        [nR] of served, overdue, exceed_ns, batches, unserved, (with acc [K]) reward, and model_batches [nR][K]."""
+        c = self._cfg(cfg)
+        nR = c.nR
+        res = {k: np.zeros(nR, np.uint64) for k in ("served", "overdue", "exceed_ns", "batches", "unserved")}
+        res["reward"] = np.zeros(nR, np.float64)
+        res["model_batches"] = np.zeros((nR, self.K), np.uint64)
+        a = None if acc is None else np.ascontiguousarray(acc, dtype=np.float64)
+        o = _Serve(*[res[k].ctypes.data for k in ("served", "overdue", "exceed_ns", "batches", "unserved", "reward")])
+        self._chk(self._L.rk_async_serve(self._p, ctypes.byref(c), N, delta_ns, _ptr(a), ctypes.byref(o),
+                                         res["model_batches"].ctypes.data, _stream(stream)), "rk_async_serve")
+        if a is None:
+            del res["reward"]
+        return res
+
+    def serve_stream(self, X, N, cfg: RewardCfg, delta_ns, v, pred_vote=None, pred_avg=None, stream=None) -> dict:
+        """NEXT-1 serving loop: Algorithm 3 batches of action v, each run through the heads and the prediction
+        of v; per-request predictions into the device buffers (-1 = unserved). Returns the counters."""
+        c = self._cfg(cfg)
+        res = {k: np.zeros(1, np.uint64) for k in ("served", "overdue", "exceed_ns", "batches", "unserved")}
+        o = _Serve(*[res[k].ctypes.data for k in ("served", "overdue", "exceed_ns", "batches", "unserved")], None)
+        nb = ctypes.c_int64()
+        self._chk(self._L.rk_serve_stream(self._p, _ptr(X), N, ctypes.byref(c), delta_ns, v, _ptr(pred_vote),
+                                          _ptr(pred_avg), ctypes.byref(o), ctypes.byref(nb), _stream(stream)),
+                  "rk_serve_stream")
+        return {k: int(res[k][0]) for k in res}
+
+    def sine_arrivals(self, out, N, ref_rate, period_ns, delta_ns, noise_std=0.1, seed=0, n0=0, stream=None):
+        """NEXT-4: arrival times (int64 ns) of global requests [n0, n0 + N) of the sine-plus-noise process
+        (reading Q16) into the device buffer `out` [N]."""
+        c = _Sine(float(ref_rate), int(period_ns), int(delta_ns), float(noise_std), int(seed))
+        self._chk(self._L.rk_sine_arrivals(self._p, ctypes.byref(c), int(n0), int(N), _ptr(out), _stream(stream)),
+                  "rk_sine_arrivals")
 
     def outputs(self):
         lg, t1, mx, ls = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()

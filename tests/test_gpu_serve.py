@@ -103,3 +103,69 @@ def test_measured_latency_profile(rk):
     assert (lat[:, 1] * 3 >= lat[:, 0]).all()
     cfg = rk.RewardCfg(B=B, beta=1.0, tau_ns=560_000_000, lat_ns=lat, rates=[128.0])  # usable as the profile
     assert cfg.lat_ns.shape == (K, len(B))
+
+
+# ---- NEXT-1 baseline: asynchronous, one model per batch (reading S2) ----------------------
+@pytest.mark.parametrize("K,B,rates,N,delta", [
+    (3, [16, 32, 48, 64], [128.0, 572.0, 1144.0], 20_000, 0),          # the paper's trio, r_l / r_u
+    (3, [16, 32, 48, 64], [572.0], 20_000, 56_000_000),
+    (8, [16, 32, 64, 128, 256], [64.0, 572.0, 2000.0, 5000.0], 50_000, 10_000_000),
+])
+def test_async_parity(rk, K, B, rates, N, delta):
+    lat = lat_profile(K, B)
+    g = rk.RewardCfg(B=B, beta=1.0, tau_ns=560_000_000, lat_ns=lat, rates=rates)
+    o = oracle.RewardCfg(B=B, beta=1.0, tau_ns=560_000_000, lat_ns=lat, rates=rates)
+    acc = np.random.default_rng(K).uniform(0.6, 0.9, K)
+    r = ctx_for(rk, K).async_serve(g, N, delta, acc=acc)
+    ro = oracle.async_serve(o, K, N, delta, acc=acc)
+    for k in KEYS + ("model_batches", "reward"):
+        np.testing.assert_array_equal(r[k], ro[k], err_msg=k)
+
+
+def test_async_hand_worked(rk):
+    from test_oracle_async import gold
+    g = gold()
+    cfg = rk.RewardCfg(B=[2], beta=1.0, tau_ns=250, lat_ns=np.array([[100], [300]]),
+                       arrival_ns=np.array(g["A_arrivals"], np.int64))
+    r = ctx_for(rk, 2).async_serve(cfg, 6, 0, acc=[0.9, 0.6])
+    assert r["overdue"][0] == g["A_overdue"][0] and r["exceed_ns"][0] == g["A_exceed"][0]
+    assert r["model_batches"][0].tolist() == [int(x) for x in g["A_model_batches"]]
+    assert r["reward"][0] == g["A_reward"][0]
+
+
+# ---- NEXT-1 serving loop: Algorithm 3 batches of one action through the heads and rk_predict ----------
+@pytest.mark.parametrize("K,C,D,v,rate", [(3, 1000, 512, 0b111, 572.0), (3, 1000, 512, 0b100, 272.0),
+                                          (5, 100, 256, 0b10110, 2000.0)])
+def test_serve_stream(rk, K, C, D, v, rate):
+    import gen
+    N = 3000
+    B = [16, 32, 48, 64]
+    psig, f0, df, sh = gen.head_params(D, C, K)
+    y = gen.labels(31, 0, N, C)
+    X = gen.features(31, 0, N, D, C, psig, False, y=y)
+    W = gen.weights(32, K, C, D, f0, df, False)
+    b = gen.bias(33, K, C, False)
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C, D, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), sh)
+    lat = lat_profile(K, B)
+    cfg = rk.RewardCfg(B=B, beta=1.0, tau_ns=560_000_000, lat_ns=lat, rates=[rate])
+    Xd = torch.from_numpy(X).cuda()
+    pv = torch.zeros(N, dtype=torch.int32, device="cuda")
+    pa = torch.zeros(N, dtype=torch.int32, device="cuda")
+    st = ctx.serve_stream(Xd, N, cfg, 56_000_000, v, pv, pa)
+    # the policy's counters are those of rk_greedy_serve for (rate, v) ...
+    gs = ctx.greedy_serve(cfg, N, 56_000_000)
+    for k in KEYS:
+        assert st[k] == gs[k][0, v - 1], k
+    # ... and every served request carries the prediction of v on its own features (oracle heads + vote /
+    # average), unserved ones -1
+    ref = oracle.logits_gemm(X, W, b, sh)
+    ov, oa = oracle.predict(ref, K, C, v)[:2]
+    served = int(st["served"])
+    pv, pa = pv.cpu().numpy(), pa.cpu().numpy()
+    np.testing.assert_array_equal(pv[:served], ov[:served])
+    ap = np.sort(oracle.predict(ref, K, C, v, want_avgprob=True)[2], axis=1)
+    clear = (ap[:, -1] - ap[:, -2]) > 1e-5 * ap[:, -1]  # rk_predict averages in fp32 (P2: exact off near-ties)
+    m = clear[:served]
+    np.testing.assert_array_equal(pa[:served][m], oa[:served][m])
+    assert (pv[served:] == -1).all() and (pa[served:] == -1).all()
