@@ -198,6 +198,50 @@ rk_status rk_serve_stream(rk_ctx* ctx, const void* X_bf16, int64_t N, const rk_r
                           uint32_t v, int32_t* pred_vote, int32_t* pred_avg, rk_serve_out* out, int64_t* n_batches,
                           void* stream);
 
+/* NEXT-2: the actor-critic scheduler (§2.4 eqs. `eq:J`, `eq:dJ`, `eq:hatJ` with the
+ * baseline V(s_t); §5.2: state, action space (2^|M|-1)*|B|, reward eq. `multi_acc_reward`;
+ * reading S3). Environment: the loaded ensemble's K models as K servers, one FIFO request queue
+ * (arrival times `arrival` [Narr], device, non-decreasing -- e.g. rk_sine_arrivals), B / c(m,b) / tau /
+ * beta from cfg (rates ignored), a(v) = acc [S] (host; e.g. cnt_vote / N of rk_subset_stats: the
+ * surrogate accuracy). At decision time t the state (F = L + K*nB + K floats) is the waits
+ * (t - t_s)/tau of the oldest L queued requests (0-padded), c(m,b)/tau, and max(0, free_m - t)/tau; the
+ * action a = (v-1)*nB + b_index; the batch (next b requests) starts at max(t, its last arrival, free_m for
+ * m in v), runs c(v,b) = max_{m in v} c(m,b) on every member; R = a(v) (b - beta * overdue); the next
+ * decision is at max(start, min_m free_m). Policy pi = softmax(W2 tanh(W1 x + b1) + b2) over A = S*nB
+ * actions, value V = v2 . tanh(V1 x + c1) + c2; params: flat fp32 [W1 H*F | b1 H | W2 A*H | b2 A |
+ * V1 H*F | c1 H | v2 H | c2 1] (row-major), n_params = rk_ac_dims. Limits: H in [1,64], A <= 2048,
+ * F <= 1024, L in [0,256]. */
+typedef struct {
+  int L;                   /* queue waits in the state                                        */
+  int H;                   /* hidden units of both networks                                   */
+  int n_steps;             /* decisions per episode (n of eq. eq:J)                           */
+  double gamma;            /* discount                                                        */
+  double reward_scale;     /* returns are formed from R * reward_scale                        */
+} rk_ac_cfg;
+/* Trajectories of E episodes x n_steps, DEVICE buffers (caller-owned): states [E][n][F] fp32,
+ * actions [E][n] int32, rewards [E][n] fp64 (unscaled R), overdue / t_dec / t_start / t_done [E][n]
+ * (int32 / int64 ns; each may be NULL). */
+typedef struct {
+  float* states; int32_t* actions; double* rewards; int32_t* overdue; int64_t* t_dec; int64_t* t_start; int64_t* t_done;
+} rk_ac_traj;
+/* F, A and the parameter count for the loaded ensemble with nB batch sizes. */
+rk_status rk_ac_dims(rk_ctx* ctx, int nB, const rk_ac_cfg* ac, int* F, int* A, int64_t* n_params);
+/* Roll out E episodes in parallel (one warp each): episode e starts at request h0[e] (device [E]) with every
+ * model idle at its arrival. forced: [E][n] device actions, or NULL to sample from the policy with a
+ * counter-based uniform of (seed, e, step). RK_EINVAL if an episode would run past Narr. */
+rk_status rk_ac_rollout(rk_ctx* ctx, const rk_reward_cfg* cfg, const double* acc, const int64_t* arrival, int64_t Narr,
+                        const rk_ac_cfg* ac, const float* params, int E, const int64_t* h0, const int32_t* forced,
+                        uint64_t seed, rk_ac_traj* traj, void* stream);
+/* Actor-critic gradient of the trajectories (states, actions, rewards): G_t = sum_{k>=t} gamma^(k-t) R_k
+ * reward_scale, A_t = G_t - V(s_t); policy loss -(1/(E n)) sum_t A_t log pi(a_t|s_t) (A_t held fixed,
+ * eq. eq:hatJ), value loss (1/(E n)) sum_t (V(s_t) - G_t)^2. grad: device [n_params] (policy then value
+ * parts, the params layout); losses: host [2] (policy, value) or NULL. Deterministic (fixed-order sums). */
+rk_status rk_ac_grad(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, const float* params,
+                     const rk_ac_traj* traj, int E, float* grad, double* losses, void* stream);
+/* One SGD step: params -= lr_pi * grad on the policy part and lr_v * grad on the value part (device). */
+rk_status rk_ac_apply(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, float* params, const float* grad,
+                      float lr_pi, float lr_v, void* stream);
+
 /* NEXT-4: the paper's request-arrival process (§7.2, eqs. `eq:r1`/`eq:r2`; reading Q16):
  * rate(t) = k sin(2 pi t / T) + b with k = 0.1 ref / (1 - s0), b = 1.1 ref - k, s0 = sin(0.3 pi) =
  * (1 + sqrt 5)/4 (the rate exceeds ref for 20 % of each period T and peaks at 1.1 ref).

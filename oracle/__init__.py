@@ -331,3 +331,58 @@ def async_serve(cfg: RewardCfg, K: int, N: int, delta_ns: int, acc=None) -> dict
     if a is not None:
         res["reward"] = rew
     return res
+
+
+# ---- NEXT-2: RL environment and actor-critic gradients (reading S3) -------------------------------
+class _Env(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int), ("nB", ctypes.c_int), ("L", ctypes.c_int), ("B", ctypes.c_void_p),
+                ("lat_ns", ctypes.c_void_p), ("tau_ns", ctypes.c_int64), ("beta", ctypes.c_double),
+                ("acc", ctypes.c_void_p), ("arrival", ctypes.c_void_p), ("Narr", ctypes.c_int64)]
+
+
+def env_rollout(K: int, B, lat_ns, tau_ns: int, beta: float, acc, arrival, L: int, actions, h0: int) -> dict:
+    """One episode of the scheduler's environment under the given actions (reading S3):
+    states [n][F], rewards, overdue, t_dec, t_start, t_done."""
+    Bv = np.ascontiguousarray(B, dtype=np.int32)
+    lat = np.ascontiguousarray(lat_ns, dtype=np.int64).reshape(K, len(B))
+    a = np.ascontiguousarray(acc, dtype=np.float64)
+    arr = np.ascontiguousarray(arrival, dtype=np.int64)
+    act = np.ascontiguousarray(actions, dtype=np.int32)
+    n = act.size
+    F = L + K * len(B) + K
+    env = _Env(K, len(B), L, _p(Bv), _p(lat), int(tau_ns), float(beta), _p(a), _p(arr), arr.size)
+    out = {"states": np.zeros((n, F), np.float32), "rewards": np.zeros(n), "overdue": np.zeros(n, np.int32),
+           "t_dec": np.zeros(n, np.int64), "t_start": np.zeros(n, np.int64), "t_done": np.zeros(n, np.int64)}
+    L_ = lib()
+    L_.or_env_rollout.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6
+    rc = L_.or_env_rollout(ctypes.byref(env), _p(act), n, h0, *[_p(out[k]) for k in
+                                                                 ("states", "rewards", "overdue", "t_dec", "t_start",
+                                                                  "t_done")])
+    if rc != OK:
+        raise OracleError(rc)
+    return out
+
+
+def ac_param_count(F: int, H: int, A: int) -> int:
+    return H * F + H + A * H + A + H * F + H + H + 1
+
+
+def ac_grad(F: int, H: int, A: int, params, states, actions, rewards, gamma: float, scale: float):
+    """Actor-critic gradients in fp64 (PAPER.md:123-131 eqs. eq:dJ / eq:hatJ with the baseline V(s_t)):
+    (grad [flat], loss_pi, loss_v) for E episodes x n steps (states [E][n][F], actions/rewards [E][n])."""
+    P = np.ascontiguousarray(params, dtype=np.float64)
+    st = np.ascontiguousarray(states, dtype=np.float32)
+    act = np.ascontiguousarray(actions, dtype=np.int32)
+    rew = np.ascontiguousarray(rewards, dtype=np.float64)
+    E, n = act.shape
+    g = np.zeros(ac_param_count(F, H, A), np.float64)
+    lp, lv = ctypes.c_double(), ctypes.c_double()
+    L_ = lib()
+    L_.or_ac_grad.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                                          ctypes.c_double, ctypes.c_void_p,
+                                                                          ctypes.c_void_p, ctypes.c_void_p]
+    rc = L_.or_ac_grad(F, H, A, _p(P), _p(st), _p(act), _p(rew), E, n, gamma, scale, _p(g), ctypes.byref(lp),
+                       ctypes.byref(lv))
+    if rc != OK:
+        raise OracleError(rc)
+    return g, lp.value, lv.value

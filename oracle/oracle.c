@@ -593,3 +593,143 @@ int or_async_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, const 
   }
   return OR_OK;
 }
+
+/* ---- NEXT-2: RL environment and actor-critic gradients (reading S3) ------- */
+static void env_features(const or_env* e, int64_t t, int64_t head, const int64_t* free_at, float* x) {
+  const int L = e->L, K = e->K, nB = e->nB;
+  int64_t tail = head;
+  while (tail < e->Narr && e->arrival[tail] <= t) ++tail;
+  for (int i = 0; i < L; ++i)
+    x[i] = (head + i < tail) ? (float)((double)(t - e->arrival[head + i]) / (double)e->tau_ns) : 0.0f;
+  for (int m = 0; m < K; ++m)
+    for (int bi = 0; bi < nB; ++bi) x[L + m * nB + bi] = (float)((double)e->lat_ns[m * nB + bi] / (double)e->tau_ns);
+  for (int m = 0; m < K; ++m) {
+    const int64_t left = free_at[m] > t ? free_at[m] - t : 0;
+    x[L + K * nB + m] = (float)((double)left / (double)e->tau_ns);
+  }
+}
+
+int or_env_rollout(const or_env* e, const int32_t* actions, int n, int64_t h0, float* states, double* rewards,
+                   int32_t* overdue, int64_t* t_dec, int64_t* t_start, int64_t* t_done) {
+  if (!e || !actions || e->K < 1 || e->K > 12 || h0 < 0 || h0 >= e->Narr) return OR_EINVAL;
+  const int K = e->K, nB = e->nB, S = (1 << K) - 1, F = e->L + K * nB + K;
+  int64_t free_at[12];
+  int64_t t = e->arrival[h0], head = h0;
+  for (int m = 0; m < K; ++m) free_at[m] = t;
+  for (int st = 0; st < n; ++st) {
+    if (states) env_features(e, t, head, free_at, states + (int64_t)st * F);
+    const int a = actions[st];
+    if (a < 0 || a >= S * nB) return OR_EINVAL;
+    const uint32_t v = (uint32_t)(a / nB) + 1u;
+    const int bi = a % nB, b = e->B[bi];
+    if (head + b > e->Narr) return OR_EINVAL;
+    int64_t start = t, c = 0;
+    if (e->arrival[head + b - 1] > start) start = e->arrival[head + b - 1];
+    for (int m = 0; m < K; ++m)
+      if ((v >> m) & 1u) {
+        if (free_at[m] > start) start = free_at[m];
+        if (e->lat_ns[m * nB + bi] > c) c = e->lat_ns[m * nB + bi];
+      }
+    const int64_t done = start + c;
+    int32_t o = 0;
+    for (int64_t s = head; s < head + b; ++s) if (done - e->arrival[s] > e->tau_ns) ++o;
+    const double R = e->acc[v - 1] * ((double)b - e->beta * (double)o);
+    for (int m = 0; m < K; ++m) if ((v >> m) & 1u) free_at[m] = done;
+    if (rewards) rewards[st] = R;
+    if (overdue) overdue[st] = o;
+    if (t_dec) t_dec[st] = t;
+    if (t_start) t_start[st] = start;
+    if (t_done) t_done[st] = done;
+    head += b;
+    int64_t fmin = free_at[0];
+    for (int m = 1; m < K; ++m) if (free_at[m] < fmin) fmin = free_at[m];
+    t = fmin > start ? fmin : start;
+  }
+  return OR_OK;
+}
+
+int or_ac_grad(int F, int H, int A, const double* P, const float* states, const int32_t* actions,
+               const double* rewards, int E, int n, double gamma, double scale, double* grad, double* loss_pi,
+               double* loss_v) {
+  if (F < 1 || H < 1 || A < 1 || E < 1 || n < 1 || !P || !states || !actions || !rewards || !grad) return OR_EINVAL;
+  const double *W1 = P, *b1 = W1 + (int64_t)H * F, *W2 = b1 + H, *b2 = W2 + (int64_t)A * H;
+  const double *V1 = b2 + A, *c1 = V1 + (int64_t)H * F, *v2 = c1 + H, *c2 = v2 + H;
+  const int64_t np = (int64_t)H * F + H + (int64_t)A * H + A + (int64_t)H * F + H + H + 1;
+  double *gW1 = grad, *gb1 = gW1 + (int64_t)H * F, *gW2 = gb1 + H, *gb2 = gW2 + (int64_t)A * H;
+  double *gV1 = gb2 + A, *gc1 = gV1 + (int64_t)H * F, *gv2 = gc1 + H, *gc2 = gv2 + H;
+  for (int64_t i = 0; i < np; ++i) grad[i] = 0.0;
+  double* x = (double*)malloc(sizeof(double) * F);
+  double* h = (double*)malloc(sizeof(double) * H);
+  double* hv = (double*)malloc(sizeof(double) * H);
+  double* z = (double*)malloc(sizeof(double) * A);
+  double* G = (double*)malloc(sizeof(double) * n);
+  double* dh = (double*)malloc(sizeof(double) * H);
+  const double inv = 1.0 / ((double)E * (double)n);
+  double lp = 0.0, lv = 0.0;
+  for (int e = 0; e < E; ++e) {
+    /* discounted return from each step (eq. eq:J), rewards scaled */
+    double g = 0.0;
+    for (int t = n - 1; t >= 0; --t) { g = rewards[(int64_t)e * n + t] * scale + gamma * g; G[t] = g; }
+    for (int t = 0; t < n; ++t) {
+      const float* xs = states + ((int64_t)e * n + t) * F;
+      for (int f = 0; f < F; ++f) x[f] = (double)xs[f];
+      /* policy forward */
+      for (int j = 0; j < H; ++j) {
+        double a = b1[j];
+        for (int f = 0; f < F; ++f) a += W1[(int64_t)j * F + f] * x[f];
+        h[j] = tanh(a);
+      }
+      double zmax = -INFINITY;
+      for (int k = 0; k < A; ++k) {
+        double a = b2[k];
+        for (int j = 0; j < H; ++j) a += W2[(int64_t)k * H + j] * h[j];
+        z[k] = a;
+        if (a > zmax) zmax = a;
+      }
+      double zs = 0.0;
+      for (int k = 0; k < A; ++k) zs += exp(z[k] - zmax);
+      const double lse = zmax + log(zs);
+      /* value forward */
+      for (int j = 0; j < H; ++j) {
+        double a = c1[j];
+        for (int f = 0; f < F; ++f) a += V1[(int64_t)j * F + f] * x[f];
+        hv[j] = tanh(a);
+      }
+      double V = c2[0];
+      for (int j = 0; j < H; ++j) V += v2[j] * hv[j];
+      const double adv = G[t] - V;  /* actor-critic: R_t - V(s_t) with the return */
+      const int at = actions[(int64_t)e * n + t];
+      lp += -adv * (z[at] - lse) * inv;
+      lv += (V - G[t]) * (V - G[t]) * inv;
+      /* d(-A log pi(a|s))/dz_k = -A (1[k = a] - pi_k) */
+      for (int j = 0; j < H; ++j) dh[j] = 0.0;
+      for (int k = 0; k < A; ++k) {
+        const double pk = exp(z[k] - lse);
+        const double dz = -adv * ((k == at ? 1.0 : 0.0) - pk) * inv;
+        gb2[k] += dz;
+        for (int j = 0; j < H; ++j) {
+          gW2[(int64_t)k * H + j] += dz * h[j];
+          dh[j] += dz * W2[(int64_t)k * H + j];
+        }
+      }
+      for (int j = 0; j < H; ++j) {
+        const double dp = dh[j] * (1.0 - h[j] * h[j]);
+        gb1[j] += dp;
+        for (int f = 0; f < F; ++f) gW1[(int64_t)j * F + f] += dp * x[f];
+      }
+      /* d (V - G)^2 / dV = 2 (V - G) */
+      const double dV = 2.0 * (V - G[t]) * inv;
+      gc2[0] += dV;
+      for (int j = 0; j < H; ++j) {
+        gv2[j] += dV * hv[j];
+        const double dp = dV * v2[j] * (1.0 - hv[j] * hv[j]);
+        gc1[j] += dp;
+        for (int f = 0; f < F; ++f) gV1[(int64_t)j * F + f] += dp * x[f];
+      }
+    }
+  }
+  if (loss_pi) *loss_pi = lp;
+  if (loss_v) *loss_v = lv;
+  free(x); free(h); free(hv); free(z); free(G); free(dh);
+  return OR_OK;
+}

@@ -123,6 +123,40 @@ int or_greedy_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, or_se
 int or_async_serve(const or_cfg* cfg, int K, int64_t N, int64_t delta_ns, const double* acc, or_serve* out,
                    double* reward, uint64_t* model_batches);
 
+/* NEXT-2: the RL scheduler's environment and actor-critic estimator (§2.4 eqs. eq:J /
+ * eq:dJ / eq:hatJ and the baseline V(s_t); §5.2 state, action, reward; reading S3).
+ * Environment: K model servers, one FIFO request queue with the given arrival times. At decision time t
+ * the state is x = [waits of the oldest L queued requests (t - t_s)/tau, 0-padded | c(m,b)/tau for m, b |
+ * max(0, free_m - t)/tau for m], each (float)((double)ns / (double)tau). Action a = (v-1)*nB + b_index
+ * (SPEC.md:603-611). The batch is the next b requests; it starts at max(t, arrival of its last request,
+ * free_m for m in v), takes c(v,b) = max_{m in v} c(m,b), occupies every m in v until done; reward
+ * R = a(v) * (b - beta * #{s : done - t_s > tau}) (eq. multi_acc_reward); the next decision is at
+ * max(start, min_m free_m). */
+typedef struct {
+  int K, nB, L;
+  const int* B;            /* [nB] */
+  const int64_t* lat_ns;   /* [K][nB] */
+  int64_t tau_ns;
+  double beta;
+  const double* acc;       /* [S] a(v) */
+  const int64_t* arrival;  /* [Narr] non-decreasing */
+  int64_t Narr;
+} or_env;
+/* One episode of n decisions from request h0 (all models idle at t = arrival[h0]) under the given actions.
+ * states [n][F] (F = L + K*nB + K), rewards [n], overdue [n], t_dec / t_start / t_done [n] (each may be NULL
+ * except actions). Returns OR_EINVAL if a batch would run past Narr. */
+int or_env_rollout(const or_env* env, const int32_t* actions, int n, int64_t h0, float* states, double* rewards,
+                   int32_t* overdue, int64_t* t_dec, int64_t* t_start, int64_t* t_done);
+/* Actor-critic gradients (fp64) for E episodes of n steps: G_t = sum_{k>=t} gamma^(k-t) R_k * scale,
+ * A_t = G_t - V(s_t); policy loss -(1/(E n)) sum A_t log pi(a_t|s_t) (A_t constant), value loss
+ * (1/(E n)) sum (V(s_t) - G_t)^2. Networks: pi = softmax(W2 tanh(W1 x + b1) + b2) over A actions,
+ * V = v2 . tanh(V1 x + c1) + c2, hidden H. params / grad: the flat layout
+ * [W1 H*F | b1 H | W2 A*H | b2 A | V1 H*F | c1 H | v2 H | c2 1] (row-major). Also returns the mean
+ * unscaled episode return sum_t R_t and the two losses (each pointer may be NULL). */
+int or_ac_grad(int F, int H, int A, const double* params, const float* states, const int32_t* actions,
+               const double* rewards, int E, int n, double gamma, double scale, double* grad, double* loss_pi,
+               double* loss_v);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1063,6 +1063,122 @@ rk_status rk_sine_arrivals(rk_ctx* ctx, const rk_sine_cfg* cfg, int64_t n0, int6
   return status;
 }
 
+// ---- NEXT-2: actor-critic scheduler ---------------------------------------------------------------------
+static rk_status ac_setup(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, RLParams& rp) {
+  if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
+  if (!cfg || !ac) return fail(ctx, RK_EINVAL, "cfg and ac required");
+  if (cfg->nB < 1 || cfg->nB > kMaxB || !cfg->B || !cfg->lat_ns) return fail(ctx, RK_EINVAL, "nB in [1,8] with B and lat_ns");
+  if (cfg->tau_ns <= 0 || !(cfg->beta == cfg->beta)) return fail(ctx, RK_EINVAL, "tau > 0, finite beta");
+  if (ac->L < 0 || ac->L > 256 || ac->H < 1 || ac->H > kRlMaxH || ac->n_steps < 1 ||
+      !(ac->gamma >= 0 && ac->gamma <= 1) || !(ac->reward_scale == ac->reward_scale))
+    return fail(ctx, RK_EINVAL, "ac: L in [0,256], H in [1,64], n_steps >= 1, gamma in [0,1]");
+  rp = RLParams{};
+  rp.K = ctx->K; rp.nB = cfg->nB; rp.L = ac->L; rp.H = ac->H; rp.n = ac->n_steps;
+  rp.F = ac->L + ctx->K * cfg->nB + ctx->K;
+  rp.A = ctx->S * cfg->nB;
+  if (rp.A > kRlMaxA || rp.F > 1024) return fail(ctx, RK_EINVAL, "ac: (2^K - 1) * nB <= 2048 actions, F <= 1024");
+  for (int bi = 0; bi < cfg->nB; ++bi) {
+    if (cfg->B[bi] < 1) return fail(ctx, RK_EINVAL, "batch sizes >= 1");
+    rp.B[bi] = cfg->B[bi];
+    for (int m = 0; m < ctx->K; ++m) {
+      if (cfg->lat_ns[m * cfg->nB + bi] < 0) return fail(ctx, RK_EINVAL, "latencies must be >= 0");
+      rp.lat[m * cfg->nB + bi] = cfg->lat_ns[m * cfg->nB + bi];
+    }
+  }
+  rp.tau = cfg->tau_ns; rp.beta = cfg->beta; rp.gamma = ac->gamma; rp.scale = ac->reward_scale;
+  return RK_OK;
+}
+
+rk_status rk_ac_dims(rk_ctx* ctx, int nB, const rk_ac_cfg* ac, int* F, int* A, int64_t* n_params) {
+  if (!ctx || !ac) return RK_EINVAL;
+  if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
+  if (nB < 1 || nB > kMaxB || ac->L < 0 || ac->H < 1) return fail(ctx, RK_EINVAL, "nB in [1,8], L >= 0, H >= 1");
+  const int f = ac->L + ctx->K * nB + ctx->K, a = ctx->S * nB;
+  if (F) *F = f;
+  if (A) *A = a;
+  if (n_params) *n_params = ac_param_count(f, ac->H, a);
+  return RK_OK;
+}
+
+rk_status rk_ac_rollout(rk_ctx* ctx, const rk_reward_cfg* cfg, const double* acc, const int64_t* arrival, int64_t Narr,
+                        const rk_ac_cfg* ac, const float* params, int E, const int64_t* h0, const int32_t* forced,
+                        uint64_t seed, rk_ac_traj* traj, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  RLParams rp;
+  rk_status s = ac_setup(ctx, cfg, ac, rp);
+  if (s != RK_OK) return s;
+  if (!acc || !traj || !traj->actions || !traj->rewards || E < 1 || Narr < 1)
+    return fail(ctx, RK_EINVAL, "acc, traj.actions, traj.rewards, E >= 1, Narr >= 1 required");
+  if (!is_device_ptr(arrival) || !is_device_ptr(h0) || (!forced && !is_device_ptr(params)) ||
+      (forced && !is_device_ptr(forced)) || !is_device_ptr(traj->actions) || !is_device_ptr(traj->rewards))
+    return fail(ctx, RK_EINVAL, "arrival, h0, params, forced and trajectory buffers must be device memory");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  // a(v) and the error flag in the serving scratch: [S] doubles + 1 word
+  if ((s = ensure(ctx, &ctx->d_serve, &ctx->serve_cap, (int64_t)ctx->S + 1)) != RK_OK) return s;
+  CK(cudaMemcpyAsync(ctx->d_serve, acc, (size_t)ctx->S * 8, cudaMemcpyHostToDevice, st));
+  unsigned int* err = reinterpret_cast<unsigned int*>(ctx->d_serve + ctx->S);
+  CK(cudaMemsetAsync(err, 0, 8, st));
+  rp.acc = reinterpret_cast<const double*>(ctx->d_serve);
+  rp.arrival = arrival; rp.Narr = Narr; rp.params = params; rp.h0 = h0; rp.forced = forced; rp.seed = seed;
+  rp.E = E; rp.err = err;
+  rp.states = traj->states; rp.actions = traj->actions; rp.rewards = traj->rewards; rp.overdue = traj->overdue;
+  rp.t_dec = traj->t_dec; rp.t_start = traj->t_start; rp.t_done = traj->t_done;
+  {
+    ProfScope ps(ctx, KK_SERVE, st, 0, 0);
+    CK(launch_ac_rollout(rp, st));
+  }
+  unsigned int herr = 0;
+  CK(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (herr & 2u) return fail(ctx, RK_EINVAL, "a forced action is outside [0, (2^K - 1) * nB)");
+  if (herr & 1u) return fail(ctx, RK_EINVAL, "an episode ran past the end of the arrival array (Narr)");
+  return RK_OK;
+}
+
+rk_status rk_ac_grad(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, const float* params,
+                     const rk_ac_traj* traj, int E, float* grad, double* losses, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  RLParams rp;
+  rk_status s = ac_setup(ctx, cfg, ac, rp);
+  if (s != RK_OK) return s;
+  if (!traj || !traj->states || !traj->actions || !traj->rewards || !grad || !params || E < 1)
+    return fail(ctx, RK_EINVAL, "traj (states, actions, rewards), params, grad, E >= 1 required");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  rp.E = E; rp.params = params;
+  rp.states = traj->states; rp.actions = traj->actions; rp.rewards = traj->rewards;
+  void* scratch = nullptr;
+  float* dl = nullptr;
+  CK(cudaMallocAsync(&scratch, ac_grad_scratch_bytes(rp), st));
+  CK(cudaMallocAsync((void**)&dl, 8, st));
+  cudaError_t e = launch_ac_grad(rp, grad, dl, scratch, st);
+  float hl[2] = {0.f, 0.f};
+  if (e == cudaSuccess && losses) e = cudaMemcpyAsync(hl, dl, 8, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(scratch, st);
+  cudaFreeAsync(dl, st);
+  if (e != cudaSuccess) return fail(ctx, RK_ECUDA, std::string("ac grad: ") + cudaGetErrorString(e));
+  if (losses) {
+    CK(cudaStreamSynchronize(st));
+    losses[0] = hl[0];
+    losses[1] = hl[1];
+  }
+  return RK_OK;
+}
+
+rk_status rk_ac_apply(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, float* params, const float* grad,
+                      float lr_pi, float lr_v, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  RLParams rp;
+  rk_status s = ac_setup(ctx, cfg, ac, rp);
+  if (s != RK_OK) return s;
+  if (!params || !grad) return fail(ctx, RK_EINVAL, "params and grad required");
+  CK(cudaSetDevice(ctx->dev));
+  const int64_t npol = (int64_t)rp.H * rp.F + rp.H + (int64_t)rp.A * rp.H + rp.A;
+  CK(launch_ac_apply(params, grad, npol, ac_param_count(rp.F, rp.H, rp.A), lr_pi, lr_v, (cudaStream_t)stream));
+  return RK_OK;
+}
+
 rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64_t* groups, void* stream) {
   if (!ctx) return RK_EINVAL;
   if (!ctx->reset_done || ctx->chunks == 0) return fail(ctx, RK_ESTATE, "no chunk accumulated since rk_subset_reset");

@@ -229,6 +229,38 @@ cudaError_t launch_sine_counts(const SineParams& p, int64_t j0, int64_t J, int64
 cudaError_t launch_sine_scatter(const SineParams& p, int64_t j0, int64_t J, const int64_t* cnt, const int64_t* bsum,
                                 int64_t base, int64_t n0, int64_t N, int64_t* out, cudaStream_t st);
 
+// ---- NEXT-2: actor-critic scheduler (rk_rl.cu, reading S3) ----------------
+constexpr int kRlMaxH = 64;     // hidden units (register tiles of the gradient kernel)
+constexpr int kRlMaxA = 2048;   // actions (2^K - 1) * nB held per warp in shared memory
+struct RLParams {
+  int K, nB, L, F, H, A, E, n;
+  int B[kMaxB];
+  int64_t lat[kMaxK * kMaxB];    // [K][nB] ns
+  int64_t tau;
+  double beta;
+  const double* acc;             // [S] a(v), device
+  const int64_t* arrival;        // [Narr] device, non-decreasing
+  int64_t Narr;
+  const float* params;           // flat [W1 | b1 | W2 | b2 | V1 | c1 | v2 | c2]
+  const int64_t* h0;             // [E] first request of each episode
+  const int32_t* forced;         // [E][n] actions or null (sample from the policy)
+  uint64_t seed;
+  float* states;                 // [E][n][F]
+  int32_t* actions;              // [E][n]
+  double* rewards;               // [E][n]
+  int32_t* overdue;              // [E][n] or null
+  int64_t *t_dec, *t_start, *t_done;  // [E][n] or null
+  unsigned int* err;
+  double gamma, scale;
+};
+int64_t ac_param_count(int F, int H, int A);
+cudaError_t launch_ac_rollout(const RLParams& p, cudaStream_t st);
+size_t ac_grad_scratch_bytes(const RLParams& p);
+cudaError_t launch_ac_grad(const RLParams& p, float* grad, float* loss2 /*device [2] or null*/, void* scratch,
+                           cudaStream_t st);
+cudaError_t launch_ac_apply(float* P, const float* g, int64_t npol, int64_t np, float lr_pi, float lr_v,
+                            cudaStream_t st);
+
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {
   const void* tmap_x;    // CUtensorMap* (host copy passed by value via __grid_constant__)

@@ -24,7 +24,8 @@ TIE_BEST_MEMBER, TIE_LOWEST_CLASS = 0, 1
 
 EXPORTS = ["rk_create", "rk_nccl_unique_id", "rk_load_ensemble", "rk_score", "rk_score_logits", "rk_subset_reset",
            "rk_subset_accumulate", "rk_subset_finalize", "rk_subset_stats", "rk_predict", "rk_greedy_serve", "rk_outputs",
-           "rk_sine_arrivals", "rk_async_serve", "rk_serve_stream",
+           "rk_sine_arrivals", "rk_async_serve", "rk_serve_stream", "rk_ac_dims", "rk_ac_rollout", "rk_ac_grad",
+           "rk_ac_apply",
            "rk_group_counts",
            "rk_set_profiling", "rk_kernel_stats", "rk_last_error", "rk_status_string", "rk_destroy"]
 
@@ -57,6 +58,15 @@ class _Sine(ctypes.Structure):
                 ("noise_std", ctypes.c_double), ("seed", ctypes.c_uint64)]
 
 
+class _AcCfg(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_int), ("H", ctypes.c_int), ("n_steps", ctypes.c_int), ("gamma", ctypes.c_double),
+                ("reward_scale", ctypes.c_double)]
+
+
+class _Traj(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("states", "actions", "rewards", "overdue", "t_dec", "t_start", "t_done")]
+
+
 class _KStat(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char_p), ("launches", ctypes.c_int64), ("total_ms", ctypes.c_double),
                 ("bytes", ctypes.c_double), ("flops", ctypes.c_double)]
@@ -87,6 +97,13 @@ def load_library(path: str | None = None):
     L.rk_async_serve.argtypes = [vp, ctypes.POINTER(_Cfg), i64, i64, vp, ctypes.POINTER(_Serve), vp, vp]
     L.rk_serve_stream.argtypes = [vp, vp, i64, ctypes.POINTER(_Cfg), i64, u32, vp, vp, ctypes.POINTER(_Serve),
                                   ctypes.POINTER(i64), vp]
+    L.rk_ac_dims.argtypes = [vp, i32, ctypes.POINTER(_AcCfg), ctypes.POINTER(i32), ctypes.POINTER(i32),
+                             ctypes.POINTER(i64)]
+    L.rk_ac_rollout.argtypes = [vp, ctypes.POINTER(_Cfg), vp, vp, i64, ctypes.POINTER(_AcCfg), vp, i32, vp, vp,
+                                ctypes.c_uint64, ctypes.POINTER(_Traj), vp]
+    L.rk_ac_grad.argtypes = [vp, ctypes.POINTER(_Cfg), ctypes.POINTER(_AcCfg), vp, ctypes.POINTER(_Traj), i32, vp, vp, vp]
+    L.rk_ac_apply.argtypes = [vp, ctypes.POINTER(_Cfg), ctypes.POINTER(_AcCfg), vp, vp, ctypes.c_float,
+                              ctypes.c_float, vp]
     L.rk_sine_arrivals.argtypes = [vp, ctypes.POINTER(_Sine), i64, i64, vp, vp]
     L.rk_set_profiling.argtypes = [vp, i32]
     L.rk_kernel_stats.argtypes = [vp, ctypes.POINTER(_KStat), i32, ctypes.POINTER(i32)]
@@ -290,6 +307,45 @@ class Context:
                                           _ptr(pred_avg), ctypes.byref(o), ctypes.byref(nb), _stream(stream)),
                   "rk_serve_stream")
         return {k: int(res[k][0]) for k in res}
+
+    # -- NEXT-2: actor-critic scheduler (argument marshalling; the loop lives in scheduler.py) --
+    @staticmethod
+    def _ac(ac):
+        return _AcCfg(int(ac["L"]), int(ac["H"]), int(ac["n_steps"]), float(ac["gamma"]), float(ac["reward_scale"]))
+
+    def ac_dims(self, nB, ac):
+        F, A, P = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        self._chk(self._L.rk_ac_dims(self._p, nB, ctypes.byref(self._ac(ac)), ctypes.byref(F), ctypes.byref(A),
+                                     ctypes.byref(P)), "rk_ac_dims")
+        return F.value, A.value, P.value
+
+    @staticmethod
+    def _traj(tr):
+        return _Traj(*[_ptr(tr.get(k)) for k in ("states", "actions", "rewards", "overdue", "t_dec", "t_start",
+                                                  "t_done")])
+
+    def ac_rollout(self, cfg: RewardCfg, acc, arrival, Narr, ac, params, E, h0, traj: dict, forced=None, seed=0,
+                   stream=None):
+        c = self._cfg(cfg)
+        a = np.ascontiguousarray(acc, dtype=np.float64)
+        t = self._traj(traj)
+        self._chk(self._L.rk_ac_rollout(self._p, ctypes.byref(c), _ptr(a), _ptr(arrival), int(Narr),
+                                        ctypes.byref(self._ac(ac)), _ptr(params), int(E), _ptr(h0), _ptr(forced),
+                                        int(seed), ctypes.byref(t), _stream(stream)), "rk_ac_rollout")
+
+    def ac_grad(self, cfg: RewardCfg, ac, params, traj: dict, E, grad, stream=None):
+        c = self._cfg(cfg)
+        t = self._traj(traj)
+        losses = np.zeros(2, np.float64)
+        self._chk(self._L.rk_ac_grad(self._p, ctypes.byref(c), ctypes.byref(self._ac(ac)), _ptr(params),
+                                     ctypes.byref(t), int(E), _ptr(grad), losses.ctypes.data, _stream(stream)),
+                  "rk_ac_grad")
+        return losses
+
+    def ac_apply(self, cfg: RewardCfg, ac, params, grad, lr_pi, lr_v, stream=None):
+        c = self._cfg(cfg)
+        self._chk(self._L.rk_ac_apply(self._p, ctypes.byref(c), ctypes.byref(self._ac(ac)), _ptr(params), _ptr(grad),
+                                      float(lr_pi), float(lr_v), _stream(stream)), "rk_ac_apply")
 
     def sine_arrivals(self, out, N, ref_rate, period_ns, delta_ns, noise_std=0.1, seed=0, n0=0, stream=None):
         """NEXT-4: arrival times (int64 ns) of global requests [n0, n0 + N) of the sine-plus-noise process
