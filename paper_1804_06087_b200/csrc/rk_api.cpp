@@ -1131,6 +1131,7 @@ rk_status rk_ac_rollout(rk_ctx* ctx, const rk_reward_cfg* cfg, const double* acc
   unsigned int herr = 0;
   CK(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (herr & 4u) return fail(ctx, RK_ENONFINITE, "the policy's probabilities are not finite (diverged parameters)");
   if (herr & 2u) return fail(ctx, RK_EINVAL, "a forced action is outside [0, (2^K - 1) * nB)");
   if (herr & 1u) return fail(ctx, RK_EINVAL, "an episode ran past the end of the arrival array (Narr)");
   return RK_OK;

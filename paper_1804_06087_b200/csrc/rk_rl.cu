@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(32 * RW) ac_rollout_kernel(const RLParams p) {
         if (lane >= o) incl += y;
       }
       const float total = __shfl_sync(FULL, incl, 31);
+      if (!(total > 0.f) || isinf(total)) {  // non-finite parameters (a diverged update)
+        if (lane == 0) atomicOr(p.err, 4u);
+        return;
+      }
       const uint64_t hr = rl_mix(rl_mix(rl_mix(p.seed ^ 0xAC7013ull) ^ (uint64_t)e) + (uint64_t)st);
       const float target = (float)((double)(hr >> 11) * 0x1.0p-53) * total;
       // the first action whose cumulative mass exceeds the target (the last positive one if rounding

@@ -42,11 +42,11 @@ def subset_accuracy(ctx, K, C, D, N):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--iters", type=int, default=150)
+    ap.add_argument("--iters", type=int, default=300)
     ap.add_argument("--episodes", type=int, default=512)
     ap.add_argument("--steps", type=int, default=32)
-    ap.add_argument("--lr-pi", type=float, default=0.5)
-    ap.add_argument("--lr-v", type=float, default=0.2)
+    ap.add_argument("--lr-pi", type=float, default=1.0)
+    ap.add_argument("--lr-v", type=float, default=0.02)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_scheduler.json"))
     a = ap.parse_args()
     K, C, D, B = 3, 1000, 2048, [16, 32, 48, 64]

@@ -143,7 +143,7 @@ def test_training_improves_return(rk):
     K, B = 3, [16, 32, 48, 64]
     ctx, arr, cfg, acc, ac = make(rk, K, B, N=400_000)
     agent = ActorCritic(ctx, cfg, acc, arr, L=16, H=32, n_steps=24, seed=0)
-    curve = agent.train(30, E=256, lr_pi=0.5, lr_v=0.2)
+    curve = agent.train(30, E=256, lr_pi=1.0, lr_v=0.02)
     first = curve[0]["return"]
     last = np.mean([c["return"] for c in curve[-5:]])
     assert last > first, (first, last)
