@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--impl", default="rk", choices=["rk", "reference"])
     ap.add_argument("--tie", default="best_member", choices=["best_member", "lowest_class"])
     ap.add_argument("--queue", action="store_true", help="queue-aware latency (reading Q15, PAPER.md:410)")
+    ap.add_argument("--unfused", action="store_true",
+                    help="rk_score + logits-based vote stage instead of the fused forward + vote (NEXT-3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -243,8 +245,16 @@ def main():
                         want_labelled=True, queue=args.queue)
     torch.cuda.synchronize()
 
+    fused = not args.unfused
+
+    def score(Xb, yb):
+        if fused:
+            ctx.score_labelled(Xb, yb, n, off, stream)  # NEXT-3: no logits stored for K <= 8, C > 128
+        else:
+            ctx.score(Xb, n, off, stream)
+
     def step():
-        ctx.score(X, n, off, stream)
+        score(X, labels)
         return ctx.subset_stats(labels, rcfg, stream)
 
     for _ in range(max(3, args.warmup)):
@@ -266,6 +276,7 @@ def main():
         dist.barrier()
     ms = e0.elapsed_time(e1)
     ks = ctx.kernel_stats()
+    diag = ctx.vote_diag() if K <= 8 else (0, 0)
     ctx.set_profiling(False)
     clk = clocks.stop()
     if dist:
@@ -281,14 +292,14 @@ def main():
     Xh.copy_(X)
     yh.copy_(labels)
     Xh_np, yh_np = Xh.numpy(), yh.numpy()
-    ctx.score(Xh_np, n, off, stream)
+    score(Xh_np, yh_np)
     ctx.subset_stats(yh_np, rcfg, stream)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        ctx.score(Xh_np, n, off, stream)
+        score(Xh_np, yh_np)
         ctx.subset_stats(yh_np, rcfg, stream)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
@@ -325,7 +336,8 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfgname, "K": K, "C": C, "N": Ntot, "D": D, "B": cfg["B"], "rates": cfg["rates"],
-                   "tie": args.tie, "queue": bool(args.queue), "subsets": S, "parallelism": f"samples sharded over {world} GPU(s)",
+                   "tie": args.tie, "queue": bool(args.queue), "subsets": S,
+                   "fused_forward_vote": bool(fused and K <= 8 and C > 128), "parallelism": f"samples sharded over {world} GPU(s)",
                    "l2": "inputs larger than L2 (X %.1f GB, logits %.1f GB)" % (Ntot * D * 2 / 1e9, Ntot * K * C * 4 / 1e9)},
         "roofline": {"bound": "tensor", "kernel": "gemm_heads_tcgen05", "achieved": gemm_tfs,
                      "peak": peak_t, "unit": "TFLOP/s", "frac": gemm_tfs / peak_t, "traffic": traffic,
@@ -345,6 +357,10 @@ def main():
         "rank0_check": {"N": int(t["N"]), "a_full_set": float(t["cnt_vote"][-1]) / max(1, int(t["N"])),
                         "a_best_single": float(t["cnt_vote"][0]) / max(1, int(t["N"]))},
     }
+    if K <= 8:
+        wl, fb = diag
+        line["vote_stage"]["worklist_frac"] = wl / max(1, n)
+        line["vote_stage"]["fallback_frac"] = fb / max(1, n)
     if vote_ms > gemm_ms:  # the vote stage dominates (K >= 9): an ALU-bound roofline kernel
         # algorithmic ops: one per (sample, subset, member) for the vote count and one for the
         # probability sum = 2 * sum_v |v| = K * 2^K per sample; peak: 148 SMs x 128 int32/fp32 lanes

@@ -86,6 +86,18 @@ rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16,
  * (larger streams go in chunks; RK_EINVAL otherwise). */
 rk_status rk_score(rk_ctx* ctx, const void* X_bf16, int64_t N, int64_t global_offset, void* stream);
 
+/* NEXT-3, fused forward + vote: A1+A2 with the labels known at scoring time. Same X / N / offset contract
+ * as rk_score; labels: [N] int32 host or device, the values rk_subset_accumulate would receive (it must then
+ * be called with the same pointer or NULL). For K <= 8 and more than 128 classes (the GEMM's per-model
+ * column tiles), the epilogue does NOT store the fp32 logits: per (row, model) it keeps the row statistics,
+ * the label's logit and the 16 largest logits with their classes, from which the vote stage decides every
+ * subset's average exactly where the bounds allow; the remaining samples' rows are recomputed with logits
+ * (inside rk_subset_accumulate) and averaged by the logits path, so the table is identical to
+ * rk_score + rk_subset_accumulate. Other shapes run exactly that path. rk_predict after this call is
+ * RK_ESTATE, and rk_outputs returns no logits. Device X must stay valid until rk_subset_accumulate. */
+rk_status rk_score_labelled(rk_ctx* ctx, const void* X_bf16, const int32_t* labels, int64_t N, int64_t global_offset,
+                            void* stream);
+
 /* Vote-stage entry on caller-provided logits: [N][K][ldc] fp32 DEVICE memory, ldc % 4 == 0,
  * ldc >= C, 16-byte aligned. The pointer is borrowed until the next rk_score* call. */
 rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, int64_t global_offset,
@@ -285,6 +297,12 @@ rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t*
  * (otherwise *gs = *groups = 0). out: host or device, cap >= groups * S bytes, may be NULL to query
  * the sizes. Blocks on `stream`. RK_ESTATE before the first accumulate after a reset. */
 rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64_t* groups, void* stream);
+
+/* Diagnostics of the LAST rk_subset_accumulate chunk (K <= 8 path): *worklist = samples whose label is an
+ * averaging candidate of some subset and that are not unanimous (the samples the averaging kernels visit),
+ * *fallback = of those, the samples a fused batch (rk_score_labelled) recomputed with logits (0 otherwise).
+ * Synchronises the device. Either pointer may be NULL. */
+rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback);
 
 /* Per-kernel device time, measured with CUDA events on the launch stream when profiling is on. */
 typedef struct {

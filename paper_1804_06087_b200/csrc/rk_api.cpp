@@ -26,9 +26,11 @@ using namespace rk;
 
 namespace {
 
-enum KernelKind { KK_GEMM = 0, KK_VOTE, KK_OVERDUE, KK_MERGE, KK_Q, KK_FOLD, KK_PREDICT, KK_ALLREDUCE, KK_SERVE, KK_COUNT };
+enum KernelKind { KK_GEMM = 0, KK_VOTE, KK_OVERDUE, KK_MERGE, KK_Q, KK_FOLD, KK_PREDICT, KK_ALLREDUCE, KK_SERVE,
+                  KK_FALLBACK, KK_COUNT };
 const char* kKernelNames[KK_COUNT] = {"gemm_heads_tcgen05", "vote_subsets", "overdue_moments", "merge_table",
-                                      "labelled_moments", "reward_fold", "predict", "nccl_allreduce", "greedy_serve"};
+                                      "labelled_moments", "reward_fold", "predict", "nccl_allreduce", "greedy_serve",
+                                      "fused_fallback"};
 
 struct Prof {
   bool on = false;
@@ -56,6 +58,18 @@ struct rk_ctx {
   float* d_bias = nullptr;
   // last rk_score* batch
   bool have_batch = false, batch_stats = false;
+  bool batch_fused = false;            // NEXT-3: rk_score_labelled kept top-T lists instead of logits
+  const uint16_t* cur_X = nullptr;     // fused: the batch's features (device), for fallback rows
+  const int32_t* cur_labels = nullptr; // fused: device labels of the batch
+  const int32_t* cur_labels_arg = nullptr;
+  float* d_ly = nullptr; float* d_tv = nullptr; uint16_t* d_ti = nullptr;
+  int64_t ly_cap = 0, tv_cap = 0, ti_cap = 0;
+  int32_t* d_fb = nullptr; int64_t fb_cap = 0;          // fallback list [N] + count, identity list [N]
+  uint16_t* d_xc = nullptr; int64_t xc_cap = 0;         // fallback rows: compact X
+  float* d_lc = nullptr; int64_t lc_cap = 0;            // fallback rows: logits
+  int32_t* d_tc = nullptr; int64_t tc_cap = 0;          // fallback rows: top1 | labels
+  float* d_sc = nullptr; int64_t sc_cap = 0;            // fallback rows: lsum | rmax
+  int64_t last_fallback = 0, last_worklist = 0;
   const float* cur_logits = nullptr;
   int64_t cur_ldc = 0, cur_N = 0, cur_off = 0;
   // GEMM workspaces
@@ -273,7 +287,8 @@ void rk_destroy(rk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
-  void* ptrs[] = {ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lsum, ctx->ws_max, ctx->ws_x,
+  void* ptrs[] = {ctx->d_ly, ctx->d_tv, ctx->d_ti, ctx->d_fb, ctx->d_xc, ctx->d_lc, ctx->d_tc, ctx->d_sc,
+                  ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lsum, ctx->ws_max, ctx->ws_x,
                   ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_pairs, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -374,23 +389,27 @@ rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16,
   return RK_OK;
 }
 
-rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* stream) {
-  if (!ctx) return RK_EINVAL;
-  if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
-  if (N < 0 || goff < 0 || (N > 0 && !X)) return fail(ctx, RK_EINVAL, "bad X / N / offset");
-  if (N > INT32_MAX) return fail(ctx, RK_EINVAL, "N per call must be < 2^31 (stream larger sets in chunks)");
+// A1+A2 over N rows; dlabels (device) != null -> the fused epilogue (NEXT-3): no logits, top-T lists.
+static rk_status score_impl(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, cudaStream_t st,
+                            const int32_t* dlabels) {
   CK(cudaSetDevice(ctx->dev));
-  cudaStream_t st = (cudaStream_t)stream;
   rk_status s;
-  if ((s = ensure(ctx, &ctx->ws_logits, &ctx->ws_cap, std::max<int64_t>(N, 1) * ctx->K * ctx->ldc)) != RK_OK) return s;
+  const bool fused = dlabels != nullptr;
+  if (!fused && (s = ensure(ctx, &ctx->ws_logits, &ctx->ws_cap, std::max<int64_t>(N, 1) * ctx->K * ctx->ldc)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_lsum, &ctx->ws_lsum_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
-  ctx->cur_logits = ctx->ws_logits;
+  if (fused) {
+    if ((s = ensure(ctx, &ctx->d_ly, &ctx->ly_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
+    if ((s = ensure(ctx, &ctx->d_tv, &ctx->tv_cap, std::max<int64_t>(N, 1) * ctx->K * kFuseT)) != RK_OK) return s;
+    if ((s = ensure(ctx, &ctx->d_ti, &ctx->ti_cap, std::max<int64_t>(N, 1) * ctx->K * kFuseT)) != RK_OK) return s;
+  }
+  ctx->cur_logits = fused ? nullptr : ctx->ws_logits;
   ctx->cur_ldc = ctx->ldc;
   ctx->cur_N = N;
   ctx->cur_off = goff;
   ctx->batch_stats = true;
+  ctx->batch_fused = fused;
   ctx->have_batch = true;
   if (N == 0) return RK_OK;
   // Host X: the H2D copy of chunk i+1 (copy stream) overlaps the GEMM of chunk i (caller stream).
@@ -427,14 +446,62 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
     gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias;
     gp.cluster = ctx->gemm_cluster;
     gp.top1 = ctx->ws_top1 + r0 * ctx->K; gp.lsum = ctx->ws_lsum + r0 * ctx->K; gp.rmax = ctx->ws_max + r0 * ctx->K;
-    gp.logits = ctx->ws_logits + r0 * ctx->K * ctx->ldc;
+    if (fused) {
+      gp.labels = dlabels + r0;
+      gp.ly = ctx->d_ly + r0 * ctx->K;
+      gp.tv = ctx->d_tv + r0 * ctx->K * kFuseT;
+      gp.ti = ctx->d_ti + r0 * ctx->K * kFuseT;
+      gp.logits = gp.tv;  // the logits tensor map is encoded but never used by the fused epilogue
+    } else {
+      gp.logits = ctx->ws_logits + r0 * ctx->K * ctx->ldc;
+    }
     int rc = gemm_build_tmaps(gp, Xd, ctx->d_W, gp.logits, ctx->tmaps);  // maps are passed by value
     if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
     const double flops = 2.0 * n * ctx->D * (double)ctx->K * ctx->C;
-    ProfScope ps(ctx, KK_GEMM, st, (double)n * ctx->D * 2 + (double)n * ctx->K * ctx->C * 4, flops);
+    const double bytes = (double)n * ctx->D * 2 + (fused ? (double)n * ctx->K * (kFuseT * 6 + 16) : (double)n * ctx->K * ctx->C * 4);
+    ProfScope ps(ctx, KK_GEMM, st, bytes, flops);
     CK(launch_gemm(gp, ctx->sm_count, st));
   }
+  ctx->cur_X = host ? ctx->ws_x : static_cast<const uint16_t*>(X);
   return RK_OK;
+}
+
+static bool fused_supported(const rk_ctx* ctx) {
+  return ctx->K <= 8 && ctx->Cp > 128 && ctx->ldc <= kMaxCFast && ctx->C <= 65535;
+}
+
+rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
+  if (N < 0 || goff < 0 || (N > 0 && !X)) return fail(ctx, RK_EINVAL, "bad X / N / offset");
+  if (N > INT32_MAX) return fail(ctx, RK_EINVAL, "N per call must be < 2^31 (stream larger sets in chunks)");
+  ctx->cur_labels_arg = nullptr;
+  return score_impl(ctx, X, N, goff, (cudaStream_t)stream, nullptr);
+}
+
+rk_status rk_score_labelled(rk_ctx* ctx, const void* X, const int32_t* labels, int64_t N, int64_t goff, void* stream) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
+  if (N < 0 || goff < 0 || (N > 0 && (!X || !labels))) return fail(ctx, RK_EINVAL, "bad X / labels / N / offset");
+  if (N > INT32_MAX) return fail(ctx, RK_EINVAL, "N per call must be < 2^31 (stream larger sets in chunks)");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!fused_supported(ctx)) {  // K > 8 or <= 128 classes: the logits path (same results)
+    rk_status s = score_impl(ctx, X, N, goff, st, nullptr);
+    ctx->cur_labels_arg = labels;
+    return s;
+  }
+  CK(cudaSetDevice(ctx->dev));
+  const int32_t* dl = labels;
+  if (N > 0 && !is_device_ptr(labels)) {
+    rk_status s;
+    if ((s = ensure(ctx, &ctx->d_labels, &ctx->labels_cap, N)) != RK_OK) return s;
+    CK(cudaMemcpyAsync(ctx->d_labels, labels, N * 4, cudaMemcpyHostToDevice, st));
+    dl = ctx->d_labels;
+  }
+  rk_status s = N > 0 ? score_impl(ctx, X, N, goff, st, dl) : score_impl(ctx, X, N, goff, st, nullptr);
+  ctx->cur_labels = dl;
+  ctx->cur_labels_arg = labels;
+  return s;
 }
 
 rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, int64_t goff, void* stream) {
@@ -450,6 +517,8 @@ rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, 
   ctx->cur_N = N;
   ctx->cur_off = goff;
   ctx->batch_stats = false;
+  ctx->batch_fused = false;
+  ctx->cur_labels_arg = nullptr;
   ctx->have_batch = true;
   return RK_OK;
 }
@@ -564,6 +633,13 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
   if (ctx->finalized) return fail(ctx, RK_ESTATE, "table already finalized (all-reduced): rk_subset_reset first");
   if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "rk_score / rk_score_logits first");
   const int64_t N = ctx->cur_N;
+  if (ctx->batch_fused) {  // NEXT-3: the labels were given to rk_score_labelled
+    if (labels && labels != ctx->cur_labels_arg)
+      return fail(ctx, RK_EINVAL, "after rk_score_labelled, pass the same labels (or NULL)");
+    labels = ctx->cur_labels;
+  } else if (!labels && ctx->cur_labels_arg) {
+    labels = ctx->cur_labels_arg;
+  }
   if (N > 0 && !labels) return fail(ctx, RK_EINVAL, "labels required");
   if (ctx->final_seen && N > 0) return fail(ctx, RK_EINVAL, "a ragged chunk must be the last one (chunks are multiples of lcm(B))");
   if (ctx->cur_off % ctx->L != 0) return fail(ctx, RK_EINVAL, "chunk offset must be a multiple of lcm(B)");
@@ -673,9 +749,53 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       vp.cta_work = ctx->d_work + 2 * N + 2;  // K >= 9: warp averaging kernel -> CTA kernel
       vp.cta_count = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 2);
       const double bytes = (double)N * ((double)K * C * 4 + 4);
+      if (ctx->batch_fused) {
+        // NEXT-3: classify from the statistics and l_y, averages from the top-T lists; undecided samples
+        // are recomputed below with logits (fallback)
+        vp.ly_in = ctx->d_ly;
+        vp.logits = nullptr;
+        if ((s = ensure(ctx, &ctx->d_fb, &ctx->fb_cap, 2 * N + 2)) != RK_OK) return s;
+        unsigned int* fbc = reinterpret_cast<unsigned int*>(ctx->d_fb + 2 * N);
+        {
+          ProfScope ps(ctx, KK_VOTE, st, (double)N * K * (kFuseT * 6 + 16 + 4) + 4.0 * N, 0);
+          CK(cudaMemsetAsync(fbc, 0, 4, st));
+          CK(launch_vote_classify(vp, st, ctx->d_work, wc, ctx->sm_count));
+          CK(launch_vote_sparse(vp, ctx->d_ly, ctx->d_tv, ctx->d_ti, ctx->d_work, wc, ctx->d_fb, fbc, ctx->sm_count, st));
+        }
+        unsigned int hc[2] = {0, 0};
+        CK(cudaMemcpyAsync(&hc[0], fbc, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&hc[1], wc, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const int64_t M = hc[0];
+        ctx->last_fallback = M;
+        ctx->last_worklist = hc[1];
+        if (M > 0) {
+          ProfScope ps(ctx, KK_FALLBACK, st, (double)M * ((double)K * C * 8 + ctx->D * 4), 2.0 * M * ctx->D * (double)K * C);
+          if ((s = ensure(ctx, &ctx->d_xc, &ctx->xc_cap, M * ctx->D)) != RK_OK) return s;
+          if ((s = ensure(ctx, &ctx->d_lc, &ctx->lc_cap, M * K * ctx->ldc)) != RK_OK) return s;
+          if ((s = ensure(ctx, &ctx->d_tc, &ctx->tc_cap, M * K + M)) != RK_OK) return s;
+          if ((s = ensure(ctx, &ctx->d_sc, &ctx->sc_cap, 2 * M * K)) != RK_OK) return s;
+          int32_t* iota = ctx->d_fb + N;
+          int32_t* yc = ctx->d_tc + M * K;
+          CK(launch_gather_rows(ctx->cur_X, ctx->D, ctx->cur_labels, ctx->d_fb, fbc, M, ctx->d_xc, yc, iota, st));
+          GemmParams gp{};
+          gp.N = M; gp.K = K; gp.C = C; gp.Cp = ctx->Cp; gp.D = ctx->D; gp.ldc = ctx->ldc;
+          gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias; gp.cluster = ctx->gemm_cluster;
+          gp.top1 = ctx->d_tc; gp.lsum = ctx->d_sc; gp.rmax = ctx->d_sc + M * K; gp.logits = ctx->d_lc;
+          int rc = gemm_build_tmaps(gp, ctx->d_xc, ctx->d_W, gp.logits, ctx->tmaps);
+          if (rc != 0) return fail(ctx, RK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
+          CK(launch_gemm(gp, ctx->sm_count, st));
+          VoteParams q = vp;
+          q.logits = ctx->d_lc; q.ldc = ctx->ldc; q.N = M;
+          q.top1_in = ctx->d_tc; q.lsum_in = ctx->d_sc; q.rmax_in = ctx->d_sc + M * K; q.ly_in = nullptr;
+          q.labels = yc;
+          CK(launch_vote_avg(q, grid, st, iota, fbc));
+        }
+      } else {
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
       if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lsum, st_max, ctx->sm_count));
       else CK(launch_vote_batch(vp, ctx->sm_count, st, ctx->d_work, wc, st_top, st_lsum, st_max));
+      }
     }
     // ---- A5: batch latency moments (label independent) ----
     const int64_t* arr = nullptr;
@@ -838,6 +958,7 @@ rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_
   if (!ctx) return RK_EINVAL;
   if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "rk_score / rk_score_logits first");
   if (v == 0 || v >= (1u << ctx->K)) return fail(ctx, RK_EINVAL, "v must be in [1, 2^K) (PAPER.md:429 excludes v = 0)");
+  if (ctx->batch_fused) return fail(ctx, RK_ESTATE, "rk_score_labelled keeps no logits: rk_score the batch for rk_predict");
   CK(cudaSetDevice(ctx->dev));
   cudaStream_t st = (cudaStream_t)stream;
   PredictParams pp{};
@@ -1195,11 +1316,23 @@ rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64
   return RK_OK;
 }
 
+rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->reset_done || ctx->chunks == 0) return fail(ctx, RK_ESTATE, "no chunk accumulated since rk_subset_reset");
+  CK(cudaSetDevice(ctx->dev));
+  unsigned int w = 0;
+  if (ctx->d_work && ctx->cur_N > 0) CK(cudaMemcpy(&w, reinterpret_cast<unsigned int*>(ctx->d_work + ctx->cur_N), 4,
+                                                   cudaMemcpyDeviceToHost));
+  if (worklist) *worklist = w;
+  if (fallback) *fallback = ctx->batch_fused ? ctx->last_fallback : 0;
+  return RK_OK;
+}
+
 rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** rmax,
                      const float** lsum, int64_t* N) {
   if (!ctx) return RK_EINVAL;
   if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "no batch scored yet");
-  if (logits) *logits = ctx->cur_logits;
+  if (logits) *logits = ctx->cur_logits;  // NULL after rk_score_labelled (fused: no logits rows)
   if (ldc) *ldc = (int)ctx->cur_ldc;
   if (top1) *top1 = ctx->batch_stats ? ctx->ws_top1 : nullptr;
   if (rmax) *rmax = ctx->batch_stats ? ctx->ws_max : nullptr;

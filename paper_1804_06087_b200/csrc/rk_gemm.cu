@@ -205,6 +205,12 @@ struct GemmArgs {
   int32_t* top1;
   float* lsum;
   float* rmax;
+  // fused forward + vote (NEXT-3; FUSED instantiation): labels [N]; outputs the label's logit ly [N][K]
+  // and the top-kFuseT logits per (row, model), values tv [N][K][T] (descending) and classes ti [N][K][T]
+  const int32_t* labels;
+  float* ly;
+  float* tv;
+  uint16_t* ti;
 };
 
 // CTA-pair (cta_group::2) forms. The TMA load lands in this CTA's shared memory but signals the
@@ -397,7 +403,7 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
 // space, so each X tile is staged once per 256 columns instead of once per model; the epilogue works
 // in 16-column blocks (each inside one model, Cp % 16 == 0) and closes a model's online statistics
 // when the next model's first block arrives.
-template <int CL, bool PACK>
+template <int CL, bool PACK, bool FUSED = false>
 __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
     gemm_heads_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                       const __grid_constant__ CUtensorMap tmo, const __grid_constant__ CUtensorMap tmo16,
@@ -533,6 +539,17 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
       const int64_t row = (int64_t)mt * BM + row_in_tile;
       float mx = -INFINITY, sum = 0.f;
       int arg = 0;
+      // FUSED: the label's logit and a descending top-T list (strict '>' insertion: among equal values the
+      // lower column stays first); candidates of a chunk are queued per thread in the (unused) store staging
+      int yl = -1;
+      float lyv = 0.f;
+      float tvr[FUSED ? kFuseT : 1];
+      int tir[FUSED ? kFuseT : 1];
+      if (FUSED) {
+        yl = row < a.N ? a.labels[row] : -1;
+#pragma unroll
+        for (int k = 0; k < kFuseT; ++k) { tvr[k] = -INFINITY; tir[k] = 0; }
+      }
       for (int j = 0; j < a.nt; ++j, ++tc) {
         const int width = min(BN, a.Cp - j * BN);
         const uint32_t as = tc & 1;
@@ -568,6 +585,38 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
             const float nml = nml_of(mx);
             sum += chunk_sum<32>(v, nml);
           }
+          if (FUSED) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) lyv = (colbase + i == yl) ? v[i] : lyv;
+            // queue this chunk's candidates (above the current T-th value) in column order, then insert
+            // them; the warp iterates max over lanes of the queue length, not the union of columns
+            const float thr = tvr[kFuseT - 1];
+            float* qv = reinterpret_cast<float*>(staging);
+            int* qc = reinterpret_cast<int*>(staging + 32 * 128 * 4);
+            const int tid = (warp - 2) * 32 + lane;
+            int qn = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (v[i] > thr) { qv[qn * 128 + tid] = v[i]; qc[qn * 128 + tid] = colbase + i; ++qn; }
+            const int qmax = __reduce_max_sync(0xffffffffu, (unsigned)qn);
+            for (int k = 0; k < qmax; ++k) {
+              if (k < qn) {
+                float cv = qv[k * 128 + tid];
+                int cc = qc[k * 128 + tid];
+#pragma unroll
+                for (int t = 0; t < kFuseT; ++t) {
+                  const bool sw = cv > tvr[t];
+                  const float t1 = tvr[t];
+                  const int t2 = tir[t];
+                  tvr[t] = sw ? cv : t1;
+                  tir[t] = sw ? cc : t2;
+                  cv = sw ? t1 : cv;
+                  cc = sw ? t2 : cc;
+                }
+              }
+            }
+            continue;
+          }
           // stage 32 rows x 32 cols (128B-swizzled) and store with TMA. (Coalesced st.global.cs
           // from the same staging box measured 18% slower for the whole kernel: DESIGN.md §6.)
           uint8_t* buf = stg + (nstore & 1) * STG_BYTES;
@@ -598,7 +647,22 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
         a.top1[row * a.K + model] = arg;
         a.lsum[row * a.K + model] = lsum_of(sum, mx);  // relative to the row max
         a.rmax[row * a.K + model] = mx;
+        if (FUSED) {
+          const size_t o = (size_t)row * a.K + model;
+          a.ly[o] = lyv;
+          float4* tv4 = reinterpret_cast<float4*>(a.tv + o * kFuseT);
+#pragma unroll
+          for (int k = 0; k < kFuseT / 4; ++k) tv4[k] = make_float4(tvr[4 * k], tvr[4 * k + 1], tvr[4 * k + 2], tvr[4 * k + 3]);
+          uint4* ti4 = reinterpret_cast<uint4*>(a.ti + o * kFuseT);
+#pragma unroll
+          for (int k = 0; k < kFuseT / 8; ++k)
+            ti4[k] = make_uint4((uint32_t)tir[8 * k] | ((uint32_t)tir[8 * k + 1] << 16),
+                                (uint32_t)tir[8 * k + 2] | ((uint32_t)tir[8 * k + 3] << 16),
+                                (uint32_t)tir[8 * k + 4] | ((uint32_t)tir[8 * k + 5] << 16),
+                                (uint32_t)tir[8 * k + 6] | ((uint32_t)tir[8 * k + 7] << 16));
+        }
       }
+      if (FUSED) __syncwarp();  // the next unit's queue writes must not overtake this unit's reads
     }
     if (lane == 0) tma_store_wait_all();
     __syncwarp();
@@ -682,19 +746,19 @@ int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits,
   return 0;
 }
 
-template <int CL, bool PACK>
+template <int CL, bool PACK, bool FUSED = false>
 static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count, cudaStream_t st) {
   const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(p.tmap_x);
   const CUtensorMap& mw = *reinterpret_cast<const CUtensorMap*>(p.tmap_w);
   const CUtensorMap& mo = *reinterpret_cast<const CUtensorMap*>(p.tmap_out);
   const CUtensorMap& m16 = *reinterpret_cast<const CUtensorMap*>(p.tmap_out16);
-  cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<CL, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<CL, PACK, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Tile<CL, PACK>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int64_t units = ((p.N + CL * BM - 1) / (CL * BM)) * a.ng;
   if (CL == 1) {
     const int grid = (int)(units < sm_count ? units : sm_count);
-    gemm_heads_kernel<CL, PACK><<<grid, 64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), Tile<CL, PACK>::SMEM_BYTES, st>>>(
+    gemm_heads_kernel<CL, PACK, FUSED><<<grid, 64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), Tile<CL, PACK>::SMEM_BYTES, st>>>(
         mx, mw, mo, m16, a);
     return cudaGetLastError();
   }
@@ -712,7 +776,7 @@ static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, gemm_heads_kernel<CL, PACK>, mx, mw, mo, m16, a);
+  e = cudaLaunchKernelEx(&cfg, gemm_heads_kernel<CL, PACK, FUSED>, mx, mw, mo, m16, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -722,10 +786,15 @@ cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
   GemmArgs a;
   a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D;
   a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lsum = p.lsum; a.rmax = p.rmax;
+  a.labels = p.labels; a.ly = p.ly; a.tv = p.tv; a.ti = p.ti;
   const bool pack = p.Cp <= 128;  // small heads: tiles span several models
   a.ng = pack ? 1 : p.K;
   a.gcols = pack ? p.K * p.Cp : p.Cp;
   a.nt = (a.gcols + BN - 1) / BN;
+  if (p.labels) {  // fused forward + vote (NEXT-3): per-model column tiles only
+    if (pack) return cudaErrorInvalidValue;
+    return p.cluster <= 1 ? launch_t<1, false, true>(a, p, sm_count, st) : launch_t<2, false, true>(a, p, sm_count, st);
+  }
   if (p.cluster <= 1) return pack ? launch_t<1, true>(a, p, sm_count, st) : launch_t<1, false>(a, p, sm_count, st);
   return pack ? launch_t<2, true>(a, p, sm_count, st) : launch_t<2, false>(a, p, sm_count, st);
 }

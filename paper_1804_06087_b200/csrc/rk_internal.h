@@ -34,6 +34,7 @@ struct VoteParams {
                              // (then computed here); p[m][c] = exp((l - rmax_m) - lsum_m)
   const int32_t* top1_in;    // [N][K] or null
   const float* rmax_in;      // [N][K] or null (row max, from the GEMM epilogue)
+  const float* ly_in;        // [N][K] label logits l[m][y] or null (fused mode: no logits rows exist)
   const int32_t* labels;     // [N] device
   int64_t N;                 // samples in this chunk
   int K, C, S, tie;
@@ -113,6 +114,19 @@ cudaError_t launch_vote_large_avg(const VoteParams& q, int sm_count, cudaStream_
 // scratch (written by kernel A when the logits came without statistics).
 cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
                              int32_t* st_top, float* st_lsum, float* st_max, int sm_count);
+
+// NEXT-3 (rk_vote_sparse.cu): averages of the classify kernel's worklist from the fused GEMM's top-kFuseT
+// lists (K <= 8); samples whose bounds leave a subset undecided are appended to fb / fb_count.
+cudaError_t launch_vote_sparse(const VoteParams& p, const float* ly, const float* tv, const uint16_t* ti,
+                               const int32_t* work, const unsigned int* work_count, int32_t* fb,
+                               unsigned int* fb_count, int sm_count, cudaStream_t st);
+// compact copies of the fallback rows' features and labels (+ the identity worklist 0..M-1)
+cudaError_t launch_gather_rows(const uint16_t* X, int D, const int32_t* labels, const int32_t* idx,
+                               const unsigned int* count, int64_t M, uint16_t* Xc, int32_t* yc, int32_t* iota,
+                               cudaStream_t st);
+// kernel A of launch_vote_warp alone (classify + votes + worklist)
+cudaError_t launch_vote_classify(const VoteParams& p, cudaStream_t st, int32_t* work, unsigned int* work_count,
+                                 int sm_count);
 
 // ---- per-sample predictions for one action v (rk_predict) ---------------------------------------
 struct PredictParams {
@@ -261,6 +275,7 @@ cudaError_t launch_ac_grad(const RLParams& p, float* grad, float* loss2 /*device
 cudaError_t launch_ac_apply(float* P, const float* g, int64_t npol, int64_t np, float lr_pi, float lr_v,
                             cudaStream_t st);
 
+constexpr int kFuseT = 16;  // NEXT-3: logits kept per (row, model) by the fused GEMM epilogue
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {
   const void* tmap_x;    // CUtensorMap* (host copy passed by value via __grid_constant__)
@@ -277,6 +292,13 @@ struct GemmParams {
   float* logits;         // [N][K][ldc]
   unsigned int* err;
   int cluster;           // 1 = one CTA per 128-row tile; 2 = CTA pair, tcgen05.mma.cta_group::2 on 256-row tiles
+  // NEXT-3 fused forward + vote (labels != null; Cp > 128): no logits stored; instead the label's logit
+  // ly [N][K] and the kFuseT largest logits per (row, model): tv [N][K][kFuseT] fp32 descending (equal
+  // values: lower class first), ti [N][K][kFuseT] classes
+  const int32_t* labels;
+  float* ly;
+  float* tv;
+  uint16_t* ti;
 };
 cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st);
 int gemm_build_tmaps(GemmParams& p, const void* X, const void* W, float* logits, void* storage /*4*128B*/);

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
         ntp = p.top1_in[nn * K + lane];
         nls = p.lsum_in[nn * K + lane];
         nmx = p.rmax_in[nn * K + lane];
-        nly = (yy >= 0 && yy < C) ? p.logits[(nn * K + lane) * p.ldc + yy] : 0.f;
+        nly = (yy >= 0 && yy < C) ? (p.ly_in ? p.ly_in[nn * K + lane] : p.logits[(nn * K + lane) * p.ldc + yy]) : 0.f;
       }
     };
     prefetch(u0);
@@ -262,6 +262,20 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
 }
 
 }  // namespace
+
+cudaError_t launch_vote_classify(const VoteParams& p, cudaStream_t st, int32_t* work, unsigned int* work_count,
+                                 int sm_count) {
+  if (p.N <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(work_count, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  if (!p.lsum_in) return cudaErrorInvalidValue;  // statistics come from the GEMM
+  const int U = p.gs > 0 ? p.gs : 16;
+  const int64_t units = (p.N + U - 1) / U;
+  int64_t ga = (units + WPC - 1) / WPC;
+  if (ga > (int64_t)sm_count * 8) ga = (int64_t)sm_count * 8;
+  vote_classify_kernel<true><<<(int)ga, WT, 0, st>>>(p, work, work_count, nullptr, nullptr, nullptr);
+  return cudaGetLastError();
+}
 
 size_t vote_warp_smem_per_warp(const VoteParams& p) { return vote_avg_smem_per_warp(p); }
 int vote_warp_threads() { return WT; }

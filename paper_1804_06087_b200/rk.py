@@ -25,7 +25,7 @@ TIE_BEST_MEMBER, TIE_LOWEST_CLASS = 0, 1
 EXPORTS = ["rk_create", "rk_nccl_unique_id", "rk_load_ensemble", "rk_score", "rk_score_logits", "rk_subset_reset",
            "rk_subset_accumulate", "rk_subset_finalize", "rk_subset_stats", "rk_predict", "rk_greedy_serve", "rk_outputs",
            "rk_sine_arrivals", "rk_async_serve", "rk_serve_stream", "rk_ac_dims", "rk_ac_rollout", "rk_ac_grad",
-           "rk_ac_apply",
+           "rk_ac_apply", "rk_score_labelled", "rk_vote_diag",
            "rk_group_counts",
            "rk_set_profiling", "rk_kernel_stats", "rk_last_error", "rk_status_string", "rk_destroy"]
 
@@ -85,6 +85,8 @@ def load_library(path: str | None = None):
     L.rk_load_ensemble.argtypes = [vp, i32, i32, i32, vp, vp, i32, vp, i32]
     L.rk_score.argtypes = [vp, vp, i64, i64, vp]
     L.rk_score_logits.argtypes = [vp, vp, i32, i64, i64, vp]
+    L.rk_score_labelled.argtypes = [vp, vp, vp, i64, i64, vp]
+    L.rk_vote_diag.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.rk_subset_reset.argtypes = [vp, ctypes.POINTER(_Cfg)]
     L.rk_subset_accumulate.argtypes = [vp, vp, vp]
     L.rk_subset_finalize.argtypes = [vp, ctypes.POINTER(_Table), vp]
@@ -204,6 +206,11 @@ class Context:
 
     def score(self, X, N, offset=0, stream=None):
         self._chk(self._L.rk_score(self._p, _ptr(X), N, offset, _stream(stream)), "rk_score")
+
+    def score_labelled(self, X, labels, N, offset=0, stream=None):
+        """NEXT-3: fused forward + vote (labels known at scoring time; no logits stored for K <= 8, C > 128)."""
+        self._chk(self._L.rk_score_labelled(self._p, _ptr(X), _ptr(labels), N, offset, _stream(stream)),
+                  "rk_score_labelled")
 
     def score_logits(self, logits, ldc, N, offset=0, stream=None):
         self._chk(self._L.rk_score_logits(self._p, _ptr(logits), ldc, N, offset, _stream(stream)), "rk_score_logits")
@@ -372,6 +379,12 @@ class Context:
             self._chk(self._L.rk_group_counts(self._p, out.ctypes.data, out.size, None, None, _stream(stream)),
                       "rk_group_counts")
         return gs.value, out
+
+    def vote_diag(self):
+        """(worklist, fallback) sample counts of the last accumulated chunk (K <= 8 path)."""
+        w, f = ctypes.c_int64(), ctypes.c_int64()
+        self._chk(self._L.rk_vote_diag(self._p, ctypes.byref(w), ctypes.byref(f)), "rk_vote_diag")
+        return w.value, f.value
 
     def set_profiling(self, on: bool):
         self._chk(self._L.rk_set_profiling(self._p, int(on)), "rk_set_profiling")
