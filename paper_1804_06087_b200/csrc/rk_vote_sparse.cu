@@ -38,7 +38,21 @@ struct SparseSmem {
   unsigned int mask[HS];        // models listing the class
   float P[HS][kMaxFuseK];       // p[m][class] where listed
   int list[HS];                 // threat slots
+  float tab[64];                // one threat's half-mask sums: LB lo [16] | LB hi [16] | UB lo [16] | UB hi [16]
 };
+
+// max over subsets v with |v| >= 2 of sum_{m in v} d_m = d_(1) + d_(2) + sum_{k >= 3} max(0, d_(k))
+__device__ __forceinline__ float best_pair_sum(const float* d, int K) {
+  float m1 = -INFINITY, m2 = -INFINITY, pos = 0.f;
+#pragma unroll
+  for (int m = 0; m < kMaxFuseK; ++m) {
+    if (m >= K) break;
+    const float x = d[m];
+    pos += fmaxf(x, 0.f);
+    if (x > m1) { m2 = m1; m1 = x; } else if (x > m2) { m2 = x; }
+  }
+  return m1 + m2 + (pos - fmaxf(m1, 0.f) - fmaxf(m2, 0.f));
+}
 
 __global__ void __launch_bounds__(32 * SW) vote_sparse_average_kernel(const VoteParams p, const float* ly,
                                                                      const float* tv, const uint16_t* ti,
@@ -103,10 +117,12 @@ __global__ void __launch_bounds__(32 * SW) vote_sparse_average_kernel(const Vote
       }
     }
     __syncwarp();
-    // 2. threats: classes that could reach y's average in some subset; and the unlisted classes' bound
-    bool oth = false;
+    // 2. threats: classes whose upper bound can reach y's average in some subset with |v| >= 2 (singletons
+    // are decided by the top-1); and the same test for the classes no model lists (bound pT_m each)
+    float d[kMaxFuseK];
 #pragma unroll
-    for (int m = 0; m < kMaxFuseK; ++m) oth |= (m < K) && pt[m] * band1 >= py[m];
+    for (int m = 0; m < kMaxFuseK; ++m) d[m] = pt[m] * band1 - py[m];
+    const bool oth = K >= 2 && best_pair_sum(d, K) >= 0.f;
     int nthr = 0;
 #pragma unroll
     for (int i = 0; i < HS / 32; ++i) {
@@ -115,49 +131,72 @@ __global__ void __launch_bounds__(32 * SW) vote_sparse_average_kernel(const Vote
       if (sh.key[s] != -1) {
         const unsigned int mk = sh.mask[s];
 #pragma unroll
-        for (int m = 0; m < kMaxFuseK; ++m)
-          if (m < K) thr |= (((mk >> m) & 1u) ? sh.P[s][m] : pt[m]) * band1 >= py[m];
+        for (int m = 0; m < kMaxFuseK; ++m) d[m] = (((mk >> m) & 1u) ? sh.P[s][m] : pt[m]) * band1 - py[m];
+        thr = K >= 2 && best_pair_sum(d, K) >= 0.f;
       }
       const unsigned int b = __ballot_sync(FULL, thr);
       if (thr) sh.list[nthr + __popc(b & ((1u << lane) - 1u))] = s;
       nthr += __popc(b);
     }
     __syncwarp();
-    // 3. every subset of this lane
-    bool undecided = false;
+    // 3. every subset of this lane: A_v(y) and the unlisted bound, then each threat's LB / UB from its
+    // half-mask tables (low models 0-3 index v & 15, high models 4-7 index v >> 4)
+    float A[JM], Ab[JM];
+    uint32_t lose = 0, und = 0, multi = 0;
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+      float a = 0.f, u = 0.f;
+#pragma unroll
+      for (int m = 0; m < kMaxFuseK; ++m)
+        if ((v >> m) & 1u) { a += py[m]; u += pt[m]; }
+      A[j] = a;
+      Ab[j] = a * band1;
+      if (v <= (uint32_t)S && __popc(v) > 1) {
+        multi |= 1u << j;
+        if (oth && u * band1 >= a) und |= 1u << j;
+      }
+    }
+    for (int t = 0; t < nthr; ++t) {
+      const int s = sh.list[t];
+      {  // lane l builds entry l & 15 of table (l >> 4): 0 = low models, 1 = high models; LB and UB
+        const unsigned int mk = sh.mask[s];
+        const int e = lane & 15, hi = lane >> 4;
+        float lb = 0.f, ub = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int m = 4 * hi + i;
+          if (m < K && ((e >> i) & 1)) {
+            const bool lst = (mk >> m) & 1u;
+            const float pm = lst ? sh.P[s][m] : 0.f;
+            lb += pm;
+            ub += lst ? pm : pt[m];
+          }
+        }
+        sh.tab[lane] = lb;
+        sh.tab[32 + lane] = ub;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < JM; ++j) {
+        const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+        const int lo = (int)(v & 15u), hi = (int)((v >> 4) & 15u);
+        const float LB = sh.tab[lo] + sh.tab[16 + hi];
+        const float UB = sh.tab[32 + lo] + sh.tab[48 + hi];
+        lose |= (LB > Ab[j]) ? (1u << j) : 0u;
+        und |= (UB * band1 >= A[j]) ? (1u << j) : 0u;
+      }
+      __syncwarp();
+    }
     uint32_t okm = 0;
 #pragma unroll
     for (int j = 0; j < JM; ++j) {
       const uint32_t v = (uint32_t)(lane + 32 * j + 1);
       if (v > (uint32_t)S) break;
-      if (__popc(v) == 1) {  // singleton: the top-1 (I1)
-        okm |= (top[__ffs(v) - 1] == y) ? (1u << j) : 0u;
-        continue;
-      }
-      float A = 0.f, UBo = 0.f;
-#pragma unroll
-      for (int m = 0; m < kMaxFuseK; ++m)
-        if ((v >> m) & 1u) { A += py[m]; UBo += pt[m]; }
-      const float Ab = A * band1;
-      bool lose = false, und = oth && UBo * band1 >= A;
-      for (int t = 0; t < nthr && !lose; ++t) {
-        const int s = sh.list[t];
-        const unsigned int mk = sh.mask[s] & v;
-        float LB = 0.f, UB = 0.f;
-#pragma unroll
-        for (int m = 0; m < kMaxFuseK; ++m)
-          if ((v >> m) & 1u) {
-            const bool lst = (mk >> m) & 1u;
-            const float pm = lst ? sh.P[s][m] : 0.f;
-            LB += pm;
-            UB += lst ? pm : pt[m];
-          }
-        lose = LB > Ab;
-        und |= UB * band1 >= A;
-      }
-      if (!lose && und) undecided = true;
-      if (!lose && !und) okm |= 1u << j;
+      if (!((multi >> j) & 1u)) okm |= (top[__ffs(v) - 1] == y) ? (1u << j) : 0u;  // singleton: top-1 (I1)
+      else if (!((lose >> j) & 1u) && !((und >> j) & 1u)) okm |= 1u << j;
     }
+    const bool undecided = (und & ~lose & multi) != 0u;
     if (__any_sync(FULL, undecided)) {
       if (lane == 0) fb[atomicAdd(fb_count, 1u)] = (int32_t)n;
     } else {

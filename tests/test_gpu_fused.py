@@ -62,8 +62,9 @@ def test_fused_parity(rk, K, C, D, N, tie):
 
 
 def test_fallback_route_taken(rk):
-    """Flat rows (a small logit scale) leave many subsets undecided by the 16-entry bounds: most worklist
-    samples go through the recompute, and the table is still the oracle's."""
+    """Flat rows (a small logit scale) leave subsets undecided by the 16-entry bounds: those samples go
+    through the recompute (GEMM with logits + the streaming averaging kernel), and the table is still the
+    oracle's."""
     K, C, D, N = 8, 1000, 256, 2000
     y, X, W, b, _ = heads(K, C, D, N, 7)
     sh = -6
@@ -71,7 +72,7 @@ def test_fallback_route_taken(rk):
     t, (work, fb) = run(rk, K, C, D, N, y, X, W, b * 0, sh, gcfg, 0, True)
     o = oracle.table(oracle.logits_gemm(X, W, b * 0, sh), y, K, C, cfg=ocfg)
     compare_tables(t, o, K=K)
-    assert fb > 0.3 * work, (work, fb)
+    assert 0 < fb < work, (work, fb)
 
 
 def test_fused_bias_offsets(rk):
