@@ -194,8 +194,9 @@ def main():
     ap.add_argument("--impl", default="rk", choices=["rk", "reference"])
     ap.add_argument("--tie", default="best_member", choices=["best_member", "lowest_class"])
     ap.add_argument("--queue", action="store_true", help="queue-aware latency (reading Q15, PAPER.md:410)")
-    ap.add_argument("--unfused", action="store_true",
-                    help="rk_score + logits-based vote stage instead of the fused forward + vote (NEXT-3)")
+    ap.add_argument("--fused", action="store_true",
+                    help="NEXT-3 fused forward + vote (rk_score_labelled) instead of rk_score + the logits vote stage "
+                         "(slower on B200 at c2-c4: DESIGN.md §6)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -245,7 +246,7 @@ def main():
                         want_labelled=True, queue=args.queue)
     torch.cuda.synchronize()
 
-    fused = not args.unfused
+    fused = args.fused
 
     def score(Xb, yb):
         if fused:

@@ -48,20 +48,28 @@ constexpr int XCH_BYTES = 4 * 32 * 12;   // (max, sum, argmax) hand-over per qua
 // CL = 1: one CTA computes a 128 x 256 tile (W tile 256 rows in its smem, 4 stages of 48 KB).
 // CL = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256): each CTA
 // holds its 128 X rows and HALF of the W tile (128 rows), 6 stages of 32 KB.
-template <int CL, bool PACK = false>
+// FUSED (NEXT-3): 8 epilogue warps (two per TMEM lane quarter, alternate 16-column halves of each chunk);
+// the staging region holds the per-thread candidate queues ([16 entries][256 threads] values and classes)
+// and a per-quarter hand-over of (max, sum, argmax, l_y, flag, T values, T classes) per row.
+constexpr int FUSED_EPI = 8;
+constexpr int XF = 5 + 2 * kFuseT;  // words per row in the fused hand-over
+template <int CL, bool PACK = false, bool FUSED = false>
 struct Tile {
   static constexpr int B_ROWS = BN / CL;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // packed mode with 3 warps per quarter: 12 x 4 KB of store staging; one operand stage makes room
-  static constexpr bool WIDE = PACK && NHP == 3;
+  static constexpr bool WIDE = (PACK && NHP == 3) || FUSED;
   static constexpr int NS = CL == 1 ? (WIDE ? 3 : 4) : (WIDE ? 5 : 6);
-  static constexpr int STG_TOTAL = WIDE ? EPI_PACK * 2 * (32 * 16 * 4) : EPI_WARPS * 2 * STG_BYTES;
-  static constexpr int SMEM_BYTES =
-      1024 /*align slack*/ + NS * STAGE_BYTES + STG_TOTAL + 256 + XCH_BYTES * (PACK ? NHP - 1 : 1);
+  static constexpr int STG_TOTAL = FUSED ? 16 * 256 * 8 : (WIDE ? EPI_PACK * 2 * (32 * 16 * 4) : EPI_WARPS * 2 * STG_BYTES);
+  static constexpr int XCH_TOTAL = FUSED ? 4 * 32 * XF * 4 : XCH_BYTES * (PACK ? NHP - 1 : 1);
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + NS * STAGE_BYTES + STG_TOTAL + 256 + XCH_TOTAL;
 };
+template <bool PACK, bool FUSED>
+__host__ __device__ constexpr int epi_warps() { return PACK ? EPI_PACK : (FUSED ? FUSED_EPI : EPI_WARPS); }
 static_assert(Tile<1>::SMEM_BYTES <= 232448 && Tile<2>::SMEM_BYTES <= 232448 && Tile<1, true>::SMEM_BYTES <= 232448 &&
-                  Tile<2, true>::SMEM_BYTES <= 232448,
+                  Tile<2, true>::SMEM_BYTES <= 232448 && Tile<1, false, true>::SMEM_BYTES <= 232448 &&
+                  Tile<2, false, true>::SMEM_BYTES <= 232448,
               "smem");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -403,12 +411,159 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
 // space, so each X tile is staged once per 256 columns instead of once per model; the epilogue works
 // in 16-column blocks (each inside one model, Cp % 16 == 0) and closes a model's online statistics
 // when the next model's first block arrives.
+// Fused epilogue (NEXT-3, FUSED instantiation, per-model column tiles). The two warps of a TMEM lane
+// quarter (half h) take the alternate 16-column halves of every 32-column chunk; per row each keeps the
+// online (max, lowest argmax, sum-exp) of its columns, the label's logit if it sees column y, and a
+// descending list of its kFuseT largest logits: a chunk's candidates (above the list's last value) are
+// queued per thread in shared memory in column order and inserted by a compare-exchange chain, so the
+// warp iterates the longest queue of its lanes instead of every column some lane needs. At the unit end
+// half 1 hands its part to half 0 (named barriers per quarter), which merges statistics and lists and
+// writes top1 / lsum / rmax / l_y / the top-T values and classes. No logits are stored.
+__device__ __forceinline__ void topk_insert(float (&tv)[kFuseT], int (&ti)[kFuseT], float cv, int cc) {
+#pragma unroll
+  for (int t = 0; t < kFuseT; ++t) {
+    const bool sw = cv > tv[t];
+    const float t1 = tv[t];
+    const int t2 = ti[t];
+    tv[t] = sw ? cv : t1;
+    ti[t] = sw ? cc : t2;
+    cv = sw ? t1 : cv;
+    cc = sw ? t2 : cc;
+  }
+}
+
+template <int CL>
+__device__ __forceinline__ void epilogue_fused(const GemmArgs& a, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
+                                               int q, int h, int lane, uint8_t* staging, float* xch, int64_t ucl0,
+                                               int64_t units, int64_t ucls, int crank, float scale) {
+  uint32_t tc = 0, nunit = 0;
+  const int row_in_tile = q * 32 + lane;
+  const int tid = h * 128 + row_in_tile;  // queue column (256 epilogue threads)
+  float* qv = reinterpret_cast<float*>(staging);
+  int* qc = reinterpret_cast<int*>(staging + 16 * 256 * 4);
+  float* xb = xch + q * 32 * XF;          // hand-over of this quarter: [XF][32]
+  constexpr int NT = 64;                  // threads of the quarter's two warps (named barriers 1+q, 5+q)
+  for (int64_t u = ucl0; u < units; u += ucls, ++nunit) {
+    const int mt = (int)(u / a.ng) * CL + crank, model = (int)(u % a.ng);
+    const int64_t row = (int64_t)mt * BM + row_in_tile;
+    const int yl = row < a.N ? a.labels[row] : -1;
+    float mx = -INFINITY, sum = 0.f, lyv = 0.f;
+    int arg = 0x7fffffff, lyset = 0;
+    float tv[kFuseT];
+    int ti[kFuseT];
+#pragma unroll
+    for (int k = 0; k < kFuseT; ++k) { tv[k] = -INFINITY; ti[k] = 0; }
+    for (int j = 0; j < a.nt; ++j, ++tc) {
+      const int width = min(BN, a.Cp - j * BN);
+      const uint32_t as = tc & 1;
+      mbar_wait(&tfull[as], (tc >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      for (int c0 = 16 * h; c0 < width; c0 += 32) {
+        float v[32];
+        tmem_ld16(tbase + c0, v);
+        const int colbase = j * BN + c0;
+        const float4* bptr = reinterpret_cast<const float4*>(a.bias + (size_t)model * a.Cp + colbase);
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) {  // Cp % 16 == 0: the 16 columns are inside the model
+          const float4 b4 = __ldg(bptr + i4);
+          const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[4 * i4 + e] = fmaf(v[4 * i4 + e], scale, bb[e]);
+        }
+        float cmax = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cmax = fmaxf(cmax, v[i]);
+        if (cmax > mx) {
+          int carg = 0;
+#pragma unroll
+          for (int i = 15; i >= 0; --i) carg = v[i] == cmax ? colbase + i : carg;
+          sum = sum * rescale_factor(mx, cmax);
+          mx = cmax;
+          arg = carg;
+        }
+        if (mx != -INFINITY) sum += chunk_sum<16>(v, nml_of(mx));
+        const int yo = yl - colbase;
+        if (yo >= 0 && yo < 16) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) lyv = (i == yo) ? v[i] : lyv;
+          lyset = 1;
+        }
+        const float thr = tv[kFuseT - 1];
+        int qn = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (v[i] > thr) { qv[qn * 256 + tid] = v[i]; qc[qn * 256 + tid] = colbase + i; ++qn; }
+        const int qmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)qn);
+        for (int k = 0; k < qmax; ++k)
+          if (k < qn) topk_insert(tv, ti, qv[k * 256 + tid], qc[k * 256 + tid]);
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CL == 1) mbar_arrive(&tempty[as]);
+        else mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[as]), 0));
+      }
+    }
+    // merge the two halves of the row
+    if (h == 1) {
+      if (nunit > 0) asm volatile("bar.sync %0, %1;" ::"r"(5 + q), "n"(NT) : "memory");  // half 0 read the last one
+      xb[0 * 32 + lane] = mx; xb[1 * 32 + lane] = sum; xb[2 * 32 + lane] = __int_as_float(arg);
+      xb[3 * 32 + lane] = lyv; xb[4 * 32 + lane] = __int_as_float(lyset);
+#pragma unroll
+      for (int k = 0; k < kFuseT; ++k) {
+        xb[(5 + k) * 32 + lane] = tv[k];
+        xb[(5 + kFuseT + k) * 32 + lane] = __int_as_float(ti[k]);
+      }
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "n"(NT) : "memory");
+    if (h == 0) {
+      const float m1 = xb[lane], s1 = xb[32 + lane];
+      const int a1 = __float_as_int(xb[64 + lane]);
+      const float ly1 = xb[96 + lane];
+      const int set1 = __float_as_int(xb[128 + lane]);
+      float M = mx;
+      int A = arg;
+      if (m1 > M) { M = m1; A = a1; }
+      else if (m1 == M && a1 < A) A = a1;
+      float S = 0.f;
+      if (mx != -INFINITY) S += sum * rescale_factor(mx, M);
+      if (m1 != -INFINITY) S += s1 * rescale_factor(m1, M);
+      if (set1) lyv = ly1;
+#pragma unroll
+      for (int k = 0; k < kFuseT; ++k) {
+        const float cv = xb[(5 + k) * 32 + lane];
+        if (cv > tv[kFuseT - 1]) topk_insert(tv, ti, cv, __float_as_int(xb[(5 + kFuseT + k) * 32 + lane]));
+      }
+      asm volatile("bar.arrive %0, %1;" ::"r"(5 + q), "n"(NT) : "memory");
+      if (row < a.N) {
+        const size_t o = (size_t)row * a.K + model;
+        a.top1[o] = A;
+        a.lsum[o] = lsum_of(S, M);
+        a.rmax[o] = M;
+        a.ly[o] = lyv;
+        float4* tv4 = reinterpret_cast<float4*>(a.tv + o * kFuseT);
+#pragma unroll
+        for (int k = 0; k < kFuseT / 4; ++k) tv4[k] = make_float4(tv[4 * k], tv[4 * k + 1], tv[4 * k + 2], tv[4 * k + 3]);
+        uint4* ti4 = reinterpret_cast<uint4*>(a.ti + o * kFuseT);
+#pragma unroll
+        for (int k = 0; k < kFuseT / 8; ++k)
+          ti4[k] = make_uint4((uint32_t)ti[8 * k] | ((uint32_t)ti[8 * k + 1] << 16),
+                              (uint32_t)ti[8 * k + 2] | ((uint32_t)ti[8 * k + 3] << 16),
+                              (uint32_t)ti[8 * k + 4] | ((uint32_t)ti[8 * k + 5] << 16),
+                              (uint32_t)ti[8 * k + 6] | ((uint32_t)ti[8 * k + 7] << 16));
+      }
+    }
+  }
+}
+
 template <int CL, bool PACK, bool FUSED = false>
-__global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
+__global__ void __launch_bounds__(64 + 32 * epi_warps<PACK, FUSED>(), 1)
     gemm_heads_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                       const __grid_constant__ CUtensorMap tmo, const __grid_constant__ CUtensorMap tmo16,
                       const GemmArgs a) {
-  using T = Tile<CL, PACK>;
+  using T = Tile<CL, PACK, FUSED>;
   constexpr int NS = T::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -421,7 +576,7 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
   uint64_t* tempty = bars + 2 * NS + 2;  // [2]  (CL = 2: the leader's counts both epilogues)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 4);
   float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [4][NHP-1][3][32] (packed)
-  constexpr int EPI = PACK ? EPI_PACK : EPI_WARPS;
+  constexpr int EPI = epi_warps<PACK, FUSED>();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mtiles = (a.N + BM - 1) / BM;
@@ -533,23 +688,15 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
     if (PACK) {
       epilogue_packed<CL>(a, tmo16, tfull, tempty, tmem_base, q, (warp - 2) >> 2, lane, stg, xch, ucl0, units, ucls,
                           crank, scale, store_policy);
+    } else if (FUSED) {
+      epilogue_fused<CL>(a, tfull, tempty, tmem_base, q, (warp - 2) >> 2, lane, staging, xch, ucl0, units, ucls, crank,
+                         scale);
     } else
     for (int64_t u = ucl0; u < units; u += ucls) {
       const int mt = (int)(u / a.ng) * CL + crank, model = (int)(u % a.ng);
       const int64_t row = (int64_t)mt * BM + row_in_tile;
       float mx = -INFINITY, sum = 0.f;
       int arg = 0;
-      // FUSED: the label's logit and a descending top-T list (strict '>' insertion: among equal values the
-      // lower column stays first); candidates of a chunk are queued per thread in the (unused) store staging
-      int yl = -1;
-      float lyv = 0.f;
-      float tvr[FUSED ? kFuseT : 1];
-      int tir[FUSED ? kFuseT : 1];
-      if (FUSED) {
-        yl = row < a.N ? a.labels[row] : -1;
-#pragma unroll
-        for (int k = 0; k < kFuseT; ++k) { tvr[k] = -INFINITY; tir[k] = 0; }
-      }
       for (int j = 0; j < a.nt; ++j, ++tc) {
         const int width = min(BN, a.Cp - j * BN);
         const uint32_t as = tc & 1;
@@ -585,38 +732,6 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
             const float nml = nml_of(mx);
             sum += chunk_sum<32>(v, nml);
           }
-          if (FUSED) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) lyv = (colbase + i == yl) ? v[i] : lyv;
-            // queue this chunk's candidates (above the current T-th value) in column order, then insert
-            // them; the warp iterates max over lanes of the queue length, not the union of columns
-            const float thr = tvr[kFuseT - 1];
-            float* qv = reinterpret_cast<float*>(staging);
-            int* qc = reinterpret_cast<int*>(staging + 32 * 128 * 4);
-            const int tid = (warp - 2) * 32 + lane;
-            int qn = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (v[i] > thr) { qv[qn * 128 + tid] = v[i]; qc[qn * 128 + tid] = colbase + i; ++qn; }
-            const int qmax = __reduce_max_sync(0xffffffffu, (unsigned)qn);
-            for (int k = 0; k < qmax; ++k) {
-              if (k < qn) {
-                float cv = qv[k * 128 + tid];
-                int cc = qc[k * 128 + tid];
-#pragma unroll
-                for (int t = 0; t < kFuseT; ++t) {
-                  const bool sw = cv > tvr[t];
-                  const float t1 = tvr[t];
-                  const int t2 = tir[t];
-                  tvr[t] = sw ? cv : t1;
-                  tir[t] = sw ? cc : t2;
-                  cv = sw ? t1 : cv;
-                  cc = sw ? t2 : cc;
-                }
-              }
-            }
-            continue;
-          }
           // stage 32 rows x 32 cols (128B-swizzled) and store with TMA. (Coalesced st.global.cs
           // from the same staging box measured 18% slower for the whole kernel: DESIGN.md §6.)
           uint8_t* buf = stg + (nstore & 1) * STG_BYTES;
@@ -647,22 +762,7 @@ __global__ void __launch_bounds__(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), 1)
         a.top1[row * a.K + model] = arg;
         a.lsum[row * a.K + model] = lsum_of(sum, mx);  // relative to the row max
         a.rmax[row * a.K + model] = mx;
-        if (FUSED) {
-          const size_t o = (size_t)row * a.K + model;
-          a.ly[o] = lyv;
-          float4* tv4 = reinterpret_cast<float4*>(a.tv + o * kFuseT);
-#pragma unroll
-          for (int k = 0; k < kFuseT / 4; ++k) tv4[k] = make_float4(tvr[4 * k], tvr[4 * k + 1], tvr[4 * k + 2], tvr[4 * k + 3]);
-          uint4* ti4 = reinterpret_cast<uint4*>(a.ti + o * kFuseT);
-#pragma unroll
-          for (int k = 0; k < kFuseT / 8; ++k)
-            ti4[k] = make_uint4((uint32_t)tir[8 * k] | ((uint32_t)tir[8 * k + 1] << 16),
-                                (uint32_t)tir[8 * k + 2] | ((uint32_t)tir[8 * k + 3] << 16),
-                                (uint32_t)tir[8 * k + 4] | ((uint32_t)tir[8 * k + 5] << 16),
-                                (uint32_t)tir[8 * k + 6] | ((uint32_t)tir[8 * k + 7] << 16));
-        }
       }
-      if (FUSED) __syncwarp();  // the next unit's queue writes must not overtake this unit's reads
     }
     if (lane == 0) tma_store_wait_all();
     __syncwarp();
@@ -753,12 +853,12 @@ static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count
   const CUtensorMap& mo = *reinterpret_cast<const CUtensorMap*>(p.tmap_out);
   const CUtensorMap& m16 = *reinterpret_cast<const CUtensorMap*>(p.tmap_out16);
   cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<CL, PACK, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Tile<CL, PACK>::SMEM_BYTES);
+                                       Tile<CL, PACK, FUSED>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int64_t units = ((p.N + CL * BM - 1) / (CL * BM)) * a.ng;
   if (CL == 1) {
     const int grid = (int)(units < sm_count ? units : sm_count);
-    gemm_heads_kernel<CL, PACK, FUSED><<<grid, 64 + 32 * (PACK ? EPI_PACK : EPI_WARPS), Tile<CL, PACK>::SMEM_BYTES, st>>>(
+    gemm_heads_kernel<CL, PACK, FUSED><<<grid, 64 + 32 * epi_warps<PACK, FUSED>(), Tile<CL, PACK, FUSED>::SMEM_BYTES, st>>>(
         mx, mw, mo, m16, a);
     return cudaGetLastError();
   }
@@ -766,8 +866,8 @@ static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count
   const int64_t clusters = units < sm_count / 2 ? units : sm_count / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * clusters));
-  cfg.blockDim = dim3(64 + 32 * (PACK ? EPI_PACK : EPI_WARPS));
-  cfg.dynamicSmemBytes = Tile<CL, PACK>::SMEM_BYTES;
+  cfg.blockDim = dim3(64 + 32 * epi_warps<PACK, FUSED>());
+  cfg.dynamicSmemBytes = Tile<CL, PACK, FUSED>::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -279,7 +279,10 @@ cudaError_t launch_vote_classify(const VoteParams& p, cudaStream_t st, int32_t* 
 
 size_t vote_warp_smem_per_warp(const VoteParams& p) { return vote_avg_smem_per_warp(p); }
 int vote_warp_threads() { return WT; }
-int vote_warp_min_blocks() { return 5; }
+#ifndef RK_AVG_MINB
+#define RK_AVG_MINB 6
+#endif
+int vote_warp_min_blocks() { return RK_AVG_MINB; }
 
 cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
                              int32_t* st_top, float* st_lsum, float* st_max, int sm_count) {
