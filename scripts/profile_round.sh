@@ -1,6 +1,6 @@
 # Round profiling: (1) launch list of the bench command (c4), (2) --set full of the GEMM,
 # (3) of the K=8 vote kernels, (4) of the K=12 vote kernels (c5 shape).
-R=${ROUND:-r01}
+R=${ROUND:-r02}
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv \
   python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${R}_launches_bench.json 2> gpurun_out/${R}_launches.err
 echo "launches rc=$?"
@@ -16,3 +16,6 @@ echo "k12 rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_heads -c 1 -o gpurun_out/${R}_gemm12 \
   python scripts/prof_vote.py --K 12 --C 100 --N 131072 --gemm 1024 --reps 1 > gpurun_out/${R}_gemm12.log 2>&1
 echo "gemm12 rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gemm_heads|vote_sparse|vote_classify|gather_rows|vote_average" -c 6 -o gpurun_out/${R}_fused \
+  python scripts/prof_fused.py --N 131072 --reps 1 > gpurun_out/${R}_fused.log 2>&1
+echo "fused rc=$?"
