@@ -90,8 +90,11 @@ struct WRec {  // one sample's vote record (warp-private)
   int32_t no;
   uint32_t mo[KM];
 };
+#ifndef RK_GC_MINB
+#define RK_GC_MINB 2
+#endif
 template <int NWL, bool STATS>
-__global__ void __launch_bounds__(BT, 2) vote_group_classify_kernel(const VoteParams p, int32_t* work,
+__global__ void __launch_bounds__(BT, RK_GC_MINB) vote_group_classify_kernel(const VoteParams p, int32_t* work,
                                                                     unsigned int* work_count, int32_t* st_top,
                                                                     float* st_lsum, float* st_max) {
   __shared__ uint32_t GE[32 * 8];        // GE[L][c] = {lo in [0,32) : popc(lo & L) >= c}
@@ -392,7 +395,7 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
   cudaError_t e;
   {
     const int64_t nb = (p.N + SB - 1) / SB;
-    const int grid = (int)(nb < (int64_t)sm_count * 2 ? nb : (int64_t)sm_count * 2);
+    const int grid = (int)(nb < (int64_t)sm_count * RK_GC_MINB ? nb : (int64_t)sm_count * RK_GC_MINB);
     constexpr int NWL = NK / 4 > 0 ? NK / 4 : 1;  // words per lane: 2^(K-5) / 32 (K = 9: half the lanes idle)
     const int dsm = (NWB << p.K) + 16;  // + padding: the copy-out reads one word past a row
     if (p.lsum_in) {
