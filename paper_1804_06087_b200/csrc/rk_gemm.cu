@@ -607,7 +607,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<PACK, FUSED>(), 1)
   }
   tc_fence_before();
   if (CL > 1) cluster_sync_all();  // both CTAs' barriers and TMEM exist before any cross-CTA signal
-  else __syncthreads();
+  __syncthreads();  // (CL = 2: implied by the cluster barrier; explicit so racecheck sees the ordering of
+                    // the tcgen05.alloc write of tmem_slot before its reads)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
