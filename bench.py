@@ -182,7 +182,7 @@ def workload_stats(ctx, labels, K, C, nsamp=4096):
     ns = min(nsamp, out["N"])
 
     class _View:  # the library's logits workspace as a torch view (no copy on the device)
-        __cuda_array_interface__ = {"shape": (ns, K, ldc), "typestr": "<f4", "data": (out["logits"], True),
+        __cuda_array_interface__ = {"shape": (ns, K, ldc), "typestr": "<f4", "data": (out["logits"], False),
                                     "version": 3}
 
     torch.cuda.synchronize()

@@ -280,6 +280,22 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // operand byte crosses L2 -> smem once per pair instead of once per CTA (B traffic halved, smem
 // stage 32 KB instead of 48 KB -> 6 stages). Each CTA's TMEM receives its own 128 rows x N
 // accumulator and its epilogue is unchanged.
+// Accumulator stage `as` drained by this epilogue warp. CL = 1: one arrive per warp. CL = 2: the pair's
+// barrier lives in the leader, whose MMAs refill both CTAs' TMEM: the leader's warps arrive locally, the
+// peer's warps meet at a named barrier and ONE thread arrives remotely (release.cluster arrives are
+// costly: one per warp and tile was 20 % of the packed epilogue's stall samples).
+template <int CL, int EPI>
+__device__ __forceinline__ void release_tmem_stage(uint64_t* tempty, uint32_t as, int crank, int lane) {
+  tc_fence_before();
+  __syncwarp();
+  if (CL == 1 || crank == 0) {
+    if (lane == 0) mbar_arrive(&tempty[as]);
+  } else {
+    asm volatile("bar.sync 12, %0;" ::"n"(EPI * 32) : "memory");
+    if (threadIdx.x == 64) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[as]), 0));  // first epilogue thread
+  }
+}
+
 // Packed-mode epilogue (see gemm_heads_kernel): 16-column blocks of the flattened column space; the
 // two warps of a TMEM lane quarter (half h) take alternating blocks and keep per-model online
 // (max, lowest argmax, sum-exp); at each model boundary half 1 hands its part to half 0 (named
@@ -394,12 +410,7 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
         }
         ++nstore;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CL == 1) mbar_arrive(&tempty[as]);
-        else mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[as]), 0));
-      }
+      release_tmem_stage<CL, EPI_PACK>(tempty, as, crank, lane);
     }
     close(cur);
   }
@@ -499,12 +510,7 @@ __device__ __forceinline__ void epilogue_fused(const GemmArgs& a, uint64_t* tful
           if (k < qn) topk_insert(tv, ti, qv[k * 256 + tid], qc[k * 256 + tid]);
         __syncwarp();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CL == 1) mbar_arrive(&tempty[as]);
-        else mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[as]), 0));
-      }
+      release_tmem_stage<CL, FUSED_EPI>(tempty, as, crank, lane);
     }
     // merge the two halves of the row
     if (h == 1) {
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<PACK, FUSED>(), 1)
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI * CL); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], CL == 1 ? EPI : EPI + 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmx) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmw) : "memory");
@@ -752,12 +758,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<PACK, FUSED>(), 1)
           }
           ++nstore;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {  // accumulator stage drained (CL = 2: signal the leader, whose MMAs refill it)
-          if (CL == 1) mbar_arrive(&tempty[as]);
-          else mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[as]), 0));
-        }
+        release_tmem_stage<CL, EPI_WARPS>(tempty, as, crank, lane);
       }
       if (row < a.N) {
         a.top1[row * a.K + model] = arg;
