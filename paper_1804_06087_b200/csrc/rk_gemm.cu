@@ -354,6 +354,9 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
       ++nclose;
     };
     uint32_t blk = 0;  // global 16-column block counter of this unit (dealt round-robin to the parts)
+    // gc / Cp by a multiply-shift: with inv = ceil(2^20 / Cp), floor(gc * inv / 2^20) = floor(gc / Cp) for
+    // gc < 2^12, Cp <= 128 (the error gc * (inv - 2^20 / Cp) / 2^20 < 1/256 is below the 1/Cp spacing)
+    const uint32_t cp_inv = ((1u << 20) + (uint32_t)a.Cp - 1u) / (uint32_t)a.Cp;
     for (int j = 0; j < a.nt; ++j, ++tc) {
       const int width = min(BN, a.gcols - j * BN);
       const uint32_t as = tc & 1;
@@ -362,7 +365,7 @@ __device__ __forceinline__ void epilogue_packed(const GemmArgs& a, const CUtenso
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       for (int c0 = 0; c0 < width; c0 += 16, ++blk) {
         const int gc = j * BN + c0;
-        const int model = gc / a.Cp, cm = gc - model * a.Cp;
+        const int model = (int)(((uint32_t)gc * cp_inv) >> 20), cm = gc - model * a.Cp;
         if (model != cur) {  // first block of the next model: close the previous one
           close(cur);
           mx = -INFINITY; sum = 0.f; arg = 0x7fffffff; cur = model;
