@@ -51,68 +51,99 @@ __global__ void overdue_kernel(const MomentParams p, unsigned int* err) {
   int64_t tot = 0;
   int64_t start[kMaxB];
   for (int bi = 0; bi < p.nB; ++bi) { start[bi] = tot; tot += (p.N / p.B[bi]) * p.nR; }
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < tot; w += (int64_t)gridDim.x * blockDim.x) {
+  // warp-uniform loop: consecutive work items of a warp share (b, r) almost always, so the per-(r, b, m)
+  // sums are reduced across the warp first and added with one shared atomic (the per-lane shared
+  // atomics on one address were 70 % of this kernel's stall samples at the c5 shape)
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < tot;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = base + lane;
+    const bool act = w < tot;
     int bi = 0;
     while (bi + 1 < p.nB && w >= start[bi + 1]) ++bi;
-    const int64_t rem = w - start[bi];
+    const int64_t rem = act ? w - start[bi] : 0;
     const int64_t nb = p.N / p.B[bi];
     const int r = (int)(rem / nb);
     const int64_t jl = rem - (int64_t)r * nb;
     const int b = p.B[bi];
-    const int64_t s0 = jl * b;  // local index of the batch's first request
-    const double rate = p.rates[r];
-    const double inv = __drcp_rn(rate);
-    const int64_t tl = arrival_at(p.arrival, s0 + b - 1, p.goff + s0 + b - 1, rate);
-    if (p.arrival && r == 0) {  // arrivals must be non-decreasing inside a batch (FIFO)
-      for (int i = 1; i < b; ++i)
-        if (p.arrival[s0 + i] < p.arrival[s0 + i - 1]) { atomicOr(err + 2, 1u); break; }
-    }
     int cnt[kMaxK];
-    int64_t fm[kMaxK];  // completion time of the batch when m is the slowest member
-    for (int m = 0; m < p.K; ++m)
-      fm[m] = p.fin ? p.fin[p.fin_off[bi] + ((int64_t)r * p.K + m) * nb + jl] : tl + p.lat[m * p.nB + bi];
-    for (int m = 0; m < p.K; ++m) {
-      // overdue <=> l(s) = F - t_s > tau <=> t_s < F - tau ; t_s non-decreasing in s. F = t_last + c
-      // (reading Q8) or the FIFO finish time (queue mode, reading Q15)
-      const int64_t thr = fm[m] - p.tau;
-      int lo = 0;  // first i with t_i >= thr
-      if (p.arrival) {  // caller arrivals: binary search
-        int hi = b;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          const int64_t tm = arrival_at(p.arrival, s0 + mid, p.goff + s0 + mid, rate);
-          if (tm < thr) lo = mid + 1; else hi = mid;
-        }
-      } else {  // uniform arrivals (reading Q9): closed-form guess, then exact local correction, so the
-                // result is the same first index the search finds (t non-decreasing in s)
-        const double est = ceil((double)thr * rate * 1e-9) - (double)(p.goff + s0);
-        lo = est <= 0.0 ? 0 : (est >= (double)b ? b : (int)est);
-        while (lo > 0 && arrival_uniform(p.goff + s0 + lo - 1, rate, inv) >= thr) --lo;
-        while (lo < b && arrival_uniform(p.goff + s0 + lo, rate, inv) < thr) ++lo;
+    unsigned long long ex[kMaxK];
+#pragma unroll
+    for (int m = 0; m < kMaxK; ++m) { cnt[m] = 0; ex[m] = 0; }
+    if (act) {
+      const int64_t s0 = jl * b;  // local index of the batch's first request
+      const double rate = p.rates[r];
+      const double inv = __drcp_rn(rate);
+      const int64_t tl = arrival_at(p.arrival, s0 + b - 1, p.goff + s0 + b - 1, rate);
+      if (p.arrival && r == 0) {  // arrivals must be non-decreasing inside a batch (FIFO)
+        for (int i = 1; i < b; ++i)
+          if (p.arrival[s0 + i] < p.arrival[s0 + i - 1]) { atomicOr(err + 2, 1u); break; }
       }
-      cnt[m] = lo;
-      atomicAdd(&so[(r * p.nB + bi) * p.K + m], (unsigned long long)lo);
-      if (p.ovd) p.ovd[p.ovd_off[bi] + (jl * p.K + m) * p.ovd_nrp + r] = (uint16_t)lo;
-    }
-    if (p.want_exceed) {
-      // E = sum_{i < cnt} (tl - t_i + c - tau): one sweep with prefix sums of t_i
-      int maxc = 0;
-      for (int m = 0; m < p.K; ++m) maxc = cnt[m] > maxc ? cnt[m] : maxc;
-      int ord[kMaxK];  // models in increasing overdue count (insertion sort; K <= 12)
+      int64_t fm[kMaxK];  // completion time of the batch when m is the slowest member
+      for (int m = 0; m < p.K; ++m)
+        fm[m] = p.fin ? p.fin[p.fin_off[bi] + ((int64_t)r * p.K + m) * nb + jl] : tl + p.lat[m * p.nB + bi];
       for (int m = 0; m < p.K; ++m) {
-        int k = m;
-        while (k > 0 && cnt[ord[k - 1]] > cnt[m]) { ord[k] = ord[k - 1]; --k; }
-        ord[k] = m;
-      }
-      int64_t pre = 0;
-      int k = 0;
-      for (int i = 0; i <= maxc; ++i) {
-        for (; k < p.K && cnt[ord[k]] == i; ++k) {
-          const int m = ord[k];
-          const unsigned long long e = (unsigned long long)((int64_t)i * (fm[m] - p.tau) - pre);
-          atomicAdd(&se[(r * p.nB + bi) * p.K + m], e);
+        // overdue <=> l(s) = F - t_s > tau <=> t_s < F - tau ; t_s non-decreasing in s. F = t_last + c
+        // (reading Q8) or the FIFO finish time (queue mode, reading Q15)
+        const int64_t thr = fm[m] - p.tau;
+        int lo = 0;  // first i with t_i >= thr
+        if (p.arrival) {  // caller arrivals: binary search
+          int hi = b;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const int64_t tm = arrival_at(p.arrival, s0 + mid, p.goff + s0 + mid, rate);
+            if (tm < thr) lo = mid + 1; else hi = mid;
+          }
+        } else {  // uniform arrivals (reading Q9): closed-form guess, then exact local correction, so the
+                  // result is the same first index the search finds (t non-decreasing in s)
+          const double est = ceil((double)thr * rate * 1e-9) - (double)(p.goff + s0);
+          lo = est <= 0.0 ? 0 : (est >= (double)b ? b : (int)est);
+          while (lo > 0 && arrival_uniform(p.goff + s0 + lo - 1, rate, inv) >= thr) --lo;
+          while (lo < b && arrival_uniform(p.goff + s0 + lo, rate, inv) < thr) ++lo;
         }
-        if (i < maxc) pre += p.arrival ? p.arrival[s0 + i] : arrival_uniform(p.goff + s0 + i, rate, inv);
+        cnt[m] = lo;
+        if (p.ovd) p.ovd[p.ovd_off[bi] + (jl * p.K + m) * p.ovd_nrp + r] = (uint16_t)lo;
+      }
+      if (p.want_exceed) {
+        // E = sum_{i < cnt} (tl - t_i + c - tau): one sweep with prefix sums of t_i
+        int maxc = 0;
+        for (int m = 0; m < p.K; ++m) maxc = cnt[m] > maxc ? cnt[m] : maxc;
+        int ord[kMaxK];  // models in increasing overdue count (insertion sort; K <= 12)
+        for (int m = 0; m < p.K; ++m) {
+          int k = m;
+          while (k > 0 && cnt[ord[k - 1]] > cnt[m]) { ord[k] = ord[k - 1]; --k; }
+          ord[k] = m;
+        }
+        int64_t pre = 0;
+        int k = 0;
+        for (int i = 0; i <= maxc; ++i) {
+          for (; k < p.K && cnt[ord[k]] == i; ++k) {
+            const int m = ord[k];
+            ex[m] = (unsigned long long)((int64_t)i * (fm[m] - p.tau) - pre);
+          }
+          if (i < maxc) pre += p.arrival ? p.arrival[s0 + i] : arrival_uniform(p.goff + s0 + i, rate, inv);
+        }
+      }
+    }
+    const int key = act ? r * p.nB + bi : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    if (grp == 0xffffffffu) {  // the whole warp on one (r, b): warp sums, one atomic per model
+#pragma unroll
+      for (int m = 0; m < kMaxK; ++m) {
+        if (m >= p.K) break;
+        const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)cnt[m]);
+        unsigned long long e = ex[m];
+        if (p.want_exceed)
+          for (int off = 16; off; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+        if (lane == 0) {
+          atomicAdd(&so[key * p.K + m], (unsigned long long)c);
+          if (p.want_exceed) atomicAdd(&se[key * p.K + m], e);
+        }
+      }
+    } else if (act) {
+      for (int m = 0; m < p.K; ++m) {
+        atomicAdd(&so[key * p.K + m], (unsigned long long)cnt[m]);
+        if (p.want_exceed) atomicAdd(&se[key * p.K + m], ex[m]);
       }
     }
   }

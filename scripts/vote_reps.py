@@ -30,5 +30,5 @@ for i in range(R):
     ctx.subset_stats(lab, cfg)
     ks = ctx.kernel_stats()
     cur = {k: v["ms"] for k, v in ks.items()}
-    print(i, " ".join(f"{k}={cur[k] - prev.get(k, 0):.3f}" for k in ("gemm_heads_tcgen05", "vote_subsets", "labelled_moments")))
+    print(i, " ".join(f"{k}={cur[k] - prev.get(k, 0):.3f}" for k in ("gemm_heads_tcgen05", "vote_subsets", "labelled_moments", "overdue_moments")))
     prev = cur
