@@ -67,3 +67,25 @@ def test_head_workload_bands():
     assert 5.5 < sc < 11.0, sc
     gain = (P.mean(1).argmax(1) == y).mean() - acc.max()
     assert 0.005 < gain < 0.07, gain
+
+
+def test_head_workload_bands_c5():
+    """c5's heads (K = 12, C = 100, D = 1024) against SURVEY.md §8(d)'s K = 12 row: per-model top-1 in the
+    0.68-0.83 range, about half the samples unanimous, mean max-softmax ~0.76, |S_c| ~8."""
+    K, C, D, N = 12, 100, 1024, 1500
+    psig, f0, df, sh = gen.head_params(D, C, K)
+    y = gen.labels(22, 0, N, C)
+    X = gen.bf16_to_f64(gen.features(22, 0, N, D, C, psig, False, y=y)).astype(np.float32)
+    W = gen.bf16_to_f64(gen.weights(1000, K, C, D, f0, df, False)).astype(np.float32)
+    b = gen.bias(2000, K, C, False).astype(np.float64)
+    L = np.einsum("nd,mcd->nmc", X, W, optimize=True).astype(np.float64) * 2.0**sh + b[None]
+    top = L.argmax(2)
+    acc = (top == y[:, None]).mean(0)
+    assert 0.68 < acc.min() and acc.max() < 0.85, acc
+    una = (top == top[:, :1]).all(1).mean()
+    assert 0.42 < una < 0.58, una
+    P = np.exp(L - L.max(2, keepdims=True))
+    P /= P.sum(2, keepdims=True)
+    assert 0.70 < P.max(2).mean() < 0.85
+    sc = (P >= (P.max(2).min(1) / K)[:, None, None]).any(1).sum(1).mean()
+    assert 5.0 < sc < 10.0, sc
