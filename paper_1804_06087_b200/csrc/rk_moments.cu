@@ -444,17 +444,52 @@ int64_t ovd_elems(int nB, const int* B, int nR, int K, int64_t N, int64_t* off) 
 // chunk (L = B[NB-1] samples) holds G0 = 2^(NB-1) groups, so a thread loads its subset's G0 group counts
 // into registers once and forms every batch size's correct counts as a pairwise-sum tree, each batch
 // end costing one 128-bit shared load of the staged overdue counts (u32 per rate) and NRP multiply-adds.
-// QC chunks are staged per pair of barriers.
+// QC chunks are staged per round; the overdue counts of round i+1 are copied to shared memory with
+// cp.async (8-byte pieces, u16 as stored) while round i is computed, so the staging latency is hidden.
 constexpr int QC = 4;
 constexpr int kQNestedBlocksPerSM = 4;
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// stage chunks qq .. qq+QC-1: level bi's region is [QC][nb][K][NRP] u16, contiguous in ovd for
+// consecutive chunks; entries past the last complete batch (reading Q13) or past q1 are zero-filled
+template <int NRP, int NB>
+__device__ __forceinline__ void q_stage(const QParams& p, const QConst& qc, uint16_t* buf, int64_t qq, int64_t q1) {
+  constexpr int G0 = 1 << (NB - 1);
+  const int K = p.K;
+  int soff = 0;  // u16 offset of level bi in the buffer
+#pragma unroll
+  for (int bi = 0; bi < NB; ++bi) {
+    const int nb = G0 >> bi;
+    const int64_t per = (int64_t)nb * K * NRP;              // u16 per chunk and level
+    const int64_t lim = min(qc.nbat[bi] * (int64_t)K * NRP,  // valid u16 of this level (complete batches,
+                            q1 * per);                       // chunks < q1)
+    const int64_t g0 = qq * per;
+    const int n8 = (int)(QC * per / 4);                      // 8-byte pieces (4 u16)
+    const uint16_t* src = p.ovd + p.ovd_off[bi];
+    for (int k = threadIdx.x; k < n8; k += QT) {
+      const int64_t g = g0 + 4 * (int64_t)k;
+      uint16_t* d = buf + soff + 4 * k;
+      if (g + 4 <= lim) cp_async8(d, src + g);
+      else *reinterpret_cast<uint2*>(d) = make_uint2(0u, 0u);  // (per and lim are multiples of 4)
+    }
+    soff += (int)(QC * per);
+  }
+}
+
 template <int NRP, int NB>
 __global__ void __launch_bounds__(QT, kQNestedBlocksPerSM)
     q_nested_kernel(const QParams p, const QConst qc, int64_t chunks_per_block, int flush) {
   constexpr int G0 = 1 << (NB - 1);   // groups (= smallest batches) per chunk
   constexpr int TOT = 2 * G0 - 1;     // batches of every size per chunk
-  extern __shared__ unsigned long long qacc[];  // [nR * NB][QT], then u32 [QC][TOT][K][NRP]
-  uint32_t* so = reinterpret_cast<uint32_t*>(qacc + (size_t)p.nR * NB * QT);
-  const int K = p.K, KR = K * NRP;
+  extern __shared__ unsigned long long qacc[];  // [nR * NB][QT], then u16 [2][QC * TOT * K * NRP]
+  const int K = p.K;
+  const int BUF = QC * TOT * K * NRP;  // u16 per staging buffer
+  uint16_t* sbuf = reinterpret_cast<uint16_t*>(qacc + (size_t)p.nR * NB * QT);
   const int v1 = blockIdx.x * QT + threadIdx.x;
   const bool own = v1 < p.S;
   for (int i = 0; i < p.nR * NB; ++i) qacc[i * QT + threadIdx.x] = 0;
@@ -473,79 +508,67 @@ __global__ void __launch_bounds__(QT, kQNestedBlocksPerSM)
   const uint8_t* gp = p.grp + (own ? v1 : 0);
   int since = 0;
   unsigned long long csum = 0;  // sum of the subset's group counts (p.cnt_vote)
-  for (int64_t qq = q0; qq < q1; qq += QC) {
+  if (q0 < q1) q_stage<NRP, NB>(p, qc, sbuf, q0, q1);
+  cp_async_commit();
+  int cur = 0;
+  for (int64_t qq = q0; qq < q1; qq += QC, cur ^= 1) {
+    if (qq + QC < q1) q_stage<NRP, NB>(p, qc, sbuf + (cur ^ 1) * BUF, qq + QC, q1);
+    cp_async_commit();
+    cp_async_wait1();  // this round's copies have landed (the next round's stay in flight)
     __syncthreads();
-    {  // stage overdue counts of chunks qq .. qq+QC-1 as u32 (one NRP-vector per (batch, model)); a level's
-       // batches of a chunk are contiguous in ovd; incomplete batches contribute 0 (reading Q13)
-      using V = typename OVec<NRP>::T;
-      int base = 0;
-#pragma unroll
-      for (int bi = 0; bi < NB; ++bi) {
-        const int nb = G0 >> bi;
-        for (int w = threadIdx.x; w < QC * nb * K; w += QT) {
-          const int c = w / (nb * K), rem = w - c * nb * K;  // rem = j * K + m
-          const int64_t jg = (qq + c) * (int64_t)nb + rem / K;
-          union { V v; uint16_t h[NRP]; } o;
-          if (qq + c < q1 && jg < qc.nbat[bi]) o.v = reinterpret_cast<const V*>(p.ovd + p.ovd_off[bi] + jg * KR)[rem % K];
-          else o.v = V{};
-          uint32_t* d = so + ((size_t)c * TOT + base) * KR + (size_t)rem * NRP;
-#pragma unroll
-          for (int r = 0; r < NRP; r += 4) *reinterpret_cast<uint4*>(d + r) = make_uint4(o.h[r], o.h[r + 1], o.h[r + 2], o.h[r + 3]);
-        }
-        base += nb;
-      }
-    }
-    __syncthreads();
-    if (!own) continue;
-    unsigned int nx[G0];  // group counts of the next chunk, loaded one chunk ahead
-#pragma unroll
-    for (int i = 0; i < G0; ++i) {
-      const int64_t g = qq * G0 + i;
-      nx[i] = g < ngroups ? gp[g * p.S] : 0u;
-    }
-#pragma unroll 1
-    for (int c = 0; c < QC; ++c) {
-      const int64_t q = qq + c;
-      if (q >= q1) break;
-      unsigned int sv[G0];
+    if (own) {
+      const uint16_t* sb = sbuf + cur * BUF;
+      unsigned int nx[G0];  // group counts of the next chunk, loaded one chunk ahead
 #pragma unroll
       for (int i = 0; i < G0; ++i) {
-        sv[i] = nx[i];
-        const int64_t g = (q + 1) * G0 + i;
-        nx[i] = (c + 1 < QC && g < ngroups) ? gp[g * p.S] : 0u;
+        const int64_t g = qq * G0 + i;
+        nx[i] = g < ngroups ? gp[g * p.S] : 0u;
       }
-      const uint32_t* sc = so + (size_t)c * TOT * KR;
-      int base = 0;
+#pragma unroll 1
+      for (int c = 0; c < QC; ++c) {
+        const int64_t q = qq + c;
+        if (q >= q1) break;
+        unsigned int sv[G0];
 #pragma unroll
-      for (int bi = 0; bi < NB; ++bi) {
-        const int nb = G0 >> bi;
-#pragma unroll
-        for (int j = 0; j < nb; ++j) {
-          if (NRP == 4) {
-            const uint4 o = *reinterpret_cast<const uint4*>(sc + (base + j) * KR + mo[bi]);
-            acc[0][bi] += sv[j] * o.x; acc[1][bi] += sv[j] * o.y;
-            acc[2][bi] += sv[j] * o.z; acc[3][bi] += sv[j] * o.w;
-          } else {
-#pragma unroll
-            for (int r = 0; r < NRP; ++r) acc[r][bi] += sv[j] * sc[(base + j) * KR + mo[bi] + r];
-          }
+        for (int i = 0; i < G0; ++i) {
+          sv[i] = nx[i];
+          const int64_t g = (q + 1) * G0 + i;
+          nx[i] = (c + 1 < QC && g < ngroups) ? gp[g * p.S] : 0u;
         }
-        base += nb;
+        int soff = 0;
 #pragma unroll
-        for (int j = 0; j < nb / 2; ++j) sv[j] = sv[2 * j] + sv[2 * j + 1];  // next batch size
-      }
-      csum += sv[0];  // the last level is the whole chunk
-      if (++since == flush || q + 1 == q1) {  // spill the u32 accumulators
-        since = 0;
+        for (int bi = 0; bi < NB; ++bi) {
+          const int nb = G0 >> bi;
+          const uint16_t* lv = sb + soff + ((size_t)c * nb) * K * NRP + mo[bi];
 #pragma unroll
-        for (int bi = 0; bi < NB; ++bi)
+          for (int j = 0; j < nb; ++j) {
+            if (NRP == 4) {
+              const uint2 o = *reinterpret_cast<const uint2*>(lv + (size_t)j * K * NRP);
+              acc[0][bi] += sv[j] * (o.x & 0xffffu); acc[1][bi] += sv[j] * (o.x >> 16);
+              acc[2][bi] += sv[j] * (o.y & 0xffffu); acc[3][bi] += sv[j] * (o.y >> 16);
+            } else {
 #pragma unroll
-          for (int r = 0; r < NRP; ++r) {
-            if (r < p.nR) qacc[(r * NB + bi) * QT + threadIdx.x] += acc[r][bi];
-            acc[r][bi] = 0;
+              for (int r = 0; r < NRP; ++r) acc[r][bi] += sv[j] * (unsigned int)lv[(size_t)j * K * NRP + r];
+            }
           }
+          soff += QC * nb * K * NRP;
+#pragma unroll
+          for (int j = 0; j < nb / 2; ++j) sv[j] = sv[2 * j] + sv[2 * j + 1];  // next batch size
+        }
+        csum += sv[0];  // the last level is the whole chunk
+        if (++since == flush || q + 1 == q1) {  // spill the u32 accumulators
+          since = 0;
+#pragma unroll
+          for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+            for (int r = 0; r < NRP; ++r) {
+              if (r < p.nR) qacc[(r * NB + bi) * QT + threadIdx.x] += acc[r][bi];
+              acc[r][bi] = 0;
+            }
+        }
       }
     }
+    __syncthreads();  // every thread is done with this buffer before the next round's copies land in it
   }
   if (!own) return;
   if (p.cnt_vote && csum) atomicAdd(p.cnt_vote + v1, csum);
@@ -618,7 +641,7 @@ cudaError_t launch_q(const QParams& p, int sm_count, cudaStream_t st) {
   for (int bi = 1; bi < p.nB; ++bi) nested = nested && p.B[bi] == 2 * p.B[bi - 1];
   if (nested && !getenv("RK_Q_GENERIC")) {  // env: tests compare against the generic kernel
     const int G0 = 1 << (p.nB - 1);
-    const size_t nsmem = acc + sizeof(uint32_t) * (size_t)QC * (2 * G0 - 1) * p.K * nrp;
+    const size_t nsmem = acc + 2 * sizeof(uint16_t) * (size_t)QC * (2 * G0 - 1) * p.K * nrp;
     int nper = (int)((200 * 1024) / (nsmem + 1024));
     nper = nper < 1 ? 1 : (nper > kQNestedBlocksPerSM ? kQNestedBlocksPerSM : nper);
     int64_t nr_ = ((int64_t)sm_count * nper) / slices;
