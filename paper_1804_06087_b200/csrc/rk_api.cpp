@@ -1263,7 +1263,7 @@ rk_status rk_ac_rollout(rk_ctx* ctx, const rk_reward_cfg* cfg, const double* acc
   CK(cudaStreamSynchronize(st));
   if (herr & 4u) return fail(ctx, RK_ENONFINITE, "the policy's probabilities are not finite (diverged parameters)");
   if (herr & 2u) return fail(ctx, RK_EINVAL, "a forced action is outside [0, (2^K - 1) * nB)");
-  if (herr & 1u) return fail(ctx, RK_EINVAL, "an episode ran past the end of the arrival array (Narr)");
+  if (herr & 1u) return fail(ctx, RK_EINVAL, "an episode starts outside or runs past the end of the arrival array (Narr)");
   return RK_OK;
 }
 

@@ -81,6 +81,10 @@ __global__ void __launch_bounds__(32 * RW) ac_rollout_kernel(const RLParams p) {
   const Net net(p.params, F, H, A);
   const int per = (A + 31) / 32, a0 = min(A, lane * per), a1 = min(A, a0 + per);
   int64_t head = p.h0[e];
+  if (head < 0 || head >= p.Narr) {  // an episode start outside the arrival array
+    if (lane == 0) atomicOr(p.err, 1u);
+    return;
+  }
   int64_t t = p.arrival[head];
   int64_t free_at[kMaxK];
   for (int m = 0; m < K; ++m) free_at[m] = t;
