@@ -147,3 +147,21 @@ def test_training_improves_return(rk):
     first = curve[0]["return"]
     last = np.mean([c["return"] for c in curve[-5:]])
     assert last > first, (first, last)
+
+
+def test_rollout_errors(rk):
+    K, B = 3, [16, 32, 48, 64]
+    ctx, arr, cfg, acc, ac = make(rk, K, B, N=20_000, n=4)
+    F, A, P = ctx.ac_dims(len(B), ac)
+    params = torch.zeros(P, device="cuda")
+    with pytest.raises(rk.RkError):  # an episode start past the arrival array
+        ctx.ac_rollout(cfg, acc, arr, arr.numel(), ac, params, 1, torch.tensor([arr.numel() + 5]).cuda(), traj(1, 4, F))
+    with pytest.raises(rk.RkError):  # an episode that runs out of arrivals
+        ctx.ac_rollout(cfg, acc, arr, arr.numel(), ac, params, 1, torch.tensor([arr.numel() - 20]).cuda(), traj(1, 4, F))
+    with pytest.raises(rk.RkError):  # a forced action outside the action space
+        ctx.ac_rollout(cfg, acc, arr, arr.numel(), ac, params, 1, torch.tensor([0]).cuda(), traj(1, 4, F),
+                       forced=torch.full((1, 4), A, dtype=torch.int32).cuda())
+    bad = dict(ac, H=65)
+    with pytest.raises(rk.RkError):  # hidden layer wider than the kernels' register tiles
+        ctx.ac_dims(len(B), bad) and ctx.ac_rollout(cfg, acc, arr, arr.numel(), bad, params, 1,
+                                                    torch.tensor([0]).cuda(), traj(1, 4, F))
