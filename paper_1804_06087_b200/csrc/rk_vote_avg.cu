@@ -169,20 +169,13 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
       for (int m = 0; m < K; ++m)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p.logits + (nnext * K + m) * p.ldc + lane * 32));
 #endif
-#ifdef RK_AVG_CURAHEAD
-    // (experiment) the current sample's rows 1..K-1 and the next sample's row 0 go to L2 at once
-    if (lane * 32 < p.ldc) {
-      for (int m = 1; m < K; ++m) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowbase + (size_t)m * p.ldc + lane * 32));
-      if (nnext >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.logits + nnext * K * p.ldc + lane * 32));
-    }
-#endif
     // candidate bits of the lane's classes (lane + 32 i) * 4 + q kept as nibble i of two registers:
     // S_c (>= θ threshold) and "not below y" (>= l[m][y]), OR-ed over the models, no shared atomics
     uint32_t B1 = 0, B2 = 0;
 #pragma unroll 1
     for (int m = 0; m < K; ++m) {
       const float* row = rowbase + (size_t)m * p.ldc;
-#if !defined(RK_AVG_SAMPLEAHEAD) && !defined(RK_AVG_CURAHEAD)
+#ifndef RK_AVG_SAMPLEAHEAD
       {  // one-row-ahead L2 prefetch (the next row, or the next sample's first row): 128 B per lane
         const float* nrow = m + 1 < K ? row + p.ldc : (nnext >= 0 ? p.logits + nnext * K * p.ldc : nullptr);
         if (nrow && lane * 32 < p.ldc) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + lane * 32));
