@@ -94,7 +94,8 @@ rk_status rk_score(rk_ctx* ctx, const void* X_bf16, int64_t N, int64_t global_of
  * subset's average exactly where the bounds allow; the remaining samples' rows are recomputed with logits
  * (inside rk_subset_accumulate) and averaged by the logits path, so the table is identical to
  * rk_score + rk_subset_accumulate. Other shapes run exactly that path. rk_predict after this call is
- * RK_ESTATE, and rk_outputs returns no logits. Device X must stay valid until rk_subset_accumulate. */
+ * RK_ESTATE, and rk_outputs returns no logits. Device X must stay valid until rk_subset_accumulate, which
+ * for such a batch synchronises `stream` once (it reads the number of recomputed rows to size their GEMM). */
 rk_status rk_score_labelled(rk_ctx* ctx, const void* X_bf16, const int32_t* labels, int64_t N, int64_t global_offset,
                             void* stream);
 

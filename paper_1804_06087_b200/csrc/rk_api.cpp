@@ -1329,6 +1329,7 @@ rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback) {
   if (!ctx) return RK_EINVAL;
   if (!ctx->reset_done || ctx->chunks == 0) return fail(ctx, RK_ESTATE, "no chunk accumulated since rk_subset_reset");
   CK(cudaSetDevice(ctx->dev));
+  CK(cudaDeviceSynchronize());  // the counts of the last accumulate, whatever stream it ran on
   unsigned int w = 0;
   if (ctx->d_work && ctx->cur_N > 0) CK(cudaMemcpy(&w, reinterpret_cast<unsigned int*>(ctx->d_work + ctx->cur_N), 4,
                                                    cudaMemcpyDeviceToHost));
