@@ -70,9 +70,6 @@ struct rk_ctx {
   int32_t* d_tc = nullptr; int64_t tc_cap = 0;          // fallback rows: top1 | labels
   float* d_sc = nullptr; int64_t sc_cap = 0;            // fallback rows: lsum | rmax
   int64_t last_fallback = 0, last_worklist = 0;
-  uint32_t* d_bm = nullptr; int64_t bm_cap = 0;   // K <= 8 split averaging stage: candidate bitmaps
-  bool split_avg = false;                         // env RK_SPLIT_AVG=1: bitmap kernel + gather kernel (measured
-                                                  // slower at c4: 7.1 vs 5.1 ms per 1M)
   const float* cur_logits = nullptr;
   int64_t cur_ldc = 0, cur_N = 0, cur_off = 0;
   // GEMM workspaces
@@ -277,7 +274,6 @@ rk_status rk_create(rk_ctx** out, int cuda_device, const void* nccl_unique_id, i
   // tests only: a tiny near-tie pair list makes the warp averaging kernel hand whole samples to the CTA kernel
   if (const char* pc = getenv("RK_PAIR_CAP")) ctx->pair_cap_test = std::max(1, atoi(pc));
   if (const char* to = getenv("RK_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::max(0.001, atof(to));
-  if (const char* sa = getenv("RK_SPLIT_AVG")) ctx->split_avg = atoi(sa) != 0;
   if (nccl_unique_id) {  // world ranks (world may be 1: a one-rank communicator, same code path)
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
@@ -291,7 +287,7 @@ void rk_destroy(rk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
-  void* ptrs[] = {ctx->d_bm, ctx->d_ly, ctx->d_tv, ctx->d_ti, ctx->d_fb, ctx->d_xc, ctx->d_lc, ctx->d_tc, ctx->d_sc,
+  void* ptrs[] = {ctx->d_ly, ctx->d_tv, ctx->d_ti, ctx->d_fb, ctx->d_xc, ctx->d_lc, ctx->d_tc, ctx->d_sc,
                   ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lsum, ctx->ws_max, ctx->ws_x,
                   ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_pairs, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
@@ -730,10 +726,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     vp.scratch = ctx->d_scratch;
     vp.scratch_cls = ctx->d_scratch_cls;
     vp.sm_count = ctx->sm_count;
-    if (warp_path && ctx->split_avg) {  // candidate bitmaps of the split averaging stage: [N][32] words
-      if ((s = ensure(ctx, &ctx->d_bm, &ctx->bm_cap, N * 32)) != RK_OK) return s;
-      vp.bitmap_ws = ctx->d_bm;
-    }
+
     {
       // worklist [N] + count, then (K >= 9) the overflow and the CTA-kernel worklists, [N] + count each,
       // and the near-tie pair count

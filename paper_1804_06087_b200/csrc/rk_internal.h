@@ -35,7 +35,6 @@ struct VoteParams {
   const int32_t* top1_in;    // [N][K] or null
   const float* rmax_in;      // [N][K] or null (row max, from the GEMM epilogue)
   const float* ly_in;        // [N][K] label logits l[m][y] or null (fused mode: no logits rows exist)
-  uint32_t* bitmap_ws;       // K <= 8: [N][32] candidate bitmaps of the split averaging stage, or null
   int sm_count;
   const int32_t* labels;     // [N] device
   int64_t N;                 // samples in this chunk

@@ -122,11 +122,8 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
 #ifndef RK_AVG_MINB
 #define RK_AVG_MINB 6
 #endif
-// PRE: the candidate bitmap of worklist entry e was built by vote_bitmap_kernel (bm[e][32]); the kernel
-// then only gathers the candidates' columns and decides (no streaming pass of its own).
-template <bool PRE>
 __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const VoteParams p, const int32_t* work,
-                                                              const unsigned int* work_count, const uint32_t* bm) {
+                                                              const unsigned int* work_count) {
   extern __shared__ __align__(16) char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WS ws;
@@ -156,9 +153,6 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
     __syncwarp();
     if (lane < K) ws.stop[lane] = tp;
     __syncwarp();
-    if (PRE) {
-      ws.bitmap[lane] = bm[e * 32 + lane];
-    } else {
     const float thr = theta_threshold(mx, ls, K, lane);
     const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;  // l[m][y]
     // ---- 1. candidate set R: one streaming pass over the sample's K rows ----------------------
@@ -219,7 +213,6 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
         if ((lane & 7) == 0) ws.bitmap[(lane >> 3) + 4 * i] = wv;
       }
     }
-    }  // !PRE
     __syncwarp();
     const uint32_t word = ws.bitmap[lane];
     const int cnt = __popc(word);
@@ -363,69 +356,6 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
   }
 }
 
-// Streaming pass of step A4 alone (the bandwidth-bound part): one warp per worklist sample, two rows of
-// loads in flight per warp and nothing else to do, so many more bytes are in flight per SM than in the
-// combined kernel; writes the sample's candidate bitmap R = S_c ∩ {c : exists m, l[m][c] >= l[m][y]}
-// (32 words, bit c) for vote_average_kernel<true>.
-constexpr int BT = 256;
-__global__ void __launch_bounds__(BT, 3) vote_bitmap_kernel(const VoteParams p, const int32_t* work,
-                                                          const unsigned int* work_count, uint32_t* bm) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = p.K, C = p.C;
-  const int F = (int)(p.ldc >> 2);
-  const int64_t gw = (int64_t)blockIdx.x * (BT / 32) + warp, nw = (int64_t)gridDim.x * (BT / 32);
-  const int64_t W = *work_count;
-  for (int64_t e = gw; e < W; e += nw) {
-    const int64_t n = work[e];
-    const int y = p.labels[n];
-    const float* rowbase = p.logits + n * K * p.ldc;
-    float mx = 0.f, ls = 0.f;
-    if (lane < K) { ls = p.lsum_in[n * K + lane]; mx = p.rmax_in[n * K + lane]; }
-    const float thr = theta_threshold(mx, ls, K, lane);
-    const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;
-    uint32_t B1 = 0, B2 = 0;
-#pragma unroll 1
-    for (int m0 = 0; m0 < K; m0 += 2) {
-      float4 v[2][8];
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c4 = lane + 32 * i;
-          v[r][i] = (m0 + r < K && c4 < F && c4 * 4 < C) ? ldg_stream(rowbase + (size_t)(m0 + r) * p.ldc + c4 * 4)
-                                                         : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int m = m0 + r < K ? m0 + r : 0;
-        const float t_m = __shfl_sync(FULL, thr, m), y_m = __shfl_sync(FULL, ly, m);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int cb = (lane + 32 * i) * 4;
-          uint32_t bits = 0, bitsB = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float x = f4c(v[r][i], q);
-            bits |= (x >= t_m && cb + q < C) ? (1u << q) : 0u;
-            bitsB |= (x >= y_m && cb + q < C) ? (1u << q) : 0u;
-          }
-          B1 |= bits << (4 * i);
-          B2 |= bitsB << (4 * i);
-        }
-      }
-    }
-    const uint32_t Rn = B1 & B2;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {  // nibble i of lanes 8k..8k+7 forms word 4i + k
-      uint32_t wv = ((Rn >> (4 * i)) & 0xfu) << (4 * (lane & 7));
-      wv |= __shfl_xor_sync(FULL, wv, 1);
-      wv |= __shfl_xor_sync(FULL, wv, 2);
-      wv |= __shfl_xor_sync(FULL, wv, 4);
-      if ((lane & 7) == 0) bm[e * 32 + (lane >> 3) + 4 * i] = wv;
-    }
-  }
-}
-
 }  // namespace
 
 size_t vote_avg_smem_per_warp(const VoteParams& p) { return warp_smem(p, nullptr, nullptr); }
@@ -433,16 +363,9 @@ size_t vote_avg_smem_per_warp(const VoteParams& p) { return warp_smem(p, nullptr
 cudaError_t launch_vote_avg(const VoteParams& q, int grid, cudaStream_t st, const int32_t* work,
                             const unsigned int* work_count) {
   const size_t smem = warp_smem(q, nullptr, nullptr) * WPC;
-  if (q.bitmap_ws && q.ldc <= 1024) {  // split: streaming bitmap kernel, then gather + decide
-    vote_bitmap_kernel<<<q.sm_count * 3, BT, 0, st>>>(q, work, work_count, q.bitmap_ws);
-    cudaError_t e = cudaFuncSetAttribute(vote_average_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    vote_average_kernel<true><<<grid, WT, smem, st>>>(q, work, work_count, q.bitmap_ws);
-    return cudaGetLastError();
-  }
-  cudaError_t e = cudaFuncSetAttribute(vote_average_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  vote_average_kernel<false><<<grid, WT, smem, st>>>(q, work, work_count, nullptr);
+  vote_average_kernel<<<grid, WT, smem, st>>>(q, work, work_count);
   return cudaGetLastError();
 }
 
