@@ -82,3 +82,20 @@ def test_moments_and_serving_on_sine_arrivals(rk):
     ro = oracle.greedy_serve(o, K, N, 56_000_000)
     for k in ("served", "overdue", "exceed_ns", "batches", "unserved"):
         np.testing.assert_array_equal(r[k], ro[k], err_msg=k)
+
+
+def test_fullsize_stream(rk):
+    """c5's 4M requests at r_u in bench.py's launch configuration (one call): bit-exact against the oracle's
+    arrival times, non-decreasing, and the mean rate over the whole span within 2 % of b (the sine term
+    integrates to ~0 over the covered periods)."""
+    N, ref, delta = 4_000_000, 572.0, 50_000_000
+    ctx = rk.Context(0)
+    g = gpu_arrivals(rk, ctx, N, ref, PERIOD, delta, 0.1, 17)
+    o = oracle.sine_arrivals(ref, PERIOD, delta, 0.1, 17, 0, N)
+    np.testing.assert_array_equal(g, o)
+    assert np.all(np.diff(g) >= 0)
+    k, b = oracle.sine_params(ref)
+    span_s = g[-1] / 1e9
+    periods = span_s / (PERIOD / 1e9)
+    assert periods > 10
+    assert abs(N / span_s - b) < 0.02 * b, (N / span_s, b)
