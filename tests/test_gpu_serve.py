@@ -169,3 +169,31 @@ def test_serve_stream(rk, K, C, D, v, rate):
     m = clear[:served]
     np.testing.assert_array_equal(pa[:served][m], oa[:served][m])
     assert (pv[served:] == -1).all() and (pa[served:] == -1).all()
+
+
+def test_async_and_stream_errors(rk):
+    c = ctx_for(rk, 2)
+    lat = np.zeros((2, 1), np.int64)
+    with pytest.raises(rk.RkError):  # no batch sizes
+        c.async_serve(rk.RewardCfg(B=[], beta=1.0, tau_ns=10, lat_ns=np.zeros((2, 0), np.int64), rates=[1.0]), 10, 0)
+    with pytest.raises(rk.RkError):  # non-positive rate
+        c.async_serve(rk.RewardCfg(B=[4], beta=1.0, tau_ns=10, lat_ns=lat, rates=[0.0]), 10, 0)
+    with pytest.raises(rk.RkError):  # negative latency
+        c.async_serve(rk.RewardCfg(B=[4], beta=1.0, tau_ns=10, lat_ns=-lat - 1, rates=[1.0]), 10, 0)
+    import gen
+    K, C, D, N = 2, 100, 128, 64
+    psig, f0, df, sh = gen.head_params(D, C, K)
+    X = torch.from_numpy(gen.features(1, 0, N, D, C, psig, False)).cuda()
+    h = rk.Context(0)
+    h.load_ensemble(K, C, D, torch.from_numpy(gen.weights(2, K, C, D, f0, df, False)).cuda(), None, sh)
+    cfg = rk.RewardCfg(B=[16], beta=1.0, tau_ns=10**9, lat_ns=np.zeros((K, 1), np.int64), rates=[100.0])
+    pv = torch.zeros(N, dtype=torch.int32, device="cuda")
+    with pytest.raises(rk.RkError):  # v = 0 is not an action
+        h.serve_stream(X, N, cfg, 0, 0, pv)
+    with pytest.raises(rk.RkError):  # two arrival streams
+        h.serve_stream(X, N, rk.RewardCfg(B=[16], beta=1.0, tau_ns=10**9, lat_ns=np.zeros((K, 1), np.int64),
+                                          rates=[100.0, 200.0]), 0, 1, pv)
+    with pytest.raises(rk.RkError):  # host features
+        h.serve_stream(X.cpu().numpy(), N, cfg, 0, 1, pv)
+    with pytest.raises(rk.RkError):  # a logits-only ensemble has no heads to serve with
+        c.serve_stream(X, N, cfg, 0, 1, pv)
