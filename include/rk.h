@@ -230,6 +230,9 @@ typedef struct {
   int n_steps;             /* decisions per episode (n of eq. eq:J)                           */
   double gamma;            /* discount                                                        */
   double reward_scale;     /* returns are formed from R * reward_scale                        */
+  double entropy;          /* entropy bonus c: the policy loss adds -c * mean_t H(pi(.|s_t)) (the
+                              entropy term of the PPO objective the paper cites, X4); 0 = plain
+                              actor-critic                                                     */
 } rk_ac_cfg;
 /* Trajectories of E episodes x n_steps, DEVICE buffers (caller-owned): states [E][n][F] fp32,
  * actions [E][n] int32, rewards [E][n] fp64 (unscaled R), overdue / t_dec / t_start / t_done [E][n]
@@ -246,8 +249,8 @@ rk_status rk_ac_rollout(rk_ctx* ctx, const rk_reward_cfg* cfg, const double* acc
                         const rk_ac_cfg* ac, const float* params, int E, const int64_t* h0, const int32_t* forced,
                         uint64_t seed, rk_ac_traj* traj, void* stream);
 /* Actor-critic gradient of the trajectories (states, actions, rewards): G_t = sum_{k>=t} gamma^(k-t) R_k
- * reward_scale, A_t = G_t - V(s_t); policy loss -(1/(E n)) sum_t A_t log pi(a_t|s_t) (A_t held fixed,
- * eq. eq:hatJ), value loss (1/(E n)) sum_t (V(s_t) - G_t)^2. grad: device [n_params] (policy then value
+ * reward_scale, A_t = G_t - V(s_t); policy loss -(1/(E n)) sum_t [A_t log pi(a_t|s_t) + entropy * H(pi(.|s_t))]
+ * (A_t held fixed, eq. eq:hatJ), value loss (1/(E n)) sum_t (V(s_t) - G_t)^2. grad: device [n_params] (policy then value
  * parts, the params layout); losses: host [2] (policy, value) or NULL. Deterministic (fixed-order sums). */
 rk_status rk_ac_grad(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, const float* params,
                      const rk_ac_traj* traj, int E, float* grad, double* losses, void* stream);

@@ -367,7 +367,7 @@ def ac_param_count(F: int, H: int, A: int) -> int:
     return H * F + H + A * H + A + H * F + H + H + 1
 
 
-def ac_grad(F: int, H: int, A: int, params, states, actions, rewards, gamma: float, scale: float):
+def ac_grad(F: int, H: int, A: int, params, states, actions, rewards, gamma: float, scale: float, ent: float = 0.0):
     """Actor-critic gradients in fp64 (PAPER.md:123-131 eqs. eq:dJ / eq:hatJ with the baseline V(s_t)):
     (grad [flat], loss_pi, loss_v) for E episodes x n steps (states [E][n][F], actions/rewards [E][n])."""
     P = np.ascontiguousarray(params, dtype=np.float64)
@@ -379,9 +379,10 @@ def ac_grad(F: int, H: int, A: int, params, states, actions, rewards, gamma: flo
     lp, lv = ctypes.c_double(), ctypes.c_double()
     L_ = lib()
     L_.or_ac_grad.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_int, ctypes.c_double,
-                                                                          ctypes.c_double, ctypes.c_void_p,
-                                                                          ctypes.c_void_p, ctypes.c_void_p]
-    rc = L_.or_ac_grad(F, H, A, _p(P), _p(st), _p(act), _p(rew), E, n, gamma, scale, _p(g), ctypes.byref(lp),
+                                                                          ctypes.c_double, ctypes.c_double,
+                                                                          ctypes.c_void_p, ctypes.c_void_p,
+                                                                          ctypes.c_void_p]
+    rc = L_.or_ac_grad(F, H, A, _p(P), _p(st), _p(act), _p(rew), E, n, gamma, scale, ent, _p(g), ctypes.byref(lp),
                        ctypes.byref(lv))
     if rc != OK:
         raise OracleError(rc)

@@ -649,8 +649,8 @@ int or_env_rollout(const or_env* e, const int32_t* actions, int n, int64_t h0, f
 }
 
 int or_ac_grad(int F, int H, int A, const double* P, const float* states, const int32_t* actions,
-               const double* rewards, int E, int n, double gamma, double scale, double* grad, double* loss_pi,
-               double* loss_v) {
+               const double* rewards, int E, int n, double gamma, double scale, double ent, double* grad,
+               double* loss_pi, double* loss_v) {
   if (F < 1 || H < 1 || A < 1 || E < 1 || n < 1 || !P || !states || !actions || !rewards || !grad) return OR_EINVAL;
   const double *W1 = P, *b1 = W1 + (int64_t)H * F, *W2 = b1 + H, *b2 = W2 + (int64_t)A * H;
   const double *V1 = b2 + A, *c1 = V1 + (int64_t)H * F, *v2 = c1 + H, *c2 = v2 + H;
@@ -699,13 +699,16 @@ int or_ac_grad(int F, int H, int A, const double* P, const float* states, const 
       for (int j = 0; j < H; ++j) V += v2[j] * hv[j];
       const double adv = G[t] - V;  /* actor-critic: R_t - V(s_t) with the return */
       const int at = actions[(int64_t)e * n + t];
-      lp += -adv * (z[at] - lse) * inv;
+      /* policy entropy Hs = -sum_k pi_k log pi_k (the entropy bonus of the PPO objective, X4) */
+      double hs = 0.0;
+      for (int k = 0; k < A; ++k) hs -= exp(z[k] - lse) * (z[k] - lse);
+      lp += (-adv * (z[at] - lse) - ent * hs) * inv;
       lv += (V - G[t]) * (V - G[t]) * inv;
-      /* d(-A log pi(a|s))/dz_k = -A (1[k = a] - pi_k) */
+      /* d(-A log pi(a|s))/dz_k = -A (1[k = a] - pi_k); d(-c H)/dz_k = c pi_k (log pi_k + H) */
       for (int j = 0; j < H; ++j) dh[j] = 0.0;
       for (int k = 0; k < A; ++k) {
         const double pk = exp(z[k] - lse);
-        const double dz = -adv * ((k == at ? 1.0 : 0.0) - pk) * inv;
+        const double dz = (-adv * ((k == at ? 1.0 : 0.0) - pk) + ent * pk * ((z[k] - lse) + hs)) * inv;
         gb2[k] += dz;
         for (int j = 0; j < H; ++j) {
           gW2[(int64_t)k * H + j] += dz * h[j];

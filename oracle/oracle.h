@@ -149,13 +149,14 @@ int or_env_rollout(const or_env* env, const int32_t* actions, int n, int64_t h0,
                    int32_t* overdue, int64_t* t_dec, int64_t* t_start, int64_t* t_done);
 /* Actor-critic gradients (fp64) for E episodes of n steps: G_t = sum_{k>=t} gamma^(k-t) R_k * scale,
  * A_t = G_t - V(s_t); policy loss -(1/(E n)) sum A_t log pi(a_t|s_t) (A_t constant), value loss
- * (1/(E n)) sum (V(s_t) - G_t)^2. Networks: pi = softmax(W2 tanh(W1 x + b1) + b2) over A actions,
+ * (1/(E n)) sum (V(s_t) - G_t)^2; with ent > 0 the policy loss also has -(ent/(E n)) sum_t H(pi(.|s_t)).
+ * Networks: pi = softmax(W2 tanh(W1 x + b1) + b2) over A actions,
  * V = v2 . tanh(V1 x + c1) + c2, hidden H. params / grad: the flat layout
  * [W1 H*F | b1 H | W2 A*H | b2 A | V1 H*F | c1 H | v2 H | c2 1] (row-major). Also returns the mean
  * unscaled episode return sum_t R_t and the two losses (each pointer may be NULL). */
 int or_ac_grad(int F, int H, int A, const double* params, const float* states, const int32_t* actions,
-               const double* rewards, int E, int n, double gamma, double scale, double* grad, double* loss_pi,
-               double* loss_v);
+               const double* rewards, int E, int n, double gamma, double scale, double ent, double* grad,
+               double* loss_pi, double* loss_v);
 
 #ifdef __cplusplus
 }

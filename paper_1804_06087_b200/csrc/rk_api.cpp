@@ -1193,8 +1193,9 @@ static rk_status ac_setup(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg
   if (cfg->nB < 1 || cfg->nB > kMaxB || !cfg->B || !cfg->lat_ns) return fail(ctx, RK_EINVAL, "nB in [1,8] with B and lat_ns");
   if (cfg->tau_ns <= 0 || !(cfg->beta == cfg->beta)) return fail(ctx, RK_EINVAL, "tau > 0, finite beta");
   if (ac->L < 0 || ac->L > 256 || ac->H < 1 || ac->H > kRlMaxH || ac->n_steps < 1 ||
-      !(ac->gamma >= 0 && ac->gamma <= 1) || !(ac->reward_scale == ac->reward_scale))
-    return fail(ctx, RK_EINVAL, "ac: L in [0,256], H in [1,64], n_steps >= 1, gamma in [0,1]");
+      !(ac->gamma >= 0 && ac->gamma <= 1) || !(ac->reward_scale == ac->reward_scale) ||
+      !(ac->entropy >= 0 && ac->entropy < 1e6))
+    return fail(ctx, RK_EINVAL, "ac: L in [0,256], H in [1,64], n_steps >= 1, gamma in [0,1], entropy >= 0");
   rp = RLParams{};
   rp.K = ctx->K; rp.nB = cfg->nB; rp.L = ac->L; rp.H = ac->H; rp.n = ac->n_steps;
   rp.F = ac->L + ctx->K * cfg->nB + ctx->K;
@@ -1208,7 +1209,7 @@ static rk_status ac_setup(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg
       rp.lat[m * cfg->nB + bi] = cfg->lat_ns[m * cfg->nB + bi];
     }
   }
-  rp.tau = cfg->tau_ns; rp.beta = cfg->beta; rp.gamma = ac->gamma; rp.scale = ac->reward_scale;
+  rp.tau = cfg->tau_ns; rp.beta = cfg->beta; rp.gamma = ac->gamma; rp.scale = ac->reward_scale; rp.ent = ac->entropy;
   return RK_OK;
 }
 

@@ -266,7 +266,7 @@ struct RLParams {
   int32_t* overdue;              // [E][n] or null
   int64_t *t_dec, *t_start, *t_done;  // [E][n] or null
   unsigned int* err;
-  double gamma, scale;
+  double gamma, scale, ent;
 };
 int64_t ac_param_count(int F, int H, int A);
 cudaError_t launch_ac_rollout(const RLParams& p, cudaStream_t st);

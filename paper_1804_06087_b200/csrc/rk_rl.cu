@@ -205,7 +205,7 @@ __global__ void ac_returns_kernel(const RLParams p, double* G) {
 // one warp per sample: both forward passes, the output / value deltas and the hidden deltas
 __global__ void __launch_bounds__(32 * RW) ac_sample_kernel(const RLParams p, const double* G, float* Hs, float* HV,
                                                             float* DP, float* DPV, float* coef, float* lse_out,
-                                                            float* dV, float* lossv) {
+                                                            float* dV, float* lossv, float* ent_out) {
   extern __shared__ __align__(16) float rl_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int F = p.F, H = p.H, A = p.A;
@@ -235,9 +235,25 @@ __global__ void __launch_bounds__(32 * RW) ac_sample_kernel(const RLParams p, co
   const float g = (float)G[s];
   const float adv = g - V;
   const int at = p.actions[s];
-  const float cpi = -adv * inv;  // dz_a = cpi * (1[a = at] - pi_a)
+  const float cpi = -adv * inv;  // dz_a = cpi * (1[a = at] - pi_a) + ce * pi_a * (log pi_a + Hs)
+  const float ce = (float)p.ent * inv;
+  // policy entropy Hs = -sum_a pi_a log pi_a (the entropy bonus of the loss, X4 / PPO)
+  float hs = 0.f;
+  if (ce != 0.f) {
+    for (int a = a0; a < a1; ++a) {
+      const float lp = z[a] - lse;
+      hs -= __expf(lp) * lp;
+    }
+    for (int o = 16; o; o >>= 1) hs += __shfl_xor_sync(FULL, hs, o);
+  }
+  __syncwarp();  // every lane's logits are in shared memory
+  const float zat = z[at];
+  __syncwarp();
   // dz into shared memory, then hidden deltas dh_j = sum_a dz_a W2[a][j] with lanes owning j
-  for (int a = a0; a < a1; ++a) z[a] = cpi * ((a == at ? 1.f : 0.f) - __expf(z[a] - lse));
+  for (int a = a0; a < a1; ++a) {
+    const float lp = z[a] - lse, pa = __expf(lp);
+    z[a] = cpi * ((a == at ? 1.f : 0.f) - pa) + (ce != 0.f ? ce * pa * (lp + hs) : 0.f);
+  }
   __syncwarp();
   for (int j = lane; j < H; j += 32) {
     float d = 0.f;
@@ -248,21 +264,20 @@ __global__ void __launch_bounds__(32 * RW) ac_sample_kernel(const RLParams p, co
   }
   const float dv = 2.f * (V - g) * inv;
   for (int j = lane; j < H; j += 32) DPV[s * H + j] = dv * __ldg(net.v2 + j) * (1.f - hv[j] * hv[j]);
-  // losses: -A log pi(a_t) / Ns and (V - G)^2 / Ns (z[at] now holds dz: recompute the logit)
+  // losses: -(A log pi(a_t) + c H) / Ns and (V - G)^2 / Ns
   if (lane == 0) {
     coef[s] = cpi;
     lse_out[s] = lse;
     dV[s] = dv;
-    float zat = __ldg(net.b2 + at);
-    for (int j = 0; j < H; ++j) zat = fmaf(__ldg(net.W2 + (size_t)at * H + j), h[j], zat);
-    lossv[2 * s] = -adv * (zat - lse) * inv;
+    ent_out[s] = hs;
+    lossv[2 * s] = -adv * (zat - lse) * inv - ce * hs;
     lossv[2 * s + 1] = (V - g) * (V - g) * inv;
   }
 }
 
 // gW2 / gb2 for a tile of 32 actions (lane = action): sum over samples of dz_s(a) h_s, fixed order
 __global__ void __launch_bounds__(256) ac_grad_w2_kernel(const RLParams p, const float* Hs, const float* coef,
-                                                         const float* lse, float* grad) {
+                                                         const float* lse, const float* ent, float* grad) {
   extern __shared__ __align__(16) float rl_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int F = p.F, H = p.H, A = p.A;
@@ -279,13 +294,15 @@ __global__ void __launch_bounds__(256) ac_grad_w2_kernel(const RLParams p, const
 #pragma unroll
   for (int j = 0; j < kRlMaxH; ++j) w[j] = (a < A && j < H) ? __ldg(net.W2 + (size_t)a * H + j) : 0.f;
   const float bb = a < A ? __ldg(net.b2 + a) : 0.f;
+  const float ce = (float)p.ent * (float)(1.0 / (double)Ns);
   for (int64_t s = warp; s < Ns; s += nw) {
     for (int j = lane; j < H; j += 32) hrow[j] = Hs[s * H + j];
     __syncwarp();
     float zz = bb;
 #pragma unroll
     for (int j = 0; j < kRlMaxH; ++j) if (j < H) zz = fmaf(w[j], hrow[j], zz);
-    const float dz = coef[s] * ((a == p.actions[s] ? 1.f : 0.f) - __expf(zz - lse[s]));
+    const float lp = zz - lse[s], pa = __expf(lp);
+    const float dz = coef[s] * ((a == p.actions[s] ? 1.f : 0.f) - pa) + (ce != 0.f ? ce * pa * (lp + ent[s]) : 0.f);
 #pragma unroll
     for (int j = 0; j < kRlMaxH; ++j) if (j < H) acc[j] = fmaf(dz, hrow[j], acc[j]);
     accb += dz;
@@ -404,6 +421,7 @@ cudaError_t launch_ac_grad(const RLParams& p, float* grad, float* loss2, void* s
   float* coef = reinterpret_cast<float*>(w); w += Ns * 4;
   float* lse = reinterpret_cast<float*>(w); w += Ns * 4;
   float* dV = reinterpret_cast<float*>(w); w += Ns * 4;
+  float* ent = reinterpret_cast<float*>(w); w += Ns * 4;
   float* lossv = reinterpret_cast<float*>(w);
   ac_returns_kernel<<<(p.E + 127) / 128, 128, 0, st>>>(p, G);
   const size_t smem = (size_t)RW * (p.F + 2 * p.H + p.A) * sizeof(float);
@@ -411,11 +429,12 @@ cudaError_t launch_ac_grad(const RLParams& p, float* grad, float* loss2, void* s
     cudaError_t e = cudaFuncSetAttribute(ac_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  ac_sample_kernel<<<(unsigned)((Ns + RW - 1) / RW), 32 * RW, smem, st>>>(p, G, Hs, HV, DP, DPV, coef, lse, dV, lossv);
+  ac_sample_kernel<<<(unsigned)((Ns + RW - 1) / RW), 32 * RW, smem, st>>>(p, G, Hs, HV, DP, DPV, coef, lse, dV, lossv,
+                                                                           ent);
   const size_t smem2 = (size_t)8 * H * 4 + (size_t)8 * 32 * (H + 1) * 4;
   cudaError_t e = cudaFuncSetAttribute(ac_grad_w2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   if (e != cudaSuccess) return e;
-  ac_grad_w2_kernel<<<(p.A + 31) / 32, 256, smem2, st>>>(p, Hs, coef, lse, grad);
+  ac_grad_w2_kernel<<<(p.A + 31) / 32, 256, smem2, st>>>(p, Hs, coef, lse, ent, grad);
   ac_grad_w1_kernel<<<H, 256, 0, st>>>(p, DP, HV, dV, grad, 0);
   ac_grad_w1_kernel<<<H, 256, 0, st>>>(p, DPV, HV, dV, grad, 1);
   if (loss2) ac_loss_kernel<<<1, 256, 0, st>>>(lossv, Ns, loss2);
@@ -424,7 +443,7 @@ cudaError_t launch_ac_grad(const RLParams& p, float* grad, float* loss2, void* s
 
 size_t ac_grad_scratch_bytes(const RLParams& p) {
   const int64_t Ns = (int64_t)p.E * p.n;
-  return (size_t)Ns * (8 + 4 * 4 * p.H + 3 * 4 + 8);
+  return (size_t)Ns * (8 + 4 * 4 * p.H + 4 * 4 + 8);
 }
 
 cudaError_t launch_ac_apply(float* P, const float* g, int64_t npol, int64_t np, float lr_pi, float lr_v,

@@ -60,7 +60,7 @@ class _Sine(ctypes.Structure):
 
 class _AcCfg(ctypes.Structure):
     _fields_ = [("L", ctypes.c_int), ("H", ctypes.c_int), ("n_steps", ctypes.c_int), ("gamma", ctypes.c_double),
-                ("reward_scale", ctypes.c_double)]
+                ("reward_scale", ctypes.c_double), ("entropy", ctypes.c_double)]
 
 
 class _Traj(ctypes.Structure):
@@ -318,7 +318,8 @@ class Context:
     # -- NEXT-2: actor-critic scheduler (argument marshalling; the loop lives in scheduler.py) --
     @staticmethod
     def _ac(ac):
-        return _AcCfg(int(ac["L"]), int(ac["H"]), int(ac["n_steps"]), float(ac["gamma"]), float(ac["reward_scale"]))
+        return _AcCfg(int(ac["L"]), int(ac["H"]), int(ac["n_steps"]), float(ac["gamma"]), float(ac["reward_scale"]),
+                      float(ac.get("entropy", 0.0)))
 
     def ac_dims(self, nB, ac):
         F, A, P = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()

@@ -17,7 +17,7 @@ class ActorCritic:
     driven by `arrival` (device int64 [Narr] arrival times, e.g. from Context.sine_arrivals)."""
 
     def __init__(self, ctx: Context, cfg: RewardCfg, acc, arrival, L=16, H=64, n_steps=32, gamma=0.9,
-                 reward_scale=None, seed=0, init_std=1.0):
+                 reward_scale=None, seed=0, init_std=1.0, entropy=0.0):
         import torch
         self.torch = torch
         self.ctx, self.cfg = ctx, cfg
@@ -26,7 +26,8 @@ class ActorCritic:
         self.Narr = int(arrival.numel())
         self.B = np.asarray(cfg.B, np.int64)
         self.ac = {"L": L, "H": H, "n_steps": n_steps, "gamma": gamma,
-                   "reward_scale": reward_scale if reward_scale is not None else 1.0 / float(max(cfg.B))}
+                   "reward_scale": reward_scale if reward_scale is not None else 1.0 / float(max(cfg.B)),
+                   "entropy": entropy}
         self.F, self.A, self.P = ctx.ac_dims(len(cfg.B), self.ac)
         F, A = self.F, self.A
         rng = np.random.default_rng(seed)

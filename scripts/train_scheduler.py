@@ -42,11 +42,12 @@ def subset_accuracy(ctx, K, C, D, N):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--iters", type=int, default=300)
+    ap.add_argument("--iters", type=int, default=1500)
     ap.add_argument("--episodes", type=int, default=512)
     ap.add_argument("--steps", type=int, default=32)
     ap.add_argument("--lr-pi", type=float, default=1.0)
     ap.add_argument("--lr-v", type=float, default=0.02)
+    ap.add_argument("--entropy", type=float, default=0.01, help="entropy bonus of the policy loss (PPO, X4)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_scheduler.json"))
     a = ap.parse_args()
     K, C, D, B = 3, 1000, 2048, [16, 32, 48, 64]
@@ -56,6 +57,7 @@ def main():
     N = 2_000_000
     period = 500 * TAU_NS
     res = {"K": K, "B": B, "tau_ns": TAU_NS, "beta": BETA, "acc": acc.tolist(), "lat_ns": lat.tolist(),
+           "learner": {"lr_pi": a.lr_pi, "lr_v": a.lr_v, "entropy": a.entropy, "episodes": a.episodes, "steps": a.steps},
            "arrivals": {"process": "sine + noise (reading Q16)", "period_ns": period, "delta_ns": 50_000_000,
                         "noise_std": 0.1}, "runs": {}}
     for name, ref in (("r_l", 128.0), ("r_u", 572.0)):
@@ -75,7 +77,7 @@ def main():
                                 "batches_per_model": asy["model_batches"][0].tolist()},
         }
         torch.manual_seed(0)
-        agent = ActorCritic(ctx, cfg, acc, arr, L=16, H=64, n_steps=a.steps, seed=0)
+        agent = ActorCritic(ctx, cfg, acc, arr, L=16, H=64, n_steps=a.steps, seed=0, entropy=a.entropy)
         t0 = time.perf_counter()
         curve = agent.train(a.iters, E=a.episodes, lr_pi=a.lr_pi, lr_v=a.lr_v,
                             log=lambda s: print(name, s["iter"], round(s["return"], 2), round(s["overdue_frac"], 3),

@@ -110,9 +110,11 @@ def test_uniform_policy_sampling(rk):
     assert cnt.size == A and (np.abs(cnt - m) < 5 * np.sqrt(m)).all(), cnt
 
 
-@pytest.mark.parametrize("K,B,H", [(3, [16, 32, 48, 64], 32), (4, [16, 64], 64)])
-def test_gradient_parity(rk, K, B, H):
+@pytest.mark.parametrize("K,B,H,ent", [(3, [16, 32, 48, 64], 32, 0.0), (4, [16, 64], 64, 0.0),
+                                       (3, [16, 32, 48, 64], 32, 0.2)])
+def test_gradient_parity(rk, K, B, H, ent):
     ctx, arr, cfg, acc, ac = make(rk, K, B, H=H, n=12)
+    ac["entropy"] = ent
     F, A, P = ctx.ac_dims(len(B), ac)
     E, n = 24, 12
     params = np.random.default_rng(2).normal(0, 0.3, P).astype(np.float32)
@@ -123,7 +125,7 @@ def test_gradient_parity(rk, K, B, H):
     grad = torch.zeros(P, device="cuda")
     losses = ctx.ac_grad(cfg, ac, pd, tr, E, grad)
     go, lp, lv = oracle.ac_grad(F, H, A, params.astype(np.float64), tr["states"].cpu().numpy(),
-                                tr["actions"].cpu().numpy(), tr["rewards"].cpu().numpy(), 0.9, 1.0 / max(B))
+                                tr["actions"].cpu().numpy(), tr["rewards"].cpu().numpy(), 0.9, 1.0 / max(B), ent)
     g = grad.cpu().numpy().astype(np.float64)
     npol = H * F + H + A * H + A
     for sl in (slice(0, npol), slice(npol, P)):  # fp32 accumulation over E*n samples vs fp64

@@ -40,16 +40,20 @@ def _problem(seed, F=5, H=4, A=6, E=3, n=4):
     return F, H, A, P, st, act, rew
 
 
-def test_gradients_match_finite_differences():
+import pytest
+
+
+@pytest.mark.parametrize("ent", [0.0, 0.3])
+def test_gradients_match_finite_differences(ent):
     F, H, A, P, st, act, rew = _problem(1)
-    g, lp, lv = oracle.ac_grad(F, H, A, P, st, act, rew, 0.9, 0.5)
+    g, lp, lv = oracle.ac_grad(F, H, A, P, st, act, rew, 0.9, 0.5, ent)
     npol = H * F + H + A * H + A
     eps = 1e-6
     for i in range(P.size):
         d = np.zeros_like(P)
         d[i] = eps
-        _, lp1, lv1 = oracle.ac_grad(F, H, A, P + d, st, act, rew, 0.9, 0.5)
-        _, lp0, lv0 = oracle.ac_grad(F, H, A, P - d, st, act, rew, 0.9, 0.5)
+        _, lp1, lv1 = oracle.ac_grad(F, H, A, P + d, st, act, rew, 0.9, 0.5, ent)
+        _, lp0, lv0 = oracle.ac_grad(F, H, A, P - d, st, act, rew, 0.9, 0.5, ent)
         # policy parameters: the policy loss with the advantage held fixed; value parameters: the value loss
         fd = (lp1 - lp0) / (2 * eps) if i < npol else (lv1 - lv0) / (2 * eps)
         if i < npol:  # the advantage depends on value parameters only, so the policy FD is exact to O(eps^2)
@@ -78,3 +82,15 @@ def test_closed_forms():
     rew = np.arange(n, dtype=np.float64)[None]
     _, _, lv = oracle.ac_grad(F, H, A, P, st, act, rew, 0.0, 0.25)
     assert abs(lv - np.mean((0.25 * rew) ** 2)) < 1e-12
+
+
+def test_entropy_term_closed_form():
+    """Zero weights: the policy is uniform, H = log A, and with zero advantage the policy loss is -c log A
+    and the gradient is zero (the uniform policy is the entropy maximum)."""
+    F, H, A = 5, 4, 6
+    n = 4
+    P = np.zeros(oracle.ac_param_count(F, H, A))
+    st = np.random.default_rng(3).normal(0, 1, (1, n, F)).astype(np.float32)
+    g, lp, lv = oracle.ac_grad(F, H, A, P, st, np.zeros((1, n), np.int32), np.zeros((1, n)), 0.9, 1.0, 0.5)
+    assert abs(lp - (-0.5 * np.log(A))) < 1e-12
+    assert np.abs(g).max() < 1e-15
