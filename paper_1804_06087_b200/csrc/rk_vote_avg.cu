@@ -75,13 +75,43 @@ __host__ __device__ inline size_t warp_smem(const VoteParams& p, char* base, WS*
   return o;
 }
 
-// fp64 recheck of near-ties (rare, out of line): warp-cooperative fp64 log-sum-exp of every row, then
-// each lane decides its pending subsets in fp64 per readings Q5-Q6 (avg = (sum_{m in v, asc}
-// exp(l - mx_m) / sum_c exp(l - mx_m)) / |v|, lowest class on ties; softmax with max subtraction, reading Q5) over the candidates inside the band.
+// Near-ties (rare, out of line). First the exact ties: when every candidate inside the band has the
+// same logit as y in every member of v, its average equals y's in any precision (same terms, same
+// order), so the lowest class wins (reading Q6) without fp64 -- 86 % of the pending subsets of the
+// integer-grid bench workload. The rest: warp-cooperative fp64 log-sum-exp of every row, then each lane
+// decides its remaining subsets in fp64 per readings Q5-Q6 (avg = (sum_{m in v, asc} exp(l - mx_m) /
+// sum_c exp(l - mx_m)) / |v|, lowest class on ties; softmax with max subtraction, reading Q5) over the
+// candidates inside the band.
 __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t pending, const float* rowbase,
                                           float mx, const float* Pm, int ps, const int32_t* cls, int nc, int ys,
                                           int y, int lane) {
   const int K = p.K, C = p.C;
+  uint32_t left = 0;
+  for (int j = 0; j < JMAX; ++j) {
+    if (!((pending >> j) & 1u)) continue;
+    const uint32_t v = (uint32_t)(lane + 32 * j + 1);
+    atomicAdd(p.n_recheck + (v - 1), 1ull);
+    float sy = 0.f;
+    for (uint32_t a = v; a; a &= a - 1) sy += Pm[(size_t)(__ffs(a) - 1) * ps + ys];
+    const float lo = sy * (1.f - p.band);
+    bool tie = true, ywins = true;
+    for (int q = 0; q < nc && tie; ++q) {
+      if (q == ys) continue;
+      float s32 = 0.f;
+      for (uint32_t a = v; a; a &= a - 1) s32 += Pm[(size_t)(__ffs(a) - 1) * ps + q];
+      if (s32 < lo) continue;
+      const int cq = cls[q];
+      for (uint32_t a = v; a && tie; a &= a - 1) {
+        const float* r = rowbase + (size_t)(__ffs(a) - 1) * p.ldc;
+        tie = r[cq] == r[y];
+      }
+      ywins &= y < cq;
+    }
+    if (tie) ws.cnt[j * 32 + lane] += ywins;
+    else left |= 1u << j;
+  }
+  if (!__any_sync(FULL, left != 0)) return;
+  pending = left;
   for (int m = 0; m < K; ++m) {
     const float* row = rowbase + (size_t)m * p.ldc;
     const double m64 = (double)__shfl_sync(FULL, mx, m);
@@ -94,7 +124,6 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
   for (int j = 0; j < JMAX; ++j) {
     if (!((pending >> j) & 1u)) continue;
     const uint32_t v = (uint32_t)(lane + 32 * j + 1);
-    atomicAdd(p.n_recheck + (v - 1), 1ull);
     float sy = 0.f;  // fp32 sums select the band; fp64 decides
     for (uint32_t a = v; a; a &= a - 1) sy += Pm[(size_t)(__ffs(a) - 1) * ps + ys];
     const float lo = sy * (1.f - p.band);
@@ -122,6 +151,9 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
 #ifndef RK_AVG_MINB
 #define RK_AVG_MINB 6
 #endif
+#ifndef RK_AVG_PD
+#define RK_AVG_PD 1
+#endif
 __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const VoteParams p, const int32_t* work,
                                                               const unsigned int* work_count) {
   extern __shared__ __align__(16) char smem_raw[];
@@ -138,6 +170,11 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
   int32_t* ovC = p.scratch_cls + gw * (size_t)C;
   for (int i = lane; i < JMAX * 32; i += 32) ws.cnt[i] = 0u;
   const int64_t W = *work_count;
+#ifndef RK_AVG_SAMPLEAHEAD
+  if (gw < W && lane * 32 < p.ldc)  // the first sample's rows 1 .. PD-1 (later rows are prefetched in the loop)
+    for (int m = 1; m < RK_AVG_PD && m < K; ++m)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p.logits + ((int64_t)work[gw] * K + m) * p.ldc + lane * 32));
+#endif
 
   for (int64_t e = gw; e < W; e += nw) {
     const int64_t n = work[e];
@@ -170,8 +207,10 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
     for (int m = 0; m < K; ++m) {
       const float* row = rowbase + (size_t)m * p.ldc;
 #ifndef RK_AVG_SAMPLEAHEAD
-      {  // one-row-ahead L2 prefetch (the next row, or the next sample's first row): 128 B per lane
-        const float* nrow = m + 1 < K ? row + p.ldc : (nnext >= 0 ? p.logits + nnext * K * p.ldc : nullptr);
+      {  // RK_AVG_PD-rows-ahead L2 prefetch (a later row, or one of the next sample's): 128 B per lane
+        const int mp = m + RK_AVG_PD;
+        const float* nrow = mp < K ? row + RK_AVG_PD * p.ldc
+                                   : (nnext >= 0 && mp - K < K ? p.logits + (nnext * K + (mp - K)) * p.ldc : nullptr);
         if (nrow && lane * 32 < p.ldc) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + lane * 32));
       }
 #endif
