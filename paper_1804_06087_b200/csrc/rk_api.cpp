@@ -89,6 +89,13 @@ struct rk_ctx {
   std::vector<cudaEvent_t> ev_chunks;
   // accumulation state
   bool reset_done = false, final_seen = false;
+  // rk_subset_reset has no stream: its device work (table zeroing, the slowest-member and backlog-carry
+  // uploads) is deferred to the next accumulate / finalize and issued on that call's stream, so a reset
+  // never synchronises the device (a previous chunk's GEMM may still be running on another stream)
+  bool reset_pending = false;
+  std::vector<uint8_t> h_slow;
+  std::vector<int64_t> h_qcarry;
+  size_t slow_cap = 0, qcarry_cap = 0;
   bool finalized = false;      // the table holds the global sum (A6 done): no more accumulate / all-reduce
   double nccl_timeout_s = 600; // bounded wait on the all-reduce (env RK_NCCL_TIMEOUT_S)
   bool has_cfg = false;
@@ -590,7 +597,6 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
     CK(cudaMalloc(&ctx->d_table, words * 8));
     ctx->table_words = words;
   }
-  CK(cudaMemset(ctx->d_table, 0, ctx->table_words * 8));
   // chunk counters: vote, avg, rc [S], tail [nB][S], osum, esum [nR][nB][K], err (4 x u32 = 2 words)
   const size_t cw = 3 * (size_t)S + (size_t)nB * S + 2 * (size_t)nR * nB * K + 2;
   if (ctx->chunk_words < cw) {
@@ -600,30 +606,50 @@ rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
     ctx->chunk_words = cw;
   }
   // slowest member of each subset at each batch size (PAPER.md:410 stragglers)
+  ctx->h_slow.clear();
   if (nB > 0) {
-    std::vector<uint8_t> slow((size_t)nB * S);
+    ctx->h_slow.resize((size_t)nB * S);
     for (int bi = 0; bi < nB; ++bi)
       for (uint32_t v = 1; v <= (uint32_t)S; ++v) {
         int sm = -1;
         for (int m = 0; m < K; ++m)
           if (((v >> m) & 1u) && (sm < 0 || ctx->lat[m * nB + bi] > ctx->lat[sm * nB + bi])) sm = m;
-        slow[(size_t)bi * S + v - 1] = (uint8_t)sm;
+        ctx->h_slow[(size_t)bi * S + v - 1] = (uint8_t)sm;
       }
-    if (ctx->d_slow) cudaFree(ctx->d_slow);
-    CK(cudaMalloc(&ctx->d_slow, slow.size()));
-    CK(cudaMemcpy(ctx->d_slow, slow.data(), slow.size(), cudaMemcpyHostToDevice));
+    if (ctx->slow_cap < ctx->h_slow.size()) {  // grow-only allocations (a cudaFree would synchronise)
+      if (ctx->d_slow) cudaFree(ctx->d_slow);
+      ctx->d_slow = nullptr;
+      CK(cudaMalloc(&ctx->d_slow, ctx->h_slow.size()));
+      ctx->slow_cap = ctx->h_slow.size();
+    }
   }
+  ctx->h_qcarry.clear();
   if (ctx->queue && nB > 0 && nR > 0) {  // backlog carry per (b, r, m): empty server
-    std::vector<int64_t> c0((size_t)nB * nR * K, INT64_MIN / 4);
-    if (ctx->d_qcarry) cudaFree(ctx->d_qcarry);
-    ctx->d_qcarry = nullptr;
-    CK(cudaMalloc(&ctx->d_qcarry, c0.size() * 8));
-    CK(cudaMemcpy(ctx->d_qcarry, c0.data(), c0.size() * 8, cudaMemcpyHostToDevice));
+    ctx->h_qcarry.assign((size_t)nB * nR * K, INT64_MIN / 4);
+    if (ctx->qcarry_cap < ctx->h_qcarry.size()) {
+      if (ctx->d_qcarry) cudaFree(ctx->d_qcarry);
+      ctx->d_qcarry = nullptr;
+      CK(cudaMalloc(&ctx->d_qcarry, ctx->h_qcarry.size() * 8));
+      ctx->qcarry_cap = ctx->h_qcarry.size();
+    }
   }
+  ctx->reset_pending = true;
   ctx->reset_done = true;
   ctx->finalized = false;
   ctx->final_seen = false;
   ctx->chunks = 0;
+  return RK_OK;
+}
+
+// the device half of rk_subset_reset, on the first accumulate / finalize stream after it
+static rk_status flush_reset(rk_ctx* ctx, cudaStream_t st) {
+  if (!ctx->reset_pending) return RK_OK;
+  CK(cudaMemsetAsync(ctx->d_table, 0, ctx->table_words * 8, st));
+  if (!ctx->h_slow.empty())
+    CK(cudaMemcpyAsync(ctx->d_slow, ctx->h_slow.data(), ctx->h_slow.size(), cudaMemcpyHostToDevice, st));
+  if (!ctx->h_qcarry.empty())
+    CK(cudaMemcpyAsync(ctx->d_qcarry, ctx->h_qcarry.data(), ctx->h_qcarry.size() * 8, cudaMemcpyHostToDevice, st));
+  ctx->reset_pending = false;
   return RK_OK;
 }
 
@@ -647,6 +673,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
   cudaStream_t st = (cudaStream_t)stream;
   const int K = ctx->K, S = ctx->S, nB = ctx->nB, nR = ctx->nR, C = ctx->C;
   rk_status s;
+  if ((s = flush_reset(ctx, st)) != RK_OK) return s;
   CK(cudaMemsetAsync(ctx->d_chunk, 0, ctx->chunk_words * 8, st));
   if (N > 0) {
     const int32_t* dl = labels;
@@ -890,6 +917,10 @@ rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream) {
   CK(cudaSetDevice(ctx->dev));
   cudaStream_t st = (cudaStream_t)stream;
   const int S = ctx->S, nB = ctx->nB, nR = ctx->nR;
+  {
+    const rk_status fr = flush_reset(ctx, st);
+    if (fr != RK_OK) return fr;
+  }
   // A6: one all-reduce of the whole integer table (order-free, bit-exact), at most once per reset: a
   // repeated finalize returns the same global table instead of summing it again
   if (ctx->comm && !ctx->finalized) {

@@ -60,7 +60,10 @@ struct Tile {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // packed mode with 3 warps per quarter: 12 x 4 KB of store staging; one operand stage makes room
   static constexpr bool WIDE = (PACK && NHP == 3) || FUSED;
-  static constexpr int NS = CL == 1 ? (WIDE ? 3 : 4) : (WIDE ? 5 : 6);
+#ifndef RK_GEMM_NS
+#define RK_GEMM_NS 6
+#endif
+  static constexpr int NS = CL == 1 ? (WIDE ? 3 : 4) : (WIDE ? 5 : RK_GEMM_NS);
   static constexpr int STG_TOTAL = FUSED ? 16 * 256 * 8 : (WIDE ? EPI_PACK * 2 * (32 * 16 * 4) : EPI_WARPS * 2 * STG_BYTES);
   static constexpr int XCH_TOTAL = FUSED ? 4 * 32 * XF * 4 : XCH_BYTES * (PACK ? NHP - 1 : 1);
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + NS * STAGE_BYTES + STG_TOTAL + 256 + XCH_TOTAL;
@@ -859,6 +862,10 @@ static cudaError_t launch_t(const GemmArgs& a, const GemmParams& p, int sm_count
   const CUtensorMap& m16 = *reinterpret_cast<const CUtensorMap*>(p.tmap_out16);
   cudaError_t e = cudaFuncSetAttribute(gemm_heads_kernel<CL, PACK, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Tile<CL, PACK, FUSED>::SMEM_BYTES);
+#ifdef RK_CARVEOUT
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_heads_kernel<CL, PACK, FUSED>, cudaFuncAttributePreferredSharedMemoryCarveout, RK_CARVEOUT);
+#endif
   if (e != cudaSuccess) return e;
   const int64_t units = ((p.N + CL * BM - 1) / (CL * BM)) * a.ng;
   if (CL == 1) {

@@ -404,6 +404,11 @@ cudaError_t launch_vote_avg(const VoteParams& q, int grid, cudaStream_t st, cons
   const size_t smem = warp_smem(q, nullptr, nullptr) * WPC;
   cudaError_t e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+#ifdef RK_CARVEOUT
+  // same (maximum) shared-memory carveout as the head GEMM, so the two can share an SM
+  e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, RK_CARVEOUT);
+  if (e != cudaSuccess) return e;
+#endif
   vote_average_kernel<<<grid, WT, smem, st>>>(q, work, work_count);
   return cudaGetLastError();
 }

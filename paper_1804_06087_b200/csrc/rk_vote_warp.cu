@@ -24,6 +24,9 @@
 //     the rest scan R; fp32 decisions inside the relative band are redone in fp64 (rare).
 // Counts are lane-owned (no atomics in the loops), flushed with one 64-bit atomic per (warp, v).
 #include <cuda_runtime.h>
+#include <stdlib.h>
+
+#include <algorithm>
 #include <math.h>
 #include <stdint.h>
 
@@ -282,7 +285,13 @@ int vote_warp_threads() { return WT; }
 #ifndef RK_AVG_MINB
 #define RK_AVG_MINB 6
 #endif
-int vote_warp_min_blocks() { return RK_AVG_MINB; }
+int vote_warp_min_blocks() {
+  static const int v = [] {
+    const char* e = getenv("RK_VOTE_PER_SM");  // development knob: averaging CTAs per SM
+    return e ? std::max(1, atoi(e)) : RK_AVG_MINB;
+  }();
+  return v;
+}
 
 cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int32_t* work, unsigned int* work_count,
                              int32_t* st_top, float* st_lsum, float* st_max, int sm_count) {
@@ -295,6 +304,10 @@ cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int
     const int64_t units = (p.N + U - 1) / U;
     int64_t ga = (units + WPC - 1) / WPC;
     if (ga > (int64_t)sm_count * 8) ga = (int64_t)sm_count * 8;
+#ifdef RK_CARVEOUT
+    cudaFuncSetAttribute(vote_classify_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, RK_CARVEOUT);
+    cudaFuncSetAttribute(vote_classify_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, RK_CARVEOUT);
+#endif
     if (p.lsum_in) vote_classify_kernel<true><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lsum, st_max);
     else vote_classify_kernel<false><<<(int)ga, WT, 0, st>>>(p, work, work_count, st_top, st_lsum, st_max);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

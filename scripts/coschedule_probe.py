@@ -43,11 +43,23 @@ def par():
 
 for f in (seq, par, seq, par):
     f()
+A.set_profiling(True)
+Bc.set_profiling(True)
+
+
+def kstats():
+    a, b = A.kernel_stats(), Bc.kernel_stats()
+    return a.get("gemm_heads_tcgen05", {}).get("ms", 0.0), b.get("vote_subsets", {}).get("ms", 0.0)
+
+
 for name, f in (("sequential", seq), ("concurrent", par)):
+    g0, v0 = kstats()
     t0 = time.perf_counter()
     for _ in range(5):
         f()
-    print(f"{name}: {(time.perf_counter() - t0) / 5 * 1e3:.2f} ms")
+    g1, v1 = kstats()
+    print(f"{name}: {(time.perf_counter() - t0) / 5 * 1e3:.2f} ms  (gemm events {(g1 - g0) / 5:.2f} ms, "
+          f"vote events {(v1 - v0) / 5:.2f} ms)")
 A.score(X[:N], N, 0, s1); torch.cuda.synchronize()
 t0 = time.perf_counter()
 for _ in range(5):
