@@ -130,6 +130,8 @@ struct rk_ctx {
   int64_t labels_cap = 0;
   int32_t* d_work = nullptr;  // vote worklist [N] + count
   int64_t work_cap = 0;
+  uint32_t* d_wrec = nullptr;  // K <= 8 logits path: worklist records [N][kRecWords]
+  int64_t wrec_cap = 0;
   uint64_t* d_pairs = nullptr;  // K >= 9: near-tie (sample, subset) pairs for the fp64 recheck kernel
   int64_t pairs_cap = 0;
   int64_t* d_arr = nullptr;
@@ -296,7 +298,7 @@ void rk_destroy(rk_ctx* ctx) {
   cudaDeviceSynchronize();
   void* ptrs[] = {ctx->d_ly, ctx->d_tv, ctx->d_ti, ctx->d_fb, ctx->d_xc, ctx->d_lc, ctx->d_tc, ctx->d_sc,
                   ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lsum, ctx->ws_max, ctx->ws_x,
-                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_pairs, ctx->d_arr, ctx->d_scratch,
+                  ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_wrec, ctx->d_pairs, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& e : ctx->prof.pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -821,6 +823,10 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
           CK(launch_vote_avg(q, grid, st, iota, fbc));
         }
       } else {
+      if (warp_path && !wide) {  // records for the averaging kernel (its inputs in one load per sample)
+        if ((s = ensure(ctx, &ctx->d_wrec, &ctx->wrec_cap, N * kRecWords)) != RK_OK) return s;
+        vp.wrec = ctx->d_wrec;
+      }
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
       if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lsum, st_max, ctx->sm_count));
       else CK(launch_vote_batch(vp, ctx->sm_count, st, ctx->d_work, wc, st_top, st_lsum, st_max));

@@ -35,6 +35,9 @@ struct VoteParams {
   const int32_t* top1_in;    // [N][K] or null
   const float* rmax_in;      // [N][K] or null (row max, from the GEMM epilogue)
   const float* ly_in;        // [N][K] label logits l[m][y] or null (fused mode: no logits rows exist)
+  uint32_t* wrec;            // K <= 8 logits path: [worklist][kRecWords] records written by the classify kernel
+                             // (l[m][y], rmax, lsum, top-1 as u16, n, y) so the averaging kernel's per-sample
+                             // inputs arrive in one coalesced load issued a sample ahead; null = read them by n
   int sm_count;
   const int32_t* labels;     // [N] device
   int64_t N;                 // samples in this chunk
@@ -276,6 +279,8 @@ cudaError_t launch_ac_grad(const RLParams& p, float* grad, float* loss2 /*device
 cudaError_t launch_ac_apply(float* P, const float* g, int64_t npol, int64_t np, float lr_pi, float lr_v,
                             cudaStream_t st);
 
+constexpr int kRecWords = 32;  // worklist record: [0,8) l[m][y], [8,16) rmax, [16,24) lsum, [24,28) top-1 u16,
+                               // 28 n, 29 y (K <= 8)
 constexpr int kFuseT = 16;  // NEXT-3: logits kept per (row, model) by the fused GEMM epilogue
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {

@@ -154,6 +154,7 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
 #ifndef RK_AVG_PD
 #define RK_AVG_PD 1
 #endif
+template <bool REC>
 __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const VoteParams p, const int32_t* work,
                                                               const unsigned int* work_count) {
   extern __shared__ __align__(16) char smem_raw[];
@@ -170,19 +171,31 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
   int32_t* ovC = p.scratch_cls + gw * (size_t)C;
   for (int i = lane; i < JMAX * 32; i += 32) ws.cnt[i] = 0u;
   const int64_t W = *work_count;
-#ifndef RK_AVG_SAMPLEAHEAD
-  if (gw < W && lane * 32 < p.ldc)  // the first sample's rows 1 .. PD-1 (later rows are prefetched in the loop)
+  if (!REC && gw < W && lane * 32 < p.ldc)  // the first sample's rows 1 .. PD-1 (later rows are prefetched in the loop)
     for (int m = 1; m < RK_AVG_PD && m < K; ++m)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(p.logits + ((int64_t)work[gw] * K + m) * p.ldc + lane * 32));
-#endif
+  // REC: the classify kernel's record of worklist entry e (lane i holds word i); the next entry's record is
+  // loaded one sample ahead, so the per-sample dependent chain (entry -> label -> l[m][y], statistics) is gone
+  uint32_t rvn = (REC && gw < W) ? __ldcs(p.wrec + (size_t)gw * kRecWords + lane) : 0u;
 
   for (int64_t e = gw; e < W; e += nw) {
-    const int64_t n = work[e];
-    const int y = p.labels[n];
+    const uint32_t rv = rvn;
+    if (REC && e + nw < W) rvn = __ldcs(p.wrec + (size_t)(e + nw) * kRecWords + lane);
+    const int64_t n = REC ? (int64_t)__shfl_sync(FULL, rv, 28) : (int64_t)work[e];
+    const int y = REC ? (int)__shfl_sync(FULL, rv, 29) : p.labels[n];
     const float* rowbase = p.logits + n * K * p.ldc;
     int tp = 0;
-    float mx = 0.f, ls = 0.f;
-    if (lane < K) {
+    float mx = 0.f, ls = 0.f, ly = INFINITY;  // ly = l[m][y]
+    if (REC) {
+      const uint32_t wmx = __shfl_sync(FULL, rv, 8 + (lane & 7)), wls = __shfl_sync(FULL, rv, 16 + (lane & 7));
+      const uint32_t wtp = __shfl_sync(FULL, rv, 24 + ((lane & 7) >> 1));
+      if (lane < K) {
+        tp = (int)((wtp >> (16 * (lane & 1))) & 0xffffu);
+        mx = __uint_as_float(wmx);
+        ls = __uint_as_float(wls);
+        ly = __uint_as_float(rv);
+      }
+    } else if (lane < K) {
       tp = p.top1_in[n * K + lane];
       ls = p.lsum_in[n * K + lane];
       mx = p.rmax_in[n * K + lane];
@@ -191,29 +204,23 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
     if (lane < K) ws.stop[lane] = tp;
     __syncwarp();
     const float thr = theta_threshold(mx, ls, K, lane);
-    const float ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;  // l[m][y]
+    if (!REC) ly = lane < K ? rowbase[(size_t)lane * p.ldc + y] : INFINITY;
     // ---- 1. candidate set R: one streaming pass over the sample's K rows ----------------------
-    const int64_t nnext = e + nw < W ? (int64_t)work[e + nw] : -1;
-#ifdef RK_AVG_SAMPLEAHEAD
-    // (experiment, slower: 6.0 vs 5.25 ms per 1M at c4) the warp's NEXT sample's K rows go to L2 at once
-    if (nnext >= 0 && lane * 32 < p.ldc)
-      for (int m = 0; m < K; ++m)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.logits + (nnext * K + m) * p.ldc + lane * 32));
-#endif
+    const int64_t nnext = REC ? -1 : (e + nw < W ? (int64_t)work[e + nw] : -1);
     // candidate bits of the lane's classes (lane + 32 i) * 4 + q kept as nibble i of two registers:
     // S_c (>= θ threshold) and "not below y" (>= l[m][y]), OR-ed over the models, no shared atomics
     uint32_t B1 = 0, B2 = 0;
 #pragma unroll 1
     for (int m = 0; m < K; ++m) {
       const float* row = rowbase + (size_t)m * p.ldc;
-#ifndef RK_AVG_SAMPLEAHEAD
       {  // RK_AVG_PD-rows-ahead L2 prefetch (a later row, or one of the next sample's): 128 B per lane
         const int mp = m + RK_AVG_PD;
+        int64_t nn = nnext;
+        if (REC && mp >= K) nn = e + nw < W ? (int64_t)__shfl_sync(FULL, rvn, 28) : -1;  // late: record arrived
         const float* nrow = mp < K ? row + RK_AVG_PD * p.ldc
-                                   : (nnext >= 0 && mp - K < K ? p.logits + (nnext * K + (mp - K)) * p.ldc : nullptr);
+                                   : (nn >= 0 && mp - K < K ? p.logits + (nn * K + (mp - K)) * p.ldc : nullptr);
         if (nrow && lane * 32 < p.ldc) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + lane * 32));
       }
-#endif
       float4 v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -402,14 +409,15 @@ size_t vote_avg_smem_per_warp(const VoteParams& p) { return warp_smem(p, nullptr
 cudaError_t launch_vote_avg(const VoteParams& q, int grid, cudaStream_t st, const int32_t* work,
                             const unsigned int* work_count) {
   const size_t smem = warp_smem(q, nullptr, nullptr) * WPC;
-  cudaError_t e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e;
+  if (q.wrec) {
+    e = cudaFuncSetAttribute(vote_average_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) vote_average_kernel<true><<<grid, WT, smem, st>>>(q, work, work_count);
+  } else {
+    e = cudaFuncSetAttribute(vote_average_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) vote_average_kernel<false><<<grid, WT, smem, st>>>(q, work, work_count);
+  }
   if (e != cudaSuccess) return e;
-#ifdef RK_CARVEOUT
-  // same (maximum) shared-memory carveout as the head GEMM, so the two can share an SM
-  e = cudaFuncSetAttribute(vote_average_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, RK_CARVEOUT);
-  if (e != cudaSuccess) return e;
-#endif
-  vote_average_kernel<<<grid, WT, smem, st>>>(q, work, work_count);
   return cudaGetLastError();
 }
 

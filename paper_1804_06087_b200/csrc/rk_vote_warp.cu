@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
   uint32_t cv[JMAX], ca[JMAX], gv[JMAX];
 #pragma unroll
   for (int j = 0; j < JMAX; ++j) { cv[j] = 0; ca[j] = 0; gv[j] = 0; }
+  __shared__ uint32_t srec[WPC][16][kRecWords];  // worklist records of the warp's current unit (U <= 16)
 
   for (int64_t unit = gw; unit < nunits; unit += nw) {
     uint32_t uni = 0, wmask = 0;
@@ -198,7 +199,19 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
       const float thr = theta_threshold(mx, ls, K, lane);
       const float lym = STATS ? lyv : (lane < K ? rowbase[(size_t)lane * p.ldc + y] : 0.f);
       const bool ycand = __any_sync(FULL, lane < K && lym >= thr);
-      if (ycand) wmask |= 1u << (int)(n - u0);
+      if (ycand) {
+        wmask |= 1u << (int)(n - u0);
+        if (p.wrec) {  // the averaging kernel's per-sample inputs, staged for one coalesced record store
+          uint32_t* r = srec[warp][n - u0];
+          if (lane < K) {
+            r[lane] = __float_as_uint(lym);
+            r[8 + lane] = __float_as_uint(mx);
+            r[16 + lane] = __float_as_uint(ls);
+            reinterpret_cast<uint16_t*>(r + 24)[lane] = (uint16_t)tp;
+          }
+          if (lane == 0) { r[28] = (uint32_t)n; r[29] = (uint32_t)y; }
+        }
+      }
       // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|, y wins iff
       // c_y > 0, no class has more votes, and the tie (if any) goes to y: LOWEST_CLASS -> no tied
       // class below y; BEST_MEMBER -> the best-ranked member among all tied voters votes y (Q2).
@@ -241,6 +254,12 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
       if (lane == 0) base = atomicAdd(work_count, (unsigned int)__popc(wmask));
       base = __shfl_sync(FULL, base, 0);
       if ((wmask >> lane) & 1u) work[base + __popc(wmask & ((1u << lane) - 1u))] = (int32_t)(u0 + lane);
+      if (p.wrec) {  // records in worklist order: one 128-byte store per worklist sample
+        __syncwarp();
+        int k = 0;
+        for (uint32_t wm = wmask; wm; wm &= wm - 1, ++k)
+          p.wrec[(size_t)(base + k) * kRecWords + lane] = srec[warp][__ffs(wm) - 1][lane];
+      }
     }
 #pragma unroll
     for (int j = 0; j < JMAX; ++j) {
