@@ -324,7 +324,7 @@ def main():
         dist.barrier()
     ms = e0.elapsed_time(e1)
     ks = ctx.kernel_stats()
-    diag = ctx.vote_diag() if K <= 8 else (0, 0)
+    diag = ctx.vote_diag() if K <= 8 else (0, 0, 0)
     ctx.set_profiling(False)
     clk = clocks.stop()
     if dist:
@@ -406,9 +406,11 @@ def main():
                         "a_best_single": float(t["cnt_vote"][0]) / max(1, int(t["N"]))},
     }
     if K <= 8:
-        wl, fb = diag
+        wl, fb, sk = diag
         line["vote_stage"]["worklist_frac"] = wl / max(1, n)
         line["vote_stage"]["fallback_frac"] = fb / max(1, n)
+        # rows of worklist samples the averaging kernel did not stream (second-largest-logit proof)
+        line["vote_stage"]["rows_skipped_frac"] = sk / max(1, wl * K)
     ws = workload_stats(ctx, labels, K, C) if rank == 0 and not fused else {}
     line["workload_stats"] = ws
     if vtraffic:  # the honest figure: ncu DRAM bytes of this workload's vote stage per launch / its time

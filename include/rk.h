@@ -293,6 +293,11 @@ rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_
  * are NULL after rk_score_logits. Any pointer argument may be NULL. Valid until the next rk_score*. */
 rk_status rk_outputs(rk_ctx* ctx, const float** logits, int* ldc, const int32_t** top1, const float** rmax,
                      const float** lsum, int64_t* N);
+/* The GEMM epilogue's second-largest logit per (row, model) of the last rk_score batch, [N][K] fp32 device
+ * memory (the row maximum over all classes but one occurrence of rmax, so equal to rmax on a tied maximum;
+ * the averaging kernel's row-skip proof), or NULL when that batch did not produce it
+ * (rk_score_logits, rk_score_labelled, C <= 128). Valid until the next rk_score*. */
+rk_status rk_outputs_s2(rk_ctx* ctx, const float** s2);
 
 /* Parity hook for the labelled moments (A5): the per-(group, subset) majority-vote correct counts of the
  * LAST rk_subset_accumulate chunk, out[g][v-1] = #{n in group g : vote of v correct} (uint8), groups of
@@ -304,9 +309,12 @@ rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64
 
 /* Diagnostics of the LAST rk_subset_accumulate chunk (K <= 8 path): *worklist = samples whose label is an
  * averaging candidate of some subset and that are not unanimous (the samples the averaging kernels visit),
- * *fallback = of those, the samples a fused batch (rk_score_labelled) recomputed with logits (0 otherwise).
- * Synchronises the device. Either pointer may be NULL. */
-rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback);
+ * *fallback = of those, the samples a fused batch (rk_score_labelled) recomputed with logits (0 otherwise),
+ * *rows_skipped = (worklist sample, model) rows the averaging kernel did not stream because the GEMM's
+ * second-largest logit proves they add only the label to the candidate set (rk_score batches with more
+ * than 128 classes; 0 otherwise; a 32-bit diagnostic counter).
+ * Synchronises the device. Any pointer may be NULL. */
+rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback, int64_t* rows_skipped);
 
 /* Per-kernel device time, measured with CUDA events on the launch stream when profiling is on. */
 typedef struct {

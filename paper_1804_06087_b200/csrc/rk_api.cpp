@@ -78,6 +78,9 @@ struct rk_ctx {
   float* ws_lsum = nullptr;
   float* ws_max = nullptr;
   int64_t ws_cap = 0, ws_top1_cap = 0, ws_lsum_cap = 0, ws_max_cap = 0;
+  float* ws_s2 = nullptr;      // [N][K] second-largest logit per row (per-model epilogue, Cp > 128)
+  int64_t ws_s2_cap = 0;
+  bool cur_s2 = false;         // the last rk_score wrote ws_s2
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[4 * 128];
@@ -297,7 +300,7 @@ void rk_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
   void* ptrs[] = {ctx->d_ly, ctx->d_tv, ctx->d_ti, ctx->d_fb, ctx->d_xc, ctx->d_lc, ctx->d_tc, ctx->d_sc,
-                  ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lsum, ctx->ws_max, ctx->ws_x,
+                  ctx->d_best_of, ctx->d_W, ctx->d_bias, ctx->ws_logits, ctx->ws_top1, ctx->ws_lsum, ctx->ws_max, ctx->ws_s2, ctx->ws_x,
                   ctx->d_table, ctx->d_chunk, ctx->d_slow, ctx->d_grp, ctx->d_ovd, ctx->d_fin, ctx->d_qcarry, ctx->d_serve, ctx->d_labels, ctx->d_work, ctx->d_wrec, ctx->d_pairs, ctx->d_arr, ctx->d_scratch,
                   ctx->d_scratch_cls, ctx->d_rew};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -408,12 +411,15 @@ static rk_status score_impl(rk_ctx* ctx, const void* X, int64_t N, int64_t goff,
   if ((s = ensure(ctx, &ctx->ws_top1, &ctx->ws_top1_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_lsum, &ctx->ws_lsum_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if ((s = ensure(ctx, &ctx->ws_max, &ctx->ws_max_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
+  const bool want_s2 = !fused && ctx->Cp > 128;  // per-model epilogue: the averaging kernel's row skipping
+  if (want_s2 && (s = ensure(ctx, &ctx->ws_s2, &ctx->ws_s2_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
   if (fused) {
     if ((s = ensure(ctx, &ctx->d_ly, &ctx->ly_cap, std::max<int64_t>(N, 1) * ctx->K)) != RK_OK) return s;
     if ((s = ensure(ctx, &ctx->d_tv, &ctx->tv_cap, std::max<int64_t>(N, 1) * ctx->K * kFuseT)) != RK_OK) return s;
     if ((s = ensure(ctx, &ctx->d_ti, &ctx->ti_cap, std::max<int64_t>(N, 1) * ctx->K * kFuseT)) != RK_OK) return s;
   }
   ctx->cur_logits = fused ? nullptr : ctx->ws_logits;
+  ctx->cur_s2 = want_s2;
   ctx->cur_ldc = ctx->ldc;
   ctx->cur_N = N;
   ctx->cur_off = goff;
@@ -455,6 +461,7 @@ static rk_status score_impl(rk_ctx* ctx, const void* X, int64_t N, int64_t goff,
     gp.scale_log2 = ctx->scale_log2; gp.bias = ctx->d_bias;
     gp.cluster = ctx->gemm_cluster;
     gp.top1 = ctx->ws_top1 + r0 * ctx->K; gp.lsum = ctx->ws_lsum + r0 * ctx->K; gp.rmax = ctx->ws_max + r0 * ctx->K;
+    gp.rs2 = want_s2 ? ctx->ws_s2 + r0 * ctx->K : nullptr;
     if (fused) {
       gp.labels = dlabels + r0;
       gp.ly = ctx->d_ly + r0 * ctx->K;
@@ -525,6 +532,7 @@ rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, 
   ctx->cur_ldc = ldc;
   ctx->cur_N = N;
   ctx->cur_off = goff;
+  ctx->cur_s2 = false;
   ctx->batch_stats = false;
   ctx->batch_fused = false;
   ctx->cur_labels_arg = nullptr;
@@ -759,7 +767,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     {
       // worklist [N] + count, then (K >= 9) the overflow and the CTA-kernel worklists, [N] + count each,
       // and the near-tie pair count
-      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, 3 * N + 4)) != RK_OK) return s;
+      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, 3 * N + 5)) != RK_OK) return s;
       if (!warp_path) {  // near-tie pairs of the warp averaging kernel (a full list sends samples to the CTA kernel)
         if ((s = ensure(ctx, &ctx->d_pairs, &ctx->pairs_cap, N / 2 + 65536)) != RK_OK) return s;
         vp.pairs = ctx->d_pairs;
@@ -826,6 +834,10 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       if (warp_path && !wide) {  // records for the averaging kernel (its inputs in one load per sample)
         if ((s = ensure(ctx, &ctx->d_wrec, &ctx->wrec_cap, N * kRecWords)) != RK_OK) return s;
         vp.wrec = ctx->d_wrec;
+        static const bool no_skip = getenv("RK_NO_ROW_SKIP") != nullptr;  // development knob (A/B timing)
+        vp.s2_in = (ctx->batch_stats && ctx->cur_s2 && !no_skip) ? ctx->ws_s2 : nullptr;
+        vp.n_skip = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 4);
+        CK(cudaMemsetAsync(vp.n_skip, 0, 4, st));
       }
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
       if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lsum, st_max, ctx->sm_count));
@@ -1356,7 +1368,7 @@ rk_status rk_group_counts(rk_ctx* ctx, uint8_t* out, int64_t cap, int* gs, int64
   return RK_OK;
 }
 
-rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback) {
+rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback, int64_t* rows_skipped) {
   if (!ctx) return RK_EINVAL;
   if (!ctx->reset_done || ctx->chunks == 0) return fail(ctx, RK_ESTATE, "no chunk accumulated since rk_subset_reset");
   CK(cudaSetDevice(ctx->dev));
@@ -1364,8 +1376,19 @@ rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback) {
   unsigned int w = 0;
   if (ctx->d_work && ctx->cur_N > 0) CK(cudaMemcpy(&w, reinterpret_cast<unsigned int*>(ctx->d_work + ctx->cur_N), 4,
                                                    cudaMemcpyDeviceToHost));
+  unsigned int k = 0;
+  if (ctx->d_work && ctx->cur_N > 0 && ctx->K <= 8 && !ctx->batch_fused)
+    CK(cudaMemcpy(&k, reinterpret_cast<unsigned int*>(ctx->d_work + 3 * ctx->cur_N + 4), 4, cudaMemcpyDeviceToHost));
   if (worklist) *worklist = w;
   if (fallback) *fallback = ctx->batch_fused ? ctx->last_fallback : 0;
+  if (rows_skipped) *rows_skipped = k;
+  return RK_OK;
+}
+
+rk_status rk_outputs_s2(rk_ctx* ctx, const float** s2) {
+  if (!ctx) return RK_EINVAL;
+  if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "no batch scored yet");
+  if (s2) *s2 = ctx->cur_s2 ? ctx->ws_s2 : nullptr;
   return RK_OK;
 }
 

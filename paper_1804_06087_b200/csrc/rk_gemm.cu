@@ -216,6 +216,7 @@ struct GemmArgs {
   int32_t* top1;
   float* lsum;
   float* rmax;
+  float* rs2;  // [N][K] second-largest logit (non-packed, non-fused epilogue; null = not written)
   // fused forward + vote (NEXT-3; FUSED instantiation): labels [N]; outputs the label's logit ly [N][K]
   // and the top-kFuseT logits per (row, model), values tv [N][K][T] (descending) and classes ti [N][K][T]
   const int32_t* labels;
@@ -708,7 +709,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<PACK, FUSED>(), 1)
     for (int64_t u = ucl0; u < units; u += ucls) {
       const int mt = (int)(u / a.ng) * CL + crank, model = (int)(u % a.ng);
       const int64_t row = (int64_t)mt * BM + row_in_tile;
-      float mx = -INFINITY, sum = 0.f;
+      float mx = -INFINITY, sum = 0.f, s2 = -INFINITY;  // s2: max over the row without one occurrence of mx
       int arg = 0;
       for (int j = 0; j < a.nt; ++j, ++tc) {
         const int width = min(BN, a.Cp - j * BN);
@@ -737,9 +738,15 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<PACK, FUSED>(), 1)
           if (cmax > mx) {  // new running max (rare after the first chunks): its lowest column (Q4)
 #pragma unroll
             for (int i = 31; i >= 0; --i) carg = v[i] == cmax ? colbase + i : carg;
+            float c2 = -INFINITY;  // this chunk's largest value other than the argmax position
+#pragma unroll
+            for (int i = 0; i < 32; ++i) c2 = fmaxf(c2, colbase + i == carg ? -INFINITY : v[i]);
+            s2 = fmaxf(mx, c2);
             sum = sum * rescale_factor(mx, cmax);
             mx = cmax;
             arg = carg;
+          } else {
+            s2 = fmaxf(s2, cmax);
           }
           if (mx != -INFINITY) {
             const float nml = nml_of(mx);
@@ -770,6 +777,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<PACK, FUSED>(), 1)
         a.top1[row * a.K + model] = arg;
         a.lsum[row * a.K + model] = lsum_of(sum, mx);  // relative to the row max
         a.rmax[row * a.K + model] = mx;
+        if (a.rs2) a.rs2[row * a.K + model] = s2;
       }
     }
     if (lane == 0) tma_store_wait_all();
@@ -897,7 +905,7 @@ cudaError_t launch_gemm(const GemmParams& p, int sm_count, cudaStream_t st) {
   if (p.N <= 0) return cudaSuccess;
   GemmArgs a;
   a.N = p.N; a.K = p.K; a.C = p.C; a.Cp = p.Cp; a.D = p.D;
-  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lsum = p.lsum; a.rmax = p.rmax;
+  a.scale_log2 = p.scale_log2; a.bias = p.bias; a.top1 = p.top1; a.lsum = p.lsum; a.rmax = p.rmax; a.rs2 = p.rs2;
   a.labels = p.labels; a.ly = p.ly; a.tv = p.tv; a.ti = p.ti;
   const bool pack = p.Cp <= 128;  // small heads: tiles span several models
   a.ng = pack ? 1 : p.K;

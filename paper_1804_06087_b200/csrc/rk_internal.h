@@ -35,6 +35,10 @@ struct VoteParams {
   const int32_t* top1_in;    // [N][K] or null
   const float* rmax_in;      // [N][K] or null (row max, from the GEMM epilogue)
   const float* ly_in;        // [N][K] label logits l[m][y] or null (fused mode: no logits rows exist)
+  const float* s2_in;        // [N][K] second-largest logit per row (GEMM epilogue) or null: rows whose top-1 is
+                             // y and whose other classes all lie below the theta threshold add only y to the
+                             // averaging candidate set, so the averaging kernel skips streaming them
+  unsigned int* n_skip;      // with s2_in: number of such rows over the worklist (diagnostic) or null
   uint32_t* wrec;            // K <= 8 logits path: [worklist][kRecWords] records written by the classify kernel
                              // (l[m][y], rmax, lsum, top-1 as u16, n, y) so the averaging kernel's per-sample
                              // inputs arrive in one coalesced load issued a sample ahead; null = read them by n
@@ -280,7 +284,7 @@ cudaError_t launch_ac_apply(float* P, const float* g, int64_t npol, int64_t np, 
                             cudaStream_t st);
 
 constexpr int kRecWords = 32;  // worklist record: [0,8) l[m][y], [8,16) rmax, [16,24) lsum, [24,28) top-1 u16,
-                               // 28 n, 29 y (K <= 8)
+                               // 28 n, 29 y, 30 mask of the rows the averaging kernel need not stream (K <= 8)
 constexpr int kFuseT = 16;  // NEXT-3: logits kept per (row, model) by the fused GEMM epilogue
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {
@@ -295,6 +299,8 @@ struct GemmParams {
   int32_t* top1;         // [N][K]
   float* lsum;           // [N][K] log sum_c exp(l - rmax) (relative to the row max)
   float* rmax;           // [N][K] row max (theta of the candidate pruning)
+  float* rs2;            // [N][K] second-largest logit (max without one occurrence of rmax), or null;
+                         // written by the per-model (Cp > 128) logits epilogue only
   float* logits;         // [N][K][ldc]
   unsigned int* err;
   int cluster;           // 1 = one CTA per 128-row tile; 2 = CTA pair, tcgen05.mma.cta_group::2 on 256-row tiles

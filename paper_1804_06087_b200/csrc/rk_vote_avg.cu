@@ -151,9 +151,6 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
 #ifndef RK_AVG_MINB
 #define RK_AVG_MINB 6
 #endif
-#ifndef RK_AVG_PD
-#define RK_AVG_PD 1
-#endif
 template <bool REC>
 __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const VoteParams p, const int32_t* work,
                                                               const unsigned int* work_count) {
@@ -171,9 +168,6 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
   int32_t* ovC = p.scratch_cls + gw * (size_t)C;
   for (int i = lane; i < JMAX * 32; i += 32) ws.cnt[i] = 0u;
   const int64_t W = *work_count;
-  if (!REC && gw < W && lane * 32 < p.ldc)  // the first sample's rows 1 .. PD-1 (later rows are prefetched in the loop)
-    for (int m = 1; m < RK_AVG_PD && m < K; ++m)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(p.logits + ((int64_t)work[gw] * K + m) * p.ldc + lane * 32));
   // REC: the classify kernel's record of worklist entry e (lane i holds word i); the next entry's record is
   // loaded one sample ahead, so the per-sample dependent chain (entry -> label -> l[m][y], statistics) is gone
   uint32_t rvn = (REC && gw < W) ? __ldcs(p.wrec + (size_t)gw * kRecWords + lane) : 0u;
@@ -210,15 +204,26 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
     // candidate bits of the lane's classes (lane + 32 i) * 4 + q kept as nibble i of two registers:
     // S_c (>= θ threshold) and "not below y" (>= l[m][y]), OR-ed over the models, no shared atomics
     uint32_t B1 = 0, B2 = 0;
+    // rows to stream: REC drops the rows the classify kernel proved add only y to R (record word 30)
+    const uint32_t live = ((1u << K) - 1u) & ~(REC ? __shfl_sync(FULL, rv, 30) : 0u);
 #pragma unroll 1
-    for (int m = 0; m < K; ++m) {
+    for (uint32_t lm = live; lm; lm &= lm - 1) {
+      const int m = __ffs(lm) - 1;
       const float* row = rowbase + (size_t)m * p.ldc;
-      {  // RK_AVG_PD-rows-ahead L2 prefetch (a later row, or one of the next sample's): 128 B per lane
-        const int mp = m + RK_AVG_PD;
-        int64_t nn = nnext;
-        if (REC && mp >= K) nn = e + nw < W ? (int64_t)__shfl_sync(FULL, rvn, 28) : -1;  // late: record arrived
-        const float* nrow = mp < K ? row + RK_AVG_PD * p.ldc
-                                   : (nn >= 0 && mp - K < K ? p.logits + (nn * K + (mp - K)) * p.ldc : nullptr);
+      {  // one-row-ahead L2 prefetch (the next live row, else the next sample's first one): 128 B per lane
+        const uint32_t rest = lm & (lm - 1);
+        const float* nrow = nullptr;
+        if (rest) {
+          nrow = rowbase + (size_t)(__ffs(rest) - 1) * p.ldc;
+        } else if (REC) {
+          if (e + nw < W) {  // late in the sample: the next record has arrived
+            const int64_t n2 = (int64_t)__shfl_sync(FULL, rvn, 28);
+            const uint32_t l2 = ((1u << K) - 1u) & ~__shfl_sync(FULL, rvn, 30);
+            if (l2) nrow = p.logits + (n2 * K + (__ffs(l2) - 1)) * p.ldc;
+          }
+        } else if (nnext >= 0) {
+          nrow = p.logits + nnext * K * p.ldc;
+        }
         if (nrow && lane * 32 < p.ldc) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + lane * 32));
       }
       float4 v[8];
@@ -247,6 +252,14 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
           B2 |= bitsB << (4 * i);
         }
       }
+    }
+    // y is in R on every worklist sample (y >= l[m][y] in each model; the classify kernel put the sample
+    // on the worklist because l[m][y] >= theta threshold in some model). With skipped rows that model's
+    // row may not have been streamed, so y's bits are set here explicitly (a no-op otherwise).
+    if (lane == ((y >> 2) & 31)) {
+      const uint32_t yb = 1u << (4 * (y >> 7) + (y & 3));
+      B1 |= yb;
+      B2 |= yb;
     }
     {  // R nibbles -> 32-class words: nibble i of lanes 8k..8k+7 forms word 4i + k
       const uint32_t Rn = B1 & B2;

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
 #pragma unroll
   for (int j = 0; j < JMAX; ++j) { cv[j] = 0; ca[j] = 0; gv[j] = 0; }
   __shared__ uint32_t srec[WPC][16][kRecWords];  // worklist records of the warp's current unit (U <= 16)
+  uint32_t nskip = 0;
 
   for (int64_t unit = gw; unit < nunits; unit += nw) {
     uint32_t uni = 0, wmask = 0;
@@ -88,13 +89,14 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
     // l[m][y] are loaded one sample ahead, off the per-sample dependent load chain
     const int ylane = (lane < U && u0 + lane < s1) ? p.labels[u0 + lane] : 0;
     int ntp = 0;
-    float nls = 0.f, nmx = 0.f, nly = 0.f;
+    float nls = 0.f, nmx = 0.f, nly = 0.f, ns2 = INFINITY;
     auto prefetch = [&](int64_t nn) {
       const int yy = __shfl_sync(FULL, ylane, (int)(nn - u0) & 31);
       if (STATS && nn < s1 && lane < K) {
         ntp = p.top1_in[nn * K + lane];
         nls = p.lsum_in[nn * K + lane];
         nmx = p.rmax_in[nn * K + lane];
+        if (p.s2_in) ns2 = p.s2_in[nn * K + lane];
         nly = (yy >= 0 && yy < C) ? (p.ly_in ? p.ly_in[nn * K + lane] : p.logits[(nn * K + lane) * p.ldc + yy]) : 0.f;
       }
     };
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
     for (int64_t n = u0; n < s1; ++n) {
       int tp = ntp;
       float mx = nmx, ls = nls;
-      const float lyv = nly;
+      const float lyv = nly, s2v = ns2;
       prefetch(n + 1);
       const int y = __shfl_sync(FULL, ylane, (int)(n - u0));
       if (y < 0 || y >= C) {
@@ -209,7 +211,13 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
             r[16 + lane] = __float_as_uint(ls);
             reinterpret_cast<uint16_t*>(r + 24)[lane] = (uint16_t)tp;
           }
-          if (lane == 0) { r[28] = (uint32_t)n; r[29] = (uint32_t)y; }
+          // rows that add only y to the candidate set R of the averaging kernel: y is the top-1 and every
+          // other class (<= the second-largest logit) lies below the theta threshold, i.e. outside S_c
+          // (y itself is in R on every worklist sample), so that kernel need not stream them; the margin
+          // absorbs any rounding difference between the two kernels' evaluations of the same threshold
+          const uint32_t skip = __ballot_sync(FULL, STATS && lane < K && tp == y && s2v < thr - (1e-4f + 1e-5f * fabsf(thr)));
+          if (lane == 0) { r[28] = (uint32_t)n; r[29] = (uint32_t)y; r[30] = skip; }
+          nskip += __popc(skip);
         }
       }
       // A3: majority vote, decided relative to y: with c_j = |v ∩ M_j|, y wins iff
@@ -273,6 +281,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
       gv[j] = 0;
     }
   }
+  if (p.n_skip && lane == 0 && nskip) atomicAdd(p.n_skip, nskip);
 #pragma unroll
   for (int j = 0; j < JMAX; ++j) {
     const int v1 = lane + 32 * j;

@@ -25,7 +25,7 @@ TIE_BEST_MEMBER, TIE_LOWEST_CLASS = 0, 1
 EXPORTS = ["rk_create", "rk_nccl_unique_id", "rk_load_ensemble", "rk_score", "rk_score_logits", "rk_subset_reset",
            "rk_subset_accumulate", "rk_subset_finalize", "rk_subset_stats", "rk_predict", "rk_greedy_serve", "rk_outputs",
            "rk_sine_arrivals", "rk_async_serve", "rk_serve_stream", "rk_ac_dims", "rk_ac_rollout", "rk_ac_grad",
-           "rk_ac_apply", "rk_score_labelled", "rk_vote_diag",
+           "rk_ac_apply", "rk_score_labelled", "rk_vote_diag", "rk_outputs_s2",
            "rk_group_counts",
            "rk_set_profiling", "rk_kernel_stats", "rk_last_error", "rk_status_string", "rk_destroy"]
 
@@ -86,13 +86,14 @@ def load_library(path: str | None = None):
     L.rk_score.argtypes = [vp, vp, i64, i64, vp]
     L.rk_score_logits.argtypes = [vp, vp, i32, i64, i64, vp]
     L.rk_score_labelled.argtypes = [vp, vp, vp, i64, i64, vp]
-    L.rk_vote_diag.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.rk_vote_diag.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.rk_subset_reset.argtypes = [vp, ctypes.POINTER(_Cfg)]
     L.rk_subset_accumulate.argtypes = [vp, vp, vp]
     L.rk_subset_finalize.argtypes = [vp, ctypes.POINTER(_Table), vp]
     L.rk_subset_stats.argtypes = [vp, vp, ctypes.POINTER(_Cfg), ctypes.POINTER(_Table), vp]
     L.rk_predict.argtypes = [vp, u32, vp, vp, vp, vp]
     L.rk_greedy_serve.argtypes = [vp, ctypes.POINTER(_Cfg), i64, i64, vp, ctypes.POINTER(_Serve), vp]
+    L.rk_outputs_s2.argtypes = [vp, ctypes.POINTER(vp)]
     L.rk_outputs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i32), ctypes.POINTER(vp), ctypes.POINTER(vp),
                              ctypes.POINTER(vp), ctypes.POINTER(i64)]
     L.rk_group_counts.argtypes = [vp, vp, i64, ctypes.POINTER(i32), ctypes.POINTER(i64), vp]
@@ -370,6 +371,12 @@ class Context:
         return {"logits": lg.value, "ldc": ldc.value, "top1": t1.value, "rmax": mx.value, "lsum": ls.value,
                 "N": n.value}
 
+    def outputs_s2(self):
+        """Device pointer of the last rk_score batch's second-largest logits [N][K] fp32, or None."""
+        s2 = ctypes.c_void_p()
+        self._chk(self._L.rk_outputs_s2(self._p, ctypes.byref(s2)), "rk_outputs_s2")
+        return s2.value
+
     def group_counts(self, stream=None):
         """Per-(group, subset) vote-correct counts of the last accumulated chunk: (gs, uint8 [groups][S])."""
         gs, ng = ctypes.c_int(), ctypes.c_int64()
@@ -382,10 +389,10 @@ class Context:
         return gs.value, out
 
     def vote_diag(self):
-        """(worklist, fallback) sample counts of the last accumulated chunk (K <= 8 path)."""
-        w, f = ctypes.c_int64(), ctypes.c_int64()
-        self._chk(self._L.rk_vote_diag(self._p, ctypes.byref(w), ctypes.byref(f)), "rk_vote_diag")
-        return w.value, f.value
+        """(worklist, fallback, rows_skipped) counts of the last accumulated chunk (K <= 8 path)."""
+        w, f, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        self._chk(self._L.rk_vote_diag(self._p, ctypes.byref(w), ctypes.byref(f), ctypes.byref(k)), "rk_vote_diag")
+        return w.value, f.value, k.value
 
     def set_profiling(self, on: bool):
         self._chk(self._L.rk_set_profiling(self._p, int(on)), "rk_set_profiling")

@@ -52,7 +52,7 @@ def run(rk, K, C, D, N, y, X, W, b, sh, cfg, tie, fused):
 def test_fused_parity(rk, K, C, D, N, tie):
     y, X, W, b, sh = heads(K, C, D, N, 40 + K)
     gcfg, ocfg = default_cfg(K)
-    t, (work, fb) = run(rk, K, C, D, N, y, X, W, b, sh, gcfg, tie, True)
+    t, (work, fb, _) = run(rk, K, C, D, N, y, X, W, b, sh, gcfg, tie, True)
     o = oracle.table(oracle.logits_gemm(X, W, b, sh), y, K, C, tie=tie, cfg=ocfg)
     compare_tables(t, o, K=K)
     tu, _ = run(rk, K, C, D, N, y, X, W, b, sh, gcfg, tie, False)
@@ -69,7 +69,7 @@ def test_fallback_route_taken(rk):
     y, X, W, b, _ = heads(K, C, D, N, 7)
     sh = -6
     gcfg, ocfg = default_cfg(K)
-    t, (work, fb) = run(rk, K, C, D, N, y, X, W, b * 0, sh, gcfg, 0, True)
+    t, (work, fb, _) = run(rk, K, C, D, N, y, X, W, b * 0, sh, gcfg, 0, True)
     o = oracle.table(oracle.logits_gemm(X, W, b * 0, sh), y, K, C, cfg=ocfg)
     compare_tables(t, o, K=K)
     assert 0 < fb < work, (work, fb)

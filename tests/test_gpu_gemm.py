@@ -66,6 +66,14 @@ def test_int_mode_bit_exact(rk, K, C, D, N, cluster, monkeypatch):
     np.testing.assert_array_equal(lg[:, :, :C], ref.astype(np.float32))
     np.testing.assert_array_equal(t1, np.argmax(ref, axis=2))
     check_row_stats(ls, ref)
+    # second-largest logit (the averaging kernel's row-skip proof): per-model epilogue only (Cp > 128);
+    # ties at the maximum are frequent on this integer grid, where it must equal the maximum
+    p2 = ctx.outputs_s2()
+    if (C + 15) // 16 * 16 > 128:
+        s2 = dev_view(p2, (N, K), "<f4")
+        np.testing.assert_array_equal(s2, np.sort(ref, axis=2)[:, :, -2].astype(np.float32))
+    else:
+        assert p2 is None
 
 
 def check_row_stats(stats, ref):

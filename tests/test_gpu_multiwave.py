@@ -7,7 +7,8 @@ its multi-iteration paths are taken:
   * c4 shape: K = 8, C = 1000, N = 131,072, B = {16, ..., 256}, the bench's 4 rates, both tie modes;
   * c5 shape: K = 12, C = 100, N = 65,536, same reward configuration, both tie modes;
   * c4 heads through rk_score (tcgen05 GEMM, integer mode) at N = 16,384 (64 CTA-pair row tiles x 8
-    models = 7 waves of work units), both tie modes.
+    models = 7 waves of work units), both tie modes; this path also runs the averaging kernel's row
+    skipping (rows proven by the GEMM's second-largest logit to add only y to the candidate set).
 
 Compared: cnt_vote, corr, O, Q, E bit-exact; cnt_avg within the oracle's ambiguous pairs; rewards within
 1e-5; and the per-(16-sample group, subset) vote counts behind Q (rk_group_counts) element by element
@@ -91,3 +92,6 @@ def test_heads_multiwave_c4(rk, tie):
     o = oracle.table(ref, y, K, C, tie=tie, cfg=ocfg, want_bits=True)
     compare_tables(t, o, K=K)
     check_groups(ctx, o, N, (1 << K) - 1)
+    # the averaging kernel's row skipping (second-largest-logit proof) was exercised on this workload
+    work, _, skipped = ctx.vote_diag()
+    assert work > 0 and 0 < skipped < work * K
