@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
   WS ws;
   warp_smem(p, smem_raw + warp * warp_smem(p, nullptr, nullptr), &ws);
   const int K = p.K, S = p.S, C = p.C;
-  const int F = (int)(p.ldc >> 2);
   const int TA = 1 << p.K1, TT = TA + (1 << (K - p.K1));
   const int CAPS = p.CAP + 1;
   const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
@@ -230,8 +229,16 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int c4 = lane + 32 * i;
-        v[i] = (c4 < F && c4 * 4 < C) ? ldg_stream(row + c4 * 4)
-                                       : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        v[i] = c4 * 4 < C ? ldg_stream(row + c4 * 4) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+      if (C & 3) {  // the padding components (c >= C, never written) of the last float4 -> -inf, once per row
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (lane + 32 * i == ((C - 1) >> 2)) {
+            if ((C & 3) < 2) v[i].y = -INFINITY;
+            if ((C & 3) < 3) v[i].z = -INFINITY;
+            v[i].w = -INFINITY;
+          }
       }
       const float t_m = __shfl_sync(FULL, thr, m);
       const float y_m = __shfl_sync(FULL, ly, m);
@@ -239,15 +246,11 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float4 x4 = v[i];
-        if (fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)) >= lo) {  // fast reject (fmaxf drops NaN padding)
-          const int cb = (lane + 32 * i) * 4;
-          uint32_t bits = 0, bitsB = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float x = f4c(x4, q);
-            bits |= (x >= t_m && cb + q < C) ? (1u << q) : 0u;
-            bitsB |= (x >= y_m && cb + q < C) ? (1u << q) : 0u;
-          }
+        if (fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w)) >= lo) {  // fast reject
+          const uint32_t bits = (x4.x >= t_m ? 1u : 0u) | (x4.y >= t_m ? 2u : 0u) | (x4.z >= t_m ? 4u : 0u) |
+                                (x4.w >= t_m ? 8u : 0u);
+          const uint32_t bitsB = (x4.x >= y_m ? 1u : 0u) | (x4.y >= y_m ? 2u : 0u) | (x4.z >= y_m ? 4u : 0u) |
+                                 (x4.w >= y_m ? 8u : 0u);
           B1 |= bits << (4 * i);
           B2 |= bitsB << (4 * i);
         }
@@ -331,17 +334,19 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
     }
     __syncwarp();
     // ---- 3. bound for candidates outside {y} ∪ D, and the exact-column half tables ------------
-#pragma unroll 1
-    for (int m = 0; m < K; ++m) {
+    {  // lane = 4 m + part: model m's competitors sl = part, part + 4, ... (K <= 8 -> all models at once)
+      const int m = lane >> 2, part = lane & 3;
       float q = 0.f;
-      for (int sl = lane; sl < nc; sl += 32) {
-        bool ex = sl == ys;
+      if (m < K)
+        for (int sl = part; sl < nc; sl += 4) {
+          bool ex = sl == ys;
 #pragma unroll
-        for (int d = 0; d < 8; ++d) ex |= (d < nd && sl == dslot[d]);
-        if (!ex) q = fmaxf(q, P[(size_t)m * ps + sl]);
-      }
-      for (int off = 16; off; off >>= 1) q = fmaxf(q, __shfl_xor_sync(FULL, q, off));
-      if (lane == 0) ws.Q[m] = q;
+          for (int d = 0; d < 8; ++d) ex |= (d < nd && sl == dslot[d]);
+          if (!ex) q = fmaxf(q, P[(size_t)m * ps + sl]);
+        }
+      q = fmaxf(q, __shfl_xor_sync(FULL, q, 1));
+      q = fmaxf(q, __shfl_xor_sync(FULL, q, 2));
+      if (part == 0 && m < K) ws.Q[m] = q;
     }
     __syncwarp();
     if (lane < TT) {  // lane h builds half-mask row h
