@@ -316,21 +316,21 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
     // ---- 2. gather p[m][c] = exp((l - mx_m) - lsum_m) for c in R ------------------------------------------
     float* P = ovf ? ovP : ws.P;
     const int ps = ovf ? C : CAPS;
-    float lsm[8], mxm[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      lsm[m] = __shfl_sync(FULL, ls, m < K ? m : 0);
-      mxm[m] = __shfl_sync(FULL, mx, m < K ? m : 0);
-    }
-    for (int sl = lane; sl < nc; sl += 32) {
-      const int cq = cls[sl];
-      float l[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m)  // K independent loads in flight (L2 hits: the rows were just streamed)
-        l[m] = m < K ? __ldg(rowbase + (size_t)m * p.ldc + cq) : 0.f;
-#pragma unroll
-      for (int m = 0; m < 8; ++m)
-        if (m < K) P[(size_t)m * ps + sl] = expf((l[m] - mxm[m]) - lsm[m]);  // exact l - mx near the max
+    {  // lane = 4 m + part gathers model m's columns sl = part, part + 4, ... (L2 hits: the rows were just
+       // streamed; skipped rows come from DRAM), all loads of a lane issued before their exponentials
+      const int m = lane >> 2, part = lane & 3;
+      const float mxl = __shfl_sync(FULL, mx, m), lsl = __shfl_sync(FULL, ls, m);
+      if (m < K) {
+        const float* row = rowbase + (size_t)m * p.ldc;
+        float* Pm = P + (size_t)m * ps;
+        int sl = part;
+        for (; sl + 4 < nc; sl += 8) {
+          const float l0 = __ldg(row + cls[sl]), l1 = __ldg(row + cls[sl + 4]);
+          Pm[sl] = expf((l0 - mxl) - lsl);  // exact l - mx near the max
+          Pm[sl + 4] = expf((l1 - mxl) - lsl);
+        }
+        if (sl < nc) Pm[sl] = expf((__ldg(row + cls[sl]) - mxl) - lsl);
+      }
     }
     __syncwarp();
     // ---- 3. bound for candidates outside {y} ∪ D, and the exact-column half tables ------------
