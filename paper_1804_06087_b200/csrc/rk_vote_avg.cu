@@ -149,7 +149,7 @@ __device__ __noinline__ void recheck_fp64(const VoteParams& p, WS& ws, uint32_t 
 }
 
 #ifndef RK_AVG_MINB
-#define RK_AVG_MINB 6
+#define RK_AVG_MINB 7
 #endif
 template <bool REC>
 __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const VoteParams p, const int32_t* work,

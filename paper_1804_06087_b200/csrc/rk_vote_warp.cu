@@ -311,7 +311,7 @@ cudaError_t launch_vote_classify(const VoteParams& p, cudaStream_t st, int32_t* 
 size_t vote_warp_smem_per_warp(const VoteParams& p) { return vote_avg_smem_per_warp(p); }
 int vote_warp_threads() { return WT; }
 #ifndef RK_AVG_MINB
-#define RK_AVG_MINB 6
+#define RK_AVG_MINB 7
 #endif
 int vote_warp_min_blocks() {
   static const int v = [] {
