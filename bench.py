@@ -376,7 +376,8 @@ def main():
     traffic = vtraffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):  # ncu dram bytes per launch of this workload (scripts/summarize_profiles.py)
-        tj = json.load(open(tp)).get(cfgname, {})
+        # the fused path (NEXT-3) moves different bytes: only its own capture's figures apply
+        tj = json.load(open(tp)).get(cfgname + ("_fused" if fused else ""), {})
         traffic, vtraffic = tj.get("gemm_heads_tcgen05"), tj.get("vote_subsets")
     launches = args.steps * kernels_per_step(K, C, cfg, args.queue, fused, diag[1] > 0)
     line = {

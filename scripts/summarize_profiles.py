@@ -58,7 +58,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "smsp__inst_executed.sum", "launch__grid_size", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
 summary = {}
-for tag in ("gemm", "vote", "k12", "gemm12"):
+for tag in ("gemm", "vote", "k12", "gemm12", "fused"):
     try:
         recs = raw(f"gpurun_out/{R}_{tag}.ncu-rep")
     except Exception as e:  # noqa: BLE001
@@ -71,7 +71,10 @@ for tag in ("gemm", "vote", "k12", "gemm12"):
             for k, v in rec.items():
                 if k.startswith(w):
                     d[k] = v
-        summary[f"{tag}:{name}"] = d
+        key = f"{tag}:{name}"
+        if key in summary:  # (the fused capture holds two GEMM instantiations / repeated kernels)
+            key += f"#{sum(1 for k in summary if k.startswith(key))}"
+        summary[key] = d
 json.dump(summary, open(f"{OUT}/{R}_ncu_full.json", "w"), indent=1)
 print(open(f"{OUT}/{R}_launches.md").read())
 for k, d in summary.items():
@@ -80,10 +83,20 @@ for k, d in summary.items():
         print("   ", kk, vv)
 
 # ---- DRAM traffic per launch for bench.py's roofline.traffic (scaled linearly in N to c4) ----------
-CAPN = {"gemm": 65536, "vote": 200000, "k12": 250000, "gemm12": 131072}  # N of the captures in scripts/profile_round.sh
+CAPN = {"gemm": 65536, "vote": 200000, "k12": 250000, "gemm12": 131072, "fused": 131072}  # N of the captures
 per_sample = {}
+fused_ps = {"gemm": 0.0, "vote": 0.0, "fallback": 0.0}  # NEXT-3 path: fused GEMM, classify + sparse, fallback
 for key, d in summary.items():
     tag, name = key.split(":", 1)
+    if tag == "fused":
+        b = 0.0
+        for mk in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            val, unit = d.get(mk, "0 byte").split()[:2]
+            b += float(val) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[unit] / CAPN["fused"]
+        part = ("gemm" if name.startswith("gemm_heads_kernel<2, 0, 1>")
+                else "vote" if name.startswith(("vote_classify", "vote_sparse")) else "fallback")
+        fused_ps[part] += b
+        continue
     if tag in ("k12", "gemm12"):
         continue  # c5 shape: reported in the summary, not part of the c4 traffic figure
     rd = float(d.get("dram__bytes_read.sum", "0 byte").split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[
@@ -109,6 +122,9 @@ tj = {"_note": f"DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per l
                f"vote 32,004 B/sample.",
       "c4": {"gemm_heads_tcgen05": round(gemm_ps * 1e6), "vote_subsets": round(vote_ps * 1e6)},
       "c5": {"vote_subsets": round(k12_ps * 4e6)},
+      "c4_fused": {"gemm_heads_tcgen05": round(fused_ps["gemm"] * 1e6), "vote_subsets": round(fused_ps["vote"] * 1e6),
+                   "fused_fallback": round(fused_ps["fallback"] * 1e6),
+                   "_note": f"NEXT-3 capture ({R}_fused, N={CAPN['fused']}) scaled to N=1,000,000"},
       "per_sample": {k: round(v, 1) for k, v in per_sample.items()}}
 json.dump(tj, open(f"{OUT}/traffic.json", "w"), indent=1)
 print(json.dumps(tj, indent=1))

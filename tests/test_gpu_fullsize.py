@@ -18,7 +18,10 @@ size:
      self-consistency check; the oracle comparison of whole tables at multi-wave sizes of these
      shapes -- c4 N = 131,072, c5 N = 65,536 -- is tests/test_gpu_multiwave.py);
   5. fold (A7) of the full-size table: rewards equal eq. `multi_acc_reward` applied
-     to the returned integer sections.
+     to the returned integer sections;
+  6. c4: the averaging kernel's row skipping (rows the GEMM's second-largest logit proves irrelevant are
+     not streamed) leaves the full-size table unchanged: the same logits through rk_score_logits, where
+     every row is streamed, give the identical table.
 """
 import numpy as np
 import pytest
@@ -136,6 +139,19 @@ def test_fullsize(rk, name):
         c2.close()
     for k in ("cnt_vote", "cnt_avg", "corr", "O", "Q", "E"):
         np.testing.assert_array_equal(acc[k], t[k], err_msg=k)
+
+    # 6. (K <= 8) the averaging kernel's row skipping and worklist records at full size: the same logits fed
+    #    back through rk_score_logits (statistics recomputed by the classify kernel, no second-largest
+    #    logit -> every row streamed) give the same table
+    if K <= 8:
+        work, _, skipped = ctx.vote_diag()
+        assert 0 < skipped < work * K
+        ctx.score_logits(torch.as_tensor(_CAI(out["logits"], (N, K, ldc), "<f4"), device="cuda"), ldc, N, 0)
+        t2 = ctx.subset_stats(labels, cfg)
+        torch.cuda.synchronize()
+        assert ctx.vote_diag()[2] == 0
+        for k in ("cnt_vote", "cnt_avg", "corr", "O", "Q", "E"):
+            np.testing.assert_array_equal(t2[k], t[k], err_msg=f"row skipping changed {k}")
 
     # 5. fold of the full-size integer table (eq. multi_acc_reward; readings Q7, Q11, Q13)
     B = np.array(c["B"], dtype=np.float64)
