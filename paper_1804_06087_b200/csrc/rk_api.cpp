@@ -135,6 +135,8 @@ struct rk_ctx {
   int64_t work_cap = 0;
   uint32_t* d_wrec = nullptr;  // K <= 8 logits path: worklist records [N][kRecWords]
   int64_t wrec_cap = 0;
+  void* h_stage = nullptr;     // page-locked host staging of the finalized table and rewards (grow-only)
+  size_t h_stage_bytes = 0;
   uint64_t* d_pairs = nullptr;  // K >= 9: near-tie (sample, subset) pairs for the fp64 recheck kernel
   int64_t pairs_cap = 0;
   int64_t* d_arr = nullptr;
@@ -309,6 +311,7 @@ void rk_destroy(rk_ctx* ctx) {
   for (auto e : ctx->ev_chunks) cudaEventDestroy(e);
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   delete ctx;
 }
@@ -969,22 +972,32 @@ rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream) {
     ProfScope ps(ctx, KK_FOLD, st, 0, 0);
     CK(launch_fold(fp, st));
   }
-  std::vector<unsigned long long> h(ctx->table_words);
-  CK(cudaMemcpyAsync(h.data(), ctx->d_table, ctx->table_words * 8, cudaMemcpyDeviceToHost, st));
-  std::vector<double> rew(2 * nrew);
-  if (nrew) CK(cudaMemcpyAsync(rew.data(), ctx->d_rew, 2 * nrew * 8, cudaMemcpyDeviceToHost, st));
+  // the table and rewards come back by DMA into a context-owned page-locked buffer (grow-only): a pageable
+  // destination made the driver stage the copy, and a fresh vector per call paid zeroing and page faults
+  const size_t need = (ctx->table_words + 2 * nrew) * 8;
+  if (ctx->h_stage_bytes < need) {
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->h_stage_bytes = 0;
+    CK(cudaMallocHost(&ctx->h_stage, need));
+    ctx->h_stage_bytes = need;
+  }
+  unsigned long long* h = static_cast<unsigned long long*>(ctx->h_stage);
+  double* rew = reinterpret_cast<double*>(h + ctx->table_words);
+  CK(cudaMemcpyAsync(h, ctx->d_table, ctx->table_words * 8, cudaMemcpyDeviceToHost, st));
+  if (nrew) CK(cudaMemcpyAsync(rew, ctx->d_rew, 2 * nrew * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   rk_status status = RK_OK;
   if (h[ctx->off_err + 0]) status = fail(ctx, RK_ENONFINITE, "non-finite logits (NaN, +inf or an all -inf row)");
   else if (h[ctx->off_err + 1]) status = fail(ctx, RK_ELABEL, "label outside [0, C)");
   else if (h[ctx->off_err + 2]) status = fail(ctx, RK_EINVAL, "arrival_ns not non-decreasing inside a batch");
   if (status != RK_OK) {
-    std::fill(h.begin(), h.end(), 0ull);
-    std::fill(rew.begin(), rew.end(), 0.0);
+    std::fill(h, h + ctx->table_words, 0ull);
+    std::fill(rew, rew + 2 * nrew, 0.0);
   }
   if (out) {
     out->N = (int64_t)h[ctx->off_N];
-    auto cp = [&](uint64_t* dst, int64_t off, size_t n) { if (dst && n) memcpy(dst, h.data() + off, n * 8); };
+    auto cp = [&](uint64_t* dst, int64_t off, size_t n) { if (dst && n) memcpy(dst, h + off, n * 8); };
     cp(out->cnt_vote, ctx->off_vote, S);
     cp(out->cnt_avg, ctx->off_avg, S);
     cp(out->n_recheck, ctx->off_rc, S);
@@ -992,8 +1005,8 @@ rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream) {
     cp(out->O, ctx->off_O, nrew);
     cp(out->Q, ctx->off_Q, ctx->want_labelled ? nrew : 0);
     cp(out->E, ctx->off_E, ctx->want_exceed ? nrew : 0);
-    if (out->reward_sur && nrew) memcpy(out->reward_sur, rew.data(), nrew * 8);
-    if (out->reward_lab && nrew) memcpy(out->reward_lab, rew.data() + nrew, nrew * 8);
+    if (out->reward_sur && nrew) memcpy(out->reward_sur, rew, nrew * 8);
+    if (out->reward_lab && nrew) memcpy(out->reward_lab, rew + nrew, nrew * 8);
   }
   return status;
 }

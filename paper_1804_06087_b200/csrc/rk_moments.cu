@@ -269,6 +269,7 @@ struct QConst {
   int nbc[kMaxB];     // batches per chunk (L / B)
   int soff[kMaxB];    // first staged batch of each size
   int64_t nbat[kMaxB];  // complete batches in this accumulate call (reading Q13)
+  uint32_t packed;      // q_nested: bit bi set when L * B[bi] < 2^16 (two rates per 32-bit multiply-add)
 };
 
 // NB = nB exactly (1..8; 0 = generic loop bound p.nB for the unstaged fallback).
@@ -540,6 +541,20 @@ __global__ void __launch_bounds__(QT, kQNestedBlocksPerSM)
         for (int bi = 0; bi < NB; ++bi) {
           const int nb = G0 >> bi;
           const uint16_t* lv = sb + soff + ((size_t)c * nb) * K * NRP + mo[bi];
+          if (NRP == 4 && (qc.packed >> bi) & 1) {
+            // two rates per 32-bit multiply-add: the staged (o_r0 | o_r1 << 16) times the batch's correct
+            // count adds sv*o_r0 to the low half and sv*o_r1 to the high half; over the level's batches of
+            // one chunk the low half sums to at most L * B[bi] < 2^16 (qc.packed), so it never carries
+            uint32_t p01 = 0, p23 = 0;
+#pragma unroll
+            for (int j = 0; j < nb; ++j) {
+              const uint2 o = *reinterpret_cast<const uint2*>(lv + (size_t)j * K * NRP);
+              p01 += sv[j] * o.x;
+              p23 += sv[j] * o.y;
+            }
+            acc[0][bi] += p01 & 0xffffu; acc[1][bi] += p01 >> 16;
+            acc[2][bi] += p23 & 0xffffu; acc[3][bi] += p23 >> 16;
+          } else
 #pragma unroll
           for (int j = 0; j < nb; ++j) {
             if (NRP == 4) {
@@ -615,6 +630,7 @@ cudaError_t launch_q(const QParams& p, int sm_count, cudaStream_t st) {
     qc.nbc[bi] = (int)(p.L / p.B[bi]);
     qc.soff[bi] = tot;
     qc.nbat[bi] = p.N / p.B[bi];
+    if ((int64_t)p.L * p.B[bi] < 65536 && !getenv("RK_Q_UNPACKED")) qc.packed |= 1u << bi;
     tot += qc.nbc[bi];
     bmax = p.B[bi] > bmax ? p.B[bi] : bmax;
   }

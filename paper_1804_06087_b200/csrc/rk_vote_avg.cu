@@ -209,25 +209,6 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
     for (uint32_t lm = live; lm; lm &= lm - 1) {
       const int m = __ffs(lm) - 1;
       const float* row = rowbase + (size_t)m * p.ldc;
-#ifdef RK_AVG_PD2
-      {  // two-rows-ahead L2 prefetch over the live rows of this sample, then of the next one
-        const uint32_t rest = lm & (lm - 1), rest2 = rest & (rest - 1);
-        const float* nrow = nullptr;
-        if (rest2) {
-          nrow = rowbase + (size_t)(__ffs(rest2) - 1) * p.ldc;
-        } else if (REC) {
-          if (e + nw < W) {
-            const int64_t n2 = (int64_t)__shfl_sync(FULL, rvn, 28);
-            uint32_t l2 = ((1u << K) - 1u) & ~__shfl_sync(FULL, rvn, 30);
-            if (!rest) l2 &= l2 - 1;  // this is the sample's last row: the next sample's second live row
-            if (l2) nrow = p.logits + (n2 * K + (__ffs(l2) - 1)) * p.ldc;
-          }
-        }
-        if (nrow && lane * 32 < p.ldc) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + lane * 32));
-        if (!REC && rest && lane * 32 < p.ldc)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(rowbase + (size_t)(__ffs(rest) - 1) * p.ldc + lane * 32));
-      }
-#else
       {  // one-row-ahead L2 prefetch (the next live row, else the next sample's first one): 128 B per lane
         const uint32_t rest = lm & (lm - 1);
         const float* nrow = nullptr;
@@ -244,7 +225,6 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
         }
         if (nrow && lane * 32 < p.ldc) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + lane * 32));
       }
-#endif
       float4 v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {

@@ -25,7 +25,8 @@ for r in rows:
     d[0] += 1
     d[1] += float(r[14]) / 1e6
 ours = {"gemm_heads_kernel", "vote_classify_kernel", "vote_average_kernel", "vote_batch", "vote_cta", "vote_wsample",
-        "vote_pair", "overdue_kernel", "merge_kernel", "q_kernel", "q_nested_kernel", "fold_kernel"}
+        "vote_pair", "overdue_kernel", "merge_kernel", "q_kernel", "q_nested_kernel", "fold_kernel",
+        "arrival_psum_kernel", "vote_sparse", "gather_rows", "queue_scan"}
 tot_ours = sum(v[1] for k, v in per.items() if any(k.startswith(o) for o in ours))
 lines = [f"# {R} launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of",
          "`python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1`",
