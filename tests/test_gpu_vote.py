@@ -261,9 +261,14 @@ def test_errors(rk):
     # empty batch
     ctx = rk.Context(0)
     ctx.load_ensemble(K, C)
+    with pytest.raises(rk.RkError) as e:  # nothing scored yet
+        ctx.outputs_s2()
+    assert e.value.status == 2  # RK_ESTATE
     ctx.score_logits(None, 12, 0)
+    assert ctx.outputs_s2() is None  # caller logits: no second-largest logits, no row skipping
     t = ctx.subset_stats(None)
     assert t["N"] == 0 and t["cnt_vote"].sum() == 0
+    assert ctx.vote_diag() == (0, 0, 0)
 
 
 QUEUE_CASES = [(3, 10, 1000, 11), (8, 1000, 300, 12), (12, 100, 200, 13), (5, 37, 517, 14)]
