@@ -81,6 +81,7 @@ struct rk_ctx {
   float* ws_s2 = nullptr;      // [N][K] second-largest logit per row (per-model epilogue, Cp > 128)
   int64_t ws_s2_cap = 0;
   bool cur_s2 = false;         // the last rk_score wrote ws_s2
+  bool last_skip_valid = false;  // the last accumulate counted skipped rows (K <= 8 logits path, ldc <= 1024)
   uint16_t* ws_x = nullptr;
   int64_t ws_x_cap = 0;
   alignas(64) uint8_t tmaps[4 * 128];
@@ -842,6 +843,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
         vp.n_skip = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 4);
         CK(cudaMemsetAsync(vp.n_skip, 0, 4, st));
       }
+      ctx->last_skip_valid = warp_path && !wide;
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);
       if (warp_path) CK(launch_vote_warp(vp, grid, st, ctx->d_work, wc, st_top, st_lsum, st_max, ctx->sm_count));
       else CK(launch_vote_batch(vp, ctx->sm_count, st, ctx->d_work, wc, st_top, st_lsum, st_max));
@@ -1390,7 +1392,7 @@ rk_status rk_vote_diag(rk_ctx* ctx, int64_t* worklist, int64_t* fallback, int64_
   if (ctx->d_work && ctx->cur_N > 0) CK(cudaMemcpy(&w, reinterpret_cast<unsigned int*>(ctx->d_work + ctx->cur_N), 4,
                                                    cudaMemcpyDeviceToHost));
   unsigned int k = 0;
-  if (ctx->d_work && ctx->cur_N > 0 && ctx->K <= 8 && !ctx->batch_fused)
+  if (ctx->d_work && ctx->cur_N > 0 && ctx->last_skip_valid && !ctx->batch_fused)
     CK(cudaMemcpy(&k, reinterpret_cast<unsigned int*>(ctx->d_work + 3 * ctx->cur_N + 4), 4, cudaMemcpyDeviceToHost));
   if (worklist) *worklist = w;
   if (fallback) *fallback = ctx->batch_fused ? ctx->last_fallback : 0;

@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
         int k = 0;
         for (uint32_t wm = wmask; wm; wm &= wm - 1, ++k)
           p.wrec[(size_t)(base + k) * kRecWords + lane] = srec[warp][__ffs(wm) - 1][lane];
+        __syncwarp();  // every lane has read the staged records before the next unit overwrites them
       }
     }
 #pragma unroll
