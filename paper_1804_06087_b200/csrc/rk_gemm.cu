@@ -43,7 +43,7 @@ constexpr int THREADS = 64 + EPI_WARPS * 32;
 #endif
 constexpr int EPI_PACK = RK_EPI_PACK;    // packed mode: EPI_PACK / 4 epilogue warps per TMEM lane quarter
 constexpr int NHP = EPI_PACK / 4;
-static_assert(EPI_PACK == 8 || EPI_PACK == 12, "packed epilogue: 2 or 3 warps per lane quarter");
+static_assert(EPI_PACK == 8 || EPI_PACK == 12 || EPI_PACK == 16, "packed epilogue: 2, 3 or 4 warps per lane quarter");
 constexpr int XCH_BYTES = 4 * 32 * 12;   // (max, sum, argmax) hand-over per quarter and partner part
 // CL = 1: one CTA computes a 128 x 256 tile (W tile 256 rows in its smem, 4 stages of 48 KB).
 // CL = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256): each CTA
@@ -58,16 +58,22 @@ struct Tile {
   static constexpr int B_ROWS = BN / CL;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // packed mode with 3 warps per quarter: 12 x 4 KB of store staging; one operand stage makes room
-  static constexpr bool WIDE = (PACK && NHP == 3) || FUSED;
+  // packed mode with 3 or 4 warps per quarter: EPI_PACK x 4 KB of store staging
+  static constexpr bool WIDE = (PACK && NHP >= 3) || FUSED;
 #ifndef RK_GEMM_NS
 #define RK_GEMM_NS 6
 #endif
-  static constexpr int NS = CL == 1 ? (WIDE ? 3 : 4) : (WIDE ? 5 : RK_GEMM_NS);
   static constexpr int STG_TOTAL = FUSED ? 16 * 256 * 8 : (WIDE ? EPI_PACK * 2 * (32 * 16 * 4) : EPI_WARPS * 2 * STG_BYTES);
   static constexpr int XCH_TOTAL = FUSED ? 4 * 32 * XF * 4 : XCH_BYTES * (PACK ? NHP - 1 : 1);
+  // operand stages: as many as the remaining shared memory holds (<= RK_GEMM_NS): 6 for the per-model
+  // CTA-pair tile, 5 (3 warps per quarter) or 4 (4 warps) for the packed one, 4 / 3 single-CTA
+  static constexpr int NS_FIT = (232448 - 1024 - STG_TOTAL - 256 - XCH_TOTAL) / STAGE_BYTES;
+  static constexpr int NS = NS_FIT < RK_GEMM_NS ? NS_FIT : RK_GEMM_NS;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + NS * STAGE_BYTES + STG_TOTAL + 256 + XCH_TOTAL;
 };
+static_assert(RK_GEMM_NS < 6 || (Tile<2>::NS == 6 && Tile<1>::NS == 4 && Tile<2, false, true>::NS == 5 &&
+                                 Tile<1, false, true>::NS == 3 && Tile<2, true>::NS == (NHP == 4 ? 4 : NHP == 3 ? 5 : 6)),
+              "operand stages of each tile shape");
 template <bool PACK, bool FUSED>
 __host__ __device__ constexpr int epi_warps() { return PACK ? EPI_PACK : (FUSED ? FUSED_EPI : EPI_WARPS); }
 static_assert(Tile<1>::SMEM_BYTES <= 232448 && Tile<2>::SMEM_BYTES <= 232448 && Tile<1, true>::SMEM_BYTES <= 232448 &&
