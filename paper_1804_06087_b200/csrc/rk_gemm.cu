@@ -37,7 +37,6 @@ constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB: this CTA's 128 rows of X
 constexpr int EPI_WARPS = 4;
 constexpr int STG_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging box (packed mode: two 32x16 boxes)
-constexpr int THREADS = 64 + EPI_WARPS * 32;
 #ifndef RK_EPI_PACK
 #define RK_EPI_PACK 12
 #endif

@@ -39,7 +39,6 @@ __device__ __forceinline__ float4 ldg_stream(const float* p) {
                : "l"(p));
   return r;
 }
-__device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 

@@ -27,15 +27,6 @@ constexpr int SB = 128;          // samples per grid-sizing unit (kernel A)
 constexpr int KM = 12;
 
 
-__device__ __forceinline__ float4 ldg_stream(const float* p) {
-  float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ float f4c(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
-__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 
 // ragged-tail counts for the correct subsets of one word (samples past the last complete batch; rare)
