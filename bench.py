@@ -315,14 +315,19 @@ def main():
     ctx.set_profiling(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # per-step boundaries for the median / min / max of SURVEY.md §8(d) (value uses the whole region)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
-    for _ in range(args.steps):
+    marks[0].record(stream)
+    for i in range(args.steps):
         t = step()
+        marks[i + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    per_step = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps))
     ks = ctx.kernel_stats()
     diag = ctx.vote_diag() if K <= 8 else (0, 0, 0)
     ctx.set_profiling(False)
@@ -384,6 +389,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "step_ms": {"median": per_step[len(per_step) // 2], "min": per_step[0], "max": per_step[-1], "rank": rank},
         "config": {"workload": cfgname, "K": K, "C": C, "N": Ntot, "D": D, "B": cfg["B"], "rates": cfg["rates"],
                    "tie": args.tie, "queue": bool(args.queue), "subsets": S,
                    "fused_forward_vote": bool(fused and K <= 8 and C > 128), "parallelism": f"samples sharded over {world} GPU(s)",
