@@ -406,7 +406,9 @@ def main():
                        "algorithmic": "(K*C*4 + 4) bytes per sample"},
         "kernels_ms_per_step": {k: ks[k]["ms"] / args.steps for k in ks if ks[k]["launches"]},
         "e2e": {"value": Ntot * S / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * D * 2 + n * 4,
-                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
+                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": e2e_s * 1e3,
+                # the bound of this path: the host->device copy of the features over PCIe (pinned source)
+                "h2d_gbs": (n * D * 2 + n * 4) / e2e_s / 1e9, "bound": "pcie h2d"},
         "gpu_launches": launches,
         "clocks": clk,
         "rank0_check": {"N": int(t["N"]), "a_full_set": float(t["cnt_vote"][-1]) / max(1, int(t["N"])),
