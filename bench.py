@@ -360,6 +360,16 @@ def main():
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
+    # the e2e path's own ceiling: a plain pinned host->device copy of the same features (cudaMemcpyAsync),
+    # device-timed, on this box
+    hp0, hp1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    X.copy_(Xh, non_blocking=True)
+    hp0.record(stream)
+    for _ in range(2):
+        X.copy_(Xh, non_blocking=True)
+    hp1.record(stream)
+    torch.cuda.synchronize()
+    h2d_peak = 2 * n * D * 2 / (hp0.elapsed_time(hp1) / 1e3) / 1e9
     nB, nR = len(cfg["B"]), len(cfg["rates"])
     d2h = 8 * (4 + 3 * S + nB * S + 3 * nR * nB * S) + 16 * nR * nB * S
 
@@ -408,7 +418,8 @@ def main():
         "e2e": {"value": Ntot * S / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * D * 2 + n * 4,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": e2e_s * 1e3,
                 # the bound of this path: the host->device copy of the features over PCIe (pinned source)
-                "h2d_gbs": (n * D * 2 + n * 4) / e2e_s / 1e9, "bound": "pcie h2d"},
+                "h2d_gbs": (n * D * 2 + n * 4) / e2e_s / 1e9, "bound": "pcie h2d",
+                "h2d_peak_gbs": h2d_peak, "frac": (n * D * 2 + n * 4) / e2e_s / 1e9 / h2d_peak},
         "gpu_launches": launches,
         "clocks": clk,
         "rank0_check": {"N": int(t["N"]), "a_full_set": float(t["cnt_vote"][-1]) / max(1, int(t["N"])),
