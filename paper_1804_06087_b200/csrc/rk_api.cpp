@@ -442,8 +442,12 @@ static rk_status score_impl(rk_ctx* ctx, const void* X, int64_t N, int64_t goff,
     CK(cudaEventRecord(ctx->ev_start, st));  // copies must not overwrite ws_x still read by earlier work
     CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_start, 0));
   }
-  for (int64_t r0 = 0, ci = 0; r0 < N; r0 += chunk, ++ci) {
-    const int64_t n = std::min(chunk, N - r0);
+  // Host X: the last chunk's GEMM runs after its copy, exposed; the final `chunk` rows therefore go in
+  // quarter-size pieces (at least 16,384 rows) so that only a short GEMM trails the last copy
+  const int64_t tail0 = host ? std::max<int64_t>(0, N - chunk) : N;
+  const int64_t piece = host ? std::max<int64_t>(16384, (chunk / 4 + 127) / 128 * 128) : N;
+  for (int64_t r0 = 0, ci = 0, n = 0; r0 < N; r0 += n, ++ci) {
+    n = std::min(r0 >= tail0 ? piece : std::min(chunk, tail0 - r0), N - r0);
     const void* Xd = X;
     if (host) {
       uint16_t* dst = ctx->ws_x + r0 * ctx->D;

@@ -134,3 +134,19 @@ def test_host_buffers_e2e(rk):
     t = ctx.subset_stats(y, None)
     o = oracle.table(oracle.logits_gemm(X, W, b, sh), y, K, C)
     compare_tables(t, o, K=K, check_moments=False)
+
+
+def test_host_buffers_chunked(rk):
+    """Host X large enough for the library's chunked staging (copies overlapping the GEMM chunks, the
+    trailing chunk split into quarter pieces): the table equals the device-X table of the same inputs."""
+    K, C, D, N = 3, 300, 128, 150_000
+    y, X, W, b, sh = make(K, C, D, N, 14, real=False)
+    ctx = rk.Context(0)
+    ctx.load_ensemble(K, C, D, W, b, sh)
+    ctx.score(torch.from_numpy(X).cuda(), N)
+    t_dev = ctx.subset_stats(torch.from_numpy(y).cuda(), None)
+    ctx.score(X, N)  # host numpy X: staged by the library in chunks
+    t_host = ctx.subset_stats(y, None)
+    for k in ("cnt_vote", "cnt_avg", "n_recheck"):
+        np.testing.assert_array_equal(t_host[k], t_dev[k], err_msg=k)
+    assert t_host["N"] == N
