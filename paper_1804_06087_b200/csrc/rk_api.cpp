@@ -19,8 +19,17 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a profiler is attached
+
 #include "../../include/rk.h"
 #include "rk_internal.h"
+
+namespace {
+struct NvtxRange {  // names each C-ABI entry point's host span on the profiler timeline (nsys / ncu --nvtx)
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using namespace rk;
 
@@ -319,6 +328,7 @@ void rk_destroy(rk_ctx* ctx) {
 
 rk_status rk_load_ensemble(rk_ctx* ctx, int K, int C, int D, const void* W_bf16, const float* bias,
                            int logit_scale_log2, const int* member_rank, rk_tie_mode tie) {
+  NvtxRange nvtx_("rk_load_ensemble");
   if (!ctx) return RK_EINVAL;
   if (K < 1 || K > kMaxK) return fail(ctx, RK_EINVAL, "K must be in [1,12]");
   if (C < 2 || C > 65535) return fail(ctx, RK_EINVAL, "C must be in [2,65535]");
@@ -495,6 +505,7 @@ static bool fused_supported(const rk_ctx* ctx) {
 }
 
 rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* stream) {
+  NvtxRange nvtx_("rk_score");
   if (!ctx) return RK_EINVAL;
   if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
   if (N < 0 || goff < 0 || (N > 0 && !X)) return fail(ctx, RK_EINVAL, "bad X / N / offset");
@@ -504,6 +515,7 @@ rk_status rk_score(rk_ctx* ctx, const void* X, int64_t N, int64_t goff, void* st
 }
 
 rk_status rk_score_labelled(rk_ctx* ctx, const void* X, const int32_t* labels, int64_t N, int64_t goff, void* stream) {
+  NvtxRange nvtx_("rk_score_labelled");
   if (!ctx) return RK_EINVAL;
   if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
   if (N < 0 || goff < 0 || (N > 0 && (!X || !labels))) return fail(ctx, RK_EINVAL, "bad X / labels / N / offset");
@@ -529,6 +541,7 @@ rk_status rk_score_labelled(rk_ctx* ctx, const void* X, const int32_t* labels, i
 }
 
 rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, int64_t goff, void* stream) {
+  NvtxRange nvtx_("rk_score_logits");
   (void)stream;
   if (!ctx) return RK_EINVAL;
   if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
@@ -549,6 +562,7 @@ rk_status rk_score_logits(rk_ctx* ctx, const float* logits, int ldc, int64_t N, 
 }
 
 rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg) {
+  NvtxRange nvtx_("rk_subset_reset");
   if (!ctx) return RK_EINVAL;
   if (!ctx->loaded) return fail(ctx, RK_ESTATE, "rk_load_ensemble first");
   CK(cudaSetDevice(ctx->dev));
@@ -672,6 +686,7 @@ static rk_status flush_reset(rk_ctx* ctx, cudaStream_t st) {
 }
 
 rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream) {
+  NvtxRange nvtx_("rk_subset_accumulate");
   if (!ctx) return RK_EINVAL;
   if (!ctx->reset_done) return fail(ctx, RK_ESTATE, "rk_subset_reset first");
   if (ctx->finalized) return fail(ctx, RK_ESTATE, "table already finalized (all-reduced): rk_subset_reset first");
@@ -939,6 +954,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
 }
 
 rk_status rk_subset_finalize(rk_ctx* ctx, rk_table* out, void* stream) {
+  NvtxRange nvtx_("rk_subset_finalize");
   if (!ctx) return RK_EINVAL;
   if (!ctx->reset_done) return fail(ctx, RK_ESTATE, "rk_subset_reset first");
   CK(cudaSetDevice(ctx->dev));
@@ -1025,6 +1041,7 @@ rk_status rk_subset_stats(rk_ctx* ctx, const int32_t* labels, const rk_reward_cf
 }
 
 rk_status rk_predict(rk_ctx* ctx, uint32_t v, int32_t* pred_vote, int32_t* pred_avg, float* avgprob, void* stream) {
+  NvtxRange nvtx_("rk_predict");
   if (!ctx) return RK_EINVAL;
   if (!ctx->have_batch) return fail(ctx, RK_ESTATE, "rk_score / rk_score_logits first");
   if (v == 0 || v >= (1u << ctx->K)) return fail(ctx, RK_EINVAL, "v must be in [1, 2^K) (PAPER.md:429 excludes v = 0)");
@@ -1080,6 +1097,7 @@ static rk_status serve_setup(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, i
 
 rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
                           rk_serve_out* out, void* stream) {
+  NvtxRange nvtx_("rk_greedy_serve");
   if (!ctx || !cfg || !out) return RK_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   ServeParams sp;
@@ -1110,6 +1128,7 @@ rk_status rk_greedy_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int6
 
 rk_status rk_async_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64_t delta_ns, const double* acc,
                          rk_serve_out* out, uint64_t* model_batches, void* stream) {
+  NvtxRange nvtx_("rk_async_serve");
   if (!ctx || !cfg || !out) return RK_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   ServeParams sp;
@@ -1143,6 +1162,7 @@ rk_status rk_async_serve(rk_ctx* ctx, const rk_reward_cfg* cfg, int64_t N, int64
 rk_status rk_serve_stream(rk_ctx* ctx, const void* X, int64_t N, const rk_reward_cfg* cfg, int64_t delta_ns,
                           uint32_t v, int32_t* pred_vote, int32_t* pred_avg, rk_serve_out* out, int64_t* n_batches,
                           void* stream) {
+  NvtxRange nvtx_("rk_serve_stream");
   if (!ctx || !cfg) return RK_EINVAL;
   if (!ctx->loaded || !ctx->has_heads) return fail(ctx, RK_ESTATE, "no heads loaded (rk_load_ensemble with W)");
   if (v == 0 || v >= (1u << ctx->K)) return fail(ctx, RK_EINVAL, "v must be in [1, 2^K) (PAPER.md:429 excludes v = 0)");
@@ -1215,6 +1235,7 @@ rk_status rk_serve_stream(rk_ctx* ctx, const void* X, int64_t N, const rk_reward
 }
 
 rk_status rk_sine_arrivals(rk_ctx* ctx, const rk_sine_cfg* cfg, int64_t n0, int64_t N, int64_t* out, void* stream) {
+  NvtxRange nvtx_("rk_sine_arrivals");
   if (!ctx || !cfg) return RK_EINVAL;
   if (!(cfg->ref_rate > 0) || cfg->ref_rate > 1e12 || cfg->period_ns <= 0 || cfg->delta_ns <= 0 ||
       !(cfg->noise_std >= 0) || cfg->noise_std > 1e3 || n0 < 0 || N < 0 || (N > 0 && !out))
@@ -1295,6 +1316,7 @@ rk_status rk_ac_dims(rk_ctx* ctx, int nB, const rk_ac_cfg* ac, int* F, int* A, i
 rk_status rk_ac_rollout(rk_ctx* ctx, const rk_reward_cfg* cfg, const double* acc, const int64_t* arrival, int64_t Narr,
                         const rk_ac_cfg* ac, const float* params, int E, const int64_t* h0, const int32_t* forced,
                         uint64_t seed, rk_ac_traj* traj, void* stream) {
+  NvtxRange nvtx_("rk_ac_rollout");
   if (!ctx) return RK_EINVAL;
   RLParams rp;
   rk_status s = ac_setup(ctx, cfg, ac, rp);
@@ -1331,6 +1353,7 @@ rk_status rk_ac_rollout(rk_ctx* ctx, const rk_reward_cfg* cfg, const double* acc
 
 rk_status rk_ac_grad(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, const float* params,
                      const rk_ac_traj* traj, int E, float* grad, double* losses, void* stream) {
+  NvtxRange nvtx_("rk_ac_grad");
   if (!ctx) return RK_EINVAL;
   RLParams rp;
   rk_status s = ac_setup(ctx, cfg, ac, rp);
@@ -1361,6 +1384,7 @@ rk_status rk_ac_grad(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac,
 
 rk_status rk_ac_apply(rk_ctx* ctx, const rk_reward_cfg* cfg, const rk_ac_cfg* ac, float* params, const float* grad,
                       float lr_pi, float lr_v, void* stream) {
+  NvtxRange nvtx_("rk_ac_apply");
   if (!ctx) return RK_EINVAL;
   RLParams rp;
   rk_status s = ac_setup(ctx, cfg, ac, rp);
