@@ -51,7 +51,16 @@ constexpr int XCH_BYTES = 4 * 32 * 12;   // (max, sum, argmax) hand-over per qua
 // the staging region holds the per-thread candidate queues ([16 entries][256 threads] values and classes)
 // and a per-quarter hand-over of (max, sum, argmax, l_y, flag, T values, T classes) per row.
 constexpr int FUSED_EPI = 8;
-constexpr int XF = 5 + 2 * kFuseT;  // words per row in the fused hand-over
+constexpr int XF = 6 + 2 * kFuseT;  // words per row in the fused hand-over
+// Fused epilogue: a thread starts each row of a model with the threshold it ended its previous row of that
+// model at, minus a margin (the 16th-largest logit varies little between rows): only the ~2 x 16 elements
+// above it are inserted into the top-T list instead of ~16 + 16 ln(504/16). A list left short (fewer than
+// T elements above the threshold; ~1 % of rows) is completed by a bound entry (class kFuseNone, value = the
+// threshold: every unlisted class lies at or below it) and the next row's threshold backs off further.
+#ifndef RK_T0_MARGIN
+#define RK_T0_MARGIN 1.5f
+#endif
+constexpr float kT0Margin = RK_T0_MARGIN, kT0Backoff = 2.0f * RK_T0_MARGIN;
 template <int CL, bool PACK = false, bool FUSED = false>
 struct Tile {
   static constexpr int B_ROWS = BN / CL;
@@ -466,16 +475,22 @@ __device__ __forceinline__ void epilogue_fused(const GemmArgs& a, uint64_t* tful
   int* qc = reinterpret_cast<int*>(staging + 16 * 256 * 4);
   float* xb = xch + q * 32 * XF;          // hand-over of this quarter: [XF][32]
   constexpr int NT = 64;                  // threads of the quarter's two warps (named barriers 1+q, 5+q)
+  float t0m[8];                           // carried starting threshold per model (K <= 8 on this path)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t0m[k] = -INFINITY;
   for (int64_t u = ucl0; u < units; u += ucls, ++nunit) {
     const int mt = (int)(u / a.ng) * CL + crank, model = (int)(u % a.ng);
     const int64_t row = (int64_t)mt * BM + row_in_tile;
     const int yl = row < a.N ? a.labels[row] : -1;
     float mx = -INFINITY, sum = 0.f, lyv = 0.f;
     int arg = 0x7fffffff, lyset = 0;
+    float thr0 = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) thr0 = k == model ? t0m[k] : thr0;
     float tv[kFuseT];
     int ti[kFuseT];
 #pragma unroll
-    for (int k = 0; k < kFuseT; ++k) { tv[k] = -INFINITY; ti[k] = 0; }
+    for (int k = 0; k < kFuseT; ++k) { tv[k] = -INFINITY; ti[k] = kFuseNone; }
     for (int j = 0; j < a.nt; ++j, ++tc) {
       const int width = min(BN, a.Cp - j * BN);
       const uint32_t as = tc & 1;
@@ -512,7 +527,7 @@ __device__ __forceinline__ void epilogue_fused(const GemmArgs& a, uint64_t* tful
           for (int i = 0; i < 16; ++i) lyv = (i == yo) ? v[i] : lyv;
           lyset = 1;
         }
-        const float thr = tv[kFuseT - 1];
+        const float thr = fmaxf(tv[kFuseT - 1], thr0);
         int qn = 0;
 #pragma unroll
         for (int i = 0; i < 16; ++i)
@@ -524,11 +539,20 @@ __device__ __forceinline__ void epilogue_fused(const GemmArgs& a, uint64_t* tful
       }
       release_tmem_stage<CL, FUSED_EPI>(tempty, as, crank, lane);
     }
+    // this half's unlisted elements are <= hb (its 16th value, or its threshold when the list is short)
+    const bool short_h = !(tv[kFuseT - 1] > -INFINITY);
+    const float hb = short_h ? thr0 : -INFINITY;
+    {
+      const float nt0 = short_h ? thr0 - kT0Backoff : tv[kFuseT - 1] - kT0Margin;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t0m[k] = k == model ? nt0 : t0m[k];
+    }
     // merge the two halves of the row
     if (h == 1) {
       if (nunit > 0) asm volatile("bar.sync %0, %1;" ::"r"(5 + q), "n"(NT) : "memory");  // half 0 read the last one
       xb[0 * 32 + lane] = mx; xb[1 * 32 + lane] = sum; xb[2 * 32 + lane] = __int_as_float(arg);
       xb[3 * 32 + lane] = lyv; xb[4 * 32 + lane] = __int_as_float(lyset);
+      xb[(5 + 2 * kFuseT) * 32 + lane] = hb;
 #pragma unroll
       for (int k = 0; k < kFuseT; ++k) {
         xb[(5 + k) * 32 + lane] = tv[k];
@@ -554,6 +578,10 @@ __device__ __forceinline__ void epilogue_fused(const GemmArgs& a, uint64_t* tful
         const float cv = xb[(5 + k) * 32 + lane];
         if (cv > tv[kFuseT - 1]) topk_insert(tv, ti, cv, __float_as_int(xb[(5 + kFuseT + k) * 32 + lane]));
       }
+      // bound for every unlisted class: the merged 16th value, or a short half's threshold if higher; the
+      // last slot then carries it as a bound-only entry (a listed 16th value below it becomes unlisted)
+      const float bnd = fmaxf(hb, xb[(5 + 2 * kFuseT) * 32 + lane]);
+      if (!(tv[kFuseT - 1] >= bnd)) { tv[kFuseT - 1] = bnd; ti[kFuseT - 1] = kFuseNone; }
       asm volatile("bar.arrive %0, %1;" ::"r"(5 + q), "n"(NT) : "memory");
       if (row < a.N) {
         const size_t o = (size_t)row * a.K + model;

@@ -286,6 +286,7 @@ cudaError_t launch_ac_apply(float* P, const float* g, int64_t npol, int64_t np, 
 constexpr int kRecWords = 32;  // worklist record: [0,8) l[m][y], [8,16) rmax, [16,24) lsum, [24,28) top-1 u16,
                                // 28 n, 29 y, 30 mask of the rows the averaging kernel need not stream (K <= 8)
 constexpr int kFuseT = 16;  // NEXT-3: logits kept per (row, model) by the fused GEMM epilogue
+constexpr int kFuseNone = 0xFFFF;  // class of a bound-only top-T entry: its value bounds every unlisted class
 // ---- GEMM (A1) -----------------------------------------------------------------------------------
 struct GemmParams {
   const void* tmap_x;    // CUtensorMap* (host copy passed by value via __grid_constant__)

@@ -6,7 +6,8 @@
 // For a subset v, with p[m][c] = exp((l - rmax_m) - lsum_m) and sums over the members of v:
 //   A_v(y) = sum p[m][y]                                   exact (l_y is kept),
 //   c listed by model m (one of its T largest):            p[m][c] exact,
-//   c not listed by m:                                     0 <= p[m][c] <= pT_m (m's T-th largest value),
+//   c not listed by m:                                     0 <= p[m][c] <= pT_m (m's T-th largest value,
+//                                                          or the bound-only entry the epilogue leaves there),
 // so every competitor c has  LB_v(c) = sum_{m listed} p[m][c]  <=  A_v(c)  <=  UB_v(c) = LB_v(c) +
 // sum_{m not listed} pT_m, and every class listed by no model has A_v(c) <= sum_m pT_m. Hence
 //   y wrong for v  if some c has LB_v(c) > A_v(y) (1 + band);
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(32 * SW) vote_sparse_average_kernel(const Vote
       if (m < K) {
         const size_t o = ((size_t)n * K + m) * T + (ent % T);
         const int c = ti[o];
-        if (c != y) {
+        if (c != y && c != kFuseNone) {  // (a bound-only entry lists no class; its value is pT_m)
           const float pv = __expf((tv[o] - rm) - lm);
           int h = (int)(((uint32_t)c * 2654435761u) >> 24);
           for (;;) {
