@@ -243,7 +243,7 @@ def main():
     ap.add_argument("--queue", action="store_true", help="queue-aware latency (reading Q15, PAPER.md:410)")
     ap.add_argument("--fused", action="store_true",
                     help="NEXT-3 fused forward + vote (rk_score_labelled) instead of rk_score + the logits vote stage "
-                         "(slower on B200 at c2-c4: DESIGN.md §6)")
+                         "(about 1.2 ms slower per c4 step on B200: DESIGN.md §6)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
