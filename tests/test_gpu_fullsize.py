@@ -21,7 +21,8 @@ size:
      to the returned integer sections;
   6. c4: the averaging kernel's row skipping (rows the GEMM's second-largest logit proves irrelevant are
      not streamed) leaves the full-size table unchanged: the same logits through rk_score_logits, where
-     every row is streamed, give the identical table.
+     every row is streamed, give the identical table;
+  7. c4: the NEXT-3 fused path (rk_score_labelled) at full size gives the identical table as well.
 """
 import numpy as np
 import pytest
@@ -152,6 +153,21 @@ def test_fullsize(rk, name):
         assert ctx.vote_diag()[2] == 0
         for k in ("cnt_vote", "cnt_avg", "corr", "O", "Q", "E"):
             np.testing.assert_array_equal(t2[k], t[k], err_msg=f"row skipping changed {k}")
+
+    # 7. (K <= 8) NEXT-3 at full size: the fused forward + vote (rk_score_labelled: top-16 lists with the
+    #    carried thresholds of every thread across its many work units, sparse averages, recompute fallback)
+    #    gives the same table as the logits path
+    if K <= 8:
+        cf = rk.Context(0)
+        cf.load_ensemble(K, C, D, W, b, sh)
+        cf.score_labelled(X, labels, N)
+        tf = cf.subset_stats(labels, cfg)
+        torch.cuda.synchronize()
+        for k in ("cnt_vote", "cnt_avg", "corr", "O", "Q", "E"):
+            np.testing.assert_array_equal(tf[k], t[k], err_msg=f"fused path changed {k}")
+        work, fb, _ = cf.vote_diag()
+        assert 0 < fb < work
+        cf.close()
 
     # 5. fold of the full-size integer table (eq. multi_acc_reward; readings Q7, Q11, Q13)
     B = np.array(c["B"], dtype=np.float64)
