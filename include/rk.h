@@ -156,7 +156,9 @@ typedef struct {
 rk_status rk_subset_reset(rk_ctx* ctx, const rk_reward_cfg* cfg);
 /* A2-A5 on the last rk_score* batch. labels: [N] int32, host or device. */
 rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream);
-/* A6 (all-reduce when world > 1) + A7 (reward fold) + copy to `out`. Blocks on `stream`.
+/* A6 (all-reduce when world > 1) + A7 (reward fold) + copy to `out`. Blocks on `stream`. The table and
+ * rewards come back through a page-locked host buffer the context allocates on first use (grow-only,
+ * freed by rk_destroy; 3.5 MB at K = 12 with 5 batch sizes and 4 rates), then are copied into `out`.
  * Returns RK_ENONFINITE / RK_ELABEL if any accumulated chunk had bad input (table zeroed).
  * The all-reduce runs once per reset: a repeated finalize returns the same global table, and
  * rk_subset_accumulate after a finalize is RK_ESTATE until the next rk_subset_reset. The wait for the
