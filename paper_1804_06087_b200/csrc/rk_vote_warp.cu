@@ -294,6 +294,22 @@ __global__ void __launch_bounds__(WT, 6) vote_classify_kernel(const VoteParams p
 
 }  // namespace
 
+// Grid of the classify kernel: its warps stride over the units, so the grid is one full wave (the CTAs that
+// fit on the SMs at once, from the occupancy API) or fewer; a grid with a partial second wave leaves most
+// SMs idle while the last CTAs finish (sm_count * 8 CTAs had been 1.33 waves at 6 resident per SM).
+template <bool STATS>
+static int64_t classify_grid(int64_t units, int sm_count) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, vote_classify_kernel<STATS>, WT, 0) != cudaSuccess || b < 1)
+      b = 6;
+    per_sm = b;
+  }
+  const int64_t ga = (units + WPC - 1) / WPC, cap = (int64_t)sm_count * per_sm;
+  return ga < cap ? ga : cap;
+}
+
 cudaError_t launch_vote_classify(const VoteParams& p, cudaStream_t st, int32_t* work, unsigned int* work_count,
                                  int sm_count) {
   if (p.N <= 0) return cudaSuccess;
@@ -302,8 +318,7 @@ cudaError_t launch_vote_classify(const VoteParams& p, cudaStream_t st, int32_t* 
   if (!p.lsum_in) return cudaErrorInvalidValue;  // statistics come from the GEMM
   const int U = p.gs > 0 ? p.gs : 16;
   const int64_t units = (p.N + U - 1) / U;
-  int64_t ga = (units + WPC - 1) / WPC;
-  if (ga > (int64_t)sm_count * 8) ga = (int64_t)sm_count * 8;
+  const int64_t ga = classify_grid<true>(units, sm_count);
   vote_classify_kernel<true><<<(int)ga, WT, 0, st>>>(p, work, work_count, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
@@ -330,8 +345,7 @@ cudaError_t launch_vote_warp(const VoteParams& p, int grid, cudaStream_t st, int
   {
     const int U = p.gs > 0 ? p.gs : 16;
     const int64_t units = (p.N + U - 1) / U;
-    int64_t ga = (units + WPC - 1) / WPC;
-    if (ga > (int64_t)sm_count * 8) ga = (int64_t)sm_count * 8;
+    const int64_t ga = p.lsum_in ? classify_grid<true>(units, sm_count) : classify_grid<false>(units, sm_count);
 #ifdef RK_CARVEOUT
     cudaFuncSetAttribute(vote_classify_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, RK_CARVEOUT);
     cudaFuncSetAttribute(vote_classify_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, RK_CARVEOUT);
