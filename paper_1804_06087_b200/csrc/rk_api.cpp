@@ -790,7 +790,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
     {
       // worklist [N] + count, then (K >= 9) the overflow and the CTA-kernel worklists, [N] + count each,
       // and the near-tie pair count
-      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, 3 * N + 5)) != RK_OK) return s;
+      if ((s = ensure(ctx, &ctx->d_work, &ctx->work_cap, 3 * N + 6)) != RK_OK) return s;
       if (!warp_path) {  // near-tie pairs of the warp averaging kernel (a full list sends samples to the CTA kernel)
         if ((s = ensure(ctx, &ctx->d_pairs, &ctx->pairs_cap, N / 2 + 65536)) != RK_OK) return s;
         vp.pairs = ctx->d_pairs;
@@ -860,7 +860,8 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
         static const bool no_skip = getenv("RK_NO_ROW_SKIP") != nullptr;  // development knob (A/B timing)
         vp.s2_in = (ctx->batch_stats && ctx->cur_s2 && !no_skip) ? ctx->ws_s2 : nullptr;
         vp.n_skip = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 4);
-        CK(cudaMemsetAsync(vp.n_skip, 0, 4, st));
+        vp.dyn_ctr = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 5);
+        CK(cudaMemsetAsync(vp.n_skip, 0, 8, st));  // n_skip and dyn_ctr
       }
       ctx->last_skip_valid = warp_path && !wide;
       ProfScope ps(ctx, KK_VOTE, st, bytes, 0);

@@ -39,6 +39,7 @@ struct VoteParams {
                              // y and whose other classes all lie below the theta threshold add only y to the
                              // averaging candidate set, so the averaging kernel skips streaming them
   unsigned int* n_skip;      // with s2_in: number of such rows over the worklist (diagnostic) or null
+  unsigned int* dyn_ctr;     // with wrec: zeroed counter from which the averaging kernel's warps grab entries
   uint32_t* wrec;            // K <= 8 logits path: [worklist][kRecWords] records written by the classify kernel
                              // (l[m][y], rmax, lsum, top-1 as u16, n, y) so the averaging kernel's per-sample
                              // inputs arrive in one coalesced load issued a sample ahead; null = read them by n

@@ -29,6 +29,7 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WT = 128;  // threads per CTA (4 warps)
 constexpr int WPC = WT / 32;
+constexpr int kAvgChunk = 2;  // worklist entries per dynamic grab (REC path)
 constexpr int JMAX = 8;  // subsets per lane (S <= 255)
 constexpr int DSTR = 9;  // exact columns: y + up to 8 distinct top-1 classes (odd stride)
 
@@ -168,11 +169,25 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
   const int64_t W = *work_count;
   // REC: the classify kernel's record of worklist entry e (lane i holds word i); the next entry's record is
   // loaded one sample ahead, so the per-sample dependent chain (entry -> label -> l[m][y], statistics) is gone
-  uint32_t rvn = (REC && gw < W) ? __ldcs(p.wrec + (size_t)gw * kRecWords + lane) : 0u;
+  // REC with p.dyn_ctr: entries are handed out dynamically in chunks of kAvgChunk (one atomic per chunk,
+  // grabbed a chunk ahead) instead of a fixed stride, so warps that drew hard samples do not leave the
+  // others idle at the end of the kernel
+  const bool dyn = REC && p.dyn_ctr != nullptr;
+  auto grab = [&]() -> int64_t {
+    unsigned int b = 0;
+    if (lane == 0) b = atomicAdd(p.dyn_ctr, (unsigned int)kAvgChunk);
+    return (int64_t)__shfl_sync(FULL, b, 0);
+  };
+  int64_t cbase = 0, cnext = 0;
+  if (dyn) { cbase = grab(); cnext = grab(); }
+  const int64_t e0 = dyn ? cbase : gw;
+  uint32_t rvn = (REC && e0 < W) ? __ldcs(p.wrec + (size_t)e0 * kRecWords + lane) : 0u;
 
-  for (int64_t e = gw; e < W; e += nw) {
+  for (int64_t e = e0, en = 0; e < W; e = en) {
+    if (dyn && e == cnext) { cbase = cnext; cnext = grab(); }  // entered the chunk grabbed ahead
+    en = dyn ? (e + 1 < cbase + kAvgChunk ? e + 1 : cnext) : e + nw;
     const uint32_t rv = rvn;
-    if (REC && e + nw < W) rvn = __ldcs(p.wrec + (size_t)(e + nw) * kRecWords + lane);
+    if (REC && en < W) rvn = __ldcs(p.wrec + (size_t)en * kRecWords + lane);
     const int64_t n = REC ? (int64_t)__shfl_sync(FULL, rv, 28) : (int64_t)work[e];
     const int y = REC ? (int)__shfl_sync(FULL, rv, 29) : p.labels[n];
     const float* rowbase = p.logits + n * K * p.ldc;
@@ -214,7 +229,7 @@ __global__ void __launch_bounds__(WT, RK_AVG_MINB) vote_average_kernel(const Vot
         if (rest) {
           nrow = rowbase + (size_t)(__ffs(rest) - 1) * p.ldc;
         } else if (REC) {
-          if (e + nw < W) {  // late in the sample: the next record has arrived
+          if (en < W) {  // late in the sample: the next record has arrived
             const int64_t n2 = (int64_t)__shfl_sync(FULL, rvn, 28);
             const uint32_t l2 = ((1u << K) - 1u) & ~__shfl_sync(FULL, rvn, 30);
             if (l2) nrow = p.logits + (n2 * K + (__ffs(l2) - 1)) * p.ldc;
