@@ -794,6 +794,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
       if (!warp_path) {  // near-tie pairs of the warp averaging kernel (a full list sends samples to the CTA kernel)
         if ((s = ensure(ctx, &ctx->d_pairs, &ctx->pairs_cap, N / 2 + 65536)) != RK_OK) return s;
         vp.pairs = ctx->d_pairs;
+        vp.dyn_ctr = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 5);  // warp averaging kernel's grabs
         vp.pair_cap = ctx->pair_cap_test > 0 ? std::min<int64_t>(ctx->pair_cap_test, ctx->pairs_cap) : ctx->pairs_cap;
         vp.pair_count = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 3);
       }

@@ -32,6 +32,7 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WT = 256;      // threads per CTA
 constexpr int WWARPS = WT / 32;
+constexpr int kWsChunk = 4;  // worklist entries per dynamic grab
 // Column groups (float4 each): y + up to 4*NG - 1 competitors; the first NR groups of the lane's TA
 // rows stay in registers, the rest are read from the warp's TAX slice. Instantiations: K <= 11 <5, 3>;
 // K = 12 (two a-slots per lane) <3, 3>, then a second pass <5, 0> over the samples it handed on (a
@@ -193,8 +194,18 @@ __global__ void __launch_bounds__(WT, 2) vote_wsample_average_kernel(const VoteP
   const int64_t W = *work_count;
   const int64_t gw = (int64_t)blockIdx.x * WWARPS + warp, nwarps = (int64_t)gridDim.x * WWARPS;
   const bool lane_ok = 4 * lane < ldc;
+  // worklist entries handed out dynamically in chunks of kWsChunk (one atomic per chunk) when q.dyn_ctr is
+  // set, instead of a fixed stride: warps that draw wide samples do not leave the others idle at the end
+  const bool dyng = p.dyn_ctr != nullptr;
+  auto grab = [&]() -> int64_t {
+    unsigned int b = 0;
+    if (lane == 0) b = atomicAdd(p.dyn_ctr, (unsigned int)kWsChunk);
+    return (int64_t)__shfl_sync(FULL, b, 0);
+  };
 #pragma unroll 1
-  for (int64_t e = gw; e < W; e += nwarps) {
+  for (int64_t cb = dyng ? grab() : gw; cb < W; cb = dyng ? grab() : cb + nwarps)
+#pragma unroll 1
+  for (int64_t e = cb, ce = dyng ? (cb + kWsChunk < W ? cb + kWsChunk : W) : cb + 1; e < ce; ++e) {
     const int64_t n = work[e];
     const int y = p.labels[n];
     // ---- statistics and θ threshold, lane m < K holds model m ----------------------
@@ -423,6 +434,7 @@ cudaError_t launch_k(const VoteParams& q, int sm_count, cudaStream_t st, const i
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vote_wsample_average_kernel<K, NG, NR>, WT, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  if (q.dyn_ctr && (e = cudaMemsetAsync(q.dyn_ctr, 0, sizeof(unsigned int), st)) != cudaSuccess) return e;
   vote_wsample_average_kernel<K, NG, NR><<<sm_count * per_sm, WT, smem, st>>>(q, work, work_count, cta_work, cta_count);
   return cudaGetLastError();
 }
