@@ -817,6 +817,7 @@ rk_status rk_subset_accumulate(rk_ctx* ctx, const int32_t* labels, void* stream)
         // are recomputed below with logits (fallback)
         vp.ly_in = ctx->d_ly;
         vp.logits = nullptr;
+        vp.dyn_ctr = reinterpret_cast<unsigned int*>(ctx->d_work + 3 * N + 5);  // sparse kernel's grabs
         if ((s = ensure(ctx, &ctx->d_fb, &ctx->fb_cap, 2 * N + 2)) != RK_OK) return s;
         unsigned int* fbc = reinterpret_cast<unsigned int*>(ctx->d_fb + 2 * N);
         {

@@ -33,6 +33,7 @@ constexpr int SW = 4;      // warps per CTA
 constexpr int HS = 256;    // hash slots per warp (>= 2 x kMaxFuseK x kFuseT)
 constexpr int kMaxFuseK = 8;
 constexpr int JM = 8;      // subsets per lane (S <= 255)
+constexpr int kSpChunk = 2;  // worklist entries per dynamic grab
 
 struct SparseSmem {
   int key[HS];                  // class or -1
@@ -72,7 +73,15 @@ __global__ void __launch_bounds__(32 * SW) vote_sparse_average_kernel(const Vote
   for (int j = 0; j < JM; ++j) cnt[j] = 0;
   const int64_t W = *work_count;
   const int64_t gw = (int64_t)blockIdx.x * SW + warp, nw = (int64_t)gridDim.x * SW;
-  for (int64_t e = gw; e < W; e += nw) {
+  // worklist entries handed out dynamically in chunks of kSpChunk when p.dyn_ctr is set (see rk_vote_avg.cu)
+  const bool dyng = p.dyn_ctr != nullptr;
+  auto grab = [&]() -> int64_t {
+    unsigned int b = 0;
+    if (lane == 0) b = atomicAdd(p.dyn_ctr, (unsigned int)kSpChunk);
+    return (int64_t)__shfl_sync(FULL, b, 0);
+  };
+  for (int64_t cb = dyng ? grab() : gw; cb < W; cb = dyng ? grab() : cb + nw)
+  for (int64_t e = cb, ce = dyng ? (cb + kSpChunk < W ? cb + kSpChunk : W) : cb + 1; e < ce; ++e) {
     const int64_t n = work[e];
     const int y = p.labels[n];
     float rmx = 0.f, lsm = 0.f, pyl = 0.f, ptl = 0.f;
@@ -238,6 +247,10 @@ cudaError_t launch_vote_sparse(const VoteParams& p, const float* ly, const float
                                const int32_t* work, const unsigned int* work_count, int32_t* fb,
                                unsigned int* fb_count, int sm_count, cudaStream_t st) {
   if (p.K > kMaxFuseK) return cudaErrorInvalidValue;
+  if (p.dyn_ctr) {
+    const cudaError_t e = cudaMemsetAsync(p.dyn_ctr, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return e;
+  }
   vote_sparse_average_kernel<<<sm_count * 8, 32 * SW, 0, st>>>(p, ly, tv, ti, work, work_count, fb, fb_count);
   return cudaGetLastError();
 }
