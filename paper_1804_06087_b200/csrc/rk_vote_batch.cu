@@ -162,7 +162,16 @@ __global__ void __launch_bounds__(BT, RK_GC_MINB) vote_group_classify_kernel(con
   uint8_t* stg = stage_dyn + (size_t)warp * (1 << K);
   uint32_t uw = 0;  // this warp's unanimous-correct samples (lane 0's count is authoritative)
   const int64_t nch = (N + CH - 1) / CH;
-  for (int64_t ch = (int64_t)blockIdx.x * NWB + warp; ch < nch; ch += (int64_t)gridDim.x * NWB) {
+  // 16-sample chunks handed out dynamically (one atomic per chunk) when p.dyn_ctr is set, so the warps that
+  // draw vote-heavy chunks do not leave the rest idle at the end
+  const bool dyng = p.dyn_ctr != nullptr;
+  auto grab = [&]() -> int64_t {
+    unsigned int b = 0;
+    if (lane == 0) b = atomicAdd(p.dyn_ctr, 1u);
+    return (int64_t)__shfl_sync(FULL, b, 0);
+  };
+  for (int64_t ch = dyng ? grab() : (int64_t)blockIdx.x * NWB + warp; ch < nch;
+       ch = dyng ? grab() : ch + (int64_t)gridDim.x * NWB) {
     const int64_t n0 = ch * CH;
     uint32_t k0[NWL], k1[NWL], k2[NWL], k3[NWL], k4[NWL];
 #pragma unroll
@@ -387,6 +396,7 @@ cudaError_t launch_nk(const VoteParams& p, int sm_count, cudaStream_t st, int32_
   {
     const int64_t nb = (p.N + SB - 1) / SB;
     const int grid = (int)(nb < (int64_t)sm_count * RK_GC_MINB ? nb : (int64_t)sm_count * RK_GC_MINB);
+    if (p.dyn_ctr && (e = cudaMemsetAsync(p.dyn_ctr, 0, sizeof(unsigned int), st)) != cudaSuccess) return e;
     constexpr int NWL = NK / 4 > 0 ? NK / 4 : 1;  // words per lane: 2^(K-5) / 32 (K = 9: half the lanes idle)
     const int dsm = (NWB << p.K) + 16;  // + padding: the copy-out reads one word past a row
     if (p.lsum_in) {
